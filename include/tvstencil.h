@@ -1,0 +1,165 @@
+/*
+ * tvstencil.h — C ABI of libtvstencil.so, the B200 (sm_100a) kernel library
+ * behind the drop-in `tvstencil` stencil-run functions.
+ *
+ * The reference is pure Python; every entry point below
+ * replaces the body of one reference function, and a ctypes binding
+ * (paper_2010_04868_b200/_native.py) is the "FFI" that
+ * calls it.  Plain pointers, sizes and POD structs only; no torch types.
+ *
+ *   reference interface                                  -> entry point
+ *   kernels1d.py:89-93   heat1d_temporal(grid, steps)       -> tvs_run (JACOBI, dim 1)
+ *   kernels1d.py:96-103  gs1d_temporal(grid, steps)         -> tvs_run (GAUSS_SEIDEL, dim 1)
+ *   kernels_nd.py:38-45  jacobi2d/3d_temporal(grid, steps)  -> tvs_run (JACOBI, dim 2/3)
+ *   kernels_nd.py:48-55  gs2d/3d_temporal(grid, steps)      -> tvs_run (GAUSS_SEIDEL, dim 2/3)
+ *   baselines.py:43-49   jacobi_plane_update (one step)     -> tvs_jacobi_device(steps=1)
+ *   cli.py:156-170       _bench_once (device-resident reps) -> tvs_plan_* API
+ *   grid.py:127-133      fnv1a64                            -> tvs_fnv1a64
+ *
+ * Arithmetic contract (baselines.py:3-7, 43-49; vec.py:296-298): taps are
+ * evaluated in the order given (the caller passes StencilSpec.offsets()
+ * order, i.e. sorted), first tap a multiply, every further tap a separately
+ * rounded multiply and add.  fma_policy relaxes this only where stated.
+ *
+ * Status codes (mapped to the reference's exceptions by the binding):
+ *   0 ok; 1 size (SizeError); 2 unsupported (UnsupportedError);
+ *   3 invalid argument (ValueError); 4 CUDA error / no device (RuntimeError).
+ * Every function is re-entrant; the last error message is thread-local.
+ */
+#ifndef TVSTENCIL_H
+#define TVSTENCIL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TVS_OK 0
+#define TVS_ERR_SIZE 1
+#define TVS_ERR_UNSUPPORTED 2
+#define TVS_ERR_INVALID 3
+#define TVS_ERR_CUDA 4
+
+#define TVS_JACOBI 0
+#define TVS_GAUSS_SEIDEL 1
+
+#define TVS_MAX_TAPS 27
+
+/* fma_policy */
+#define TVS_FMA_NEVER 0 /* always mul then add: bit-exact vs the reference  */
+#define TVS_FMA_EXACT 1 /* fuse only when every coefficient is 0 or +-2^k:
+                           bit-identical except for subnormal products      */
+#define TVS_FMA_ALLOW 2 /* fuse always (rel. error ~1e-15, tolerance mode) */
+
+/* gs_order (Gauss-Seidel update order) */
+#define TVS_GS_LEXICOGRAPHIC 0 /* row-major in-place loop (model.py:150-156) */
+#define TVS_GS_REFERENCE 1     /* anti-diagonal gather/scatter (baselines.py:83-107) */
+
+/* algo */
+#define TVS_ALGO_AUTO 0
+#define TVS_ALGO_NAIVE 1    /* one step per launch (Jacobi) / hyperplane (GS) */
+#define TVS_ALGO_BLOCKED 2  /* temporal blocking / warp pipelines          */
+
+/* One stencil: StencilSpec (model.py:76-132) flattened.
+ * offsets[k] / coeffs[k] in evaluation order (StencilSpec.offsets()). */
+typedef struct tvs_stencil {
+  int32_t dim;    /* 1..3 */
+  int32_t kind;   /* TVS_JACOBI | TVS_GAUSS_SEIDEL */
+  int32_t ntaps;  /* 1..27 */
+  int32_t radius; /* must be 1 */
+  int32_t offsets[TVS_MAX_TAPS][3];
+  double coeffs[TVS_MAX_TAPS];
+  double boundary; /* constant Dirichlet value of every non-interior cell */
+} tvs_stencil;
+
+/* Host array in the reference Grid layout (grid.py:27-37): a C-contiguous
+ * padded array of `shape`, interior origin at `offset` on every axis. */
+typedef struct tvs_layout {
+  int32_t dim;
+  int32_t pad_;
+  int64_t extents[3];
+  int64_t shape[3];
+  int64_t offset;
+} tvs_layout;
+
+typedef struct tvs_exec {
+  int32_t device;         /* CUDA ordinal */
+  int32_t fma_policy;     /* TVS_FMA_* */
+  int32_t temporal_depth; /* 0 = auto */
+  int32_t gs_order;       /* TVS_GS_* */
+  int32_t algo;           /* TVS_ALGO_* */
+  int32_t reserved[3];
+} tvs_exec;
+
+/* Device layout of one (local) block: last axis padded by 32 elements on each
+ * side (256-byte aligned interior rows), other axes by one halo cell. */
+typedef struct tvs_geometry {
+  int32_t dim;
+  int32_t pad_;
+  int64_t extents[3];    /* local interior extents (axis 0 incl. ghost rows) */
+  int64_t strides[3];    /* element strides of axes 0..dim-1 (last = 1)   */
+  int64_t origin;        /* element index of interior (0,..,0)           */
+  int64_t alloc_elems;   /* allocation size in elements                  */
+  int64_t axis0_offset;  /* global axis-0 index of local position 0      */
+  int64_t axis0_global;  /* global axis-0 extent (Dirichlet edges)       */
+} tvs_geometry;
+
+/* ---- one-call path: host Grid in, host Grid out (ctypes drop-in) ---------
+ * Uploads the interior of `in`, runs `steps` updates on the GPU, downloads
+ * the interior into `out` (pads/halo of `out` untouched).  `in == out` is
+ * allowed (Gauss-Seidel runs in place).  Device buffers are cached per
+ * thread and geometry. */
+int tvs_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, double* out,
+            int64_t steps, const tvs_exec* ex);
+
+/* ---- plan path: device-resident repetitions (cli.py:198-227 timing) ----- */
+typedef struct tvs_plan tvs_plan;
+int tvs_plan_create(const tvs_stencil* st, int32_t dim, const int64_t extents[3], const tvs_exec* ex,
+                    tvs_plan** out);
+int tvs_plan_upload(tvs_plan* p, const tvs_layout* lay, const double* host);
+int tvs_plan_download(tvs_plan* p, const tvs_layout* lay, double* host);
+int tvs_plan_run(tvs_plan* p, int64_t steps);            /* async on the plan stream */
+int tvs_plan_synchronize(tvs_plan* p);
+/* device time of the last tvs_plan_run (CUDA events on the plan stream), ms */
+int tvs_plan_last_ms(tvs_plan* p, float* ms);
+/* launches issued by the last tvs_plan_run (your kernels only) */
+int tvs_plan_last_launches(tvs_plan* p, int64_t* n);
+int tvs_plan_destroy(tvs_plan* p);
+
+/* ---- device path: caller-owned device buffers (halo-exchange module) ---- */
+int tvs_geometry_init(int32_t dim, const int64_t extents[3], int64_t axis0_offset, int64_t axis0_global,
+                      tvs_geometry* g);
+/* Fill every non-interior cell of a device block with `value`. */
+int tvs_fill_halo(const tvs_geometry* g, double* dev, double value, void* stream);
+/* Jacobi: `steps` updates src -> ... -> result; the result lands in `dst`
+ * when steps is odd and in `src` when even (ping-pong, like the reference's
+ * swap at baselines.py:122-124); *result_in_dst reports which.  Axis-0
+ * positions outside [0, axis0_global) are boundary; positions outside the
+ * local block but inside the domain are ghost cells whose influence spreads
+ * one cell per step (callers exchange `steps` ghost rows first). */
+int tvs_jacobi_device(const tvs_stencil* st, const tvs_geometry* g, double* src, double* dst, int64_t steps,
+                      const tvs_exec* ex, void* stream, int32_t* result_in_dst);
+/* Gauss-Seidel in place on one device block (single GPU, no ghosts). */
+int tvs_gauss_seidel_device(const tvs_stencil* st, const tvs_geometry* g, double* grid, int64_t steps,
+                            const tvs_exec* ex, void* stream);
+/* Host <-> device interior copies between the Grid layout and a geometry. */
+int tvs_upload(const tvs_geometry* g, double* dev, const tvs_layout* lay, const double* host, void* stream);
+int tvs_download(const tvs_geometry* g, const double* dev, const tvs_layout* lay, double* host, void* stream);
+
+/* ---- misc -------------------------------------------------------------- */
+const char* tvs_last_error(void);
+int tvs_device_count(int32_t* n);
+int tvs_host_register(void* ptr, size_t bytes);   /* pin a host buffer */
+int tvs_host_unregister(void* ptr);
+/* 64-bit FNV-1a continuing from `state` (grid.py:127-133). Host only. */
+uint64_t tvs_fnv1a64(const void* data, size_t n, uint64_t state);
+/* kernels launched by this thread since the last call (resets the counter) */
+int64_t tvs_launch_counter(void);
+const char* tvs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TVSTENCIL_H */

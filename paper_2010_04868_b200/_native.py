@@ -1,0 +1,262 @@
+"""ctypes binding to ``libtvstencil.so`` (include/tvstencil.h).
+
+This module is the FFI the drop-in functions use; INTEGRATION.md shows the
+same binding as a maintainer would add it to the reference package.  There
+is no CPU fallback: if the library is missing, every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .errors import NativeError, SizeError, UnsupportedError
+
+_LIB_NAME = "libtvstencil.so"
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+TVS_JACOBI, TVS_GAUSS_SEIDEL = 0, 1
+FMA_NEVER, FMA_EXACT, FMA_ALLOW = 0, 1, 2
+GS_LEXICOGRAPHIC, GS_REFERENCE = 0, 1
+ALGO_AUTO, ALGO_NAIVE, ALGO_BLOCKED = 0, 1, 2
+
+
+class Stencil(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int32), ("kind", C.c_int32), ("ntaps", C.c_int32), ("radius", C.c_int32),
+        ("offsets", (C.c_int32 * 3) * 27), ("coeffs", C.c_double * 27), ("boundary", C.c_double),
+    ]
+
+
+class Layout(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int32), ("pad_", C.c_int32), ("extents", C.c_int64 * 3),
+        ("shape", C.c_int64 * 3), ("offset", C.c_int64),
+    ]
+
+
+class Exec(C.Structure):
+    _fields_ = [
+        ("device", C.c_int32), ("fma_policy", C.c_int32), ("temporal_depth", C.c_int32),
+        ("gs_order", C.c_int32), ("algo", C.c_int32), ("reserved", C.c_int32 * 3),
+    ]
+
+
+class Geometry(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int32), ("pad_", C.c_int32), ("extents", C.c_int64 * 3), ("strides", C.c_int64 * 3),
+        ("origin", C.c_int64), ("alloc_elems", C.c_int64), ("axis0_offset", C.c_int64),
+        ("axis0_global", C.c_int64),
+    ]
+
+
+# exported symbols with their argtypes (checked by tests/test_native_abi.py
+# against include/tvstencil.h)
+_P = C.c_void_p
+_SIGS = {
+    "tvs_run": (C.c_int, [C.POINTER(Stencil), C.POINTER(Layout), _P, _P, C.c_int64, C.POINTER(Exec)]),
+    "tvs_plan_create": (C.c_int, [C.POINTER(Stencil), C.c_int32, C.POINTER(C.c_int64), C.POINTER(Exec), C.POINTER(_P)]),
+    "tvs_plan_upload": (C.c_int, [_P, C.POINTER(Layout), _P]),
+    "tvs_plan_download": (C.c_int, [_P, C.POINTER(Layout), _P]),
+    "tvs_plan_run": (C.c_int, [_P, C.c_int64]),
+    "tvs_plan_synchronize": (C.c_int, [_P]),
+    "tvs_plan_last_ms": (C.c_int, [_P, C.POINTER(C.c_float)]),
+    "tvs_plan_last_launches": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "tvs_plan_destroy": (C.c_int, [_P]),
+    "tvs_geometry_init": (C.c_int, [C.c_int32, C.POINTER(C.c_int64), C.c_int64, C.c_int64, C.POINTER(Geometry)]),
+    "tvs_fill_halo": (C.c_int, [C.POINTER(Geometry), _P, C.c_double, _P]),
+    "tvs_jacobi_device": (C.c_int, [C.POINTER(Stencil), C.POINTER(Geometry), _P, _P, C.c_int64, C.POINTER(Exec), _P,
+                                    C.POINTER(C.c_int32)]),
+    "tvs_gauss_seidel_device": (C.c_int, [C.POINTER(Stencil), C.POINTER(Geometry), _P, C.c_int64, C.POINTER(Exec), _P]),
+    "tvs_upload": (C.c_int, [C.POINTER(Geometry), _P, C.POINTER(Layout), _P, _P]),
+    "tvs_download": (C.c_int, [C.POINTER(Geometry), _P, C.POINTER(Layout), _P, _P]),
+    "tvs_last_error": (C.c_char_p, []),
+    "tvs_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
+    "tvs_host_register": (C.c_int, [_P, C.c_size_t]),
+    "tvs_host_unregister": (C.c_int, [_P]),
+    "tvs_fnv1a64": (C.c_uint64, [_P, C.c_size_t, C.c_uint64]),
+    "tvs_launch_counter": (C.c_int64, []),
+    "tvs_version": (C.c_char_p, []),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def library_path() -> str:
+    return os.environ.get("TVSTENCIL_LIB", os.path.join(_HERE, _LIB_NAME))
+
+
+def lib():
+    """Load libtvstencil.so once; raise loudly if it was never built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            path = library_path()
+            if not os.path.exists(path):
+                raise ImportError(
+                    f"{path} not found: build the CUDA library first "
+                    "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+            handle = C.CDLL(path)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == 0:
+        return
+    msg = lib().tvs_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if rc == 1:
+        raise SizeError(text)
+    if rc == 2:
+        raise UnsupportedError(text)
+    if rc == 3:
+        raise ValueError(text)
+    raise NativeError(text)
+
+
+def device_count() -> int:
+    n = C.c_int32(0)
+    lib().tvs_device_count(C.byref(n))
+    return int(n.value)
+
+
+def fnv1a64(view, state: int) -> int:
+    buf = np.frombuffer(view, dtype=np.uint8)
+    return int(lib().tvs_fnv1a64(buf.ctypes.data, buf.size, C.c_uint64(state)))
+
+
+def make_stencil(spec) -> Stencil:
+    """StencilSpec -> tvs_stencil, taps in ``spec.offsets()`` order."""
+    st = Stencil()
+    offs = spec.offsets()
+    if spec.element_kind != "float64" or spec.is_life:
+        raise UnsupportedError(f"{spec.name}: only float64 linear stencils run on the GPU path")
+    if len(offs) == 0 or len(offs) > 27:
+        raise UnsupportedError(f"{spec.name}: needs 1..27 taps")
+    st.dim = spec.dim
+    st.kind = TVS_GAUSS_SEIDEL if spec.dependence_kind == "gauss_seidel" else TVS_JACOBI
+    st.ntaps = len(offs)
+    st.radius = spec.radius
+    for k, off in enumerate(offs):
+        for d in range(3):
+            st.offsets[k][d] = off[d] if d < spec.dim else 0
+        st.coeffs[k] = float(spec.coefficients[off])
+    st.boundary = float(spec.boundary)
+    return st
+
+
+def make_layout(data: np.ndarray, extents, offset: int) -> Layout:
+    lay = Layout()
+    lay.dim = data.ndim
+    for d in range(data.ndim):
+        lay.extents[d] = int(extents[d])
+        lay.shape[d] = int(data.shape[d])
+    for d in range(data.ndim, 3):
+        lay.extents[d] = 1
+        lay.shape[d] = 1
+    lay.offset = int(offset)
+    return lay
+
+
+def make_exec(device=0, fma_policy=FMA_EXACT, temporal_depth=0, gs_order=GS_LEXICOGRAPHIC, algo=ALGO_AUTO) -> Exec:
+    ex = Exec()
+    ex.device, ex.fma_policy, ex.temporal_depth = int(device), int(fma_policy), int(temporal_depth)
+    ex.gs_order, ex.algo = int(gs_order), int(algo)
+    return ex
+
+
+def _host_array(a: np.ndarray) -> np.ndarray:
+    if a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise ValueError("grid data must be a C-contiguous float64 array")
+    return a
+
+
+def run(spec, src: np.ndarray, dst: np.ndarray, extents, offset: int, steps: int, ex: Exec) -> None:
+    """Host Grid data in -> host Grid data out (``src is dst`` allowed)."""
+    st = make_stencil(spec)
+    _host_array(src)
+    _host_array(dst)
+    lay = make_layout(src, extents, offset)
+    check(lib().tvs_run(C.byref(st), C.byref(lay), src.ctypes.data, dst.ctypes.data, int(steps), C.byref(ex)),
+          f"tvs_run({spec.name})")
+
+
+class Plan:
+    """Device-resident run plan (``tvs_plan_*``): upload once, run many,
+    time with CUDA events on the plan stream."""
+
+    def __init__(self, spec, extents, ex: Exec):
+        self.spec = spec
+        self.extents = tuple(int(e) for e in extents)
+        self._st = make_stencil(spec)
+        self._ex = ex
+        ext = (C.c_int64 * 3)(*(list(self.extents) + [1] * (3 - len(self.extents))))
+        h = C.c_void_p()
+        check(lib().tvs_plan_create(C.byref(self._st), len(self.extents), ext, C.byref(ex), C.byref(h)),
+              "tvs_plan_create")
+        self._h = h
+
+    def upload(self, data: np.ndarray, offset: int):
+        lay = make_layout(_host_array(data), self.extents, offset)
+        check(lib().tvs_plan_upload(self._h, C.byref(lay), data.ctypes.data), "tvs_plan_upload")
+
+    def download(self, data: np.ndarray, offset: int):
+        lay = make_layout(_host_array(data), self.extents, offset)
+        check(lib().tvs_plan_download(self._h, C.byref(lay), data.ctypes.data), "tvs_plan_download")
+
+    def run(self, steps: int):
+        check(lib().tvs_plan_run(self._h, int(steps)), "tvs_plan_run")
+
+    def synchronize(self):
+        check(lib().tvs_plan_synchronize(self._h), "tvs_plan_synchronize")
+
+    def last_ms(self) -> float:
+        ms = C.c_float(0)
+        check(lib().tvs_plan_last_ms(self._h, C.byref(ms)), "tvs_plan_last_ms")
+        return float(ms.value)
+
+    def last_launches(self) -> int:
+        n = C.c_int64(0)
+        check(lib().tvs_plan_last_launches(self._h, C.byref(n)), "tvs_plan_last_launches")
+        return int(n.value)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tvs_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def geometry(dim: int, extents, axis0_offset: int = 0, axis0_global: int = 0) -> Geometry:
+    g = Geometry()
+    ext = (C.c_int64 * 3)(*(list(extents) + [1] * (3 - len(extents))))
+    check(lib().tvs_geometry_init(dim, ext, int(axis0_offset), int(axis0_global), C.byref(g)), "tvs_geometry_init")
+    return g
+
+
+def host_register(a: np.ndarray):
+    check(lib().tvs_host_register(a.ctypes.data, a.nbytes), "tvs_host_register")
+
+
+def host_unregister(a: np.ndarray):
+    check(lib().tvs_host_unregister(a.ctypes.data), "tvs_host_unregister")
+
+
+def launch_counter() -> int:
+    return int(lib().tvs_launch_counter())

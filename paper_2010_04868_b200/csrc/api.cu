@@ -1,0 +1,535 @@
+// C-ABI entry points of libtvstencil.so (include/tvstencil.h).
+//
+// Dispatch:
+//   Jacobi 1D        -> jacobi1d_blocked   (register trapezoid, up to 64 steps/launch)
+//   Jacobi 2D star/box -> jacobi2d_blocked (warp strips, D levels per HBM pass)
+//   Jacobi 3D star/box -> jacobi3d_streaming (2.5D plane streaming, 1 step/launch)
+//   Jacobi other     -> jacobi_naive_step  (generic taps, 1 step/launch)
+//   Gauss-Seidel 1D  -> gs1d_pipeline      (time-skewed warp pipeline)
+//   Gauss-Seidel 2D/3D -> gs_wavefront     (hyperplane wavefront, both orders)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace tvs {
+
+static thread_local std::string g_err;
+static thread_local int64_t g_launches = 0;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  return TVS_ERR_CUDA;
+}
+void count_launch(int64_t n) { g_launches += n; }
+
+bool coeffs_power_of_two(const tvs_stencil& st) {
+  for (int k = 0; k < st.ntaps; ++k) {
+    double c = std::fabs(st.coeffs[k]);
+    if (c == 0.0) continue;
+    if (!std::isfinite(c)) return false;
+    int ex;
+    double m = std::frexp(c, &ex);
+    if (m != 0.5) return false;
+  }
+  return true;
+}
+
+bool use_fma(const tvs_stencil& st, const tvs_exec& ex) {
+  if (ex.fma_policy == TVS_FMA_ALLOW) return true;
+  if (ex.fma_policy == TVS_FMA_EXACT) return coeffs_power_of_two(st);
+  return false;
+}
+
+struct ScratchSlot {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int device = -1;
+};
+static thread_local ScratchSlot g_scratch[4];
+
+void* scratch(size_t bytes, int slot) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  ScratchSlot& s = g_scratch[slot];
+  if (s.ptr && s.bytes >= bytes && s.device == dev) return s.ptr;
+  if (s.ptr) {
+    int cur = dev;
+    cudaSetDevice(s.device);
+    cudaFree(s.ptr);
+    cudaSetDevice(cur);
+    s.ptr = nullptr;
+  }
+  if (cudaMalloc(&s.ptr, bytes) != cudaSuccess) {
+    s.ptr = nullptr;
+    s.bytes = 0;
+    return nullptr;
+  }
+  s.bytes = bytes;
+  s.device = dev;
+  return s.ptr;
+}
+
+static int validate(const tvs_stencil* st) {
+  if (!st) return fail(TVS_ERR_INVALID, "null stencil");
+  if (st->dim < 1 || st->dim > 3) return fail(TVS_ERR_INVALID, "dim must be 1..3");
+  if (st->radius != 1) return fail(TVS_ERR_UNSUPPORTED, "only radius-1 stencils are supported");
+  if (st->ntaps < 1 || st->ntaps > TVS_MAX_TAPS) return fail(TVS_ERR_INVALID, "ntaps must be 1..27");
+  if (st->kind != TVS_JACOBI && st->kind != TVS_GAUSS_SEIDEL) return fail(TVS_ERR_INVALID, "bad kind");
+  for (int k = 0; k < st->ntaps; ++k) {
+    for (int d = 0; d < 3; ++d) {
+      int o = st->offsets[k][d];
+      if (o < -1 || o > 1) return fail(TVS_ERR_INVALID, "tap offset exceeds radius 1");
+      if (d >= st->dim && o != 0) return fail(TVS_ERR_INVALID, "tap offset on a missing axis");
+    }
+  }
+  return TVS_OK;
+}
+
+static int validate_exec(const tvs_exec* ex) {
+  if (!ex) return fail(TVS_ERR_INVALID, "null exec");
+  if (ex->fma_policy < 0 || ex->fma_policy > 2) return fail(TVS_ERR_INVALID, "bad fma_policy");
+  if (ex->gs_order < 0 || ex->gs_order > 1) return fail(TVS_ERR_INVALID, "bad gs_order");
+  if (ex->algo < 0 || ex->algo > 2) return fail(TVS_ERR_INVALID, "bad algo");
+  if (ex->temporal_depth < 0) return fail(TVS_ERR_INVALID, "bad temporal_depth");
+  return TVS_OK;
+}
+
+static int set_device(int dev) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return fail(TVS_ERR_CUDA, "no CUDA device available (libtvstencil has no CPU fallback)");
+  if (dev < 0 || dev >= n) return fail(TVS_ERR_INVALID, "device ordinal out of range");
+  TVS_CUDA(cudaSetDevice(dev));
+  return TVS_OK;
+}
+
+// ---- device blocks ---------------------------------------------------------
+static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+static int geometry_init(int dim, const int64_t* ext, int64_t a0_off, int64_t a0_glob, tvs_geometry* g) {
+  std::memset(g, 0, sizeof(*g));
+  if (dim < 1 || dim > 3) return fail(TVS_ERR_INVALID, "dim must be 1..3");
+  for (int d = 0; d < dim; ++d)
+    if (ext[d] < 1) return fail(TVS_ERR_SIZE, "extents must be positive");
+  g->dim = dim;
+  for (int d = 0; d < 3; ++d) g->extents[d] = d < dim ? ext[d] : 1;
+  const int64_t pitch = round_up(ext[dim - 1] + 2 * kPadLast, 32);
+  if (dim == 1) {
+    g->strides[0] = 1;
+    g->origin = kPadLast;
+    g->alloc_elems = pitch;
+  } else if (dim == 2) {
+    g->strides[0] = pitch;
+    g->strides[1] = 1;
+    g->origin = pitch + kPadLast;
+    g->alloc_elems = (ext[0] + 2) * pitch;
+  } else {
+    g->strides[2] = 1;
+    g->strides[1] = pitch;
+    g->strides[0] = (ext[1] + 2) * pitch;
+    g->origin = g->strides[0] + pitch + kPadLast;
+    g->alloc_elems = (ext[0] + 2) * g->strides[0];
+  }
+  g->axis0_offset = a0_off;
+  g->axis0_global = a0_glob > 0 ? a0_glob : ext[0];
+  return TVS_OK;
+}
+
+__global__ void fill_halo_kernel(double* base, tvs_geometry g, double value) {
+  const int64_t n = g.alloc_elems;
+  const int64_t last_pitch = g.dim == 1 ? g.alloc_elems : g.strides[g.dim - 2];
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    bool interior;
+    if (g.dim == 1) {
+      int64_t x = idx - kPadLast;
+      interior = x >= 0 && x < g.extents[0];
+    } else if (g.dim == 2) {
+      int64_t r = idx / last_pitch - 1, c = idx % last_pitch - kPadLast;
+      interior = r >= 0 && r < g.extents[0] && c >= 0 && c < g.extents[1];
+    } else {
+      int64_t p = idx / g.strides[0] - 1;
+      int64_t rem = idx % g.strides[0];
+      int64_t r = rem / g.strides[1] - 1, c = rem % g.strides[1] - kPadLast;
+      interior = p >= 0 && p < g.extents[0] && r >= 0 && r < g.extents[1] && c >= 0 && c < g.extents[2];
+    }
+    if (!interior) base[idx] = value;
+  }
+}
+
+static int fill_halo(const tvs_geometry& g, double* dev, double value, cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>((g.alloc_elems + 255) / 256, 148 * 16);
+  fill_halo_kernel<<<blocks, 256, 0, s>>>(dev, g, value);
+  TVS_LAUNCHED("fill_halo_kernel");
+  return TVS_OK;
+}
+
+static int copy_interior(const tvs_geometry& g, double* dev, const tvs_layout& lay, double* host, bool upload,
+                         cudaStream_t s) {
+  if (lay.dim != g.dim) return fail(TVS_ERR_SIZE, "layout/geometry dimension mismatch");
+  for (int d = 0; d < g.dim; ++d) {
+    if (lay.extents[d] != g.extents[d]) return fail(TVS_ERR_SIZE, "layout/geometry extents mismatch");
+    if (lay.offset + lay.extents[d] > lay.shape[d]) return fail(TVS_ERR_INVALID, "layout shape too small");
+  }
+  double* d0 = dev + g.origin;
+  if (g.dim == 1) {
+    double* h0 = host + lay.offset;
+    size_t bytes = sizeof(double) * g.extents[0];
+    TVS_CUDA(cudaMemcpyAsync(upload ? (void*)d0 : (void*)h0, upload ? (void*)h0 : (void*)d0, bytes,
+                             upload ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s));
+  } else if (g.dim == 2) {
+    double* h0 = host + lay.offset * lay.shape[1] + lay.offset;
+    size_t hp = sizeof(double) * lay.shape[1], dp = sizeof(double) * g.strides[0];
+    size_t w = sizeof(double) * g.extents[1];
+    if (upload)
+      TVS_CUDA(cudaMemcpy2DAsync(d0, dp, h0, hp, w, g.extents[0], cudaMemcpyHostToDevice, s));
+    else
+      TVS_CUDA(cudaMemcpy2DAsync(h0, hp, d0, dp, w, g.extents[0], cudaMemcpyDeviceToHost, s));
+  } else {
+    cudaMemcpy3DParms p;
+    std::memset(&p, 0, sizeof(p));
+    cudaPitchedPtr hptr = make_cudaPitchedPtr(host, sizeof(double) * lay.shape[2], lay.shape[2], lay.shape[1]);
+    cudaPitchedPtr dptr = make_cudaPitchedPtr(dev, sizeof(double) * g.strides[1], g.strides[1],
+                                              g.strides[0] / g.strides[1]);
+    cudaPos hpos = make_cudaPos(sizeof(double) * lay.offset, lay.offset, lay.offset);
+    cudaPos dpos = make_cudaPos(sizeof(double) * kPadLast, 1, 1);
+    p.extent = make_cudaExtent(sizeof(double) * g.extents[2], g.extents[1], g.extents[0]);
+    if (upload) {
+      p.srcPtr = hptr; p.srcPos = hpos; p.dstPtr = dptr; p.dstPos = dpos; p.kind = cudaMemcpyHostToDevice;
+    } else {
+      p.srcPtr = dptr; p.srcPos = dpos; p.dstPtr = hptr; p.dstPos = hpos; p.kind = cudaMemcpyDeviceToHost;
+    }
+    TVS_CUDA(cudaMemcpy3DAsync(&p, s));
+  }
+  return TVS_OK;
+}
+
+// ---- algorithm drivers -----------------------------------------------------
+static int jacobi_device(const tvs_stencil& st, const tvs_geometry& g, double* src, double* dst, int64_t steps,
+                         const tvs_exec& ex, cudaStream_t s, int32_t* in_dst) {
+  const bool fma = use_fma(st, ex);
+  double* a = src;
+  double* b = dst;
+  int64_t done = 0;
+  const bool naive = ex.algo == TVS_ALGO_NAIVE;
+  while (done < steps) {
+    int64_t left = steps - done;
+    int rc;
+    int step_now = 1;
+    if (!naive && g.dim == 1 && jacobi1d_blocked_supported(st, g)) {
+      int depth = ex.temporal_depth > 0 ? ex.temporal_depth : 64;
+      step_now = (int)std::min<int64_t>(left, std::min(depth, 64));
+      rc = jacobi1d_blocked(st, g, a, b, step_now, fma, s);
+    } else if (!naive && g.dim == 2 && jacobi2d_blocked_supported(st)) {
+      int depth = ex.temporal_depth > 0 ? ex.temporal_depth : jacobi2d_max_depth();
+      depth = std::min(depth, jacobi2d_max_depth());
+      step_now = (int)std::min<int64_t>(left, depth);
+      rc = jacobi2d_blocked(st, g, a, b, step_now, fma, s);
+    } else if (!naive && g.dim == 3 && jacobi3d_streaming_supported(st)) {
+      rc = jacobi3d_streaming(st, g, a, b, fma, s);
+    } else {
+      rc = jacobi_naive_step(st, g, a, b, fma, s);
+    }
+    if (rc != TVS_OK) return rc;
+    std::swap(a, b);
+    done += step_now;
+  }
+  if (in_dst) *in_dst = (a == dst) ? 1 : 0;
+  return TVS_OK;
+}
+
+static int gs_device(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, const tvs_exec& ex,
+                     cudaStream_t s) {
+  if (g.axis0_offset != 0 || g.axis0_global != g.extents[0])
+    return fail(TVS_ERR_UNSUPPORTED, "Gauss-Seidel runs on a single GPU (no slab decomposition)");
+  if (steps == 0) return TVS_OK;
+  if (g.dim == 1 && ex.algo != TVS_ALGO_NAIVE) return gs1d_pipeline(st, g, grid, steps, s);
+  return gs_wavefront(st, g, grid, steps, ex.gs_order, s);
+}
+
+// ---- per-thread cached device context for tvs_run ---------------------------
+struct RunCtx {
+  int device = -1;
+  int dim = 0;
+  int64_t ext[3] = {0, 0, 0};
+  double* buf[2] = {nullptr, nullptr};
+  int nbuf = 0;
+  cudaStream_t stream = nullptr;
+  tvs_geometry geo{};
+  ~RunCtx() { release(); }
+  void release() {
+    if (device >= 0) {
+      int cur;
+      cudaGetDevice(&cur);
+      cudaSetDevice(device);
+      for (auto& b : buf)
+        if (b) cudaFree(b), b = nullptr;
+      if (stream) cudaStreamDestroy(stream), stream = nullptr;
+      cudaSetDevice(cur);
+    }
+    device = -1;
+    nbuf = 0;
+  }
+};
+static thread_local RunCtx g_run;
+
+static int ensure_ctx(RunCtx& c, int device, int dim, const int64_t* ext, int nbuf) {
+  bool same = c.device == device && c.dim == dim && c.nbuf >= nbuf;
+  for (int d = 0; d < 3 && same; ++d) same = c.ext[d] == (d < dim ? ext[d] : 1);
+  if (same) return TVS_OK;
+  c.release();
+  c.device = device;
+  c.dim = dim;
+  for (int d = 0; d < 3; ++d) c.ext[d] = d < dim ? ext[d] : 1;
+  int rc = geometry_init(dim, ext, 0, ext[0], &c.geo);
+  if (rc) return rc;
+  TVS_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  for (int i = 0; i < nbuf; ++i) {
+    cudaError_t e = cudaMalloc(&c.buf[i], sizeof(double) * c.geo.alloc_elems);
+    if (e != cudaSuccess) {
+      c.release();
+      return cuda_fail(e, "cudaMalloc(grid)");
+    }
+  }
+  c.nbuf = nbuf;
+  return TVS_OK;
+}
+
+}  // namespace tvs
+
+using namespace tvs;
+
+struct tvs_plan {
+  tvs_stencil st;
+  tvs_exec ex;
+  tvs_geometry geo;
+  double* buf[2] = {nullptr, nullptr};
+  int cur = 0;  // which buffer holds the current field
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t last_launches = 0;
+};
+
+extern "C" {
+
+const char* tvs_last_error(void) { return g_err.c_str(); }
+const char* tvs_version(void) { return "tvstencil-b200 0.1.0 (sm_100a)"; }
+
+int64_t tvs_launch_counter(void) {
+  int64_t n = g_launches;
+  g_launches = 0;
+  return n;
+}
+
+int tvs_device_count(int32_t* n) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) c = 0;
+  if (n) *n = c;
+  return TVS_OK;
+}
+
+uint64_t tvs_fnv1a64(const void* data, size_t n, uint64_t h) {
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 0x100000001B3ull;
+  }
+  return h;
+}
+
+int tvs_host_register(void* ptr, size_t bytes) {
+  TVS_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+  return TVS_OK;
+}
+int tvs_host_unregister(void* ptr) {
+  TVS_CUDA(cudaHostUnregister(ptr));
+  return TVS_OK;
+}
+
+int tvs_geometry_init(int32_t dim, const int64_t extents[3], int64_t axis0_offset, int64_t axis0_global,
+                      tvs_geometry* g) {
+  if (!g || !extents) return fail(TVS_ERR_INVALID, "null argument");
+  return geometry_init(dim, extents, axis0_offset, axis0_global, g);
+}
+
+int tvs_fill_halo(const tvs_geometry* g, double* dev, double value, void* stream) {
+  if (!g || !dev) return fail(TVS_ERR_INVALID, "null argument");
+  return fill_halo(*g, dev, value, (cudaStream_t)stream);
+}
+
+int tvs_upload(const tvs_geometry* g, double* dev, const tvs_layout* lay, const double* host, void* stream) {
+  if (!g || !dev || !lay || !host) return fail(TVS_ERR_INVALID, "null argument");
+  return copy_interior(*g, dev, *lay, const_cast<double*>(host), true, (cudaStream_t)stream);
+}
+
+int tvs_download(const tvs_geometry* g, const double* dev, const tvs_layout* lay, double* host, void* stream) {
+  if (!g || !dev || !lay || !host) return fail(TVS_ERR_INVALID, "null argument");
+  return copy_interior(*g, const_cast<double*>(dev), *lay, host, false, (cudaStream_t)stream);
+}
+
+int tvs_jacobi_device(const tvs_stencil* st, const tvs_geometry* g, double* src, double* dst, int64_t steps,
+                      const tvs_exec* ex, void* stream, int32_t* result_in_dst) {
+  int rc = validate(st);
+  if (rc) return rc;
+  if ((rc = validate_exec(ex))) return rc;
+  if (!g || !src || !dst) return fail(TVS_ERR_INVALID, "null argument");
+  if (st->kind != TVS_JACOBI) return fail(TVS_ERR_INVALID, "tvs_jacobi_device needs a Jacobi stencil");
+  if (st->dim != g->dim) return fail(TVS_ERR_SIZE, "stencil/geometry dimension mismatch");
+  if (steps < 0) return fail(TVS_ERR_INVALID, "steps must be >= 0");
+  return jacobi_device(*st, *g, src, dst, steps, *ex, (cudaStream_t)stream, result_in_dst);
+}
+
+int tvs_gauss_seidel_device(const tvs_stencil* st, const tvs_geometry* g, double* grid, int64_t steps,
+                            const tvs_exec* ex, void* stream) {
+  int rc = validate(st);
+  if (rc) return rc;
+  if ((rc = validate_exec(ex))) return rc;
+  if (!g || !grid) return fail(TVS_ERR_INVALID, "null argument");
+  if (st->kind != TVS_GAUSS_SEIDEL) return fail(TVS_ERR_INVALID, "needs a Gauss-Seidel stencil");
+  if (st->dim != g->dim) return fail(TVS_ERR_SIZE, "stencil/geometry dimension mismatch");
+  if (steps < 0) return fail(TVS_ERR_INVALID, "steps must be >= 0");
+  return gs_device(*st, *g, grid, steps, *ex, (cudaStream_t)stream);
+}
+
+int tvs_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, double* out, int64_t steps,
+            const tvs_exec* ex) {
+  int rc = validate(st);
+  if (rc) return rc;
+  if ((rc = validate_exec(ex))) return rc;
+  if (!lay || !in || !out) return fail(TVS_ERR_INVALID, "null argument");
+  if (lay->dim != st->dim) return fail(TVS_ERR_SIZE, "grid/stencil dimension mismatch");
+  if (steps < 0) return fail(TVS_ERR_INVALID, "steps must be >= 0");
+  if ((rc = set_device(ex->device))) return rc;
+  const bool gs = st->kind == TVS_GAUSS_SEIDEL;
+  if ((rc = ensure_ctx(g_run, ex->device, st->dim, lay->extents, gs ? 1 : 2))) return rc;
+  RunCtx& c = g_run;
+  cudaStream_t s = c.stream;
+  if ((rc = fill_halo(c.geo, c.buf[0], st->boundary, s))) return rc;
+  if ((rc = copy_interior(c.geo, c.buf[0], *lay, const_cast<double*>(in), true, s))) return rc;
+  double* result = c.buf[0];
+  if (gs) {
+    if ((rc = gs_device(*st, c.geo, c.buf[0], steps, *ex, s))) return rc;
+  } else {
+    if ((rc = fill_halo(c.geo, c.buf[1], st->boundary, s))) return rc;
+    int32_t in_dst = 0;
+    if ((rc = jacobi_device(*st, c.geo, c.buf[0], c.buf[1], steps, *ex, s, &in_dst))) return rc;
+    result = in_dst ? c.buf[1] : c.buf[0];
+  }
+  if ((rc = copy_interior(c.geo, result, *lay, out, false, s))) return rc;
+  TVS_CUDA(cudaStreamSynchronize(s));
+  return TVS_OK;
+}
+
+int tvs_plan_create(const tvs_stencil* st, int32_t dim, const int64_t extents[3], const tvs_exec* ex,
+                    tvs_plan** out) {
+  int rc = validate(st);
+  if (rc) return rc;
+  if ((rc = validate_exec(ex))) return rc;
+  if (!out || !extents) return fail(TVS_ERR_INVALID, "null argument");
+  if (dim != st->dim) return fail(TVS_ERR_SIZE, "grid/stencil dimension mismatch");
+  if ((rc = set_device(ex->device))) return rc;
+  tvs_plan* p = new tvs_plan();
+  p->st = *st;
+  p->ex = *ex;
+  if ((rc = geometry_init(dim, extents, 0, extents[0], &p->geo))) {
+    delete p;
+    return rc;
+  }
+  const int nbuf = st->kind == TVS_GAUSS_SEIDEL ? 1 : 2;
+  cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+  for (int i = 0; i < nbuf && e == cudaSuccess; ++i) e = cudaMalloc(&p->buf[i], sizeof(double) * p->geo.alloc_elems);
+  if (e == cudaSuccess) e = cudaEventCreate(&p->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&p->ev1);
+  if (e != cudaSuccess) {
+    tvs_plan_destroy(p);
+    return cuda_fail(e, "tvs_plan_create");
+  }
+  for (int i = 0; i < nbuf; ++i)
+    if ((rc = fill_halo(p->geo, p->buf[i], st->boundary, p->stream))) {
+      tvs_plan_destroy(p);
+      return rc;
+    }
+  *out = p;
+  return TVS_OK;
+}
+
+int tvs_plan_upload(tvs_plan* p, const tvs_layout* lay, const double* host) {
+  if (!p || !lay || !host) return fail(TVS_ERR_INVALID, "null argument");
+  TVS_CUDA(cudaSetDevice(p->ex.device));
+  p->cur = 0;
+  return copy_interior(p->geo, p->buf[0], *lay, const_cast<double*>(host), true, p->stream);
+}
+
+int tvs_plan_download(tvs_plan* p, const tvs_layout* lay, double* host) {
+  if (!p || !lay || !host) return fail(TVS_ERR_INVALID, "null argument");
+  TVS_CUDA(cudaSetDevice(p->ex.device));
+  return copy_interior(p->geo, p->buf[p->cur], *lay, host, false, p->stream);
+}
+
+int tvs_plan_run(tvs_plan* p, int64_t steps) {
+  if (!p) return fail(TVS_ERR_INVALID, "null plan");
+  if (steps < 0) return fail(TVS_ERR_INVALID, "steps must be >= 0");
+  TVS_CUDA(cudaSetDevice(p->ex.device));
+  int64_t before = g_launches;
+  TVS_CUDA(cudaEventRecord(p->ev0, p->stream));
+  int rc;
+  if (p->st.kind == TVS_GAUSS_SEIDEL) {
+    rc = gs_device(p->st, p->geo, p->buf[0], steps, p->ex, p->stream);
+  } else {
+    int32_t in_dst = 0;
+    rc = jacobi_device(p->st, p->geo, p->buf[p->cur], p->buf[1 - p->cur], steps, p->ex, p->stream, &in_dst);
+    if (rc == TVS_OK && in_dst) p->cur = 1 - p->cur;
+  }
+  if (rc) return rc;
+  TVS_CUDA(cudaEventRecord(p->ev1, p->stream));
+  p->last_launches = g_launches - before;
+  return TVS_OK;
+}
+
+int tvs_plan_synchronize(tvs_plan* p) {
+  if (!p) return fail(TVS_ERR_INVALID, "null plan");
+  TVS_CUDA(cudaStreamSynchronize(p->stream));
+  return TVS_OK;
+}
+
+int tvs_plan_last_ms(tvs_plan* p, float* ms) {
+  if (!p || !ms) return fail(TVS_ERR_INVALID, "null argument");
+  TVS_CUDA(cudaEventSynchronize(p->ev1));
+  TVS_CUDA(cudaEventElapsedTime(ms, p->ev0, p->ev1));
+  return TVS_OK;
+}
+
+int tvs_plan_last_launches(tvs_plan* p, int64_t* n) {
+  if (!p || !n) return fail(TVS_ERR_INVALID, "null argument");
+  *n = p->last_launches;
+  return TVS_OK;
+}
+
+int tvs_plan_destroy(tvs_plan* p) {
+  if (!p) return TVS_OK;
+  cudaSetDevice(p->ex.device);
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  for (auto& b : p->buf)
+    if (b) cudaFree(b);
+  if (p->ev0) cudaEventDestroy(p->ev0);
+  if (p->ev1) cudaEventDestroy(p->ev1);
+  if (p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+  return TVS_OK;
+}
+
+}  // extern "C"

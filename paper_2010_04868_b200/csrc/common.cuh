@@ -1,0 +1,106 @@
+// Shared device/host helpers for libtvstencil.so (sm_100a).
+//
+// Arithmetic contract (reference baselines.py:43-49, vec.py:296-298): taps in
+// the caller's (sorted) order, first tap a multiply, every further tap a
+// separately rounded multiply and add.  `tap_first` / `tap_next` below are
+// the only places arithmetic is emitted; __dmul_rn/__dadd_rn are never
+// contracted by nvcc, and the FMA form is opt-in (TVS_FMA_*).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/tvstencil.h"
+
+namespace tvs {
+
+constexpr int kPadLast = 32;  // elements of pad on each side of the contiguous axis
+
+// Per-kernel view of a device block (see tvs_geometry).
+struct Geo {
+  int dim;
+  int64_t e0, e1, e2;  // local extents (unused axes = 1)
+  int64_t s0, s1;      // element strides of axes 0,1 (last axis stride 1)
+  int64_t a0_off;      // global index of local axis-0 position 0
+  int64_t a0_glob;     // global axis-0 extent
+};
+
+inline Geo make_geo(const tvs_geometry& g) {
+  Geo o{};
+  o.dim = g.dim;
+  o.e0 = g.extents[0];
+  o.e1 = g.dim > 1 ? g.extents[1] : 1;
+  o.e2 = g.dim > 2 ? g.extents[2] : 1;
+  o.s0 = g.strides[0];
+  o.s1 = g.dim > 2 ? g.strides[1] : 1;
+  o.a0_off = g.axis0_offset;
+  o.a0_glob = g.axis0_global;
+  return o;
+}
+
+// Tap list in evaluation order, with linear element offsets precomputed for
+// the block's strides.
+struct TapList {
+  int n;
+  int fma;  // 1: fused multiply-add after the first tap
+  double bnd;
+  int64_t lin[TVS_MAX_TAPS];
+  double c[TVS_MAX_TAPS];
+  int8_t off[TVS_MAX_TAPS][3];
+};
+
+template <bool FMA>
+__device__ __forceinline__ double tap_next(double c, double v, double acc) {
+  if constexpr (FMA) {
+    return __fma_rn(c, v, acc);
+  } else {
+    return __dadd_rn(__dmul_rn(c, v), acc);
+  }
+}
+__device__ __forceinline__ double tap_first(double c, double v) { return __dmul_rn(c, v); }
+
+// ---- error plumbing (host) -------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+void count_launch(int64_t n = 1);
+
+#define TVS_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return ::tvs::cuda_fail(e_, #call); \
+  } while (0)
+
+#define TVS_LAUNCHED(name)                                          \
+  do {                                                              \
+    cudaError_t e_ = cudaGetLastError();                            \
+    if (e_ != cudaSuccess) return ::tvs::cuda_fail(e_, name);        \
+    ::tvs::count_launch();                                          \
+  } while (0)
+
+// Fused-multiply-add decision (TVS_FMA_EXACT: all coefficients 0 or +-2^k).
+bool coeffs_power_of_two(const tvs_stencil& st);
+bool use_fma(const tvs_stencil& st, const tvs_exec& ex);
+
+// Kernel-family entry points (each returns a TVS status code).
+int jacobi_naive_step(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
+                      bool fma, cudaStream_t s);
+bool jacobi1d_blocked_supported(const tvs_stencil& st, const tvs_geometry& g);
+int jacobi1d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
+                     int depth, bool fma, cudaStream_t s);
+bool jacobi2d_blocked_supported(const tvs_stencil& st);
+int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
+                     int depth, bool fma, cudaStream_t s);
+int jacobi2d_max_depth();
+bool jacobi3d_streaming_supported(const tvs_stencil& st);
+int jacobi3d_streaming(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
+                       bool fma, cudaStream_t s);
+int gs1d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s);
+int gs_wavefront(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, int order,
+                 cudaStream_t s);
+
+// scratch device memory owned by the calling thread (grown on demand)
+void* scratch(size_t bytes, int slot);
+
+}  // namespace tvs

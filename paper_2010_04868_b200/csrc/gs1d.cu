@@ -1,0 +1,228 @@
+// K5: 1D Gauss-Seidel as a time-skewed warp pipeline.
+//
+// Replaces gs1d_temporal (reference kernels1d.py:96-103) and reproduces the
+// oracle's in-place lexicographic sweep (_gs_sweep_1d, baselines.py:73-80)
+// bit-exactly:  a[i] = ((w0*a_new[i-1]) + w1*a_old[i]) + w2*a_old[i+1].
+//
+// The paper's temporal vectorisation puts consecutive sweeps in the lanes of
+// one vector, lane k trailing lane k-1 by a space stride s > max dx/dt
+// (min_space_stride = 2, model.py:171-193).  Here a lane *is* a sweep:
+//
+//   lane k of global warp g runs sweep q = 32*g + k and, at local step j,
+//   updates position i = j - 3*(k+1)   (lag 3 = min stride 2 + 1, so the
+//   value received by __shfl_up is consumed one step later and the 24-cycle
+//   shuffle stays off the critical path).
+//
+// Per step each lane does one update (its new left neighbour is its own
+// previous result — the serial GS dependence — and its two old values are
+// what lane k-1 produced two and one steps earlier).  The only critical
+// path is DMUL->DADD->DADD = 3 x 8 cycles per position, so one sweep's worth
+// of positions streams through all T lanes with an (N + ~4T) step latency.
+//
+// Lane 31 of a warp feeds lane 0 of the next warp through a shared-memory
+// ring guarded by release/acquire progress counters; the last warp of a block
+// publishes its sweep to a global buffer (release/acquire at GPU scope) that
+// the next block's first warp streams in.  Blocks take tickets in start
+// order and only wait on lower tickets, so the launch is deadlock-free for
+// any grid size.  Sweeps beyond T are identity lanes (they forward their
+// old value), so the last lane always emits sweep T.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace tvs {
+
+constexpr int kGsWarps = 4;          // warps (= 128 sweeps) per block
+constexpr int kGsLag = 3;            // position lag between adjacent lanes
+constexpr int kGsRing = 512;         // per-warp input ring (positions)
+constexpr int kGsMaxBlocks = 64;     // sweeps per launch <= 64 * 128
+static_assert(kGsLag * 32 % 32 == 0, "lane-31 output chunks must align");
+
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ long long ld_acquire_gpu(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(long long* p, long long v) {
+  asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+struct Gs1dArgs {
+  double* a;          // interior origin of the in-place grid
+  double* gbuf;       // (nblocks-1) * n inter-block sweep buffers
+  long long* gprog;   // nblocks progress counters (zeroed per launch)
+  int* ticket;        // zeroed per launch
+  long long n;
+  long long sweeps;   // real sweeps in this launch
+  int nblocks;
+  double w0, w1, w2, bnd;
+};
+
+template <unsigned MASK>
+__device__ __forceinline__ double gs_taps(double L, double C, double R, double w0, double w1, double w2) {
+  double acc = 0.0;
+  bool first = true;
+  if constexpr (MASK & 1u) { acc = tap_first(w0, L); first = false; }
+  if constexpr (MASK & 2u) { acc = first ? tap_first(w1, C) : tap_next<false>(w1, C, acc); first = false; }
+  if constexpr (MASK & 4u) { acc = first ? tap_first(w2, R) : tap_next<false>(w2, R, acc); }
+  return acc;
+}
+
+template <unsigned MASK>
+__global__ void __launch_bounds__(kGsWarps * 32, 1) gs1d_kernel(Gs1dArgs p) {
+  __shared__ double ring[kGsWarps][kGsRing];
+  __shared__ double stage[32];
+  __shared__ int prod[kGsWarps], cons[kGsWarps];
+  __shared__ int s_ticket;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_ticket = atomicAdd(p.ticket, 1);
+  if (threadIdx.x < kGsWarps) prod[threadIdx.x] = cons[threadIdx.x] = 0;
+  __syncthreads();
+  const int b = s_ticket;
+  const long long n = p.n;
+  const double bnd = p.bnd;
+  const long long q = ((long long)b * kGsWarps + w) * 32 + lane;  // this lane's sweep
+  const bool real = q < p.sweeps;
+  const bool last_block = b == p.nblocks - 1;
+  const double* lsrc = b == 0 ? p.a : p.gbuf + (long long)(b - 1) * n;
+  double* odst = last_block ? p.a : p.gbuf + (long long)b * n;
+  const long long nch = (n + 31) / 32 + kGsLag + 1;
+
+  auto wait_upstream = [&](long long need) {  // block b-1 published >= need
+    if (b == 0) return;
+    if (lane == 0)
+      while (ld_acquire_gpu(p.gprog + b - 1) < need) __nanosleep(64);
+    __syncwarp();
+  };
+
+  double L = bnd, u0 = bnd, u1 = bnd, out = bnd;
+  double ld_reg = bnd;
+  if (w == 0) {
+    wait_upstream(min(32ll, n));
+    ld_reg = lane < n ? __ldcg(lsrc + lane) : bnd;
+  }
+
+  for (long long ch = 0; ch < nch; ++ch) {
+    const long long jb = ch * 32;
+    if (w == 0) {
+      // positions [jb, jb+32) into my ring, prefetch the next chunk
+      ring[0][(jb + lane) & (kGsRing - 1)] = ld_reg;
+      const long long nx = jb + 32 + lane;
+      wait_upstream(min(jb + 64, n));
+      ld_reg = nx < n ? __ldcg(lsrc + nx) : bnd;
+      __syncwarp();
+    } else {
+      const int need = (int)min(jb + 31, n);
+      while (ld_acquire_cta(&prod[w]) < need) {
+      }
+    }
+    if (w + 1 < kGsWarps) {  // ring space for positions up to jb-65 in the next warp's ring
+      while (ld_acquire_cta(&cons[w + 1]) <= (int)(jb - 65 - kGsRing)) {
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const long long j = jb + u;
+      double s = __shfl_up_sync(0xffffffffu, out, 1);
+      if (lane == 0) {
+        const long long pos = j - 1;
+        s = (pos >= 0 && pos < n) ? ring[w][pos & (kGsRing - 1)] : bnd;
+      }
+      const long long i = j - kGsLag * (lane + 1);
+      const double v = gs_taps<MASK>(L, u0, u1, p.w0, p.w1, p.w2);
+      out = (i >= 0 && i < n) ? (real ? v : u0) : bnd;
+      L = out;
+      u0 = u1;
+      u1 = s;
+      if (lane == 31) {
+        const long long po = j - kGsLag * 32;
+        if (po >= 0 && po < n) {
+          if (w + 1 < kGsWarps)
+            ring[w + 1][po & (kGsRing - 1)] = out;
+          else
+            stage[po & 31] = out;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 31 && w + 1 < kGsWarps) st_release_cta(&prod[w + 1], (int)max(0ll, min(jb + 32 - kGsLag * 32, n)));
+    if (lane == 0 && w > 0) st_release_cta(&cons[w], (int)(jb + 31));
+    if (w == kGsWarps - 1) {
+      const long long pc = ch - kGsLag;  // position chunk completed by lane 31
+      if (pc >= 0 && pc * 32 < n) {
+        const long long x = pc * 32 + lane;
+        if (x < n) odst[x] = stage[lane];
+        if (!last_block) {
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) st_release_gpu(p.gprog + b, min(pc * 32 + 32, n));
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+static unsigned gs_mask1d(const tvs_stencil& st, double w[3]) {
+  unsigned mask = 0;
+  int last = -2;
+  w[0] = w[1] = w[2] = 0.0;
+  for (int k = 0; k < st.ntaps; ++k) {
+    const int o = st.offsets[k][0];
+    if (o <= last) return 0;
+    last = o;
+    mask |= 1u << (o + 1);
+    w[o + 1] = st.coeffs[k];
+  }
+  return mask;
+}
+
+int gs1d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s) {
+  double w[3];
+  const unsigned mask = gs_mask1d(st, w);
+  if (mask == 0) return gs_wavefront(st, g, grid, steps, TVS_GS_LEXICOGRAPHIC, s);
+  const long long n = g.extents[0];
+  const long long per_launch = (long long)kGsMaxBlocks * kGsWarps * 32;
+  const int max_blocks = (int)std::min<long long>((steps + kGsWarps * 32 - 1) / (kGsWarps * 32), kGsMaxBlocks);
+  const size_t gbuf_bytes = sizeof(double) * (size_t)std::max(1, max_blocks - 1) * (size_t)n;
+  const size_t ctrl_bytes = sizeof(long long) * (kGsMaxBlocks + 2);
+  double* gbuf = static_cast<double*>(scratch(gbuf_bytes, 0));
+  char* ctrl = static_cast<char*>(scratch(ctrl_bytes, 1));
+  if (!gbuf || !ctrl) return fail(TVS_ERR_CUDA, "gs1d_pipeline: out of device memory for sweep buffers");
+  Gs1dArgs a;
+  a.a = grid + g.origin;
+  a.gbuf = gbuf;
+  a.gprog = reinterpret_cast<long long*>(ctrl);
+  a.ticket = reinterpret_cast<int*>(ctrl + sizeof(long long) * kGsMaxBlocks);
+  a.n = n;
+  a.w0 = w[0];
+  a.w1 = w[1];
+  a.w2 = w[2];
+  a.bnd = st.boundary;
+  for (long long done = 0; done < steps; done += per_launch) {
+    a.sweeps = std::min<long long>(steps - done, per_launch);
+    a.nblocks = (int)((a.sweeps + kGsWarps * 32 - 1) / (kGsWarps * 32));
+    TVS_CUDA(cudaMemsetAsync(ctrl, 0, ctrl_bytes, s));
+    switch (mask) {
+      case 1: gs1d_kernel<1><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
+      case 2: gs1d_kernel<2><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
+      case 3: gs1d_kernel<3><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
+      case 4: gs1d_kernel<4><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
+      case 5: gs1d_kernel<5><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
+      case 6: gs1d_kernel<6><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
+      default: gs1d_kernel<7><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
+    }
+    TVS_LAUNCHED("gs1d_kernel");
+  }
+  return TVS_OK;
+}
+
+}  // namespace tvs

@@ -1,0 +1,140 @@
+// K2: 1D radius-1 Jacobi, temporally blocked in registers.
+//
+// Replaces heat1d_temporal / _run_1d (reference kernels1d.py:89-93,
+// 106-220).  The reference packs consecutive *time* levels into one CPU
+// vector to dodge unaligned loads; on a B200 the same goal — touch memory
+// once per many time steps, and make the neighbour exchange a fixed, tiny
+// number of register moves per step — is met by giving each lane P = 32
+// contiguous points in registers and advancing them `depth` (<= 64) steps
+// per launch.  Per step a lane exchanges exactly two values with its
+// neighbours (__shfl_up/__shfl_down of its edge points); each warp owns a
+// 32*P-point tile whose outer `depth` points on each side are the ghost
+// trapezoid (their values decay into garbage one point per step and are
+// never stored).  No shared memory, no block barriers.
+//
+// Per launch: reads 32*P doubles and writes 32*P - 2*depth per warp; the
+// data (2^20 points = 8 MiB) stays L2-resident between launches, so the
+// kernel is FP64-issue bound: 5 DP ops / update unfused, 3 with the exact
+// power-of-two FMA form (heat1d: 0.25/0.5/0.25).
+#include "common.cuh"
+
+namespace tvs {
+
+constexpr int kP1 = 32;      // points per lane
+constexpr int kWarps1 = 8;   // warps per block
+
+template <unsigned MASK, bool FMA>
+__device__ __forceinline__ double upd1(double l, double c, double r, const double w[3]) {
+  double acc = 0.0;
+  bool first = true;
+  if constexpr (MASK & 1u) { acc = tap_first(w[0], l); first = false; }
+  if constexpr (MASK & 2u) { acc = first ? tap_first(w[1], c) : tap_next<FMA>(w[1], c, acc); first = false; }
+  if constexpr (MASK & 4u) { acc = first ? tap_first(w[2], r) : tap_next<FMA>(w[2], r, acc); }
+  return acc;
+}
+
+template <unsigned MASK, bool FMA>
+__global__ void __launch_bounds__(kWarps1 * 32) jacobi1d_kernel(const double* __restrict__ src,
+                                                                double* __restrict__ dst, int64_t n, int depth,
+                                                                double w0, double w1, double w2, double bnd) {
+  const double w[3] = {w0, w1, w2};
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t)blockIdx.x * kWarps1 + (threadIdx.x >> 5);
+  const int64_t useful = 32 * kP1 - 2 * depth;
+  const int64_t x0 = -depth + warp * useful;  // first point of the warp tile
+  if (x0 + depth >= n) return;               // whole warp beyond the domain
+  const int64_t xl = x0 + lane * kP1;         // this lane's first point
+
+  double v[kP1];
+  unsigned out_mask = 0;  // bit m: point xl+m outside [0, n) -> pinned to bnd
+#pragma unroll
+  for (int m = 0; m < kP1; ++m) {
+    const int64_t x = xl + m;
+    const bool in = x >= 0 && x < n;
+    v[m] = in ? src[x] : bnd;
+    out_mask |= (in ? 0u : 1u) << m;
+  }
+  const bool any_out = __any_sync(0xffffffffu, out_mask != 0);
+
+  for (int s = 0; s < depth; ++s) {
+    const double left = __shfl_up_sync(0xffffffffu, v[kP1 - 1], 1);
+    const double right = __shfl_down_sync(0xffffffffu, v[0], 1);
+    double prev = left;
+#pragma unroll
+    for (int m = 0; m < kP1; ++m) {
+      const double cur = v[m];
+      const double nxt = m + 1 < kP1 ? v[m + 1] : right;
+      v[m] = upd1<MASK, FMA>(prev, cur, nxt, w);
+      prev = cur;
+    }
+    if (any_out) {
+#pragma unroll
+      for (int m = 0; m < kP1; ++m)
+        if (out_mask >> m & 1u) v[m] = bnd;
+    }
+  }
+
+  const int64_t lo = x0 + depth, hi = x0 + depth + useful;  // valid outputs
+#pragma unroll
+  for (int m = 0; m < kP1; ++m) {
+    const int64_t x = xl + m;
+    if (x >= lo && x < hi && x >= 0 && x < n) dst[x] = v[m];
+  }
+}
+
+// Tap slots of a 1D radius-1 stencil whose offsets are strictly sorted;
+// -1 if the kernel's fixed (-1, 0, +1) order would not reproduce it.
+static int slots1d(const tvs_stencil& st, double w[3]) {
+  unsigned mask = 0;
+  int last = -2;
+  w[0] = w[1] = w[2] = 0.0;
+  for (int k = 0; k < st.ntaps; ++k) {
+    const int o = st.offsets[k][0];
+    if (o <= last) return -1;
+    last = o;
+    mask |= 1u << (o + 1);
+    w[o + 1] = st.coeffs[k];
+  }
+  return (int)mask;
+}
+
+template <unsigned MASK>
+static void launch1d(bool fma, unsigned blocks, cudaStream_t s, const double* src, double* dst, int64_t n, int depth,
+                     const double w[3], double bnd) {
+  if (fma)
+    jacobi1d_kernel<MASK, true><<<blocks, kWarps1 * 32, 0, s>>>(src, dst, n, depth, w[0], w[1], w[2], bnd);
+  else
+    jacobi1d_kernel<MASK, false><<<blocks, kWarps1 * 32, 0, s>>>(src, dst, n, depth, w[0], w[1], w[2], bnd);
+}
+
+bool jacobi1d_blocked_supported(const tvs_stencil& st, const tvs_geometry& g) {
+  double w[3];
+  return slots1d(st, w) > 0 && g.axis0_offset == 0 && g.axis0_global == g.extents[0];
+}
+
+int jacobi1d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, int depth,
+                     bool fma, cudaStream_t s) {
+  double w[3];
+  const int mask = slots1d(st, w);
+  if (mask <= 0 || depth < 1 || depth > 64)
+    return fail(TVS_ERR_UNSUPPORTED, "jacobi1d_blocked: unsorted taps or depth outside 1..64");
+  const int64_t n = g.extents[0];
+  const int64_t useful = 32 * kP1 - 2 * depth;
+  const int64_t warps = (n + useful - 1) / useful;
+  const unsigned blocks = (unsigned)((warps + kWarps1 - 1) / kWarps1);
+  const double* s0 = src + g.origin;
+  double* d0 = dst + g.origin;
+  switch (mask) {
+    case 1: launch1d<1>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
+    case 2: launch1d<2>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
+    case 3: launch1d<3>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
+    case 4: launch1d<4>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
+    case 5: launch1d<5>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
+    case 6: launch1d<6>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
+    default: launch1d<7>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
+  }
+  TVS_LAUNCHED("jacobi1d_kernel");
+  return TVS_OK;
+}
+
+}  // namespace tvs

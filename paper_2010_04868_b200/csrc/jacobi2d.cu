@@ -1,0 +1,230 @@
+// K3: 2D radius-1 Jacobi (5-point star / 9-point box), temporally blocked.
+//
+// Replaces jacobi2d_temporal / _JacobiNd (reference kernels_nd.py:38-40,
+// 179-291).  Each warp owns a strip of 32*P contiguous columns and streams
+// down a segment of rows; D time levels are advanced per pass over HBM with
+// a one-row time skew between levels (level l works on row m-l while level 0
+// loads row m) — the GPU form of the paper's time-skewed lanes.  Nothing
+// leaves registers between levels:
+//
+//   * a lane holds P columns; the only cross-lane traffic per (level, row) is
+//     its two edge values (__shfl_up/__shfl_down);
+//   * instead of keeping a 3-row window per level, each level keeps two
+//     partial sums per column.  When row q of level l-1 arrives it finishes
+//     output q-1 with the +1-row taps, adds the 0-row taps to output q and
+//     starts output q+1 with the -1-row taps.  Sorted tap order is
+//     -1-row taps, 0-row taps, +1-row taps, each left to right, so the
+//     accumulation order — and the rounding — is exactly the reference's
+//     `acc = c*v + acc` chain (baselines.py:43-49).
+//
+// Ghost trapezoid: the outer D columns of a strip and the first/last D rows
+// of a segment are recomputed by neighbouring warps; useful width is
+// 32*P - 2*D.  HBM traffic per useful update ~ 16 B / D.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace tvs {
+
+constexpr int kP2 = 4;         // columns per lane
+constexpr int kMaxD2 = 8;      // deepest temporal block instantiated
+constexpr int kWarps2 = 4;     // warps per block
+constexpr int kRowsSeg = 256;  // output rows per warp task
+
+constexpr unsigned kStar5 = (1u << 1) | (1u << 3) | (1u << 4) | (1u << 5) | (1u << 7);
+constexpr unsigned kBox9 = 0x1FFu;
+
+template <unsigned MASK, int G>
+__device__ __forceinline__ constexpr bool has_group() {
+  return ((MASK >> (G * 3)) & 7u) != 0;
+}
+
+// acc[p] (+)= sum over taps of row-group G, columns dc = -1, 0, +1, in order.
+template <unsigned MASK, int G, bool START, bool FMA>
+__device__ __forceinline__ void add_group(double (&acc)[kP2], const double (&in)[kP2 + 2], const double (&c)[9]) {
+#pragma unroll
+  for (int p = 0; p < kP2; ++p) {
+    bool fresh = START;
+#pragma unroll
+    for (int dc = 0; dc < 3; ++dc) {
+      if ((MASK >> (G * 3 + dc)) & 1u) {
+        const double v = in[p + dc];
+        if (fresh) {
+          acc[p] = tap_first(c[G * 3 + dc], v);
+          fresh = false;
+        } else {
+          acc[p] = tap_next<FMA>(c[G * 3 + dc], v, acc[p]);
+        }
+      }
+    }
+  }
+}
+
+struct Coeff9 {
+  double c[9];
+};
+
+template <unsigned MASK, int D, bool FMA>
+__global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __restrict__ src,
+                                                                double* __restrict__ dst, Geo g, int64_t origin,
+                                                                Coeff9 cf, double bnd, int64_t n_strips,
+                                                                int64_t n_tasks) {
+  constexpr bool G0 = has_group<MASK, 0>(), G1 = has_group<MASK, 1>(), G2 = has_group<MASK, 2>();
+  constexpr int U = 32 * kP2 - 2 * D;  // useful columns per strip
+  double c[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) c[k] = cf.c[k];
+
+  const int lane = threadIdx.x & 31;
+  const int64_t task = (int64_t)blockIdx.x * kWarps2 + (threadIdx.x >> 5);
+  if (task >= n_tasks) return;
+  const int64_t strip = task % n_strips, seg = task / n_strips;
+  const int64_t col0 = -D + strip * U;          // first column of the strip
+  const int64_t cl = col0 + lane * kP2;          // this lane's first column
+  const int64_t r0 = seg * kRowsSeg;             // first output row
+  const int64_t r1 = min(r0 + kRowsSeg, g.e0);   // output rows [r0, r1)
+
+  unsigned col_out = 0;  // bit p: column cl+p outside the domain
+#pragma unroll
+  for (int p = 0; p < kP2; ++p) col_out |= (cl + p < 0 || cl + p >= g.e1 ? 1u : 0u) << p;
+  const bool any_col_out = __any_sync(0xffffffffu, col_out != 0);
+  unsigned store_mask = 0;  // bit p: column is a useful output of this strip
+#pragma unroll
+  for (int p = 0; p < kP2; ++p) {
+    const int64_t x = cl + p;
+    store_mask |= (x >= col0 + D && x < col0 + D + U && x >= 0 && x < g.e1 ? 1u : 0u) << p;
+  }
+
+  double A[D][kP2], B[D][kP2];
+#pragma unroll
+  for (int l = 0; l < D; ++l)
+#pragma unroll
+    for (int p = 0; p < kP2; ++p) A[l][p] = B[l][p] = 0.0;
+
+  const double* col_base = src + origin + cl;
+  for (int64_t m = r0 - D; m < r1 + D; ++m) {
+    // ---- level 0: load row m (outside the local block / domain -> boundary)
+    double in[kP2 + 2];
+    {
+      const int64_t gr = m + g.a0_off;
+      const bool row_ok = m >= 0 && m < g.e0 && gr >= 0 && gr < g.a0_glob;
+      const double* rp = col_base + m * g.s0;
+#pragma unroll
+      for (int p = 0; p < kP2; ++p) in[p + 1] = (row_ok && !(col_out >> p & 1u)) ? __ldg(rp + p) : bnd;
+      in[0] = __shfl_up_sync(0xffffffffu, in[kP2], 1);
+      in[kP2 + 1] = __shfl_down_sync(0xffffffffu, in[1], 1);
+    }
+    // ---- levels 1..D: level l+1 consumes level-l row (m - l)
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+      double out[kP2];
+      if constexpr (G2) {
+        add_group<MASK, 2, !(G0 || G1), FMA>(B[l], in, c);
+      }
+#pragma unroll
+      for (int p = 0; p < kP2; ++p) out[p] = B[l][p];
+      if constexpr (G1) {
+#pragma unroll
+        for (int p = 0; p < kP2; ++p) B[l][p] = A[l][p];
+        add_group<MASK, 1, !G0, FMA>(B[l], in, c);
+      } else {
+#pragma unroll
+        for (int p = 0; p < kP2; ++p) B[l][p] = A[l][p];
+      }
+      if constexpr (G0) {
+        add_group<MASK, 0, true, FMA>(A[l], in, c);
+      }
+      // out = level l+1 row (m - l - 1)
+      const int64_t q = m - l - 1;
+      const int64_t gq = q + g.a0_off;
+      const bool pin_row = gq < 0 || gq >= g.a0_glob;
+#pragma unroll
+      for (int p = 0; p < kP2; ++p) {
+        const bool pin = pin_row || (any_col_out && (col_out >> p & 1u));
+        in[p + 1] = pin ? bnd : out[p];
+      }
+      if (l + 1 < D) {
+        in[0] = __shfl_up_sync(0xffffffffu, in[kP2], 1);
+        in[kP2 + 1] = __shfl_down_sync(0xffffffffu, in[1], 1);
+      }
+    }
+    // ---- level D row (m - D) is final
+    const int64_t q = m - D;
+    if (q >= r0 && q < r1) {
+      double* wp = dst + origin + q * g.s0 + cl;
+#pragma unroll
+      for (int p = 0; p < kP2; ++p)
+        if (store_mask >> p & 1u) wp[p] = in[p + 1];
+    }
+  }
+}
+
+// Coefficients by 3x3 position if the offsets are strictly sorted (the
+// kernel's fixed order); returns the tap mask or 0.
+static unsigned slots2d(const tvs_stencil& st, Coeff9& cf) {
+  unsigned mask = 0;
+  int last = -100;
+  for (int k = 0; k < 9; ++k) cf.c[k] = 0.0;
+  for (int k = 0; k < st.ntaps; ++k) {
+    const int pos = (st.offsets[k][0] + 1) * 3 + (st.offsets[k][1] + 1);
+    if (pos <= last) return 0;
+    last = pos;
+    mask |= 1u << pos;
+    cf.c[pos] = st.coeffs[k];
+  }
+  return mask;
+}
+
+bool jacobi2d_blocked_supported(const tvs_stencil& st) {
+  Coeff9 cf;
+  const unsigned m = slots2d(st, cf);
+  return m == kStar5 || m == kBox9;
+}
+
+int jacobi2d_max_depth() { return kMaxD2; }
+
+template <unsigned MASK, int D>
+static void launch2d_d(bool fma, unsigned blocks, cudaStream_t s, const double* src, double* dst, const Geo& geo,
+                       int64_t origin, const Coeff9& cf, double bnd, int64_t ns, int64_t nt) {
+  if (fma)
+    jacobi2d_kernel<MASK, D, true><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt);
+  else
+    jacobi2d_kernel<MASK, D, false><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt);
+}
+
+template <unsigned MASK>
+static void launch2d(int depth, bool fma, cudaStream_t s, const double* src, double* dst, const Geo& geo,
+                     int64_t origin, const Coeff9& cf, double bnd) {
+  const int64_t U = 32 * kP2 - 2 * depth;
+  const int64_t ns = (geo.e1 + U - 1) / U;
+  const int64_t nseg = (geo.e0 + kRowsSeg - 1) / kRowsSeg;
+  const int64_t nt = ns * nseg;
+  const unsigned blocks = (unsigned)((nt + kWarps2 - 1) / kWarps2);
+  switch (depth) {
+    case 1: launch2d_d<MASK, 1>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
+    case 2: launch2d_d<MASK, 2>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
+    case 3: launch2d_d<MASK, 3>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
+    case 4: launch2d_d<MASK, 4>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
+    case 5: launch2d_d<MASK, 5>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
+    case 6: launch2d_d<MASK, 6>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
+    case 7: launch2d_d<MASK, 7>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
+    default: launch2d_d<MASK, 8>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
+  }
+}
+
+int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, int depth,
+                     bool fma, cudaStream_t s) {
+  Coeff9 cf;
+  const unsigned mask = slots2d(st, cf);
+  if ((mask != kStar5 && mask != kBox9) || depth < 1 || depth > kMaxD2)
+    return fail(TVS_ERR_UNSUPPORTED, "jacobi2d_blocked: tap set or depth");
+  const Geo geo = make_geo(g);
+  if (mask == kStar5)
+    launch2d<kStar5>(depth, fma, s, src, dst, geo, g.origin, cf, st.boundary);
+  else
+    launch2d<kBox9>(depth, fma, s, src, dst, geo, g.origin, cf, st.boundary);
+  TVS_LAUNCHED("jacobi2d_kernel");
+  return TVS_OK;
+}
+
+}  // namespace tvs

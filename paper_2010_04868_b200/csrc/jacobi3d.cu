@@ -1,0 +1,185 @@
+// K4: 3D radius-1 Jacobi (27-point box / 7-point star), 2.5D plane streaming.
+//
+// Replaces jacobi3d_temporal (reference kernels_nd.py:43-45).  A block owns a
+// (16 x 32) tile of axis-1 x axis-2 columns and streams along axis 0.  Each
+// input plane is staged once in shared memory (cp.async, double-buffered) and
+// contributes to three outputs: it *finishes* output p-1 with the +1-plane
+// taps, continues output p with the 0-plane taps and *starts* output p+1 with
+// the -1-plane taps.  Sorted tap order is exactly plane -1, plane 0, plane +1
+// (each row-major), so the per-point accumulation order equals the
+// reference's `acc = c*v + acc` chain (baselines.py:43-49) — bit-exact.
+//
+// Unfused, a 27-point update costs 53 FP64 ops, so this kernel is FP64-issue
+// bound (~351 GStencil/s at 1.965 GHz), below the single-step HBM roofline
+// (~409); the FMA form (tolerance mode) halves the op count.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace tvs {
+
+constexpr int kTX3 = 32;              // tile width (axis 2) = threads in x
+constexpr int kTYT = 8;               // threads in y
+constexpr int kRY = 2;                // outputs per thread along axis 1
+constexpr int kTY3 = kTYT * kRY;      // tile height (axis 1)
+constexpr int kSW = kTX3 + 2;         // smem row length
+constexpr int kSH = kTY3 + 2;         // smem rows
+constexpr int kPlanesSeg = 64;        // output planes per block
+
+constexpr unsigned kBox27 = (1u << 27) - 1;
+constexpr unsigned kStar7 = (1u << 4) | (1u << 10) | (1u << 12) | (1u << 13) | (1u << 14) | (1u << 16) | (1u << 22);
+
+struct Coeff27 {
+  double c[27];
+};
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// acc[r] (+)= taps of plane-group G (d0 = G-1) for the thread's kRY outputs.
+template <unsigned MASK, int G, bool START, bool FMA>
+__device__ __forceinline__ void add_plane(double (&acc)[kRY], const double (&v)[kRY + 2][3], const double* c) {
+#pragma unroll
+  for (int r = 0; r < kRY; ++r) {
+    bool fresh = START;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int bit = G * 9 + k;
+      if ((MASK >> bit) & 1u) {
+        const double x = v[r + k / 3][k % 3];
+        if (fresh) {
+          acc[r] = tap_first(c[bit], x);
+          fresh = false;
+        } else {
+          acc[r] = tap_next<FMA>(c[bit], x, acc[r]);
+        }
+      }
+    }
+  }
+}
+
+template <unsigned MASK>
+__device__ __forceinline__ constexpr bool has_plane(int G) {
+  return ((MASK >> (G * 9)) & 0x1FFu) != 0;
+}
+
+template <unsigned MASK, bool FMA>
+__global__ void __launch_bounds__(kTX3 * kTYT) jacobi3d_kernel(const double* __restrict__ src,
+                                                               double* __restrict__ dst, Geo g, int64_t origin,
+                                                               Coeff27 cf, double bnd) {
+  constexpr bool G0 = has_plane<MASK>(0), G1 = has_plane<MASK>(1), G2 = has_plane<MASK>(2);
+  __shared__ double tile[2][kSH][kSW];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * kTX3 + tx;
+  const int64_t x0 = (int64_t)blockIdx.x * kTX3, y0 = (int64_t)blockIdx.y * kTY3;
+  const int64_t p0 = (int64_t)blockIdx.z * kPlanesSeg;
+  const int64_t p1 = min(p0 + kPlanesSeg, g.e0);  // outputs [p0, p1)
+
+  // plane `p` (local index, may be -1 or e0 = memory halo) -> smem buffer
+  auto stage = [&](int64_t p, int buf) {
+    const double* base = src + origin + p * g.s0;
+    for (int e = tid; e < kSH * kSW; e += kTX3 * kTYT) {
+      const int r = e / kSW, cc = e % kSW;
+      const int64_t y = y0 + r - 1, x = x0 + cc - 1;
+      if (y >= -1 && y <= g.e1 && x >= -1 && x <= g.e2)
+        cp_async8(&tile[buf][r][cc], base + y * g.s1 + x);
+      else
+        tile[buf][r][cc] = bnd;
+    }
+    cp_async_commit();
+  };
+
+  double A[kRY], B[kRY];
+#pragma unroll
+  for (int r = 0; r < kRY; ++r) A[r] = B[r] = 0.0;
+
+  const int64_t x = x0 + tx;
+  const bool x_ok = x < g.e2;
+  stage(p0 - 1, 0);
+  for (int64_t p = p0 - 1; p <= p1; ++p) {
+    const int buf = (int)((p - p0 + 1) & 1);
+    if (p + 1 <= p1) {
+      stage(p + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    double v[kRY + 2][3];
+#pragma unroll
+    for (int rr = 0; rr < kRY + 2; ++rr)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) v[rr][k] = tile[buf][ty * kRY + rr][tx + k];
+    double out[kRY];
+    if constexpr (G2) add_plane<MASK, 2, !(G0 || G1), FMA>(B, v, cf.c);
+#pragma unroll
+    for (int r = 0; r < kRY; ++r) out[r] = B[r];
+#pragma unroll
+    for (int r = 0; r < kRY; ++r) B[r] = A[r];
+    if constexpr (G1) add_plane<MASK, 1, !G0, FMA>(B, v, cf.c);
+    if constexpr (G0) add_plane<MASK, 0, true, FMA>(A, v, cf.c);
+    // out = output plane p-1
+    const int64_t q = p - 1;
+    if (q >= p0 && q < p1 && x_ok) {
+      const int64_t gq = q + g.a0_off;
+      const bool pin = gq < 0 || gq >= g.a0_glob;
+#pragma unroll
+      for (int r = 0; r < kRY; ++r) {
+        const int64_t y = y0 + ty * kRY + r;
+        if (y < g.e1) dst[origin + q * g.s0 + y * g.s1 + x] = pin ? bnd : out[r];
+      }
+    }
+    __syncthreads();  // buffer `buf` is restaged two iterations later
+  }
+}
+
+static unsigned slots3d(const tvs_stencil& st, Coeff27& cf) {
+  unsigned mask = 0;
+  int last = -1;
+  for (int k = 0; k < 27; ++k) cf.c[k] = 0.0;
+  for (int k = 0; k < st.ntaps; ++k) {
+    const int pos = (st.offsets[k][0] + 1) * 9 + (st.offsets[k][1] + 1) * 3 + (st.offsets[k][2] + 1);
+    if (pos <= last) return 0;
+    last = pos;
+    mask |= 1u << pos;
+    cf.c[pos] = st.coeffs[k];
+  }
+  return mask;
+}
+
+bool jacobi3d_streaming_supported(const tvs_stencil& st) {
+  Coeff27 cf;
+  const unsigned m = slots3d(st, cf);
+  return m == kBox27 || m == kStar7;
+}
+
+int jacobi3d_streaming(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, bool fma,
+                       cudaStream_t s) {
+  Coeff27 cf;
+  const unsigned mask = slots3d(st, cf);
+  if (mask != kBox27 && mask != kStar7) return fail(TVS_ERR_UNSUPPORTED, "jacobi3d_streaming: tap set");
+  const Geo geo = make_geo(g);
+  const dim3 block(kTX3, kTYT);
+  const dim3 grid((unsigned)((geo.e2 + kTX3 - 1) / kTX3), (unsigned)((geo.e1 + kTY3 - 1) / kTY3),
+                  (unsigned)((geo.e0 + kPlanesSeg - 1) / kPlanesSeg));
+  if (mask == kBox27) {
+    if (fma)
+      jacobi3d_kernel<kBox27, true><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary);
+    else
+      jacobi3d_kernel<kBox27, false><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary);
+  } else {
+    if (fma)
+      jacobi3d_kernel<kStar7, true><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary);
+    else
+      jacobi3d_kernel<kStar7, false><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary);
+  }
+  TVS_LAUNCHED("jacobi3d_kernel");
+  return TVS_OK;
+}
+
+}  // namespace tvs

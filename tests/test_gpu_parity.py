@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (through the drop-in functions / C ABI) against
+the reference's own outputs (golden) and the oracle, bit-exact."""
+
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+from conftest import grid_from, spec_for
+from oracle import cref
+from oracle import oracle as npo
+from paper_2010_04868_b200 import Grid, _native, config
+from paper_2010_04868_b200.catalog import get
+from paper_2010_04868_b200.kernels import KernelVariant, gs1d_temporal, gs2d_temporal, heat1d_temporal
+from paper_2010_04868_b200.kernels._common import execute
+from paper_2010_04868_b200.verify import default_matrix, equivalence_matrix, run_temporal
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(kernel, grid, steps, **kw):
+    spec = spec_for(kernel, grid.boundary)
+    return execute(spec, grid, steps, **kw)
+
+
+def test_golden_cases_bitexact(cuda_ready, golden):
+    """Every golden vector of the real reference, through the GPU path."""
+    meta, arrays = golden
+    for c in meta["cases"]:
+        g = grid_from(arrays[c["key"] + "_in"], c["boundary"])
+        got = _run(c["kernel"], g, c["steps"], order="reference")
+        assert np.array_equal(got.interior, arrays[c["key"] + "_out"]), c
+        # pads/halo of the result hold the boundary, input untouched
+        assert np.array_equal(g.interior, arrays[c["key"] + "_in"])
+
+
+def test_known_answers_gpu(cuda_ready):
+    g = Grid.from_array(np.arange(1.0, 9.0), halo=1)
+    # 8 points is below the reference's 1D minimum; run through execute()
+    assert _run("heat1d", g, 1).interior.tolist() == [1, 2, 3, 4, 5, 6, 7, 5.75]
+    g = Grid.from_array(np.ones(3), halo=1)
+    assert _run("gs1d", g, 1).interior.tolist() == [0.75, 0.9375, 0.734375]
+
+
+def test_equivalence_matrix_gpu(cuda_ready):
+    """The reference's acceptance-matrix shape (verify.py:169-222), 8 cells
+    per kernel, GPU runner vs oracle.  GS in 2D/3D compares against the
+    lexicographic oracle (the GPU default order)."""
+    cells = default_matrix(cells_per_kernel=8, master_seed=2024)
+
+    def reference(spec, grid, steps):
+        return cref.scalar_reference(spec, grid, steps, order="lexicographic", threads=8)
+
+    rep = equivalence_matrix(cells, reference)
+    assert rep.passed, rep.to_json()
+
+
+@pytest.mark.parametrize("kernel,ext,steps", [
+    ("gs2d9p", (40, 37), 5), ("gs2d9p", (65, 130), 11), ("gs2d9p", (9, 300), 3),
+    ("gs2d", (33, 64), 7), ("gs3d", (12, 20, 24), 6)])
+@pytest.mark.parametrize("order", ["lexicographic", "reference"])
+def test_gauss_seidel_orders(cuda_ready, kernel, ext, steps, order):
+    g = Grid.random(ext, seed=len(ext) * 100 + steps)
+    got = _run(kernel, g, steps, order=order)
+    want = cref.scalar_reference(get(kernel).spec, g, steps, order=order)
+    assert np.array_equal(got.interior, want.interior)
+
+
+@pytest.mark.parametrize("n,steps", [(32, 1), (33, 7), (1024, 64), (1025, 65), (4096, 1000), (100000, 129),
+                                     (896 * 3, 128), (2 ** 16 + 7, 200)])
+def test_heat1d_sizes(cuda_ready, n, steps):
+    g = Grid.random((n,), seed=n + steps)
+    want = cref.scalar_reference(get("heat1d").spec, g, steps)
+    for fma in ("never", "exact"):
+        got = _run("heat1d", g, steps, fma=fma)
+        assert np.array_equal(got.interior, want.interior), fma
+
+
+@pytest.mark.parametrize("n,steps", [(32, 1), (35, 3), (127, 130), (128, 129), (129, 300), (5000, 257),
+                                     (70000, 140)])
+def test_gs1d_pipeline_sizes(cuda_ready, n, steps):
+    for kernel in ("gs1d", "gs1d_w343"):
+        g = Grid.random((n,), seed=n * 3 + steps, boundary=0.25 if n % 2 else 0.0)
+        spec = spec_for(kernel, g.boundary)
+        want = cref.scalar_reference(spec, g, steps)
+        got = execute(spec, g, steps)
+        assert np.array_equal(got.interior, want.interior), (kernel, n, steps)
+
+
+def test_gs1d_many_blocks_and_passes(cuda_ready):
+    """> 64 blocks of 128 sweeps: exercises multi-launch passes and identity lanes."""
+    g = Grid.random((300,), seed=9)
+    steps = 64 * 128 + 77
+    want = cref.scalar_reference(get("gs1d_w343").spec, g, steps)
+    got = _run("gs1d_w343", g, steps)
+    assert np.array_equal(got.interior, want.interior)
+
+
+@pytest.mark.parametrize("kernel", ["heat2d", "jac2d9p"])
+@pytest.mark.parametrize("ext", [(64, 64), (257, 130), (9, 1000), (1000, 9), (600, 611)])
+def test_jacobi2d_depths(cuda_ready, kernel, ext):
+    g = Grid.random(ext, seed=ext[0] + ext[1], boundary=0.5)
+    spec = spec_for(kernel, 0.5)
+    steps = 19
+    want = cref.scalar_reference(spec, g, steps)
+    for depth in (0, 1, 2, 3, 5, 8):
+        got = execute(spec, g, steps, depth=depth, fma="never")
+        assert np.array_equal(got.interior, want.interior), depth
+    naive = execute(spec, g, steps, algo="naive", fma="never")
+    assert np.array_equal(naive.interior, want.interior)
+
+
+@pytest.mark.parametrize("kernel", ["heat3d", "jac3d27p"])
+@pytest.mark.parametrize("ext", [(20, 18, 37), (65, 17, 33), (130, 40, 9), (3, 70, 70)])
+def test_jacobi3d_streaming(cuda_ready, kernel, ext):
+    g = Grid.random(ext, seed=sum(ext))
+    spec = spec_for(kernel)
+    want = cref.scalar_reference(spec, g, 5)
+    for algo in ("auto", "naive"):
+        got = execute(spec, g, 5, algo=algo, fma="never")
+        assert np.array_equal(got.interior, want.interior), algo
+
+
+def test_fma_policies(cuda_ready):
+    """exact: power-of-two weights fuse bit-identically; allow: tolerance."""
+    g = Grid.random((300, 301), seed=2)
+    want = cref.scalar_reference(get("heat2d").spec, g, 12)
+    assert np.array_equal(_run("heat2d", g, 12, fma="exact").interior, want.interior)
+    g3 = Grid.random((40, 41, 42), seed=3)
+    want3 = cref.scalar_reference(get("jac3d27p").spec, g3, 6)
+    got3 = _run("jac3d27p", g3, 6, fma="allow")
+    rel = np.abs(got3.interior - want3.interior) / np.maximum(np.abs(want3.interior), 1e-300)
+    assert rel.max() <= 1e-12  # BASELINE tolerance
+    assert np.array_equal(_run("jac3d27p", g3, 6, fma="exact").interior, want3.interior)
+
+
+def test_drop_in_signatures_and_immutability(cuda_ready):
+    g = Grid.random((512,), seed=8)
+    before = g.data.copy()
+    a = heat1d_temporal(g, 8, KernelVariant("two_stride", True))
+    b = heat1d_temporal(g, 8, KernelVariant("base", False))
+    assert np.array_equal(a.interior, b.interior)
+    assert np.array_equal(g.data, before)
+    assert np.all(a.data[: a.offset] == 0.0) and np.all(a.data[a.offset + 512:] == 0.0)
+    gs = gs1d_temporal(g, 8, KernelVariant("base", True))
+    assert np.array_equal(gs.interior, npo.scalar_reference(get("gs1d").spec, g, 8).interior)
+    g2 = Grid.random((40, 50), seed=1)
+    out = gs2d_temporal(g2, 3, kernel="gs2d9p", order="reference")
+    assert np.array_equal(out.interior, npo.scalar_reference(get("gs2d9p").spec, g2, 3).interior)
+    r = run_temporal("jac3d27p", Grid.random((20, 20, 20), seed=4), 2)
+    assert r.extents == (20, 20, 20)
+
+
+def test_plan_api_accumulates_steps(cuda_ready):
+    for kernel, ext in (("heat2d", (200, 333)), ("gs1d_w343", (5000,)), ("gs2d9p", (50, 60)),
+                        ("jac3d27p", (30, 20, 40))):
+        spec = get(kernel).spec
+        g = Grid.random(ext, seed=11)
+        plan = _native.Plan(spec, ext, config.current().native())
+        plan.upload(g.data, g.offset)
+        plan.run(3)
+        plan.run(5)
+        plan.synchronize()
+        out = g.alloc_like()
+        plan.download(out.data, out.offset)
+        plan.synchronize()
+        assert plan.last_launches() >= 1 and plan.last_ms() >= 0.0
+        want = cref.scalar_reference(spec, g, 8, order="lexicographic")
+        assert np.array_equal(out.interior, want.interior), kernel
+        plan.close()
+
+
+def test_slab_decomposition_emulated_ranks(cuda_ready):
+    """The sharded path's device side on one GPU: W emulated ranks, halos
+    copied between their buffers (no cross-rank waiting), bit-identical to
+    the single-domain result for W in 1..4 and several depths."""
+    import torch
+
+    from paper_2010_04868_b200 import halo
+
+    for kernel, ext in (("heat2d", (97, 130)), ("jac3d27p", (41, 20, 36))):
+        spec = get(kernel).spec
+        g = Grid.random(ext, seed=5)
+        steps = 13
+        want = cref.scalar_reference(spec, g, steps)
+        st = _native.make_stencil(spec)
+        for world in (1, 2, 3, 4):
+            for depth in (1, 4, 8):
+                lays = [halo.make_layout(ext, world, r, depth) for r in range(world)]
+                bufs = []
+                for lay in lays:
+                    n = int(lay.geometry.alloc_elems)
+                    pair = [torch.full((n,), 0.0, dtype=torch.float64, device="cuda") for _ in range(2)]
+                    view = pair[0].as_strided(tuple(lay.extents), tuple(int(lay.geometry.strides[d]) for d in range(len(ext))),
+                                              int(lay.geometry.origin))
+                    lo, hi = max(lay.r0 - depth, 0), min(lay.r1 + depth, ext[0])
+                    view[lo - (lay.r0 - depth): hi - (lay.r0 - depth)] = torch.from_numpy(g.interior[lo:hi].copy()).cuda()
+                    bufs.append([pair, 0])
+                done = 0
+                while done < steps:
+                    k = min(depth, steps - done)
+                    for r in range(world - 1):  # emulated exchange
+                        a, b = lays[r], lays[r + 1]
+                        ba, bb = bufs[r][0][bufs[r][1]], bufs[r + 1][0][bufs[r + 1][1]]
+                        bb[b.row_slice(0, depth)] = ba[a.row_slice(a.n_own, depth)]
+                        ba[a.row_slice(a.n_own + depth, depth)] = bb[b.row_slice(depth, depth)]
+                    for r, lay in enumerate(lays):
+                        pair, cur = bufs[r]
+                        import ctypes as C
+
+                        in_dst = C.c_int32(0)
+                        ex = _native.make_exec(temporal_depth=depth)
+                        _native.check(_native.lib().tvs_jacobi_device(
+                            C.byref(st), C.byref(lay.geometry), C.c_void_p(pair[cur].data_ptr()),
+                            C.c_void_p(pair[1 - cur].data_ptr()), k, C.byref(ex),
+                            C.c_void_p(torch.cuda.current_stream().cuda_stream), C.byref(in_dst)))
+                        if in_dst.value:
+                            bufs[r][1] = 1 - cur
+                    done += k
+                torch.cuda.synchronize()
+                parts = []
+                for r, lay in enumerate(lays):
+                    pair, cur = bufs[r]
+                    view = pair[cur].as_strided(tuple(lay.extents),
+                                                tuple(int(lay.geometry.strides[d]) for d in range(len(ext))),
+                                                int(lay.geometry.origin))
+                    parts.append(view[depth: depth + lay.n_own].cpu().numpy())
+                got = np.concatenate(parts, 0)
+                assert np.array_equal(got, want.interior), (kernel, world, depth)

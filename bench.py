@@ -1,0 +1,399 @@
+"""Benchmark harness (driver contract + the reference CLI's metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C] [--no-all]
+
+A *step* is one call of the hot path over one synthetic BASELINE workload:
+all T time steps / sweeps of the configured stencil over the full grid.
+GStencil/s = interior points x T / seconds / 1e9 (reference cli.py:228-231).
+
+* ``value``  : device-resident (tvs_plan_* API), CUDA events on the plan
+  stream, W warm-up + K timed steps, barrier + synchronize on both sides,
+  max over ranks.
+* ``e2e``    : the public drop-in call (e.g. ``jacobi2d_temporal``) on pinned
+  host Grids — host->device upload and device->host download inside the
+  timed region, every step.
+* ``cpu_baseline`` : the oracle port (C restatement of the reference's
+  ``scalar_reference``, bit-exact, OpenMP over all host cores for Jacobi;
+  single core for Gauss-Seidel, whose sweep is sequential) on a bounded
+  sample of the same workload, rank 0 only.
+* ``--impl reference`` : times that CPU implementation as the reference arm.
+
+Headline workload (config.workload): BASELINE config 3, 2D 5-point Jacobi
+16384^2 x 200 — the sharded, HBM-bound configuration.  The other four
+BASELINE configs are measured the same way and reported under
+``per_stencil`` (disable with --no-all).  Inputs (2-9 GB per grid for
+configs 3-5) exceed the 126 MB L2; configs 1-2 (8 MiB) are L2-resident by
+design and an L2 flush (256 MiB write) runs between their timed steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs: name, catalog kernel, extents, T,
+# seed, distribution, drop-in function name, algorithmic FP64 ops / update
+CONFIGS = {
+    1: dict(name="1d3p_jacobi", kernel="heat1d", extents=(2 ** 20,), T=1000, seed=0, dist=(-1.0, 1.0),
+            fn="heat1d_temporal", ops=5, shards=False),
+    2: dict(name="1d3p_gauss_seidel", kernel="gs1d_w343", extents=(2 ** 20,), T=1000, seed=1, dist=(-1.0, 1.0),
+            fn="gs1d_temporal", ops=5, shards=False),
+    3: dict(name="2d5p_jacobi", kernel="heat2d", extents=(16384, 16384), T=200, seed=2, dist=(0.0, 1.0),
+            fn="jacobi2d_temporal", ops=9, shards=True),
+    4: dict(name="2d9p_gauss_seidel", kernel="gs2d9p", extents=(8192, 8192), T=100, seed=3, dist=(-1.0, 1.0),
+            fn="gs2d_temporal", ops=17, shards=False),
+    5: dict(name="3d27p_jacobi", kernel="jac3d27p", extents=(1024, 1024, 1024), T=100, seed=5, dist=(0.0, 1.0),
+            fn="jacobi3d_temporal", ops=53, shards=True),
+}
+HEADLINE = 3
+BYTES_PER_UPDATE = 16  # 8 B read + 8 B write per point update
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def make_grid(cfg, pinned=False):
+    from paper_2010_04868_b200 import Grid
+
+    g = Grid(cfg["extents"], 1, boundary=0.0)
+    lo, hi = cfg["dist"]
+    rng = np.random.default_rng(cfg["seed"])
+    g.set_interior(rng.uniform(lo, hi, size=cfg["extents"]))
+    return g
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device=0):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def flush_l2(buf):
+    if buf is not None:
+        buf.fill_(1.0)
+
+
+def device_time(cfg, K, W, pinned_host=None):
+    """Device-resident timing through the plan API; returns ms per step list,
+    launches per step, and per-launch kernel timings."""
+    import torch
+
+    from paper_2010_04868_b200 import _native, config
+    from paper_2010_04868_b200.catalog import get
+
+    spec = get(cfg["kernel"]).spec
+    g = pinned_host if pinned_host is not None else make_grid(cfg)
+    plan = _native.Plan(spec, cfg["extents"], config.current().native())
+    stream = torch.cuda.ExternalStream(plan.stream_handle())
+    l2 = torch.empty(256 * 2 ** 20 // 8, dtype=torch.float64, device="cuda") if g.data.nbytes < 2 ** 30 else None
+    times, launches = [], 0
+    plan.upload(g.data, g.offset)
+    plan.synchronize()
+    for i in range(W + K):
+        if i >= W:
+            flush_l2(l2)
+            torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        plan.run(cfg["T"])
+        e1.record(stream)
+        e1.synchronize()
+        if i >= W:
+            times.append(e0.elapsed_time(e1))
+            launches = plan.last_launches()
+        # re-upload so every step starts from the same input field
+        plan.upload(g.data, g.offset)
+        plan.synchronize()
+    plan.close()
+    return times, launches
+
+
+def e2e_time(cfg, K, W):
+    """Public drop-in call, pinned host buffers, H2D + D2H inside the timing."""
+    from paper_2010_04868_b200 import _native, kernels
+
+    g = make_grid(cfg)
+    out = g.copy()
+    _native.host_register(g.data)
+    _native.host_register(out.data)
+    fn = getattr(kernels, cfg["fn"])
+    kw = {"kernel": cfg["kernel"]}
+    try:
+        times = []
+        for i in range(W + K):
+            t0 = time.perf_counter()
+            fn(g, cfg["T"], out=out, **kw)
+            t1 = time.perf_counter()
+            if i >= W:
+                times.append((t1 - t0) * 1e3)
+    finally:
+        _native.host_unregister(g.data)
+        _native.host_unregister(out.data)
+    nbytes = int(np.prod(cfg["extents"])) * 8
+    return times, nbytes, out
+
+
+def cpu_sample(cfg, budget_s=12.0):
+    """Oracle port on the host: bounded sample of the same workload.  Jacobi:
+    full grid, T_cpu steps on all cores; GS: full grid, T_cpu sweeps on one
+    core.  Returns (GStencil/s, cores, description)."""
+    from oracle import cref
+    from paper_2010_04868_b200.catalog import get
+
+    spec = get(cfg["kernel"]).spec
+    g = make_grid(cfg)
+    gauss = spec.dependence_kind == "gauss_seidel"
+    cores = 1 if gauss else (os.cpu_count() or 1)
+    pts = int(np.prod(cfg["extents"]))
+    t0 = time.perf_counter()
+    cref.scalar_reference(spec, g, 1, order="lexicographic", threads=cores)
+    one = time.perf_counter() - t0
+    steps = int(max(1, min(cfg["T"], budget_s / max(one, 1e-6))))
+    t0 = time.perf_counter()
+    cref.scalar_reference(spec, g, steps, order="lexicographic", threads=cores)
+    dt = time.perf_counter() - t0
+    rate = pts * steps / dt / 1e9
+    desc = (f"oracle C port of scalar_reference, full {'x'.join(map(str, cfg['extents']))} grid, "
+            f"{steps} of {cfg['T']} {'sweeps' if gauss else 'steps'}, {dt:.1f} s")
+    return rate, cores, desc
+
+
+def measure_config(cfg, K, W, with_e2e=True, with_cpu=True):
+    hbm_peak, peak_src = peaks()
+    pts = int(np.prod(cfg["extents"]))
+    updates = pts * cfg["T"]
+    with ClockSampler() as clk:
+        times, launches = device_time(cfg, K, W)
+    ms = statistics.mean(times)
+    value = updates / (ms * 1e-3) / 1e9
+    res = {
+        "value": value, "unit": "GStencil/s", "ms_per_step": ms, "ms_per_step_min": min(times), "steps": K,
+        "warmup": W, "gpu_launches": launches * K, "launches_per_step": launches, "clocks": clk.summary(),
+        "workload": f"{cfg['name']} {'x'.join(map(str, cfg['extents']))} T={cfg['T']}",
+    }
+    achieved = BYTES_PER_UPDATE * updates / (ms * 1e-3) / 1e9
+    res["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                       "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+                       "note": "achieved = 16 B/update algorithmic (effective) bandwidth of the step's kernels"}
+    sm = res["clocks"].get("sm_mhz") or 1965.0
+    fp64_peak = 148 * 64 * sm * 1e6 / 1e12  # DP ops/s (DADD/DMUL/DFMA each 1 op), measured 63.4/clk/SM
+    fp64 = cfg["ops"] * updates / (ms * 1e-3) / 1e12
+    res["fp64"] = {"achieved_tops": fp64, "peak_tops": fp64_peak, "frac": fp64 / fp64_peak,
+                   "ops_per_update": cfg["ops"], "note": "unfused algorithmic FP64 ops; peak = 148 SM x 64/clk x median SM clock"}
+    if with_e2e:
+        etimes, nbytes, _ = e2e_time(cfg, K, W)
+        ems = statistics.mean(etimes)
+        res["e2e"] = {"value": updates / (ems * 1e-3) / 1e9, "unit": "GStencil/s", "ms_per_step": ems,
+                      "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
+    if with_cpu:
+        rate, cores, desc = cpu_sample(cfg)
+        res["cpu_baseline"] = {"value": rate, "unit": "GStencil/s", "cores": cores, "kind": "port", "sample": desc}
+    return res
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port) on the host."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    from oracle import cref
+    from paper_2010_04868_b200.catalog import get
+
+    spec = get(cfg["kernel"]).spec
+    g = make_grid(cfg)
+    gauss = spec.dependence_kind == "gauss_seidel"
+    cores = 1 if gauss else (os.cpu_count() or 1)
+    pts = int(np.prod(cfg["extents"]))
+    t0 = time.perf_counter()
+    cref.scalar_reference(spec, g, 1, order="lexicographic", threads=cores)
+    one = time.perf_counter() - t0
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    t_cpu = int(max(1, min(cfg["T"], budget / max(one, 1e-6))))
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        cref.scalar_reference(spec, g, t_cpu, order="lexicographic", threads=cores)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    sec = statistics.mean(times)
+    value = pts * t_cpu / sec / 1e9
+    desc = (f"oracle C port of scalar_reference (reference not compiled: pure Python), full "
+            f"{'x'.join(map(str, cfg['extents']))} grid, {t_cpu} of {cfg['T']} steps per step")
+    line = {
+        "metric": "GStencil/s", "value": value, "unit": "GStencil/s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE seeds)",
+        "config": {"workload": f"{cfg['name']} {'x'.join(map(str, cfg['extents']))} T={cfg['T']}",
+                   "sample_steps": t_cpu},
+        "cpu_baseline": {"value": value, "unit": "GStencil/s", "cores": cores, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": "GStencil/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_sharded(args):
+    """N>1: slab-sharded Jacobi over torch.distributed (NCCL), strong scaling."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2010_04868_b200.catalog import get
+    from paper_2010_04868_b200.halo import ShardedJacobi
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[args.config]
+    if not cfg["shards"]:
+        cfg = CONFIGS[HEADLINE]
+    spec = get(cfg["kernel"]).spec
+    full = make_grid(cfg).interior
+    sj = ShardedJacobi(spec, cfg["extents"], dist, depth=8, device=torch.device("cuda", local))
+    times = []
+    for i in range(args.warmup + args.steps):
+        sj.cur = 0
+        sj.load_global(full)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        sj.run(cfg["T"])
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        if i >= args.warmup:
+            t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            times.append(float(t.item()))
+    ms = statistics.mean(times)
+    updates = int(np.prod(cfg["extents"])) * cfg["T"]
+    if rank == 0:
+        hbm_peak, peak_src = peaks()
+        achieved = BYTES_PER_UPDATE * updates / world / (ms * 1e-3) / 1e9
+        print(json.dumps({
+            "metric": "GStencil/s", "value": updates / (ms * 1e-3) / 1e9, "unit": "GStencil/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE seeds)",
+            "config": {"workload": f"{cfg['name']} {'x'.join(map(str, cfg['extents']))} T={cfg['T']}",
+                       "parallelism": f"slab{world} (axis-0 rows, NCCL halo depth 8)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None, "per": "GPU"},
+        }))
+    dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, default=HEADLINE, choices=sorted(CONFIGS))
+    ap.add_argument("--no-all", action="store_true", help="skip the per_stencil sweep of the other configs")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        return run_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_sharded(args)
+    cfg = CONFIGS[args.config]
+    head = measure_config(cfg, args.steps, args.warmup, with_e2e=True, with_cpu=not args.no_cpu)
+    line = {
+        "metric": "GStencil/s", "value": head["value"], "unit": "GStencil/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE seeds)",
+        "config": {"workload": head["workload"], "l2": "inputs larger than L2 (2.1 GB per grid)",
+                   "parallelism": "single GPU", "fma": "exact (power-of-two weights fused bit-identically)"},
+        "gpu_launches": head["gpu_launches"], "clocks": head["clocks"], "e2e": head.get("e2e"),
+        "roofline": head["roofline"], "fp64": head["fp64"], "cpu_baseline": head.get("cpu_baseline"),
+    }
+    if not args.no_all:
+        per = {}
+        for cid, c in CONFIGS.items():
+            if cid == args.config:
+                continue
+            try:
+                r = measure_config(c, max(2, min(args.steps, 3)), args.warmup, with_e2e=True,
+                                   with_cpu=not args.no_cpu)
+                per[c["name"]] = {k: r[k] for k in ("value", "unit", "ms_per_step", "steps", "workload", "roofline",
+                                                     "fp64", "e2e", "cpu_baseline", "clocks", "launches_per_step")
+                                  if k in r}
+            except Exception as exc:  # report, never hide
+                per[c["name"]] = {"error": repr(exc)}
+        line["per_stencil"] = per
+    print(json.dumps(line))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

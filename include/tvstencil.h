@@ -126,6 +126,8 @@ int tvs_plan_synchronize(tvs_plan* p);
 int tvs_plan_last_ms(tvs_plan* p, float* ms);
 /* launches issued by the last tvs_plan_run (your kernels only) */
 int tvs_plan_last_launches(tvs_plan* p, int64_t* n);
+/* the plan's CUDA stream (cudaStream_t), e.g. for torch.cuda.ExternalStream */
+int tvs_plan_stream(tvs_plan* p, void** stream);
 int tvs_plan_destroy(tvs_plan* p);
 
 /* ---- device path: caller-owned device buffers (halo-exchange module) ---- */
@@ -133,9 +135,9 @@ int tvs_geometry_init(int32_t dim, const int64_t extents[3], int64_t axis0_offse
                       tvs_geometry* g);
 /* Fill every non-interior cell of a device block with `value`. */
 int tvs_fill_halo(const tvs_geometry* g, double* dev, double value, void* stream);
-/* Jacobi: `steps` updates src -> ... -> result; the result lands in `dst`
- * when steps is odd and in `src` when even (ping-pong, like the reference's
- * swap at baselines.py:122-124); *result_in_dst reports which.  Axis-0
+/* Jacobi: `steps` updates, ping-ponging src <-> dst (like the reference's
+ * swap at baselines.py:122-124; a temporally blocked launch advances several
+ * steps per swap); *result_in_dst reports which buffer holds the result.  Axis-0
  * positions outside [0, axis0_global) are boundary; positions outside the
  * local block but inside the domain are ghost cells whose influence spreads
  * one cell per step (callers exchange `steps` ghost rows first). */

@@ -65,6 +65,7 @@ _SIGS = {
     "tvs_plan_synchronize": (C.c_int, [_P]),
     "tvs_plan_last_ms": (C.c_int, [_P, C.POINTER(C.c_float)]),
     "tvs_plan_last_launches": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "tvs_plan_stream": (C.c_int, [_P, C.POINTER(_P)]),
     "tvs_plan_destroy": (C.c_int, [_P]),
     "tvs_geometry_init": (C.c_int, [C.c_int32, C.POINTER(C.c_int64), C.c_int64, C.c_int64, C.POINTER(Geometry)]),
     "tvs_fill_halo": (C.c_int, [C.POINTER(Geometry), _P, C.c_double, _P]),
@@ -230,6 +231,11 @@ class Plan:
         n = C.c_int64(0)
         check(lib().tvs_plan_last_launches(self._h, C.byref(n)), "tvs_plan_last_launches")
         return int(n.value)
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        check(lib().tvs_plan_stream(self._h, C.byref(s)), "tvs_plan_stream")
+        return int(s.value or 0)
 
     def close(self):
         if getattr(self, "_h", None):

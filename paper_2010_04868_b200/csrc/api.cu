@@ -519,6 +519,12 @@ int tvs_plan_last_launches(tvs_plan* p, int64_t* n) {
   return TVS_OK;
 }
 
+int tvs_plan_stream(tvs_plan* p, void** stream) {
+  if (!p || !stream) return fail(TVS_ERR_INVALID, "null argument");
+  *stream = (void*)p->stream;
+  return TVS_OK;
+}
+
 int tvs_plan_destroy(tvs_plan* p) {
   if (!p) return TVS_OK;
   cudaSetDevice(p->ex.device);

@@ -128,7 +128,10 @@ def test_fma_policies(cuda_ready):
     g = Grid.random((300, 301), seed=2)
     want = cref.scalar_reference(get("heat2d").spec, g, 12)
     assert np.array_equal(_run("heat2d", g, 12, fma="exact").interior, want.interior)
-    g3 = Grid.random((40, 41, 42), seed=3)
+    # config 5's distribution: uniform[0, 1) (signed data makes pointwise
+    # relative error unbounded near zeros, which is why FMA is opt-in)
+    g3 = Grid((40, 41, 42), 1)
+    g3.set_interior(np.random.default_rng(5).uniform(0.0, 1.0, (40, 41, 42)))
     want3 = cref.scalar_reference(get("jac3d27p").spec, g3, 6)
     got3 = _run("jac3d27p", g3, 6, fma="allow")
     rel = np.abs(got3.interior - want3.interior) / np.maximum(np.abs(want3.interior), 1e-300)

@@ -234,7 +234,7 @@ static int jacobi_device(const tvs_stencil& st, const tvs_geometry& g, double* s
       step_now = (int)std::min<int64_t>(left, std::min(depth, 64));
       rc = jacobi1d_blocked(st, g, a, b, step_now, fma, s);
     } else if (!naive && g.dim == 2 && jacobi2d_blocked_supported(st)) {
-      int depth = ex.temporal_depth > 0 ? ex.temporal_depth : jacobi2d_max_depth();
+      int depth = ex.temporal_depth > 0 ? ex.temporal_depth : jacobi2d_default_depth();
       depth = std::min(depth, jacobi2d_max_depth());
       step_now = (int)std::min<int64_t>(left, depth);
       rc = jacobi2d_blocked(st, g, a, b, step_now, fma, s);

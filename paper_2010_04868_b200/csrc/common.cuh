@@ -93,6 +93,7 @@ bool jacobi2d_blocked_supported(const tvs_stencil& st);
 int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
                      int depth, bool fma, cudaStream_t s);
 int jacobi2d_max_depth();
+int jacobi2d_default_depth();
 bool jacobi3d_streaming_supported(const tvs_stencil& st);
 int jacobi3d_streaming(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
                        bool fma, cudaStream_t s);

@@ -36,6 +36,8 @@ constexpr int kGsWarps = 4;          // warps (= 128 sweeps) per block
 constexpr int kGsLag = 3;            // position lag between adjacent lanes
 constexpr int kGsRing = 512;         // per-warp input ring (positions)
 constexpr int kGsMaxBlocks = 64;     // sweeps per launch <= 64 * 128
+constexpr int kGsPubChunks = 4;      // cross-block publication every 4 x 32 positions
+constexpr int kGsPrefetch = 4;       // warp-0 input prefetch distance (chunks)
 static_assert(kGsLag * 32 % 32 == 0, "lane-31 output chunks must align");
 
 __device__ __forceinline__ int ld_acquire_cta(const int* p) {
@@ -78,92 +80,127 @@ __device__ __forceinline__ double gs_taps(double L, double C, double R, double w
 
 template <unsigned MASK>
 __global__ void __launch_bounds__(kGsWarps * 32, 1) gs1d_kernel(Gs1dArgs p) {
-  __shared__ double ring[kGsWarps][kGsRing];
-  __shared__ double stage[32];
-  __shared__ int prod[kGsWarps], cons[kGsWarps];
+  // ring[w]: input positions of warp w; ring[kGsWarps]: staging of the last
+  // warp's sweep before it is flushed to global memory.
+  __shared__ double ring[kGsWarps + 1][kGsRing];
+  __shared__ int prod[kGsWarps], cons[kGsWarps + 1];
   __shared__ int s_ticket;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_ticket = atomicAdd(p.ticket, 1);
-  if (threadIdx.x < kGsWarps) prod[threadIdx.x] = cons[threadIdx.x] = 0;
+  if (threadIdx.x < kGsWarps) prod[threadIdx.x] = 0;
+  if (threadIdx.x <= kGsWarps) cons[threadIdx.x] = 0;
   __syncthreads();
   const int b = s_ticket;
-  const long long n = p.n;
+  const int n = (int)p.n;  // host guarantees n < 2^30
   const double bnd = p.bnd;
   const long long q = ((long long)b * kGsWarps + w) * 32 + lane;  // this lane's sweep
   const bool real = q < p.sweeps;
   const bool last_block = b == p.nblocks - 1;
-  const double* lsrc = b == 0 ? p.a : p.gbuf + (long long)(b - 1) * n;
-  double* odst = last_block ? p.a : p.gbuf + (long long)b * n;
-  const long long nch = (n + 31) / 32 + kGsLag + 1;
+  const double* lsrc = b == 0 ? p.a : p.gbuf + (long long)(b - 1) * p.n;
+  double* odst = last_block ? p.a : p.gbuf + (long long)b * p.n;
+  const int nch = (n + 31) / 32 + kGsLag + 1;
+  const int lane_off = kGsLag * (lane + 1);
+  const double* rin = ring[w];
+  double* rout = ring[w + 1];
+  const bool writer = lane == 31;
+  const bool warp_real = __all_sync(0xffffffffu, real);
 
-  auto wait_upstream = [&](long long need) {  // block b-1 published >= need
+  auto wait_upstream = [&](int need) {  // block b-1 published >= need positions
     if (b == 0) return;
-    if (lane == 0)
-      while (ld_acquire_gpu(p.gprog + b - 1) < need) __nanosleep(64);
+    if (lane == 0) {
+      long long want = need;
+      while (ld_acquire_gpu(p.gprog + b - 1) < want) __nanosleep(32);
+    }
     __syncwarp();
   };
 
   double L = bnd, u0 = bnd, u1 = bnd, out = bnd;
-  double ld_reg = bnd;
+  // warp 0 streams its input (the grid, or block b-1's sweep) into ring[0]
+  // with cp.async, kGsPrefetch chunks ahead of consumption
+  auto load_chunk = [&](int c) {
+    const int x = c * 32 + lane;
+    wait_upstream(min(((c * 32) / (32 * kGsPubChunks) + 1) * 32 * kGsPubChunks, n));
+    double* slot = &ring[0][x & (kGsRing - 1)];
+    if (x < n) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(slot);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(lsrc + x));
+    } else {
+      *slot = bnd;
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
   if (w == 0) {
-    wait_upstream(min(32ll, n));
-    ld_reg = lane < n ? __ldcg(lsrc + lane) : bnd;
+#pragma unroll 1
+    for (int c = 0; c < kGsPrefetch; ++c) load_chunk(c);
   }
 
-  for (long long ch = 0; ch < nch; ++ch) {
-    const long long jb = ch * 32;
+  for (int ch = 0; ch < nch; ++ch) {
+    const int jb = ch * 32;
     if (w == 0) {
-      // positions [jb, jb+32) into my ring, prefetch the next chunk
-      ring[0][(jb + lane) & (kGsRing - 1)] = ld_reg;
-      const long long nx = jb + 32 + lane;
-      wait_upstream(min(jb + 64, n));
-      ld_reg = nx < n ? __ldcg(lsrc + nx) : bnd;
+      load_chunk(ch + kGsPrefetch);  // (chunks past n just store bnd)
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kGsPrefetch));  // chunk ch landed
       __syncwarp();
     } else {
-      const int need = (int)min(jb + 31, n);
+      const int need = min(jb + 31, n);
       while (ld_acquire_cta(&prod[w]) < need) {
       }
     }
-    if (w + 1 < kGsWarps) {  // ring space for positions up to jb-65 in the next warp's ring
-      while (ld_acquire_cta(&cons[w + 1]) <= (int)(jb - 65 - kGsRing)) {
+    {  // ring space in the consumer of my lane-31 stream: positions up to jb-65
+      const int lim = jb - 65 - kGsRing;
+      while (ld_acquire_cta(&cons[w + 1]) <= lim) {
       }
     }
+    // steady chunk: every lane real and every position of the chunk inside
+    // [0, n) — no selects on the DMUL->DADD->DADD chain
+    const bool steady = warp_real && jb - kGsLag * 32 >= 0 && jb + 31 - kGsLag < n;
+    if (steady) {
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const long long j = jb + u;
-      double s = __shfl_up_sync(0xffffffffu, out, 1);
-      if (lane == 0) {
-        const long long pos = j - 1;
-        s = (pos >= 0 && pos < n) ? ring[w][pos & (kGsRing - 1)] : bnd;
+      for (int u = 0; u < 32; ++u) {
+        const int j = jb + u;
+        const double sh = __shfl_up_sync(0xffffffffu, out, 1);
+        const double rv = rin[(j - 1) & (kGsRing - 1)];  // same address for all lanes: broadcast
+        const double sv = lane == 0 ? rv : sh;
+        out = gs_taps<MASK>(L, u0, u1, p.w0, p.w1, p.w2);
+        L = out;
+        u0 = u1;
+        u1 = sv;
+        const int po = j - kGsLag * 32;
+        if (writer) rout[po & (kGsRing - 1)] = out;
       }
-      const long long i = j - kGsLag * (lane + 1);
-      const double v = gs_taps<MASK>(L, u0, u1, p.w0, p.w1, p.w2);
-      out = (i >= 0 && i < n) ? (real ? v : u0) : bnd;
-      L = out;
-      u0 = u1;
-      u1 = s;
-      if (lane == 31) {
-        const long long po = j - kGsLag * 32;
-        if (po >= 0 && po < n) {
-          if (w + 1 < kGsWarps)
-            ring[w + 1][po & (kGsRing - 1)] = out;
-          else
-            stage[po & 31] = out;
-        }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int j = jb + u;
+        const double sh = __shfl_up_sync(0xffffffffu, out, 1);
+        const int pos = j - 1;
+        const double rv = rin[pos & (kGsRing - 1)];
+        const double up = (unsigned)pos < (unsigned)n ? rv : bnd;
+        const double sv = lane == 0 ? up : sh;
+        const int i = j - lane_off;
+        const double v = gs_taps<MASK>(L, u0, u1, p.w0, p.w1, p.w2);
+        out = (unsigned)i < (unsigned)n ? (real ? v : u0) : bnd;
+        L = out;
+        u0 = u1;
+        u1 = sv;
+        const int po = j - kGsLag * 32;
+        if (writer && (unsigned)po < (unsigned)n) rout[po & (kGsRing - 1)] = out;
       }
     }
     __syncwarp();
-    if (lane == 31 && w + 1 < kGsWarps) st_release_cta(&prod[w + 1], (int)max(0ll, min(jb + 32 - kGsLag * 32, n)));
-    if (lane == 0 && w > 0) st_release_cta(&cons[w], (int)(jb + 31));
+    if (writer && w + 1 < kGsWarps) st_release_cta(&prod[w + 1], max(0, min(jb + 32 - kGsLag * 32, n)));
+    if (lane == 0 && w > 0) st_release_cta(&cons[w], jb + 31);
     if (w == kGsWarps - 1) {
-      const long long pc = ch - kGsLag;  // position chunk completed by lane 31
+      const int pc = ch - kGsLag;  // position chunk completed by lane 31
       if (pc >= 0 && pc * 32 < n) {
-        const long long x = pc * 32 + lane;
-        if (x < n) odst[x] = stage[lane];
-        if (!last_block) {
+        const int x = pc * 32 + lane;
+        if (x < n) odst[x] = rout[x & (kGsRing - 1)];
+        __syncwarp();
+        if (lane == 0) st_release_cta(&cons[kGsWarps], x + 1 - lane);  // staging slots consumed
+        const bool batch_end = ((pc + 1) % kGsPubChunks == 0) || (pc + 1) * 32 >= n;
+        if (!last_block && batch_end) {
           __threadfence();
           __syncwarp();
-          if (lane == 0) st_release_gpu(p.gprog + b, min(pc * 32 + 32, n));
+          if (lane == 0) st_release_gpu(p.gprog + b, min((pc + 1) * 32, n));
         }
       }
       __syncwarp();
@@ -190,6 +227,7 @@ int gs1d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, in
   const unsigned mask = gs_mask1d(st, w);
   if (mask == 0) return gs_wavefront(st, g, grid, steps, TVS_GS_LEXICOGRAPHIC, s);
   const long long n = g.extents[0];
+  if (n >= (1ll << 30)) return fail(TVS_ERR_UNSUPPORTED, "gs1d_pipeline: N >= 2^30");
   const long long per_launch = (long long)kGsMaxBlocks * kGsWarps * 32;
   const int max_blocks = (int)std::min<long long>((steps + kGsWarps * 32 - 1) / (kGsWarps * 32), kGsMaxBlocks);
   const size_t gbuf_bytes = sizeof(double) * (size_t)std::max(1, max_blocks - 1) * (size_t)n;

@@ -21,6 +21,7 @@
 // of a segment are recomputed by neighbouring warps; useful width is
 // 32*P - 2*D.  HBM traffic per useful update ~ 16 B / D.
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -64,35 +65,50 @@ struct Coeff9 {
   double c[9];
 };
 
+// One level update when row q of the level below arrives (see header):
+// out(q-1) = F + taps(+1 row); N(q) = M + taps(0 row); M'(q+1) = taps(-1 row).
+// F is finished in place (it becomes the fresh accumulator), so calling this
+// with (F, M) and then (M, F) on the next row rotates roles without copies.
+template <unsigned MASK, bool FMA>
+__device__ __forceinline__ void level_row(double (&F)[kP2], double (&M)[kP2], const double (&in)[kP2 + 2],
+                                          const double (&c)[9], double (&out)[kP2]) {
+  constexpr bool G0 = has_group<MASK, 0>(), G1 = has_group<MASK, 1>(), G2 = has_group<MASK, 2>();
+  if constexpr (G2) add_group<MASK, 2, !(G0 || G1), FMA>(F, in, c);
+#pragma unroll
+  for (int p = 0; p < kP2; ++p) out[p] = F[p];
+  if constexpr (G1) add_group<MASK, 1, !G0, FMA>(M, in, c);
+  if constexpr (G0) add_group<MASK, 0, true, FMA>(F, in, c);
+}
+
 template <unsigned MASK, int D, bool FMA>
 __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __restrict__ src,
                                                                 double* __restrict__ dst, Geo g, int64_t origin,
                                                                 Coeff9 cf, double bnd, int64_t n_strips,
                                                                 int64_t n_tasks) {
-  constexpr bool G0 = has_group<MASK, 0>(), G1 = has_group<MASK, 1>(), G2 = has_group<MASK, 2>();
   constexpr int U = 32 * kP2 - 2 * D;  // useful columns per strip
-  double c[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) c[k] = cf.c[k];
+  constexpr int PF = 2;                // rows prefetched ahead (registers)
+  const double(&c)[9] = cf.c;          // constant-bank operands
 
   const int lane = threadIdx.x & 31;
   const int64_t task = (int64_t)blockIdx.x * kWarps2 + (threadIdx.x >> 5);
   if (task >= n_tasks) return;
   const int64_t strip = task % n_strips, seg = task / n_strips;
-  const int64_t col0 = -D + strip * U;          // first column of the strip
-  const int64_t cl = col0 + lane * kP2;          // this lane's first column
-  const int64_t r0 = seg * kRowsSeg;             // first output row
-  const int64_t r1 = min(r0 + kRowsSeg, g.e0);   // output rows [r0, r1)
+  const int col0 = (int)(-D + strip * U);  // first column of the strip
+  const int cl = col0 + lane * kP2;        // this lane's first column
+  const int r0 = (int)(seg * kRowsSeg);    // first output row
+  const int r1 = (int)(r0 + kRowsSeg < g.e0 ? r0 + kRowsSeg : g.e0);
+  const int e0 = (int)g.e0, e1 = (int)g.e1;
+  const int a0 = (int)g.a0_off, ag = (int)g.a0_glob;
 
   unsigned col_out = 0;  // bit p: column cl+p outside the domain
 #pragma unroll
-  for (int p = 0; p < kP2; ++p) col_out |= (cl + p < 0 || cl + p >= g.e1 ? 1u : 0u) << p;
+  for (int p = 0; p < kP2; ++p) col_out |= (cl + p < 0 || cl + p >= e1 ? 1u : 0u) << p;
   const bool any_col_out = __any_sync(0xffffffffu, col_out != 0);
   unsigned store_mask = 0;  // bit p: column is a useful output of this strip
 #pragma unroll
   for (int p = 0; p < kP2; ++p) {
-    const int64_t x = cl + p;
-    store_mask |= (x >= col0 + D && x < col0 + D + U && x >= 0 && x < g.e1 ? 1u : 0u) << p;
+    const int x = cl + p;
+    store_mask |= (x >= col0 + D && x < col0 + D + U && x >= 0 && x < e1 ? 1u : 0u) << p;
   }
 
   double A[D][kP2], B[D][kP2];
@@ -102,60 +118,88 @@ __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __
     for (int p = 0; p < kP2; ++p) A[l][p] = B[l][p] = 0.0;
 
   const double* col_base = src + origin + cl;
-  for (int64_t m = r0 - D; m < r1 + D; ++m) {
-    // ---- level 0: load row m (outside the local block / domain -> boundary)
-    double in[kP2 + 2];
-    {
-      const int64_t gr = m + g.a0_off;
-      const bool row_ok = m >= 0 && m < g.e0 && gr >= 0 && gr < g.a0_glob;
-      const double* rp = col_base + m * g.s0;
+  auto load_row = [&](int m, double (&r)[kP2]) {
+    const bool row_ok = m >= 0 && m < e0 && m + a0 >= 0 && m + a0 < ag;
+    const double* rp = col_base + (int64_t)m * g.s0;
 #pragma unroll
-      for (int p = 0; p < kP2; ++p) in[p + 1] = (row_ok && !(col_out >> p & 1u)) ? __ldg(rp + p) : bnd;
-      in[0] = __shfl_up_sync(0xffffffffu, in[kP2], 1);
-      in[kP2 + 1] = __shfl_down_sync(0xffffffffu, in[1], 1);
-    }
-    // ---- levels 1..D: level l+1 consumes level-l row (m - l)
+    for (int p = 0; p < kP2; ++p) r[p] = (row_ok && !(col_out >> p & 1u)) ? __ldg(rp + p) : bnd;
+  };
+  double pre[PF][kP2];
+  const int m_begin = r0 - D, m_end = r1 + D;
+#pragma unroll
+  for (int k = 0; k < PF; ++k) load_row(m_begin + k, pre[k]);
+
+  // One stream step: level-0 row m enters, level-D row m-D leaves.  EVEN
+  // selects which accumulator set finishes (role swap every step).
+  auto step = [&](int m, double (&row)[kP2], auto even_tag) {
+    constexpr bool EVEN = decltype(even_tag)::value;
+    double in[kP2 + 2];
+#pragma unroll
+    for (int p = 0; p < kP2; ++p) in[p + 1] = row[p];
+    in[0] = __shfl_up_sync(0xffffffffu, in[kP2], 1);
+    in[kP2 + 1] = __shfl_down_sync(0xffffffffu, in[1], 1);
+    // rows m-1-l (l < D) produced this step; all inside the domain?
+    const bool rows_in = m - D + a0 >= 0 && m - 1 + a0 < ag;
+    const bool fast = rows_in && !any_col_out;
 #pragma unroll
     for (int l = 0; l < D; ++l) {
       double out[kP2];
-      if constexpr (G2) {
-        add_group<MASK, 2, !(G0 || G1), FMA>(B[l], in, c);
-      }
+      if constexpr (EVEN)
+        level_row<MASK, FMA>(B[l], A[l], in, c, out);
+      else
+        level_row<MASK, FMA>(A[l], B[l], in, c, out);
+      if (fast) {
 #pragma unroll
-      for (int p = 0; p < kP2; ++p) out[p] = B[l][p];
-      if constexpr (G1) {
-#pragma unroll
-        for (int p = 0; p < kP2; ++p) B[l][p] = A[l][p];
-        add_group<MASK, 1, !G0, FMA>(B[l], in, c);
+        for (int p = 0; p < kP2; ++p) in[p + 1] = out[p];
       } else {
+        const int gq = m - l - 1 + a0;
+        const bool pin_row = gq < 0 || gq >= ag;
 #pragma unroll
-        for (int p = 0; p < kP2; ++p) B[l][p] = A[l][p];
-      }
-      if constexpr (G0) {
-        add_group<MASK, 0, true, FMA>(A[l], in, c);
-      }
-      // out = level l+1 row (m - l - 1)
-      const int64_t q = m - l - 1;
-      const int64_t gq = q + g.a0_off;
-      const bool pin_row = gq < 0 || gq >= g.a0_glob;
-#pragma unroll
-      for (int p = 0; p < kP2; ++p) {
-        const bool pin = pin_row || (any_col_out && (col_out >> p & 1u));
-        in[p + 1] = pin ? bnd : out[p];
+        for (int p = 0; p < kP2; ++p) in[p + 1] = (pin_row || (col_out >> p & 1u)) ? bnd : out[p];
       }
       if (l + 1 < D) {
         in[0] = __shfl_up_sync(0xffffffffu, in[kP2], 1);
         in[kP2 + 1] = __shfl_down_sync(0xffffffffu, in[1], 1);
       }
     }
-    // ---- level D row (m - D) is final
-    const int64_t q = m - D;
+    const int q = m - D;  // level-D row leaving
     if (q >= r0 && q < r1) {
-      double* wp = dst + origin + q * g.s0 + cl;
+      double* wp = dst + origin + (int64_t)q * g.s0 + cl;
 #pragma unroll
       for (int p = 0; p < kP2; ++p)
         if (store_mask >> p & 1u) wp[p] = in[p + 1];
     }
+  };
+
+  using T0 = std::true_type;
+  using T1 = std::false_type;
+  int m = m_begin;
+  for (; m + PF <= m_end; m += PF) {
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+      double row[kP2];
+#pragma unroll
+      for (int p = 0; p < kP2; ++p) row[p] = pre[k][p];
+      load_row(m + k + PF, pre[k]);
+      if (k % 2 == 0)
+        step(m + k, row, T0{});
+      else
+        step(m + k, row, T1{});
+    }
+  }
+  // tail (fewer than PF rows left); parity continues from the unrolled loop
+  for (int k = 0; m < m_end; ++m, ++k) {
+    double row[kP2];
+#pragma unroll
+    for (int p = 0; p < kP2; ++p) row[p] = pre[0][p];
+#pragma unroll
+    for (int kk = 0; kk + 1 < PF; ++kk)
+#pragma unroll
+      for (int p = 0; p < kP2; ++p) pre[kk][p] = pre[kk + 1][p];
+    if (((m - m_begin) & 1) == 0)
+      step(m, row, T0{});
+    else
+      step(m, row, T1{});
   }
 }
 
@@ -182,6 +226,7 @@ bool jacobi2d_blocked_supported(const tvs_stencil& st) {
 }
 
 int jacobi2d_max_depth() { return kMaxD2; }
+int jacobi2d_default_depth() { return 4; }  // measured best at P=4 (register pressure above)
 
 template <unsigned MASK, int D>
 static void launch2d_d(bool fma, unsigned blocks, cudaStream_t s, const double* src, double* dst, const Geo& geo,

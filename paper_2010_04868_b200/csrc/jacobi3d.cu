@@ -1,8 +1,9 @@
 // K4: 3D radius-1 Jacobi (27-point box / 7-point star), 2.5D plane streaming.
 //
 // Replaces jacobi3d_temporal (reference kernels_nd.py:43-45).  A block owns a
-// (16 x 32) tile of axis-1 x axis-2 columns and streams along axis 0.  Each
-// input plane is staged once in shared memory (cp.async, double-buffered) and
+// (32 x 32) tile of axis-1 x axis-2 columns (4 outputs per thread) and streams
+// along axis 0.  Each input plane is staged once in shared memory (16-byte
+// cp.async, three buffers, one barrier per plane) and
 // contributes to three outputs: it *finishes* output p-1 with the +1-plane
 // taps, continues output p with the 0-plane taps and *starts* output p+1 with
 // the -1-plane taps.  Sorted tap order is exactly plane -1, plane 0, plane +1
@@ -20,10 +21,14 @@ namespace tvs {
 
 constexpr int kTX3 = 32;              // tile width (axis 2) = threads in x
 constexpr int kTYT = 8;               // threads in y
-constexpr int kRY = 2;                // outputs per thread along axis 1
-constexpr int kTY3 = kTYT * kRY;      // tile height (axis 1)
-constexpr int kSW = kTX3 + 2;         // smem row length
-constexpr int kSH = kTY3 + 2;         // smem rows
+constexpr int kRY = 4;                // outputs per thread along axis 1
+constexpr int kTY3 = kTYT * kRY;      // tile height (axis 1) = 32
+constexpr int kSW = kTX3 + 4;         // smem row: x0-2 .. x0+33 (16-byte aligned start)
+constexpr int kSH = kTY3 + 2;         // smem rows: y0-1 .. y0+32
+constexpr int kChunks = kSH * kSW / 2;  // 16-byte copies per plane
+constexpr int kThreads3 = kTX3 * kTYT;
+constexpr int kSlots = (kChunks + kThreads3 - 1) / kThreads3;
+constexpr int kBufs3 = 3;             // plane buffers (one barrier per plane)
 constexpr int kPlanesSeg = 64;        // output planes per block
 
 constexpr unsigned kBox27 = (1u << 27) - 1;
@@ -33,9 +38,9 @@ struct Coeff27 {
   double c[27];
 };
 
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -69,28 +74,38 @@ __device__ __forceinline__ constexpr bool has_plane(int G) {
 }
 
 template <unsigned MASK, bool FMA>
-__global__ void __launch_bounds__(kTX3 * kTYT) jacobi3d_kernel(const double* __restrict__ src,
-                                                               double* __restrict__ dst, Geo g, int64_t origin,
-                                                               Coeff27 cf, double bnd) {
+__global__ void __launch_bounds__(kThreads3) jacobi3d_kernel(const double* __restrict__ src,
+                                                            double* __restrict__ dst, Geo g, int64_t origin,
+                                                            Coeff27 cf, double bnd) {
   constexpr bool G0 = has_plane<MASK>(0), G1 = has_plane<MASK>(1), G2 = has_plane<MASK>(2);
-  __shared__ double tile[2][kSH][kSW];
+  __shared__ __align__(16) double tile[kBufs3][kSH][kSW];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * kTX3 + tx;
   const int64_t x0 = (int64_t)blockIdx.x * kTX3, y0 = (int64_t)blockIdx.y * kTY3;
   const int64_t p0 = (int64_t)blockIdx.z * kPlanesSeg;
   const int64_t p1 = min(p0 + kPlanesSeg, g.e0);  // outputs [p0, p1)
 
-  // plane `p` (local index, may be -1 or e0 = memory halo) -> smem buffer
+  // per-thread staging slots, fixed for every plane: smem offset + global
+  // offset relative to the plane base; rows beyond the halo are not read
+  int soff[kSlots];
+  int64_t goff[kSlots];
+  bool sval[kSlots];
+#pragma unroll
+  for (int k = 0; k < kSlots; ++k) {
+    const int e = tid + k * kThreads3;
+    const int r = e / (kSW / 2), c2 = e % (kSW / 2);
+    const int64_t y = y0 + r - 1;
+    soff[k] = r * kSW + 2 * c2;
+    goff[k] = y * g.s1 + (x0 - 2 + 2 * c2);
+    sval[k] = e < kChunks && y <= g.e1;
+  }
+  const double* base = src + origin;
   auto stage = [&](int64_t p, int buf) {
-    const double* base = src + origin + p * g.s0;
-    for (int e = tid; e < kSH * kSW; e += kTX3 * kTYT) {
-      const int r = e / kSW, cc = e % kSW;
-      const int64_t y = y0 + r - 1, x = x0 + cc - 1;
-      if (y >= -1 && y <= g.e1 && x >= -1 && x <= g.e2)
-        cp_async8(&tile[buf][r][cc], base + y * g.s1 + x);
-      else
-        tile[buf][r][cc] = bnd;
-    }
+    const double* pb = base + p * g.s0;
+    double* tb = &tile[buf][0][0];
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k)
+      if (sval[k]) cp_async16(tb + soff[k], pb + goff[k]);
     cp_async_commit();
   };
 
@@ -102,19 +117,21 @@ __global__ void __launch_bounds__(kTX3 * kTYT) jacobi3d_kernel(const double* __r
   const bool x_ok = x < g.e2;
   stage(p0 - 1, 0);
   for (int64_t p = p0 - 1; p <= p1; ++p) {
-    const int buf = (int)((p - p0 + 1) & 1);
+    const int buf = (int)((p - p0 + 1) % kBufs3);
     if (p + 1 <= p1) {
-      stage(p + 1, buf ^ 1);
+      // buffer of plane p-2: every thread finished reading it before the
+      // previous iteration's barrier
+      stage(p + 1, (int)((p - p0 + 2) % kBufs3));
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
-    __syncthreads();
+    __syncthreads();  // plane p landed for everyone; plane p-2's buffer is free
     double v[kRY + 2][3];
 #pragma unroll
     for (int rr = 0; rr < kRY + 2; ++rr)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) v[rr][k] = tile[buf][ty * kRY + rr][tx + k];
+      for (int k = 0; k < 3; ++k) v[rr][k] = tile[buf][ty * kRY + rr][tx + 1 + k];
     double out[kRY];
     if constexpr (G2) add_plane<MASK, 2, !(G0 || G1), FMA>(B, v, cf.c);
 #pragma unroll
@@ -128,13 +145,13 @@ __global__ void __launch_bounds__(kTX3 * kTYT) jacobi3d_kernel(const double* __r
     if (q >= p0 && q < p1 && x_ok) {
       const int64_t gq = q + g.a0_off;
       const bool pin = gq < 0 || gq >= g.a0_glob;
+      double* op = dst + origin + q * g.s0 + x;
 #pragma unroll
       for (int r = 0; r < kRY; ++r) {
         const int64_t y = y0 + ty * kRY + r;
-        if (y < g.e1) dst[origin + q * g.s0 + y * g.s1 + x] = pin ? bnd : out[r];
+        if (y < g.e1) op[y * g.s1] = pin ? bnd : out[r];
       }
     }
-    __syncthreads();  // buffer `buf` is restaged two iterations later
   }
 }
 

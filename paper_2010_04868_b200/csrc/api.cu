@@ -6,7 +6,8 @@
 //   Jacobi 3D star/box -> jacobi3d_streaming (2.5D plane streaming, 1 step/launch)
 //   Jacobi other     -> jacobi_naive_step  (generic taps, 1 step/launch)
 //   Gauss-Seidel 1D  -> gs1d_pipeline      (time-skewed warp pipeline)
-//   Gauss-Seidel 2D/3D -> gs_wavefront     (hyperplane wavefront, both orders)
+//   Gauss-Seidel 2D lexicographic -> gs2d_pipeline (time-lane chain)
+//   Gauss-Seidel 2D reference order / 3D -> gs_wavefront (hyperplane wavefront)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -257,6 +258,8 @@ static int gs_device(const tvs_stencil& st, const tvs_geometry& g, double* grid,
     return fail(TVS_ERR_UNSUPPORTED, "Gauss-Seidel runs on a single GPU (no slab decomposition)");
   if (steps == 0) return TVS_OK;
   if (g.dim == 1 && ex.algo != TVS_ALGO_NAIVE) return gs1d_pipeline(st, g, grid, steps, s);
+  if (g.dim == 2 && ex.algo != TVS_ALGO_NAIVE && ex.gs_order == TVS_GS_LEXICOGRAPHIC && gs2d_pipe_supported(st))
+    return gs2d_pipeline(st, g, grid, steps, s);
   return gs_wavefront(st, g, grid, steps, ex.gs_order, s);
 }
 

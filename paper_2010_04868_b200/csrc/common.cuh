@@ -50,6 +50,15 @@ struct TapList {
   int8_t off[TVS_MAX_TAPS][3];
 };
 
+// Spin-wait watchdog: a pipeline kernel that waits ~2^28 times on one flag
+// is deadlocked; trap (CUDA error) instead of hanging the device.
+struct SpinGuard {
+  unsigned n = 0;
+  __device__ __forceinline__ void tick() {
+    if (++n > (1u << 28)) __trap();
+  }
+};
+
 template <bool FMA>
 __device__ __forceinline__ double tap_next(double c, double v, double acc) {
   if constexpr (FMA) {
@@ -98,6 +107,8 @@ bool jacobi3d_streaming_supported(const tvs_stencil& st);
 int jacobi3d_streaming(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
                        bool fma, cudaStream_t s);
 int gs1d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s);
+bool gs2d_pipe_supported(const tvs_stencil& st);
+int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s);
 int gs_wavefront(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, int order,
                  cudaStream_t s);
 

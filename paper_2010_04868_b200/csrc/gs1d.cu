@@ -27,12 +27,13 @@
 // any grid size.  Sweeps beyond T are identity lanes (they forward their
 // old value), so the last lane always emits sweep T.
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
 namespace tvs {
 
-constexpr int kGsWarps = 4;          // warps (= 128 sweeps) per block
 constexpr int kGsLag = 3;            // position lag between adjacent lanes
 constexpr int kGsRing = 512;         // per-warp input ring (positions)
 constexpr int kGsMaxBlocks = 64;     // sweeps per launch <= 64 * 128
@@ -78,7 +79,7 @@ __device__ __forceinline__ double gs_taps(double L, double C, double R, double w
   return acc;
 }
 
-template <unsigned MASK>
+template <unsigned MASK, int kGsWarps>
 __global__ void __launch_bounds__(kGsWarps * 32, 1) gs1d_kernel(Gs1dArgs p) {
   // ring[w]: input positions of warp w; ring[kGsWarps]: staging of the last
   // warp's sweep before it is flushed to global memory.
@@ -109,7 +110,11 @@ __global__ void __launch_bounds__(kGsWarps * 32, 1) gs1d_kernel(Gs1dArgs p) {
     if (b == 0) return;
     if (lane == 0) {
       long long want = need;
-      while (ld_acquire_gpu(p.gprog + b - 1) < want) __nanosleep(32);
+      SpinGuard sg;
+      while (ld_acquire_gpu(p.gprog + b - 1) < want) {
+        __nanosleep(32);
+        sg.tick();
+      }
     }
     __syncwarp();
   };
@@ -142,13 +147,13 @@ __global__ void __launch_bounds__(kGsWarps * 32, 1) gs1d_kernel(Gs1dArgs p) {
       __syncwarp();
     } else {
       const int need = min(jb + 31, n);
-      while (ld_acquire_cta(&prod[w]) < need) {
-      }
+      SpinGuard sg;
+      while (ld_acquire_cta(&prod[w]) < need) sg.tick();
     }
     {  // ring space in the consumer of my lane-31 stream: positions up to jb-65
       const int lim = jb - 65 - kGsRing;
-      while (ld_acquire_cta(&cons[w + 1]) <= lim) {
-      }
+      SpinGuard sg;
+      while (ld_acquire_cta(&cons[w + 1]) <= lim) sg.tick();
     }
     // steady chunk: every lane real and every position of the chunk inside
     // [0, n) — no selects on the DMUL->DADD->DADD chain
@@ -228,8 +233,13 @@ int gs1d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, in
   if (mask == 0) return gs_wavefront(st, g, grid, steps, TVS_GS_LEXICOGRAPHIC, s);
   const long long n = g.extents[0];
   if (n >= (1ll << 30)) return fail(TVS_ERR_UNSUPPORTED, "gs1d_pipeline: N >= 2^30");
-  const long long per_launch = (long long)kGsMaxBlocks * kGsWarps * 32;
-  const int max_blocks = (int)std::min<long long>((steps + kGsWarps * 32 - 1) / (kGsWarps * 32), kGsMaxBlocks);
+  static const int warps = [] {
+    const char* e = getenv("TVS_GS1D_WARPS");
+    const int v = e ? atoi(e) : 4;
+    return (v == 1 || v == 2 || v == 4) ? v : 4;
+  }();
+  const long long per_launch = (long long)kGsMaxBlocks * warps * 32;
+  const int max_blocks = (int)std::min<long long>((steps + warps * 32 - 1) / (warps * 32), kGsMaxBlocks);
   const size_t gbuf_bytes = sizeof(double) * (size_t)std::max(1, max_blocks - 1) * (size_t)n;
   const size_t ctrl_bytes = sizeof(long long) * (kGsMaxBlocks + 2);
   double* gbuf = static_cast<double*>(scratch(gbuf_bytes, 0));
@@ -245,19 +255,28 @@ int gs1d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, in
   a.w1 = w[1];
   a.w2 = w[2];
   a.bnd = st.boundary;
+  auto launch = [&](auto warps_tag) {
+    constexpr int W = decltype(warps_tag)::value;
+    switch (mask) {
+      case 1: gs1d_kernel<1, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
+      case 2: gs1d_kernel<2, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
+      case 3: gs1d_kernel<3, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
+      case 4: gs1d_kernel<4, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
+      case 5: gs1d_kernel<5, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
+      case 6: gs1d_kernel<6, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
+      default: gs1d_kernel<7, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
+    }
+  };
   for (long long done = 0; done < steps; done += per_launch) {
     a.sweeps = std::min<long long>(steps - done, per_launch);
-    a.nblocks = (int)((a.sweeps + kGsWarps * 32 - 1) / (kGsWarps * 32));
+    a.nblocks = (int)((a.sweeps + warps * 32 - 1) / (warps * 32));
     TVS_CUDA(cudaMemsetAsync(ctrl, 0, ctrl_bytes, s));
-    switch (mask) {
-      case 1: gs1d_kernel<1><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
-      case 2: gs1d_kernel<2><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
-      case 3: gs1d_kernel<3><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
-      case 4: gs1d_kernel<4><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
-      case 5: gs1d_kernel<5><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
-      case 6: gs1d_kernel<6><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
-      default: gs1d_kernel<7><<<a.nblocks, kGsWarps * 32, 0, s>>>(a); break;
-    }
+    if (warps == 1)
+      launch(std::integral_constant<int, 1>{});
+    else if (warps == 2)
+      launch(std::integral_constant<int, 2>{});
+    else
+      launch(std::integral_constant<int, 4>{});
     TVS_LAUNCHED("gs1d_kernel");
   }
   return TVS_OK;

@@ -48,8 +48,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
       __threadfence();
       atomicAdd(bar + 1, 1u);
     } else {
-      while (*gen == g0) {
-      }
+      SpinGuard sg;
+      while (*gen == g0) sg.tick();
     }
     __threadfence();
   }

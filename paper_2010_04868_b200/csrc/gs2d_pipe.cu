@@ -35,6 +35,7 @@
 // the requested sweep count are identity lanes.  Lane 127 writes the final
 // sweep of row d - 127 back to the grid in place.
 #include <algorithm>
+#include <climits>
 
 #include "common.cuh"
 
@@ -46,15 +47,16 @@ constexpr int kWarpsG = 4;
 constexpr int kG = 4;                // groups per block
 constexpr int kC = 4;                // iterations per chunk (sync granularity)
 constexpr int kR = 32;               // ring depth (iterations), power of two
-constexpr int kSlots = kLanes + 1;   // slot 0 = virtual lane -1
+constexpr int kSlots = kLanes + 2;   // [0] virtual lane -1, [1] pad, [2 + t] lane t (16-B aligned pairs)
 constexpr int kLam = 2;              // column lag lane t-1 -> t
 constexpr int kMu = 3;               // extra lag warp w-1 -> w (>= kC + 1 - kLam)
 constexpr int kBig = 5;              // lag group g-1 -> g (>= kC + 1)
 constexpr int kBase = 10;            // every producer starts left of column 0 (>= kLam + kBig + 2)
 constexpr int kRG = 256;             // global ring depth (iterations)
 constexpr int kK = 256;              // global ring slots (boundaries in flight)
+constexpr int kPub = 8;              // IO warp publishes downstream every kPub chunks
 constexpr int kComputeWarps = kG * kWarpsG;
-constexpr int kThreads = (kComputeWarps + 1) * 32;
+constexpr int kThreads = (kComputeWarps + 2) * 32;  // + loader warp + drainer warp
 constexpr size_t kSmem = sizeof(double) * (size_t)(kG + 1) * kR * kSlots;
 static_assert(kMu >= kC + 1 - kLam && kBig >= kC + 1, "lags too small for chunked sync");
 }  // namespace gs2p
@@ -91,6 +93,17 @@ __device__ __forceinline__ void st_rel_gpu(unsigned long long* p, unsigned long 
   asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Wait until a shared-memory progress counter reaches `v`; back off so the
+// spinning warps do not starve the IO warp of issue slots.
+__device__ __forceinline__ void wait_ge(const int* p, int v) {
+  if (ld_acq_cta(p) >= v) return;
+  SpinGuard sg;
+  while (ld_acq_cta(p) < v) {
+    __nanosleep(40);
+    sg.tick();
+  }
+}
+
 // taps in sorted order: NW N NE W C E SW S SE (mask bit k = position k)
 template <unsigned MASK>
 __device__ __forceinline__ double gs9(const double* w, double nw, double n, double ne, double ww, double c, double e,
@@ -113,7 +126,10 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
   using namespace gs2p;
   extern __shared__ __align__(16) double smem[];
   // rings[0] = phantom (previous block's last group), rings[g+1] = group g
-  auto ring = [&](int gi, int it, int slot) -> double& { return smem[((size_t)gi * kR + (it & (kR - 1))) * kSlots + slot]; };
+  auto ring = [&](int gi, int it, int slot) -> double& {
+    return smem[((size_t)gi * kR + (it & (kR - 1))) * kSlots + (slot == 0 ? 0 : slot + 1)];
+  };
+  auto ring_lane0 = [&](int gi, int it) -> double* { return &smem[((size_t)gi * kR + (it & (kR - 1))) * kSlots + 2]; };
   __shared__ int prog[kComputeWarps];
   __shared__ int io_load, io_store;
   __shared__ int s_ticket;
@@ -128,76 +144,98 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
   const double bnd = p.bnd;
   const int e0 = p.e0, e1 = p.e1;
 
+  const bool has_up = n > 0, has_down = n + 1 < p.nctas;
+  const int up_slot = (n + kK - 1) % kK, dn_slot = n % kK;
+  const unsigned long long up_tag = (unsigned long long)n << 32;        // boundary n-1 -> tag n
+  const unsigned long long dn_tag = (unsigned long long)(n + 1) << 32;  // boundary n -> tag n+1
   if (wi == kComputeWarps) {
-    // ======================= IO warp =======================
-    const bool has_up = n > 0, has_down = n + 1 < p.nctas;
-    const int up_slot = (n - 1) % kK, dn_slot = n % kK;
-    const unsigned long long up_tag = (unsigned long long)n << 32;        // boundary n-1 -> tag n
-    const unsigned long long dn_tag = (unsigned long long)(n + 1) << 32;  // boundary n -> tag n+1
+    // ============ loader warp: grid rows (slot 0) + previous block's last group ============
     const double* up_ring = p.gring + (size_t)up_slot * kRG * kLanes;
-    double* dn_ring = p.gring + (size_t)dn_slot * kRG * kLanes;
-    int kl = 0, ks = 0;
-    bool slot_ok = !has_down || n < kK;
-    unsigned long long up_seen = 0, dn_cons_seen = 0;
-    SpinGuard io_guard;
-    while (kl < nch || ks < nch) {
-      bool did = false;
-      if (kl < nch) {
-        // WAR: every compute warp finished chunk kl-5 (ring chunk kl-8 reusable)
-        bool ok = true;
-        const int need = (kl - 4) * kC;
-        if (need > 0)
-          for (int q = 0; q < kComputeWarps && ok; ++q) ok = ld_acq_cta(&prog[q]) >= need;
-        const int it_hi = kl * kC + kC;  // exclusive
-        const int up_need = min(it_hi + kBig * kG, p.c_end);
-        if (ok && has_up) {
-          if ((up_seen & 0xffffffffull) < (unsigned long long)up_need || (up_seen >> 32) != (up_tag >> 32)) {
-            up_seen = lane == 0 ? ld_acq_gpu(p.gprod + up_slot) : 0ull;
-            up_seen = __shfl_sync(0xffffffffu, up_seen, 0);
-          }
+    unsigned long long up_seen = 0;
+    SpinGuard guard;
+    for (int kl = 0; kl < nch; ++kl) {
+      const int it_lo = kl * kC, it_hi = it_lo + kC;
+      // WAR: every compute warp finished chunk kl-5 (ring chunk kl-8 reusable)
+      const int need = (kl - 4) * kC;
+      // upstream data for producer iterations up to it_hi + Lambda*G
+      const int up_need = min(it_hi + kBig * kG, p.c_end);
+      for (;;) {
+        const int mine = lane < kComputeWarps ? ld_acq_cta(&prog[lane]) : INT_MAX;
+        bool ok = __reduce_min_sync(0xffffffffu, mine) >= need;
+        if (ok && has_up && ((up_seen >> 32) != (up_tag >> 32) || (up_seen & 0xffffffffull) < (unsigned long long)up_need)) {
+          up_seen = lane == 0 ? ld_acq_gpu(p.gprod + up_slot) : 0ull;
+          up_seen = __shfl_sync(0xffffffffu, up_seen, 0);
           ok = (up_seen >> 32) == (up_tag >> 32) && (up_seen & 0xffffffffull) >= (unsigned long long)up_need;
         }
-        if (ok) {
-          // slot 0 of rings -1..G-1: grid row d0+g+1 at column it + lam - Lambda*g - base
-          if (lane < (kG + 1) * kC) {
-            const int g = lane / kC - 1, it = kl * kC + lane % kC;
-            const int row = d0 + g + 1, col = it + kLam - kBig * g - kBase;
-            double v = bnd;
-            if (row >= 0 && row < e0 && col >= 0 && col < e1) v = __ldcg(p.a + (long long)row * p.s0 + col);
-            ring(g + 1, it, 0) = v;
-          }
-          // phantom slots 1..128: previous block's last group at iteration it + Lambda*G
-#pragma unroll 4
-          for (int e = lane; e < kC * kLanes; e += 32) {
-            const int it = kl * kC + e / kLanes, t = e % kLanes;
-            const int pit = it + kBig * kG;
-            double v = bnd;
-            if (has_up && pit < p.c_end) v = __ldcg(up_ring + (size_t)(pit % kRG) * kLanes + t);
-            ring(0, it, t + 1) = v;
-          }
-          __syncwarp();
-          if (lane == 0) {
-            st_rel_cta(&io_load, it_hi);
-            if (has_up) {
-              const int consumed = it_hi + kBig * kG;  // producer iterations no longer needed
-              st_rel_gpu(p.gcons + up_slot, up_tag | (unsigned long long)min(consumed, p.c_end));
-            }
-          }
-          ++kl;
-          did = true;
+        if (ok) break;
+        __nanosleep(20);
+        guard.tick();
+      }
+      // slot 0 of rings -1..G-1: grid row d0+g+1 at column it + lam - Lambda*g - base
+      if (lane < (kG + 1) * kC) {
+        const int g = lane / kC - 1, it = it_lo + lane % kC;
+        const int row = d0 + g + 1, col = it + kLam - kBig * g - kBase;
+        double* dst = &ring(g + 1, it, 0);
+        if (row >= 0 && row < e0 && col >= 0 && col < e1) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(p.a + (long long)row * p.s0 + col));
+        } else {
+          *dst = bnd;
         }
       }
-      if (ks < nch) {
-        bool ok = true;
-        for (int w = 0; w < kWarpsG && ok; ++w) ok = ld_acq_cta(&prog[(kG - 1) * kWarpsG + w]) >= (ks + 1) * kC;
+      // phantom lanes: 4 iterations x 64 pairs, 16-byte copies (L2 only: the
+      // global ring is rewritten every kRG iterations)
+#pragma unroll
+      for (int q = 0; q < kC * kLanes / 64; ++q) {
+        const int e = lane + 32 * q;  // pair index
+        const int it = it_lo + e / (kLanes / 2), t = 2 * (e % (kLanes / 2));
+        const int pit = it + kBig * kG;
+        double* dst = ring_lane0(0, it) + t;
+        if (has_up && pit < p.c_end) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(up_ring + (size_t)(pit % kRG) * kLanes + t));
+        } else {
+          dst[0] = bnd;
+          dst[1] = bnd;
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+      // publish the previous chunk once its copies landed (two chunks in flight)
+      if (kl > 0) {
+        asm volatile("cp.async.wait_group 1;\n" ::);
+        __syncwarp();
+        if (lane == 0) st_rel_cta(&io_load, it_lo);
+      }
+      if (has_up && ((kl + 1) % kPub == 0 || kl + 1 == nch)) {
+        // everything below producer iteration it_hi + Lambda*G is staged in
+        // smem; the global slots it came from may be rewritten
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncwarp();
+        if (lane == 0) st_rel_gpu(p.gcons + up_slot, up_tag | (unsigned long long)min(it_hi + kBig * kG, p.c_end));
+      }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncwarp();
+    if (lane == 0) st_rel_cta(&io_load, p.c_end);
+    return;
+  }
+  if (wi == kComputeWarps + 1) {
+    // ============ drainer warp: last group -> next block (global ring) ============
+    double* dn_ring = p.gring + (size_t)dn_slot * kRG * kLanes;
+    bool slot_ok = !has_down || n < kK;
+    unsigned long long dn_cons_seen = 0;
+    SpinGuard guard;
+    for (int ks = 0; ks < nch; ++ks) {
+      const int lo = ks * kC;
+      for (;;) {
+        const int mine = lane < kWarpsG ? ld_acq_cta(&prog[(kG - 1) * kWarpsG + lane]) : INT_MAX;
+        bool ok = __reduce_min_sync(0xffffffffu, mine) >= lo + kC;
         if (ok && has_down && !slot_ok) {  // previous user of this global slot fully consumed
           unsigned long long v = lane == 0 ? ld_acq_gpu(p.gcons + dn_slot) : 0ull;
           v = __shfl_sync(0xffffffffu, v, 0);
-          const unsigned long long prev_tag = (unsigned long long)(n + 1 - kK) << 32;
-          slot_ok = v >= (prev_tag | (unsigned long long)p.c_end);
+          slot_ok = v >= (((unsigned long long)(n + 1 - kK) << 32) | (unsigned long long)p.c_end);
           ok = slot_ok;
         }
-        const int lo = ks * kC;
         if (ok && has_down && lo + kC > kRG) {  // global back-pressure
           const unsigned long long need = dn_tag | (unsigned long long)(lo + kC - kRG);
           if (dn_cons_seen < need) {
@@ -206,31 +244,25 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
           }
           ok = dn_cons_seen >= need;
         }
-        if (ok && !has_down) {  // last block: nothing to forward, just free the ring
-          if (lane == 0) st_rel_cta(&io_store, lo + kC);
-          ++ks;
-          did = true;
-        } else if (ok) {
-#pragma unroll 4
-          for (int e = lane; e < kC * kLanes; e += 32) {
-            const int it = lo + e / kLanes, t = e % kLanes;
-            dn_ring[(size_t)(it % kRG) * kLanes + t] = ring(kG, it, t + 1);
-          }
-          __threadfence();
-          __syncwarp();
-          if (lane == 0) {
-            st_rel_gpu(p.gprod + dn_slot, dn_tag | (unsigned long long)(lo + kC));
-            st_rel_cta(&io_store, lo + kC);
-          }
-          ++ks;
-          did = true;
+        if (ok) break;
+        __nanosleep(20);
+        guard.tick();
+      }
+      if (has_down) {
+#pragma unroll
+        for (int q = 0; q < kC * kLanes / 64; ++q) {
+          const int e = lane + 32 * q;
+          const int it = lo + e / (kLanes / 2), t = 2 * (e % (kLanes / 2));
+          const double2 v = *reinterpret_cast<const double2*>(ring_lane0(kG, it) + t);
+          *reinterpret_cast<double2*>(dn_ring + (size_t)(it % kRG) * kLanes + t) = v;
         }
       }
-      if (!did) {
-        __nanosleep(32);
-        io_guard.tick();
-      } else {
-        io_guard.n = 0;
+      __syncwarp();
+      if (lane == 0) st_rel_cta(&io_store, lo + kC);
+      if (has_down && ((ks + 1) % kPub == 0 || ks + 1 == nch)) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_rel_gpu(p.gprod + dn_slot, dn_tag | (unsigned long long)(lo + kC));
       }
     }
     return;
@@ -267,19 +299,22 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
 
   for (int k = 0; k < nch; ++k) {
     const int cb = k * kC;
-    // RAW: producers finished chunk k-1 (lags >= chunk + dependency distance)
-    { SpinGuard sg; while (ld_acq_cta(dep_prev) < cb) sg.tick(); }
-    { SpinGuard sg; while (ld_acq_cta(dep_prev2) < cb) sg.tick(); }
-    { SpinGuard sg; while (ld_acq_cta(dep_left) < cb) sg.tick(); }
-    if (g == 0 || w == 0) {
-      { SpinGuard sg; while (ld_acq_cta(&io_load) < cb + kC) sg.tick(); }
-    }
-    // WAR: readers of my ring slots finished chunk k-5
-    const int need = (k - 4) * kC;
-    if (need > 0) {
-      { SpinGuard sg; while (ld_acq_cta(war0) < need) sg.tick(); }
-      { SpinGuard sg; while (ld_acq_cta(war1) < need) sg.tick(); }
-      { SpinGuard sg; while (ld_acq_cta(war2) < need) sg.tick(); }
+    // RAW: producers finished chunk k-1 (lags >= chunk + dependency distance);
+    // WAR: readers of my ring slots finished chunk k-5.  All counters are
+    // read with independent loads, one round trip per poll.
+    {
+      const int need = (k - 4) * kC;
+      SpinGuard sg;
+      for (;;) {
+        const int v0 = ld_acq_cta(dep_prev), v1 = ld_acq_cta(dep_prev2), v2 = ld_acq_cta(dep_left);
+        const int v3 = (g == 0 || w == 0) ? ld_acq_cta(&io_load) : INT_MAX;
+        const int v4 = ld_acq_cta(war0), v5 = ld_acq_cta(war1), v6 = ld_acq_cta(war2);
+        const bool raw_ok = v0 >= cb && v1 >= cb && v2 >= cb && v3 >= cb + kC;
+        const bool war_ok = need <= 0 || (v4 >= need && v5 >= need && v6 >= need);
+        if (raw_ok && war_ok) break;
+        __nanosleep(32);
+        sg.tick();
+      }
     }
     // steady chunk: all columns of the chunk inside [0, e1), every lane real
     // and on a grid row, and no negative ring iterations

@@ -27,8 +27,7 @@
 
 namespace tvs {
 
-constexpr int kP2 = 4;         // columns per lane
-constexpr int kMaxD2 = 8;      // deepest temporal block instantiated
+constexpr int kMaxD2 = 12;     // deepest temporal block instantiated (P = 2)
 constexpr int kWarps2 = 4;     // warps per block
 constexpr int kRowsSeg = 256;  // output rows per warp task
 
@@ -41,7 +40,7 @@ __device__ __forceinline__ constexpr bool has_group() {
 }
 
 // acc[p] (+)= sum over taps of row-group G, columns dc = -1, 0, +1, in order.
-template <unsigned MASK, int G, bool START, bool FMA>
+template <unsigned MASK, int G, bool START, bool FMA, int kP2>
 __device__ __forceinline__ void add_group(double (&acc)[kP2], const double (&in)[kP2 + 2], const double (&c)[9]) {
 #pragma unroll
   for (int p = 0; p < kP2; ++p) {
@@ -69,18 +68,18 @@ struct Coeff9 {
 // out(q-1) = F + taps(+1 row); N(q) = M + taps(0 row); M'(q+1) = taps(-1 row).
 // F is finished in place (it becomes the fresh accumulator), so calling this
 // with (F, M) and then (M, F) on the next row rotates roles without copies.
-template <unsigned MASK, bool FMA>
+template <unsigned MASK, bool FMA, int kP2>
 __device__ __forceinline__ void level_row(double (&F)[kP2], double (&M)[kP2], const double (&in)[kP2 + 2],
                                           const double (&c)[9], double (&out)[kP2]) {
   constexpr bool G0 = has_group<MASK, 0>(), G1 = has_group<MASK, 1>(), G2 = has_group<MASK, 2>();
-  if constexpr (G2) add_group<MASK, 2, !(G0 || G1), FMA>(F, in, c);
+  if constexpr (G2) add_group<MASK, 2, !(G0 || G1), FMA, kP2>(F, in, c);
 #pragma unroll
   for (int p = 0; p < kP2; ++p) out[p] = F[p];
-  if constexpr (G1) add_group<MASK, 1, !G0, FMA>(M, in, c);
-  if constexpr (G0) add_group<MASK, 0, true, FMA>(F, in, c);
+  if constexpr (G1) add_group<MASK, 1, !G0, FMA, kP2>(M, in, c);
+  if constexpr (G0) add_group<MASK, 0, true, FMA, kP2>(F, in, c);
 }
 
-template <unsigned MASK, int D, bool FMA>
+template <unsigned MASK, int D, bool FMA, int kP2>
 __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __restrict__ src,
                                                                 double* __restrict__ dst, Geo g, int64_t origin,
                                                                 Coeff9 cf, double bnd, int64_t n_strips,
@@ -145,9 +144,9 @@ __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __
     for (int l = 0; l < D; ++l) {
       double out[kP2];
       if constexpr (EVEN)
-        level_row<MASK, FMA>(B[l], A[l], in, c, out);
+        level_row<MASK, FMA, kP2>(B[l], A[l], in, c, out);
       else
-        level_row<MASK, FMA>(A[l], B[l], in, c, out);
+        level_row<MASK, FMA, kP2>(A[l], B[l], in, c, out);
       if (fast) {
 #pragma unroll
         for (int p = 0; p < kP2; ++p) in[p + 1] = out[p];
@@ -228,32 +227,44 @@ bool jacobi2d_blocked_supported(const tvs_stencil& st) {
 int jacobi2d_max_depth() { return kMaxD2; }
 int jacobi2d_default_depth() { return 4; }  // measured best at P=4 (register pressure above)
 
-template <unsigned MASK, int D>
+template <unsigned MASK, int D, int P>
 static void launch2d_d(bool fma, unsigned blocks, cudaStream_t s, const double* src, double* dst, const Geo& geo,
                        int64_t origin, const Coeff9& cf, double bnd, int64_t ns, int64_t nt) {
   if (fma)
-    jacobi2d_kernel<MASK, D, true><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt);
+    jacobi2d_kernel<MASK, D, true, P><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt);
   else
-    jacobi2d_kernel<MASK, D, false><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt);
+    jacobi2d_kernel<MASK, D, false, P><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt);
+}
+
+
+template <unsigned MASK, int D>
+static void launch2d_one(bool fma, cudaStream_t s, const double* src, double* dst, const Geo& geo, int64_t origin,
+                         const Coeff9& cf, double bnd) {
+  constexpr int P = D <= 4 ? 4 : 2;
+  const int64_t U = 32 * P - 2 * D;
+  const int64_t ns = (geo.e1 + U - 1) / U;
+  const int64_t nseg = (geo.e0 + kRowsSeg - 1) / kRowsSeg;
+  const int64_t nt = ns * nseg;
+  const unsigned blocks = (unsigned)((nt + kWarps2 - 1) / kWarps2);
+  launch2d_d<MASK, D, P>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt);
 }
 
 template <unsigned MASK>
 static void launch2d(int depth, bool fma, cudaStream_t s, const double* src, double* dst, const Geo& geo,
                      int64_t origin, const Coeff9& cf, double bnd) {
-  const int64_t U = 32 * kP2 - 2 * depth;
-  const int64_t ns = (geo.e1 + U - 1) / U;
-  const int64_t nseg = (geo.e0 + kRowsSeg - 1) / kRowsSeg;
-  const int64_t nt = ns * nseg;
-  const unsigned blocks = (unsigned)((nt + kWarps2 - 1) / kWarps2);
   switch (depth) {
-    case 1: launch2d_d<MASK, 1>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
-    case 2: launch2d_d<MASK, 2>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
-    case 3: launch2d_d<MASK, 3>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
-    case 4: launch2d_d<MASK, 4>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
-    case 5: launch2d_d<MASK, 5>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
-    case 6: launch2d_d<MASK, 6>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
-    case 7: launch2d_d<MASK, 7>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
-    default: launch2d_d<MASK, 8>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt); break;
+    case 1: launch2d_one<MASK, 1>(fma, s, src, dst, geo, origin, cf, bnd); break;
+    case 2: launch2d_one<MASK, 2>(fma, s, src, dst, geo, origin, cf, bnd); break;
+    case 3: launch2d_one<MASK, 3>(fma, s, src, dst, geo, origin, cf, bnd); break;
+    case 4: launch2d_one<MASK, 4>(fma, s, src, dst, geo, origin, cf, bnd); break;
+    case 5: launch2d_one<MASK, 5>(fma, s, src, dst, geo, origin, cf, bnd); break;
+    case 6: launch2d_one<MASK, 6>(fma, s, src, dst, geo, origin, cf, bnd); break;
+    case 7: launch2d_one<MASK, 7>(fma, s, src, dst, geo, origin, cf, bnd); break;
+    case 8: launch2d_one<MASK, 8>(fma, s, src, dst, geo, origin, cf, bnd); break;
+    case 9: launch2d_one<MASK, 9>(fma, s, src, dst, geo, origin, cf, bnd); break;
+    case 10: launch2d_one<MASK, 10>(fma, s, src, dst, geo, origin, cf, bnd); break;
+    case 11: launch2d_one<MASK, 11>(fma, s, src, dst, geo, origin, cf, bnd); break;
+    default: launch2d_one<MASK, 12>(fma, s, src, dst, geo, origin, cf, bnd); break;
   }
 }
 

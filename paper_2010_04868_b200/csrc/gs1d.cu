@@ -158,7 +158,27 @@ __global__ void __launch_bounds__(kGsWarps * 32, 1) gs1d_kernel(Gs1dArgs p) {
     // steady chunk: every lane real and every position of the chunk inside
     // [0, n) — no selects on the DMUL->DADD->DADD chain
     const bool steady = warp_real && jb - kGsLag * 32 >= 0 && jb + 31 - kGsLag < n;
-    if (steady) {
+    if (steady && MASK == 7u) {
+      // full 3-tap stencil: the products w1*C and w2*R are formed as soon as
+      // their operands arrive, so the loop-carried chain is exactly
+      // L -> DMUL -> DADD -> DADD (bit-identical: same products, same adds)
+      double pa = __dmul_rn(p.w1, u0), pb = __dmul_rn(p.w2, u1);
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int j = jb + u;
+        const double sh = __shfl_up_sync(0xffffffffu, out, 1);
+        const double rv = rin[(j - 1) & (kGsRing - 1)];  // same address for all lanes: broadcast
+        const double sv = lane == 0 ? rv : sh;
+        out = __dadd_rn(pb, __dadd_rn(pa, __dmul_rn(p.w0, L)));
+        pa = __dmul_rn(p.w1, u1);  // next iteration's C is this iteration's R
+        pb = __dmul_rn(p.w2, sv);  // next iteration's R just arrived
+        L = out;
+        u0 = u1;
+        u1 = sv;
+        const int po = j - kGsLag * 32;
+        if (writer) rout[po & (kGsRing - 1)] = out;
+      }
+    } else if (steady) {
 #pragma unroll
       for (int u = 0; u < 32; ++u) {
         const int j = jb + u;

@@ -36,10 +36,29 @@
 // sweep of row d - 127 back to the grid in place.
 #include <algorithm>
 #include <climits>
+#include <type_traits>
 
 #include "common.cuh"
 
 namespace tvs {
+
+#ifdef GS2P_TRACE
+// [cta][event] globaltimer stamps: 0 start, 1 group0 chunk 0 begins, 2 group0 chunk 100,
+// 3 last group chunk 100, 4 first downstream publish, 5 compute done
+__device__ unsigned long long g_trace[4096][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(n, e) do { if ((n) < 4096) g_trace[(n)][(e)] = gtimer(); } while (0)
+// [cta<2][role] = {wait cycles, total cycles} over the first 100 chunks
+// roles: 0 warp(0,0) 1 warp(0,3) 2 warp(3,0) 3 warp(3,3) 4 loader 5 drainer
+__device__ unsigned long long g_wait[2][6][2];
+#define WAITACC(n, r, w, t) do { if ((n) < 2) { atomicAdd(&g_wait[(n)][(r)][0], (w)); atomicAdd(&g_wait[(n)][(r)][1], (t)); } } while (0)
+#else
+#define TRACE(n, e) do { } while (0)
+#endif
 
 namespace gs2p {
 constexpr int kLanes = 128;          // sweeps per pass (4 warps)
@@ -54,10 +73,11 @@ constexpr int kBig = 5;              // lag group g-1 -> g (>= kC + 1)
 constexpr int kBase = 10;            // every producer starts left of column 0 (>= kLam + kBig + 2)
 constexpr int kRG = 256;             // global ring depth (iterations)
 constexpr int kK = 256;              // global ring slots (boundaries in flight)
-constexpr int kPub = 8;              // IO warp publishes downstream every kPub chunks
+constexpr int kPub = 4;              // IO warps publish up/downstream every kPub chunks
 constexpr int kComputeWarps = kG * kWarpsG;
 constexpr int kThreads = (kComputeWarps + 2) * 32;  // + loader warp + drainer warp
-constexpr size_t kSmem = sizeof(double) * (size_t)(kG + 1) * kR * kSlots;
+constexpr int kRows = kR + kC;       // ring rows incl. kC mirror rows (chunk reads never wrap)
+constexpr size_t kSmem = sizeof(double) * (size_t)(kG + 1) * kRows * kSlots;
 static_assert(kMu >= kC + 1 - kLam && kBig >= kC + 1, "lags too small for chunked sync");
 }  // namespace gs2p
 
@@ -72,6 +92,7 @@ struct Gs2pArgs {
   unsigned long long* gprod; // kK tagged counters: (boundary+1) << 32 | iterations written
   unsigned long long* gcons; // kK tagged counters: (boundary+1) << 32 | iterations consumed
   int* ticket;
+  const double* bndpad;       // 32 copies of the boundary value
   double w[9];
   double bnd;
 };
@@ -84,6 +105,14 @@ __device__ __forceinline__ int ld_acq_cta(const int* p) {
 __device__ __forceinline__ void st_rel_cta(int* p, int v) {
   asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
 }
+// loader publication of io_load (experiment switch GS2P_RELAXED_LOAD)
+__device__ __forceinline__ void st_io_load(int* p, int v) {
+#ifdef GS2P_RELAXED_LOAD
+  asm volatile("st.volatile.shared::cta.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+#else
+  st_rel_cta(p, v);
+#endif
+}
 __device__ __forceinline__ unsigned long long ld_acq_gpu(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -91,6 +120,30 @@ __device__ __forceinline__ unsigned long long ld_acq_gpu(const unsigned long lon
 }
 __device__ __forceinline__ void st_rel_gpu(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---- mbarrier chunk-completion rings (hardware-suspended waits) ----
+// Warp X (compute warps 0..15, loader 16, drainer 17) completes its chunks in
+// order; completion of chunk m is phase (m >> 3) of barrier bar[X][m & 7].
+// Every waiter is at most 5 chunks behind / 3 ahead of the warp it waits on
+// (RAW/WAR bounds), so a slot never wraps under a waiter (no ABA).
+__device__ __forceinline__ unsigned smaddr(const void* q) { return (unsigned)__cvta_generic_to_shared(q); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smaddr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(smaddr(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
+  unsigned ok;
+  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+               : "=r"(ok) : "r"(smaddr(b)), "r"(parity), "r"(20000u) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  unsigned n = 0;
+  while (!mbar_try(b, parity))
+    if (++n > (1u << 18)) __trap();  // watchdog (~5 s of suspended waits)
 }
 
 // Wait until a shared-memory progress counter reaches `v`; back off so the
@@ -127,18 +180,30 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
   extern __shared__ __align__(16) double smem[];
   // rings[0] = phantom (previous block's last group), rings[g+1] = group g
   auto ring = [&](int gi, int it, int slot) -> double& {
-    return smem[((size_t)gi * kR + (it & (kR - 1))) * kSlots + (slot == 0 ? 0 : slot + 1)];
+    return smem[((size_t)gi * kRows + (it & (kR - 1))) * kSlots + (slot == 0 ? 0 : slot + 1)];
   };
-  auto ring_lane0 = [&](int gi, int it) -> double* { return &smem[((size_t)gi * kR + (it & (kR - 1))) * kSlots + 2]; };
-  __shared__ int prog[kComputeWarps];
-  __shared__ int io_load, io_store;
+  auto ring_lane0 = [&](int gi, int it) -> double* { return &smem[((size_t)gi * kRows + (it & (kR - 1))) * kSlots + 2]; };
+  // a write of ring row r < kC also goes to mirror row kR + r
+  auto mirror_of = [&](double* p_row_elem, int it) -> double* { return (it & (kR - 1)) < kC ? p_row_elem + (size_t)kR * kSlots : nullptr; };
+  constexpr int kLoader = kComputeWarps, kDrainer = kComputeWarps + 1;
+  __shared__ unsigned long long bar[kComputeWarps + 2][8];
   __shared__ int s_ticket;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_ticket = atomicAdd(p.ticket, 1);
-  if (threadIdx.x < kComputeWarps) prog[threadIdx.x] = 0;
-  if (threadIdx.x == 0) io_load = io_store = 0;
+  if (threadIdx.x == 0) {
+    s_ticket = atomicAdd(p.ticket, 1);
+    for (int x = 0; x < kComputeWarps + 2; ++x)
+      for (int q = 0; q < 8; ++q) mbar_init(&bar[x][q], x == kLoader ? 32u : 1u);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
+  // "warp x completed chunk m" / "I completed chunk m"
+  auto wait_chunk = [&](int x, int m) {
+#ifndef GS2P_NOWAIT
+    if (m >= 0) mbar_wait(&bar[x][m & 7], (unsigned)(m >> 3) & 1u);
+#endif
+  };
   const int n = s_ticket;           // block index along the chain
+  if (threadIdx.x == 0) TRACE(n, 0);
   const int d0 = n * kG;            // first group (diagonal) of this block
   const int nch = p.c_end / kC;
   const double bnd = p.bnd;
@@ -152,36 +217,44 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
     // ============ loader warp: grid rows (slot 0) + previous block's last group ============
     const double* up_ring = p.gring + (size_t)up_slot * kRG * kLanes;
     unsigned long long up_seen = 0;
-    SpinGuard guard;
+#ifdef GS2P_TRACE
+    long long lw = 0, lt0 = clock64();
+#endif
+    const double* bndsrc = p.bndpad;  // 32 copies of the boundary value (cp.async source)
     for (int kl = 0; kl < nch; ++kl) {
+#ifdef GS2P_TRACE
+      const long long lws = clock64();
+      if (kl == 100 && lane == 0) WAITACC(n, 4, (unsigned long long)lw, (unsigned long long)(lws - lt0));
+#endif
       const int it_lo = kl * kC, it_hi = it_lo + kC;
-      // WAR: every compute warp finished chunk kl-5 (ring chunk kl-8 reusable)
-      const int need = (kl - 4) * kC;
+      // WAR: the readers of the slots written below (group 0 -> phantom slots,
+      // every group's warp 0 -> slot 0) finished chunk kl-5 (ring chunk kl-8 reusable)
+      for (int q = 0; q < kWarpsG; ++q) wait_chunk(q, kl - 5);
+      for (int g = 1; g < kG; ++g) wait_chunk(g * kWarpsG, kl - 5);
       // upstream data for producer iterations up to it_hi + Lambda*G
-      const int up_need = min(it_hi + kBig * kG, p.c_end);
-      for (;;) {
-        const int mine = lane < kComputeWarps ? ld_acq_cta(&prog[lane]) : INT_MAX;
-        bool ok = __reduce_min_sync(0xffffffffu, mine) >= need;
-        if (ok && has_up && ((up_seen >> 32) != (up_tag >> 32) || (up_seen & 0xffffffffull) < (unsigned long long)up_need)) {
+      if (has_up) {
+        const int up_need = min(it_hi + kBig * kG, p.c_end);
+        SpinGuard guard;
+        while ((up_seen >> 32) != (up_tag >> 32) || (up_seen & 0xffffffffull) < (unsigned long long)up_need) {
           up_seen = lane == 0 ? ld_acq_gpu(p.gprod + up_slot) : 0ull;
           up_seen = __shfl_sync(0xffffffffu, up_seen, 0);
-          ok = (up_seen >> 32) == (up_tag >> 32) && (up_seen & 0xffffffffull) >= (unsigned long long)up_need;
+          if ((up_seen >> 32) == (up_tag >> 32) && (up_seen & 0xffffffffull) >= (unsigned long long)up_need) break;
+          __nanosleep(64);
+          guard.tick();
         }
-        if (ok) break;
-        __nanosleep(20);
-        guard.tick();
       }
+#ifdef GS2P_TRACE
+      lw += clock64() - lws;
+#endif
       // slot 0 of rings -1..G-1: grid row d0+g+1 at column it + lam - Lambda*g - base
       if (lane < (kG + 1) * kC) {
         const int g = lane / kC - 1, it = it_lo + lane % kC;
         const int row = d0 + g + 1, col = it + kLam - kBig * g - kBase;
         double* dst = &ring(g + 1, it, 0);
-        if (row >= 0 && row < e0 && col >= 0 && col < e1) {
-          const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(p.a + (long long)row * p.s0 + col));
-        } else {
-          *dst = bnd;
-        }
+        double* mir = mirror_of(dst, it);
+        const double* src = (row >= 0 && row < e0 && col >= 0 && col < e1) ? p.a + (long long)row * p.s0 + col : bndsrc;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smaddr(dst)), "l"(src));
+        if (mir) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smaddr(mir)), "l"(src));
       }
       // phantom lanes: 4 iterations x 64 pairs, 16-byte copies (L2 only: the
       // global ring is rewritten every kRG iterations)
@@ -191,32 +264,20 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
         const int it = it_lo + e / (kLanes / 2), t = 2 * (e % (kLanes / 2));
         const int pit = it + kBig * kG;
         double* dst = ring_lane0(0, it) + t;
-        if (has_up && pit < p.c_end) {
-          const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(up_ring + (size_t)(pit % kRG) * kLanes + t));
-        } else {
-          dst[0] = bnd;
-          dst[1] = bnd;
-        }
+        double* mir = mirror_of(dst, it);
+        const double* src = (has_up && pit < p.c_end) ? up_ring + (size_t)(pit % kRG) * kLanes + t : bndsrc;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smaddr(dst)), "l"(src));
+        if (mir) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smaddr(mir)), "l"(src));
       }
-      asm volatile("cp.async.commit_group;\n" ::);
-      // publish the previous chunk once its copies landed (two chunks in flight)
-      if (kl > 0) {
-        asm volatile("cp.async.wait_group 1;\n" ::);
-        __syncwarp();
-        if (lane == 0) st_rel_cta(&io_load, it_lo);
-      }
+      // the chunk's barrier phase completes when every lane's copies landed
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smaddr(&bar[kLoader][kl & 7])) : "memory");
       if (has_up && ((kl + 1) % kPub == 0 || kl + 1 == nch)) {
-        // everything below producer iteration it_hi + Lambda*G is staged in
-        // smem; the global slots it came from may be rewritten
-        asm volatile("cp.async.wait_group 0;\n" ::);
-        __syncwarp();
+        // producer iterations below it_hi + Lambda*G are no longer read from
+        // the global ring once this chunk's copies completed
+        wait_chunk(kLoader, kl);
         if (lane == 0) st_rel_gpu(p.gcons + up_slot, up_tag | (unsigned long long)min(it_hi + kBig * kG, p.c_end));
       }
     }
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    __syncwarp();
-    if (lane == 0) st_rel_cta(&io_load, p.c_end);
     return;
   }
   if (wi == kComputeWarps + 1) {
@@ -225,11 +286,21 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
     bool slot_ok = !has_down || n < kK;
     unsigned long long dn_cons_seen = 0;
     SpinGuard guard;
+#ifdef GS2P_TRACE
+    long long dw = 0, dt0 = clock64();
+#endif
     for (int ks = 0; ks < nch; ++ks) {
       const int lo = ks * kC;
+#ifdef GS2P_TRACE
+      const long long dws = clock64();
+      if (ks == 100 && lane == 0) WAITACC(n, 5, (unsigned long long)dw, (unsigned long long)(dws - dt0));
+#endif
+      // the last group (forwarded downstream) and every group's warp 3
+      // (lane 127 = the final sweep, written back to the grid here)
+      for (int q = 0; q < kWarpsG; ++q) wait_chunk((kG - 1) * kWarpsG + q, ks);
+      for (int g = 0; g + 1 < kG; ++g) wait_chunk(g * kWarpsG + kWarpsG - 1, ks);
       for (;;) {
-        const int mine = lane < kWarpsG ? ld_acq_cta(&prog[(kG - 1) * kWarpsG + lane]) : INT_MAX;
-        bool ok = __reduce_min_sync(0xffffffffu, mine) >= lo + kC;
+        bool ok = true;
         if (ok && has_down && !slot_ok) {  // previous user of this global slot fully consumed
           unsigned long long v = lane == 0 ? ld_acq_gpu(p.gcons + dn_slot) : 0ull;
           v = __shfl_sync(0xffffffffu, v, 0);
@@ -248,6 +319,10 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
         __nanosleep(20);
         guard.tick();
       }
+#ifdef GS2P_TRACE
+      dw += clock64() - dws;
+#endif
+#ifndef GS2P_NODRAIN
       if (has_down) {
 #pragma unroll
         for (int q = 0; q < kC * kLanes / 64; ++q) {
@@ -257,12 +332,20 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
           *reinterpret_cast<double2*>(dn_ring + (size_t)(it % kRG) * kLanes + t) = v;
         }
       }
+      if (lane < kG * kC) {  // final outputs: lane 127 of group g = row d_g - 127
+        const int g = lane / kC, it = lo + lane % kC;
+        const int row = d0 + g - (kLanes - 1);
+        const int col = it - (kBase + kLam * (kLanes - 1) + kMu * (kWarpsG - 1) + kBig * g);
+        if (row >= 0 && row < e0 && col >= 0 && col < e1) p.a[(long long)row * p.s0 + col] = ring(g + 1, it, kLanes);
+      }
+#endif
       __syncwarp();
-      if (lane == 0) st_rel_cta(&io_store, lo + kC);
+      if (lane == 0) mbar_arrive(&bar[kDrainer][ks & 7]);
       if (has_down && ((ks + 1) % kPub == 0 || ks + 1 == nch)) {
         __threadfence();
         __syncwarp();
         if (lane == 0) st_rel_gpu(p.gprod + dn_slot, dn_tag | (unsigned long long)(lo + kC));
+        if (lane == 0 && ks + 1 == kPub) TRACE(n, 4);
       }
     }
     return;
@@ -275,68 +358,102 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
   const int row = d - t;
   const bool row_ok = row >= 0 && row < e0;
   const bool real = t < p.sweeps;
+  // per-lane output mode: 0 compute, 1 identity (beyond the sweep count), 2 outside the grid
+  const int mode = row_ok ? (real ? 0 : 1) : 2;
+  const bool warp_pure = __all_sync(0xffffffffu, mode == 0);
   const int col_off = kBase + kLam * t + kMu * w + kBig * g;  // column = iteration - col_off
   const int offE = 1 - kLam - kBig - ((lane == 0 && w > 0) ? kMu : 0);
   const int offSE = 1 - kLam - (w > 0 ? kMu : 0);   // lane 0 only
-  const int slotE = t;                               // lane t-1 (or virtual lane -1)
-  const int slotSE = w * 32;
-  const int gi_prev = g, gi_cur = g + 1;
-  const bool last_lane = t == kLanes - 1;
-  double* out_row = p.a + (long long)(row_ok ? row : 0) * p.s0;
-  double wk[9];
+  const int idxE = t == 0 ? 0 : t + 1;               // element index of lane t-1's slot (or virtual lane -1)
+  const int idxSE = w == 0 ? 0 : 32 * w + 1;         // lane 32w-1 (or virtual lane -1)
+  double* const base_prev = smem + (size_t)g * kRows * kSlots;        // ring of group g-1 (or phantom)
+  double* const base_cur = smem + (size_t)(g + 1) * kRows * kSlots;   // ring of group g
+  double wk[9];  // coefficients in registers (a shuffle makes them runtime values)
 #pragma unroll
-  for (int k = 0; k < 9; ++k) wk[k] = p.w[k];
-  const bool warp_rows_ok = __all_sync(0xffffffffu, row_ok && real);
+  for (int k = 0; k < 9; ++k) wk[k] = __shfl_sync(0xffffffffu, p.w[k], 0);
   // progress of the warps I read from / that read me
-  const int* dep_prev = g > 0 ? &prog[(g - 1) * kWarpsG + w] : &io_load;
-  const int* dep_prev2 = g > 0 ? &prog[(g - 1) * kWarpsG + (w > 0 ? w - 1 : 0)] : &io_load;
-  const int* dep_left = w > 0 ? &prog[g * kWarpsG + w - 1] : &io_load;
-  const int* war0 = g + 1 < kG ? &prog[(g + 1) * kWarpsG + w] : &io_store;
-  const int* war1 = g + 1 < kG ? &prog[(g + 1) * kWarpsG + (w + 1 < kWarpsG ? w + 1 : w)] : &io_store;
-  const int* war2 = w + 1 < kWarpsG ? &prog[g * kWarpsG + w + 1] : war0;
+  // warps I read from (RAW, chunk k-1) and that read me (WAR, chunk k-5)
+  const int dep_prev = g > 0 ? (g - 1) * kWarpsG + w : kLoader;
+  const int dep_prev2 = (g > 0 && w > 0) ? (g - 1) * kWarpsG + w - 1 : -1;
+  const int dep_left = w > 0 ? g * kWarpsG + w - 1 : -1;
+  const bool needs_io = g == 0 || w == 0;
+  const int war0 = g + 1 < kG ? (g + 1) * kWarpsG + w : kDrainer;
+  const int war1 = (g + 1 < kG && w + 1 < kWarpsG) ? (g + 1) * kWarpsG + w + 1 : -1;
+  // warp 3's lane 127 is read by the drainer (final outputs), the others by warp w+1
+  const int war2 = w + 1 < kWarpsG ? g * kWarpsG + w + 1 : kDrainer;
 
   double nw = bnd, nn = bnd, ne = bnd, cc = bnd, ee = bnd, sw = bnd, ss = bnd, se = bnd, ww = bnd, out = bnd;
+#ifdef GS2P_TRACE
+  long long t_wait = 0, t_start = 0;
+#endif
 
   for (int k = 0; k < nch; ++k) {
     const int cb = k * kC;
-    // RAW: producers finished chunk k-1 (lags >= chunk + dependency distance);
-    // WAR: readers of my ring slots finished chunk k-5.  All counters are
-    // read with independent loads, one round trip per poll.
-    {
-      const int need = (k - 4) * kC;
-      SpinGuard sg;
-      for (;;) {
-        const int v0 = ld_acq_cta(dep_prev), v1 = ld_acq_cta(dep_prev2), v2 = ld_acq_cta(dep_left);
-        const int v3 = (g == 0 || w == 0) ? ld_acq_cta(&io_load) : INT_MAX;
-        const int v4 = ld_acq_cta(war0), v5 = ld_acq_cta(war1), v6 = ld_acq_cta(war2);
-        const bool raw_ok = v0 >= cb && v1 >= cb && v2 >= cb && v3 >= cb + kC;
-        const bool war_ok = need <= 0 || (v4 >= need && v5 >= need && v6 >= need);
-        if (raw_ok && war_ok) break;
-        __nanosleep(32);
-        sg.tick();
-      }
+    if (lane == 0 && w == 0 && g == 0 && (k == 0 || k == 100)) TRACE(n, k == 0 ? 1 : 2);
+    if (lane == 0 && w == kWarpsG - 1 && g == kG - 1 && k == 100) TRACE(n, 3);
+#ifdef GS2P_TRACE
+    const long long tw0 = clock64();
+    if (k == 0) t_start = tw0;
+#endif
+    // RAW: producers finished chunk k-1 (the loader: chunk k); WAR: readers
+    // of my ring slots finished chunk k-5 (the ring holds 8 chunks)
+    if (g > 0) wait_chunk(dep_prev, k - 1);
+    if (dep_prev2 >= 0) wait_chunk(dep_prev2, k - 1);
+    if (dep_left >= 0) wait_chunk(dep_left, k - 1);
+    if (needs_io) wait_chunk(kLoader, k);
+    wait_chunk(war0, k - 5);
+    if (war1 >= 0) wait_chunk(war1, k - 5);
+    wait_chunk(war2, k - 5);
+#ifdef GS2P_TRACE
+    t_wait += clock64() - tw0;
+    if (k == 100 && lane == 0) {
+      const int role = (g == 0 && w == 0) ? 0 : (g == 0 && w == kWarpsG - 1) ? 1 : (g == kG - 1 && w == 0) ? 2 : (g == kG - 1 && w == kWarpsG - 1) ? 3 : -1;
+      if (role >= 0) WAITACC(n, role, (unsigned long long)t_wait, (unsigned long long)(clock64() - t_start));
     }
-    // steady chunk: all columns of the chunk inside [0, e1), every lane real
-    // and on a grid row, and no negative ring iterations
+#endif
+    // steady chunk: every column of the chunk inside [0, e1) for every lane
+    // of the warp and no negative ring iteration -> no guards, base pointers
+    // with immediate per-iteration offsets (the ring has kC mirror rows)
     const int jmin = cb - (kBase + kLam * (w * 32 + 31) + kMu * w + kBig * g);
     const int jmax = cb + kC - 1 - (kBase + kLam * (w * 32) + kMu * w + kBig * g);
-    const bool steady = warp_rows_ok && jmin >= 0 && jmax < e1 && cb + offE - kMu >= 0;
+    const bool steady = jmin >= 0 && jmax < e1 && cb + offSE - kBig - kMu >= 0;
     if (steady) {
+      const double* pNE = base_prev + ((cb + 1 - kBig) & (kR - 1)) * kSlots + t + 2;
+      const double* pE = base_prev + ((cb + offE) & (kR - 1)) * kSlots + idxE;
+      const double* pSE = base_cur + ((cb + offSE) & (kR - 1)) * kSlots + idxSE;
+      double* pOut = base_cur + (cb & (kR - 1)) * kSlots + t + 2;
+      const bool mirror = (cb & (kR - 1)) == 0;  // rows 0..kC-1 are mirrored at kR..kR+kC-1
+      double outs[kC];
+      auto body = [&](auto pure_tag) {
+        constexpr bool PURE = decltype(pure_tag)::value;
 #pragma unroll
-      for (int u = 0; u < kC; ++u) {
-        const int c = cb + u;
-        const double ne_new = ring(gi_prev, c + 1 - kBig, t + 1);
-        const double e_new = ring(gi_prev, c + offE, slotE);
-        const double sh = __shfl_up_sync(0xffffffffu, out, 1);
-        const double sl = ring(gi_cur, c + offSE, slotSE);
-        const double se_new = lane == 0 ? sl : sh;
-        nw = nn; nn = ne; ne = ne_new;
-        cc = ee; ee = e_new;
-        sw = ss; ss = se; se = se_new;
-        out = gs9<MASK>(wk, nw, nn, ne, ww, cc, ee, sw, ss, se);
-        ww = out;
-        ring(gi_cur, c, t + 1) = out;
-        if (last_lane) out_row[c - col_off] = out;
+        for (int u = 0; u < kC; ++u) {
+          const double ne_new = pNE[u * kSlots];
+          const double e_new = pE[u * kSlots];
+          const double sh = __shfl_up_sync(0xffffffffu, out, 1);
+          const double sl = pSE[u * kSlots];
+          const double se_new = lane == 0 ? sl : sh;
+          nw = nn; nn = ne; ne = ne_new;
+          cc = ee; ee = e_new;
+          sw = ss; ss = se; se = se_new;
+          const double v = gs9<MASK>(wk, nw, nn, ne, ww, cc, ee, sw, ss, se);
+          if constexpr (PURE) {
+            out = v;
+          } else {
+            out = mode == 0 ? v : (mode == 1 ? cc : bnd);
+          }
+          ww = out;
+          pOut[u * kSlots] = out;
+          outs[u] = out;
+        }
+      };
+      if (warp_pure)
+        body(std::true_type{});
+      else
+        body(std::false_type{});
+      if (mirror) {
+#pragma unroll
+        for (int u = 0; u < kC; ++u) pOut[(kR + u) * kSlots] = outs[u];
       }
     } else {
 #pragma unroll
@@ -344,10 +461,10 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
         const int c = cb + u;
         const int j = c - col_off;
         const int i1 = c + 1 - kBig, i2 = c + offE, i3 = c + offSE;
-        const double ne_new = i1 >= 0 ? ring(gi_prev, i1, t + 1) : bnd;
-        const double e_new = i2 >= 0 ? ring(gi_prev, i2, slotE) : bnd;
+        const double ne_new = i1 >= 0 ? base_prev[(i1 & (kR - 1)) * kSlots + t + 2] : bnd;
+        const double e_new = i2 >= 0 ? base_prev[(i2 & (kR - 1)) * kSlots + idxE] : bnd;
         const double sh = __shfl_up_sync(0xffffffffu, out, 1);
-        const double sl = i3 >= 0 ? ring(gi_cur, i3, slotSE) : bnd;
+        const double sl = i3 >= 0 ? base_cur[(i3 & (kR - 1)) * kSlots + idxSE] : bnd;
         const double se_new = lane == 0 ? sl : sh;
         nw = nn; nn = ne; ne = ne_new;
         cc = ee; ee = e_new;
@@ -356,12 +473,13 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
         const bool inside = row_ok && j >= 0 && j < e1;
         out = inside ? (real ? v : cc) : bnd;
         ww = out;
-        ring(gi_cur, c, t + 1) = out;
-        if (last_lane && inside) out_row[j] = out;
+        const int r = c & (kR - 1);
+        base_cur[r * kSlots + t + 2] = out;
+        if (r < kC) base_cur[(r + kR) * kSlots + t + 2] = out;
       }
     }
     __syncwarp();
-    if (lane == 0) st_rel_cta(&prog[wi], cb + kC);
+    if (lane == 0) mbar_arrive(&bar[wi][k & 7]);
   }
 }
 
@@ -412,6 +530,14 @@ int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, in
   a.gprod = reinterpret_cast<unsigned long long*>(ctrl);
   a.gcons = a.gprod + kK;
   a.ticket = reinterpret_cast<int*>(a.gcons + kK);
+  double* bndpad = static_cast<double*>(scratch(sizeof(double) * 32, 2));
+  if (!bndpad) return fail(TVS_ERR_CUDA, "gs2d_pipeline: scratch");
+  {
+    double h[32];
+    for (double& x : h) x = st.boundary;
+    TVS_CUDA(cudaMemcpyAsync(bndpad, h, sizeof(h), cudaMemcpyHostToDevice, s));
+  }
+  a.bndpad = bndpad;
   auto kern = mask == 0x1FFu ? gs2d_pipe_kernel<0x1FFu> : gs2d_pipe_kernel<kStar>;
   TVS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
   for (int64_t done = 0; done < steps; done += kLanes) {

@@ -69,6 +69,18 @@ def peaks():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
+def measured_traffic(cfg):
+    """ncu DRAM bytes per launch of this config's dominant kernel (committed
+    evidence, profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)
+        cid = next(k for k, v in CONFIGS.items() if v is cfg or v["name"] == cfg["name"])
+        return t["configs"][str(cid)]
+    except Exception:
+        return None
+
+
 def make_grid(cfg, pinned=False):
     from paper_2010_04868_b200 import Grid
 
@@ -245,10 +257,22 @@ def measure_config(cfg, K, W, with_e2e=True, with_cpu=True):
         "warmup": W, "gpu_launches": launches * K, "launches_per_step": launches, "clocks": clk.summary(),
         "workload": f"{cfg['name']} {'x'.join(map(str, cfg['extents']))} T={cfg['T']}",
     }
-    achieved = BYTES_PER_UPDATE * updates / (ms * 1e-3) / 1e9
+    # per launch of the dominant kernel (every launch of a step is that kernel
+    # here): algorithmic bytes = 16 B x updates per launch, duration = step
+    # time / launches, both from the CUDA events above
+    per_launch_ms = ms / max(launches, 1)
+    upd_launch = updates / max(launches, 1)
+    achieved = BYTES_PER_UPDATE * upd_launch / (per_launch_ms * 1e-3) / 1e9
+    traffic = measured_traffic(cfg)
     res["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                       "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
-                       "note": "achieved = 16 B/update algorithmic (effective) bandwidth of the step's kernels"}
+                       "frac": achieved / hbm_peak,
+                       "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+                       "traffic_bytes_per_update": traffic["dram_bytes_per_update"] if traffic else None,
+                       "algorithmic_bytes_per_launch": BYTES_PER_UPDATE * upd_launch,
+                       "launch_ms": per_launch_ms, "peak_source": peak_src,
+                       "note": "achieved = 16 B/update x updates per launch / launch time (effective bandwidth; "
+                               "temporal blocking makes it exceed HBM peak). traffic = ncu dram read+write per "
+                               "launch of the same kernel (profiles/traffic.json)"}
     sm = res["clocks"].get("sm_mhz") or 1965.0
     fp64_peak = 148 * 64 * sm * 1e6 / 1e12  # DP ops/s (DADD/DMUL/DFMA each 1 op), measured 63.4/clk/SM
     fp64 = cfg["ops"] * updates / (ms * 1e-3) / 1e12

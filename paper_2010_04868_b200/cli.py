@@ -1,0 +1,194 @@
+"""Command-line harness mirroring the reference CLI (tvstencil/cli.py:73-286).
+
+    python -m paper_2010_04868_b200.cli --mode bench --kernel heat2d --nx 16384 --ny 16384 --t 200 --reps 5
+    python -m paper_2010_04868_b200.cli --mode verify --kernel all --cells 8
+
+Same flags, JSON ``--config`` defaults (explicit flags win), metric
+(GStencil/s = interior points x T / median seconds / 1e9, cli.py:228-231),
+median of ``--reps`` after one warm-up, and CSV schema
+``kernel,variant,dim,nx,ny,nz,t,threads,tile,reps,gstencils_per_s,checksum``
+(cli.py:39) with the FNV-1a checksum of the final grid's TSTN dump — so a
+GPU row and a reference CPU row of the same run carry the same checksum.
+Appended columns: ``backend,device_ms,depth``.
+
+``--mode verify`` runs on the GPU only (the product never embeds the CPU
+oracle): the reference's known-answer vectors (test_baselines.py:17-36) and,
+for every cell of the reference-shaped acceptance matrix, the temporally
+blocked / pipelined kernels against the independent one-step (Jacobi) and
+hyperplane-wavefront (Gauss-Seidel) kernels, bit-exact.  Oracle parity
+proper lives in tests/.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import statistics
+import sys
+import time
+
+import numpy as np
+
+from . import _native, config
+from .catalog import DEFAULT_CATALOG, get as catalog_get
+from .grid import Grid, fnv1a64
+from .kernels import KernelVariant
+from .verify import default_matrix, run_temporal
+
+CSV_HEADER = "kernel,variant,dim,nx,ny,nz,t,threads,tile,reps,gstencils_per_s,checksum"
+CSV_EXTRA = "backend,device_ms,depth"
+DEFAULT_SIZES = {1: (1_000_000,), 2: (512, 512), 3: (64, 64, 64)}
+GPU_KERNELS = [k for k, e in DEFAULT_CATALOG.items() if e.spec.element_kind == "float64"]
+
+
+def build_parser() -> argparse.ArgumentParser:
+    p = argparse.ArgumentParser(prog="tvstencil-b200", description=__doc__,
+                                formatter_class=argparse.RawDescriptionHelpFormatter)
+    p.add_argument("--mode", choices=("verify", "bench"), required=True)
+    p.add_argument("--kernel", default="all", help=f"one of {GPU_KERNELS} or 'all'")
+    p.add_argument("--variant", default="base", choices=("base", "two-stride"))
+    p.add_argument("--nx", type=int)
+    p.add_argument("--ny", type=int)
+    p.add_argument("--nz", type=int)
+    p.add_argument("--t", type=int, dest="steps")
+    p.add_argument("--reps", type=int, default=5)
+    p.add_argument("--csv", help="append benchmark rows to this file")
+    p.add_argument("--dump", help="write the final grid dump (TSTN) here")
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--cells", type=int, default=8, help="verify-mode cells per kernel")
+    p.add_argument("--config", help="JSON file with flag defaults")
+    p.add_argument("--order", default="lexicographic", choices=("lexicographic", "reference"),
+                   help="Gauss-Seidel update order (2D/3D)")
+    p.add_argument("--fma", default="exact", choices=("exact", "never", "allow"))
+    p.add_argument("--depth", type=int, default=0, help="temporal block depth (0 = kernel default)")
+    return p
+
+
+def _apply_config(args, argv):
+    if not args.config:
+        return args
+    with open(args.config) as fh:
+        cfg = json.load(fh)
+    passed = {a.split("=")[0].lstrip("-").replace("-", "_") for a in argv if a.startswith("--")}
+    for key, value in cfg.items():
+        attr = "steps" if key == "t" else key.replace("-", "_")
+        if key in passed or attr in passed or not hasattr(args, attr):
+            continue
+        setattr(args, attr, value)
+    return args
+
+
+def _kernels(arg):
+    if arg == "all":
+        return GPU_KERNELS
+    if arg not in GPU_KERNELS:
+        raise SystemExit(f"unknown or non-GPU kernel {arg!r}; known: {GPU_KERNELS}")
+    return [arg]
+
+
+def _grid_size(args, dim):
+    size = list(DEFAULT_SIZES[dim])
+    for i, v in enumerate((args.nx, args.ny, args.nz)[:dim]):
+        if v:
+            size[i] = v
+    return tuple(size)
+
+
+def _bench(args) -> int:
+    rows = []
+    scheme = args.variant.replace("-", "_")
+    for kernel in _kernels(args.kernel):
+        entry = catalog_get(kernel)
+        dim = entry.spec.dim
+        size = _grid_size(args, dim)
+        steps = args.steps or 64
+        grid = Grid.random(size, seed=args.seed)
+        opts = {"order": args.order} if entry.spec.dependence_kind == "gauss_seidel" and dim > 1 else {}
+        with config.using(fma=args.fma, depth=args.depth):
+            # device-resident time (plan API) for the device_ms column
+            plan = _native.Plan(entry.spec, size, config.current().native(order=args.order))
+            plan.upload(grid.data, grid.offset)
+            plan.run(steps)
+            plan.synchronize()
+            dev = []
+            for _ in range(args.reps):
+                plan.upload(grid.data, grid.offset)
+                plan.run(steps)
+                dev.append(plan.last_ms())
+            plan.close()
+            run_temporal(kernel, grid, steps, KernelVariant(scheme, entry.spec.dependence_kind != "jacobi"), **opts)
+            times = []
+            out = None
+            for _ in range(args.reps):
+                t0 = time.perf_counter()
+                out = run_temporal(kernel, grid, steps,
+                                   KernelVariant(scheme, entry.spec.dependence_kind != "jacobi"), **opts)
+                times.append(time.perf_counter() - t0)
+        pts = int(np.prod(size))
+        rate = pts * steps / statistics.median(times) / 1e9
+        check = fnv1a64(out.dump_bytes())
+        if args.dump:
+            out.dump(args.dump)
+        s3 = tuple(size) + (0, 0)
+        row = (f"{kernel},{args.variant},{dim},{s3[0]},{s3[1] or ''},{s3[2] or ''},{steps},1,,{args.reps},"
+               f"{rate:.6f},{check:016x},cuda-sm100a,{statistics.median(dev):.3f},{args.depth}")
+        rows.append(row)
+        print(row)
+    if args.csv:
+        try:
+            new = not open(args.csv).read(1)
+        except OSError:
+            new = True
+        with open(args.csv, "a") as fh:
+            if new:
+                fh.write(CSV_HEADER + "," + CSV_EXTRA + "\n")
+            fh.write("\n".join(rows) + "\n")
+    return 0
+
+
+_KNOWN = [  # reference test_baselines.py:17-21, 32-36
+    ("heat1d", np.arange(1.0, 9.0), [1.0, 2.0, 3.0, 4.0, 5.0, 6.0, 7.0, 5.75]),
+    ("gs1d", np.ones(3), [0.75, 0.9375, 0.734375]),
+]
+
+
+def _verify(args) -> int:
+    from .kernels._common import execute
+
+    ok = True
+    for kernel, values, want in _KNOWN:
+        got = execute(catalog_get(kernel).spec, Grid.from_array(values, halo=1), 1).interior.tolist()
+        good = got == want
+        ok &= good
+        print(f"  {'PASS' if good else 'FAIL'} known answer {kernel}: {got}")
+    cells = default_matrix(cells_per_kernel=args.cells, kernels=_kernels(args.kernel))
+    t0 = time.time()
+    bad = 0
+    for cell in cells:
+        entry = catalog_get(cell.kernel)
+        g = Grid.random(cell.size, seed=cell.seed)
+        opts = {"order": args.order} if entry.spec.dependence_kind == "gauss_seidel" and entry.spec.dim > 1 else {}
+        fast = execute(entry.spec, g, cell.steps, algo="auto", **opts)
+        slow = execute(entry.spec, g, cell.steps, algo="naive", **opts)
+        if not np.array_equal(fast.interior, slow.interior):
+            bad += 1
+            pos = tuple(int(i) for i in np.argwhere(fast.interior != slow.interior)[0])
+            print(f"  FAIL {cell.describe()} first divergence {pos}")
+    ok &= bad == 0
+    print(f"equivalence (blocked vs naive, GPU): {len(cells)} cells, {'PASS' if bad == 0 else 'FAIL'} "
+          f"({time.time() - t0:.1f}s)")
+    print("verify:", "PASS" if ok else "FAIL")
+    return 0 if ok else 1
+
+
+def main(argv=None) -> int:
+    parser = build_parser()
+    args = parser.parse_args(argv)
+    args = _apply_config(args, sys.argv[1:] if argv is None else argv)
+    if args.mode == "verify":
+        return _verify(args)
+    return _bench(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

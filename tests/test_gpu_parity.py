@@ -232,3 +232,20 @@ def test_slab_decomposition_emulated_ranks(cuda_ready):
                     parts.append(view[depth: depth + lay.n_own].cpu().numpy())
                 got = np.concatenate(parts, 0)
                 assert np.array_equal(got, want.interior), (kernel, world, depth)
+
+
+def test_cli_bench_and_verify(cuda_ready, tmp_path):
+    """The reference-CLI mirror: CSV row with the reference schema whose FNV
+    checksum equals the oracle result's; verify mode passes."""
+    from paper_2010_04868_b200 import cli
+    from paper_2010_04868_b200.grid import fnv1a64
+
+    csv = tmp_path / "rows.csv"
+    assert cli.main(["--mode", "bench", "--kernel", "heat2d", "--nx", "200", "--ny", "150", "--t", "9",
+                     "--reps", "2", "--csv", str(csv)]) == 0
+    header, row = csv.read_text().strip().splitlines()
+    assert header.startswith(cli.CSV_HEADER)
+    fields = row.split(",")
+    want = cref.scalar_reference(get("heat2d").spec, Grid.random((200, 150), seed=0), 9)
+    assert fields[11] == f"{fnv1a64(want.dump_bytes()):016x}"
+    assert cli.main(["--mode", "verify", "--kernel", "gs2d9p", "--cells", "3"]) == 0

@@ -197,3 +197,14 @@ def test_default_matrix_classes():
         e = get(k)
         assert {0, 1, 2, 3} <= {c.steps % e.vl for c in sub}
         assert {0, 1, e.vl - 1} & {c.size[0] % (4 * e.s * e.vl) for c in sub}
+
+
+def test_cli_parser_and_config(tmp_path):
+    from paper_2010_04868_b200.cli import CSV_HEADER, _apply_config, build_parser
+
+    assert CSV_HEADER == "kernel,variant,dim,nx,ny,nz,t,threads,tile,reps,gstencils_per_s,checksum"  # cli.py:39
+    cfg = tmp_path / "c.json"
+    cfg.write_text('{"t": 7, "nx": 300, "reps": 2}')
+    argv = ["--mode", "bench", "--kernel", "heat1d", "--nx", "500", "--config", str(cfg)]
+    args = _apply_config(build_parser().parse_args(argv), argv)
+    assert args.steps == 7 and args.nx == 500 and args.reps == 2  # explicit flags win

@@ -69,6 +69,62 @@ __device__ __forceinline__ double tap_next(double c, double v, double acc) {
 }
 __device__ __forceinline__ double tap_first(double c, double v) { return __dmul_rn(c, v); }
 
+// ---- mbarriers and bulk (TMA) copies -------------------------------------
+__device__ __forceinline__ unsigned smaddr(const void* q) { return (unsigned)__cvta_generic_to_shared(q); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smaddr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(smaddr(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
+  unsigned ok;
+  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+               : "=r"(ok) : "r"(smaddr(b)), "r"(parity), "r"(20000u) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  unsigned n = 0;
+  while (!mbar_try(b, parity))
+    if (++n > (1u << 18)) __trap();  // watchdog (~5 s of suspended waits)
+}
+
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(smaddr(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// global -> shared bulk copy (16-byte aligned, bytes % 16 == 0), completion
+// counted as transaction bytes on mbarrier `b`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smaddr(dst)), "l"(src), "r"(bytes), "r"(smaddr(b)) : "memory");
+}
+
+// Variants whose control flow stays inside the asm, so the compiler's
+// divergence analysis still sees warp-uniform code (keeps shuffles free of
+// BRA.DIV scaffolding).  `leader`: only that thread issues.
+__device__ __forceinline__ void mbar_wait_uniform(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{ .reg .pred p; .reg .u32 n; mov.u32 n, 0;\n"
+      "TVS_WAIT: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 100000;\n"
+      "@p bra TVS_DONE; add.u32 n, n, 1; setp.lt.u32 p, n, 1000000; @p bra TVS_WAIT; trap;\n"
+      "TVS_DONE: }" ::"r"(smaddr(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_leader(bool leader, void* dst, const void* src, unsigned bytes,
+                                                unsigned long long* b) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.u32 p, %4, 0;\n"
+      "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n"
+      "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3]; }"
+      ::"r"(smaddr(dst)), "l"(src), "r"(bytes), "r"(smaddr(b)), "r"((unsigned)leader) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(bool leader, unsigned long long* b) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %1, 0; @p mbarrier.arrive.shared::cta.b64 _, [%0]; }"
+               ::"r"(smaddr(b)), "r"((unsigned)leader) : "memory");
+}
+
 // ---- error plumbing (host) -------------------------------------------------
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);

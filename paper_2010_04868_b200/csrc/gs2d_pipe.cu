@@ -127,25 +127,6 @@ __device__ __forceinline__ void st_rel_gpu(unsigned long long* p, unsigned long 
 // order; completion of chunk m is phase (m >> 3) of barrier bar[X][m & 7].
 // Every waiter is at most 5 chunks behind / 3 ahead of the warp it waits on
 // (RAW/WAR bounds), so a slot never wraps under a waiter (no ABA).
-__device__ __forceinline__ unsigned smaddr(const void* q) { return (unsigned)__cvta_generic_to_shared(q); }
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smaddr(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
-  asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(smaddr(b)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
-  unsigned ok;
-  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
-               : "=r"(ok) : "r"(smaddr(b)), "r"(parity), "r"(20000u) : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  unsigned n = 0;
-  while (!mbar_try(b, parity))
-    if (++n > (1u << 18)) __trap();  // watchdog (~5 s of suspended waits)
-}
-
 // Wait until a shared-memory progress counter reaches `v`; back off so the
 // spinning warps do not starve the IO warp of issue slots.
 __device__ __forceinline__ void wait_ge(const int* p, int v) {

@@ -27,9 +27,12 @@
 
 namespace tvs {
 
-constexpr int kMaxD2 = 12;     // deepest temporal block instantiated (P = 2)
-constexpr int kWarps2 = 4;     // warps per block
-constexpr int kRowsSeg = 256;  // output rows per warp task
+constexpr int kMaxD2 = 12;     // deepest temporal block instantiated (P = 4 up to D = 8, P = 2 above)
+constexpr int kWarps2 = 1;     // warps per block (task = blockIdx.x: warp-uniform control flow)
+#ifndef J2D_SEG
+#define J2D_SEG 256
+#endif
+constexpr int kRowsSeg = J2D_SEG;  // output rows per warp task
 
 constexpr unsigned kStar5 = (1u << 1) | (1u << 3) | (1u << 4) | (1u << 5) | (1u << 7);
 constexpr unsigned kBox9 = 0x1FFu;
@@ -89,7 +92,7 @@ __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __
   const double(&c)[9] = cf.c;          // constant-bank operands
 
   const int lane = threadIdx.x & 31;
-  const int64_t task = (int64_t)blockIdx.x * kWarps2 + (threadIdx.x >> 5);
+  const int64_t task = kWarps2 == 1 ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * kWarps2 + (threadIdx.x >> 5);
   if (task >= n_tasks) return;
   const int64_t strip = task % n_strips, seg = task / n_strips;
   const int col0 = (int)(-D + strip * U);  // first column of the strip
@@ -123,55 +126,62 @@ __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __
 #pragma unroll
     for (int p = 0; p < kP2; ++p) r[p] = (row_ok && !(col_out >> p & 1u)) ? __ldg(rp + p) : bnd;
   };
-  double pre[PF][kP2];
   const int m_begin = r0 - D, m_end = r1 + D;
-#pragma unroll
-  for (int k = 0; k < PF; ++k) load_row(m_begin + k, pre[k]);
-
   // One stream step: level-0 row m enters, level-D row m-D leaves.  EVEN
-  // selects which accumulator set finishes (role swap every step).
+  // selects which accumulator set finishes (role swap every step).  The
+  // interior/boundary choice is made once per step (warp-uniform), so the
+  // interior body is straight-line code with no selects or merge copies.
   auto step = [&](int m, double (&row)[kP2], auto even_tag) {
     constexpr bool EVEN = decltype(even_tag)::value;
-    double in[kP2 + 2];
+    auto body = [&](auto fast_tag) {
+      constexpr bool FAST = decltype(fast_tag)::value;
+      double in[kP2 + 2];
 #pragma unroll
-    for (int p = 0; p < kP2; ++p) in[p + 1] = row[p];
-    in[0] = __shfl_up_sync(0xffffffffu, in[kP2], 1);
-    in[kP2 + 1] = __shfl_down_sync(0xffffffffu, in[1], 1);
+      for (int p = 0; p < kP2; ++p) in[p + 1] = row[p];
+      in[0] = __shfl_up_sync(0xffffffffu, in[kP2], 1);
+      in[kP2 + 1] = __shfl_down_sync(0xffffffffu, in[1], 1);
+#pragma unroll
+      for (int l = 0; l < D; ++l) {
+        double out[kP2];
+        if constexpr (EVEN)
+          level_row<MASK, FMA, kP2>(B[l], A[l], in, c, out);
+        else
+          level_row<MASK, FMA, kP2>(A[l], B[l], in, c, out);
+        if constexpr (FAST) {
+#pragma unroll
+          for (int p = 0; p < kP2; ++p) in[p + 1] = out[p];
+        } else {
+          const int gq = m - l - 1 + a0;
+          const bool pin_row = gq < 0 || gq >= ag;
+#pragma unroll
+          for (int p = 0; p < kP2; ++p) in[p + 1] = (pin_row || (col_out >> p & 1u)) ? bnd : out[p];
+        }
+        if (l + 1 < D) {
+          in[0] = __shfl_up_sync(0xffffffffu, in[kP2], 1);
+          in[kP2 + 1] = __shfl_down_sync(0xffffffffu, in[1], 1);
+        }
+      }
+      const int q = m - D;  // level-D row leaving
+      if (q >= r0 && q < r1) {
+        double* wp = dst + origin + (int64_t)q * g.s0 + cl;
+#pragma unroll
+        for (int p = 0; p < kP2; ++p)
+          if (store_mask >> p & 1u) wp[p] = in[p + 1];
+      }
+    };
     // rows m-1-l (l < D) produced this step; all inside the domain?
     const bool rows_in = m - D + a0 >= 0 && m - 1 + a0 < ag;
-    const bool fast = rows_in && !any_col_out;
-#pragma unroll
-    for (int l = 0; l < D; ++l) {
-      double out[kP2];
-      if constexpr (EVEN)
-        level_row<MASK, FMA, kP2>(B[l], A[l], in, c, out);
-      else
-        level_row<MASK, FMA, kP2>(A[l], B[l], in, c, out);
-      if (fast) {
-#pragma unroll
-        for (int p = 0; p < kP2; ++p) in[p + 1] = out[p];
-      } else {
-        const int gq = m - l - 1 + a0;
-        const bool pin_row = gq < 0 || gq >= ag;
-#pragma unroll
-        for (int p = 0; p < kP2; ++p) in[p + 1] = (pin_row || (col_out >> p & 1u)) ? bnd : out[p];
-      }
-      if (l + 1 < D) {
-        in[0] = __shfl_up_sync(0xffffffffu, in[kP2], 1);
-        in[kP2 + 1] = __shfl_down_sync(0xffffffffu, in[1], 1);
-      }
-    }
-    const int q = m - D;  // level-D row leaving
-    if (q >= r0 && q < r1) {
-      double* wp = dst + origin + (int64_t)q * g.s0 + cl;
-#pragma unroll
-      for (int p = 0; p < kP2; ++p)
-        if (store_mask >> p & 1u) wp[p] = in[p + 1];
-    }
+    if (rows_in && !any_col_out)
+      body(std::true_type{});
+    else
+      body(std::false_type{});
   };
 
   using T0 = std::true_type;
   using T1 = std::false_type;
+  double pre[PF][kP2];
+#pragma unroll
+  for (int k = 0; k < PF; ++k) load_row(m_begin + k, pre[k]);
   int m = m_begin;
   for (; m + PF <= m_end; m += PF) {
 #pragma unroll
@@ -187,7 +197,7 @@ __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __
     }
   }
   // tail (fewer than PF rows left); parity continues from the unrolled loop
-  for (int k = 0; m < m_end; ++m, ++k) {
+  for (; m < m_end; ++m) {
     double row[kP2];
 #pragma unroll
     for (int p = 0; p < kP2; ++p) row[p] = pre[0][p];
@@ -225,7 +235,7 @@ bool jacobi2d_blocked_supported(const tvs_stencil& st) {
 }
 
 int jacobi2d_max_depth() { return kMaxD2; }
-int jacobi2d_default_depth() { return 4; }  // measured best at P=4 (register pressure above)
+int jacobi2d_default_depth() { return 8; }  // measured best (config 3: D=4 1235, 6 1540, 8 1593 GSt/s)
 
 template <unsigned MASK, int D, int P>
 static void launch2d_d(bool fma, unsigned blocks, cudaStream_t s, const double* src, double* dst, const Geo& geo,
@@ -236,11 +246,10 @@ static void launch2d_d(bool fma, unsigned blocks, cudaStream_t s, const double* 
     jacobi2d_kernel<MASK, D, false, P><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt);
 }
 
-
 template <unsigned MASK, int D>
 static void launch2d_one(bool fma, cudaStream_t s, const double* src, double* dst, const Geo& geo, int64_t origin,
                          const Coeff9& cf, double bnd) {
-  constexpr int P = D <= 4 ? 4 : 2;
+  constexpr int P = D <= 8 ? 4 : 2;
   const int64_t U = 32 * P - 2 * D;
   const int64_t ns = (geo.e1 + U - 1) / U;
   const int64_t nseg = (geo.e0 + kRowsSeg - 1) / kRowsSeg;

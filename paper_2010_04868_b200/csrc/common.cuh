@@ -106,10 +106,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // divergence analysis still sees warp-uniform code (keeps shuffles free of
 // BRA.DIV scaffolding).  `leader`: only that thread issues.
 __device__ __forceinline__ void mbar_wait_uniform(unsigned long long* b, unsigned parity) {
+  // watchdog: trap after ~2^34 cycles (~9 s) without the phase completing
   asm volatile(
-      "{ .reg .pred p; .reg .u32 n; mov.u32 n, 0;\n"
-      "TVS_WAIT: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 100000;\n"
-      "@p bra TVS_DONE; add.u32 n, n, 1; setp.lt.u32 p, n, 1000000; @p bra TVS_WAIT; trap;\n"
+      "{ .reg .pred p; .reg .u64 t0, t1; mov.u64 t0, %%clock64;\n"
+      "TVS_WAIT: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+      "@p bra TVS_DONE; mov.u64 t1, %%clock64; sub.u64 t1, t1, t0; setp.lt.u64 p, t1, 17179869184;\n"
+      "@p bra TVS_WAIT; trap;\n"
       "TVS_DONE: }" ::"r"(smaddr(b)), "r"(parity) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s_leader(bool leader, void* dst, const void* src, unsigned bytes,

@@ -19,13 +19,34 @@
 // path is DMUL->DADD->DADD = 3 x 8 cycles per position, so one sweep's worth
 // of positions streams through all T lanes with an (N + ~4T) step latency.
 //
-// Lane 31 of a warp feeds lane 0 of the next warp through a shared-memory
-// ring guarded by release/acquire progress counters; the last warp of a block
-// publishes its sweep to a global buffer (release/acquire at GPU scope) that
-// the next block's first warp streams in.  Blocks take tickets in start
-// order and only wait on lower tickets, so the launch is deadlock-free for
-// any grid size.  Sweeps beyond T are identity lanes (they forward their
-// old value), so the last lane always emits sweep T.
+// Data movement and synchronisation are kept off the compute warps:
+//
+//   * a LOADER warp streams the block's input (the grid for block 0, block
+//     b-1's published sweep otherwise) into compute warp 0's ring;
+//   * compute warp w's lane 31 writes its sweep into warp w+1's ring (the
+//     last compute warp into a staging ring);
+//   * a FLUSHER warp copies the staging ring to global memory and publishes
+//     progress (GPU-scope release) for block b+1's loader.
+//
+// Everything advances in chunks of kCH = 128 positions.  Completion of chunk
+// k by warp X is phase k / kNB of mbarrier bar[X][k % kNB] (hardware-suspended
+// waits; no fences or acquire spins on the compute warps).  Ring bounds
+// (R = 4 chunks of positions per ring):
+//   compute w at chunk c needs positions < min(n, (c+1)*kCH - 1), complete
+//     once warp w-1 (lane 31 lags 96 positions) finished chunk
+//     ceil((need + 96) / kCH) - 1 <= c + 1;
+//   writing positions up to (c+1)*kCH - 97 into a ring overwrites position
+//     p - R, consumed once the reader finished chunk c - 4  (4 * 128 < R + 96);
+//   the loader's chunk k overwrites chunk k - 4, consumed once warp 0 finished
+//     chunk k - 3.
+// A waiter is never more than 5 chunks away from the phase it waits for, so
+// kNB = 8 barrier slots never alias.  Blocks take tickets in start order and
+// only wait on lower tickets, so the launch is deadlock-free for any grid
+// size.  The last block runs only as many warps as it has sweeps, and its last
+// warp emits sweep T from lane (T-1) % 32 (lag 3 * (lane+1) <= 96, so every
+// bound above stays conservative; its staging writes are reused once the
+// flusher finished chunk c - 3).  No lane ever selects between sweep and
+// identity, so the loop-carried chain is the same in every warp.
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
@@ -34,21 +55,19 @@
 
 namespace tvs {
 
-constexpr int kGsLag = 3;            // position lag between adjacent lanes
-constexpr int kGsRing = 512;         // per-warp input ring (positions)
-constexpr int kGsMaxBlocks = 64;     // sweeps per launch <= 64 * 128
-constexpr int kGsPubChunks = 4;      // cross-block publication every 4 x 32 positions
-constexpr int kGsPrefetch = 4;       // warp-0 input prefetch distance (chunks)
-static_assert(kGsLag * 32 % 32 == 0, "lane-31 output chunks must align");
+constexpr int kGsLag = 3;                 // position lag between adjacent lanes
+constexpr int kCH = 128;                  // positions per chunk
+constexpr int kSub = kCH / 32;            // 32-position unrolled sub-chunks per chunk
+constexpr int kRingCh = 4;                // ring = 4 chunks
+constexpr int kGsRing = kCH * kRingCh;    // ring positions (power of two)
+constexpr int kNB = 8;                    // mbarrier ring per warp
+constexpr int kWar = 4;                   // ring reuse: reader finished chunk c - kWar
+constexpr int kGsMaxBlocks = 64;          // sweeps per launch <= 64 * 32 * kGsWarps
+constexpr int kShiftLane31 = kGsLag * 32; // lane 31's position lag (96)
+static_assert((kGsRing & (kGsRing - 1)) == 0, "ring must be a power of two");
+static_assert(kWar * kCH < kGsRing + kShiftLane31, "ring reuse bound");
+static_assert(kCH >= kShiftLane31, "consumer waits at most one chunk ahead");
 
-__device__ __forceinline__ int ld_acquire_cta(const int* p) {
-  int v;
-  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_cta(int* p, int v) {
-  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
-}
 __device__ __forceinline__ long long ld_acquire_gpu(const long long* p) {
   long long v;
   asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -80,156 +99,166 @@ __device__ __forceinline__ double gs_taps(double L, double C, double R, double w
 }
 
 template <unsigned MASK, int kGsWarps>
-__global__ void __launch_bounds__(kGsWarps * 32, 1) gs1d_kernel(Gs1dArgs p) {
-  // ring[w]: input positions of warp w; ring[kGsWarps]: staging of the last
-  // warp's sweep before it is flushed to global memory.
-  __shared__ double ring[kGsWarps + 1][kGsRing];
-  __shared__ int prod[kGsWarps], cons[kGsWarps + 1];
+__global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p) {
+  constexpr int kLoader = kGsWarps, kFlusher = kGsWarps + 1;
+  // ring[w]: input positions of compute warp w; ring[kGsWarps]: staging of
+  // the last compute warp's sweep before the flusher writes it out.
+  __shared__ __align__(16) double ring[kGsWarps + 1][kGsRing];
+  // bar[x][k % kNB]: chunk k done by compute warp x (x < kGsWarps), loaded
+  // (x = kLoader) or flushed (x = kFlusher)
+  __shared__ __align__(8) unsigned long long bar[kGsWarps + 2][kNB];
   __shared__ int s_ticket;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_ticket = atomicAdd(p.ticket, 1);
-  if (threadIdx.x < kGsWarps) prod[threadIdx.x] = 0;
-  if (threadIdx.x <= kGsWarps) cons[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    s_ticket = atomicAdd(p.ticket, 1);
+    for (int x = 0; x < kGsWarps + 2; ++x)
+      for (int k = 0; k < kNB; ++k) mbar_init(&bar[x][k], 1);
+    fence_mbar_init();
+  }
   __syncthreads();
   const int b = s_ticket;
   const int n = (int)p.n;  // host guarantees n < 2^30
   const double bnd = p.bnd;
-  const long long q = ((long long)b * kGsWarps + w) * 32 + lane;  // this lane's sweep
-  const bool real = q < p.sweeps;
   const bool last_block = b == p.nblocks - 1;
-  const double* lsrc = b == 0 ? p.a : p.gbuf + (long long)(b - 1) * p.n;
-  double* odst = last_block ? p.a : p.gbuf + (long long)b * p.n;
-  const int nch = (n + 31) / 32 + kGsLag + 1;
-  const int lane_off = kGsLag * (lane + 1);
-  const double* rin = ring[w];
-  double* rout = ring[w + 1];
-  const bool writer = lane == 31;
-  const bool warp_real = __all_sync(0xffffffffu, real);
-
-  auto wait_upstream = [&](int need) {  // block b-1 published >= need positions
-    if (b == 0) return;
-    if (lane == 0) {
-      long long want = need;
-      SpinGuard sg;
-      while (ld_acquire_gpu(p.gprog + b - 1) < want) {
-        __nanosleep(32);
-        sg.tick();
-      }
-    }
+  const int nch = (n + kShiftLane31 + kCH - 1) / kCH;  // lane 31 finishes position n-1 in chunk nch-1
+  // compute warps with sweeps in this block; the last one feeds the flusher
+  const int nw = last_block ? (int)((p.sweeps - (long long)b * kGsWarps * 32 + 31) / 32) : kGsWarps;
+  auto done = [&](int x, int k) { mbar_wait_uniform(&bar[x][k % kNB], (unsigned)(k / kNB) & 1u); };
+  auto signal = [&](int x, int k) {  // all lanes past their work on chunk k
     __syncwarp();
+    mbar_arrive_leader(lane == 0, &bar[x][k % kNB]);
   };
 
-  double L = bnd, u0 = bnd, u1 = bnd, out = bnd;
-  // warp 0 streams its input (the grid, or block b-1's sweep) into ring[0]
-  // with cp.async, kGsPrefetch chunks ahead of consumption
-  auto load_chunk = [&](int c) {
-    const int x = c * 32 + lane;
-    wait_upstream(min(((c * 32) / (32 * kGsPubChunks) + 1) * 32 * kGsPubChunks, n));
-    double* slot = &ring[0][x & (kGsRing - 1)];
-    if (x < n) {
-      const unsigned sa = (unsigned)__cvta_generic_to_shared(slot);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(lsrc + x));
-    } else {
-      *slot = bnd;
+  if (w == kLoader) {
+    // block b-1's published prefix (or the grid) -> ring[0]
+    const double* src = b == 0 ? p.a : p.gbuf + (long long)(b - 1) * p.n;
+    for (int k = 0; k < nch; ++k) {
+      if (k >= kWar - 1) done(0, k - (kWar - 1));
+      const int lo = k * kCH, hi = min(n, lo + kCH);
+      if (b > 0 && lo < n) {
+        if (lane == 0) {
+          SpinGuard sg;
+          while (ld_acquire_gpu(p.gprog + b - 1) < hi) {
+            __nanosleep(64);
+            sg.tick();
+          }
+        }
+        __syncwarp();
+      }
+      double v[kSub];
+#pragma unroll
+      for (int s = 0; s < kSub; ++s) {
+        const int x = lo + s * 32 + lane;
+        v[s] = x < hi ? __ldcg(src + x) : bnd;
+      }
+#pragma unroll
+      for (int s = 0; s < kSub; ++s) ring[0][(lo + s * 32 + lane) & (kGsRing - 1)] = v[s];
+      signal(kLoader, k);
     }
-    asm volatile("cp.async.commit_group;\n" ::);
-  };
-  if (w == 0) {
-#pragma unroll 1
-    for (int c = 0; c < kGsPrefetch; ++c) load_chunk(c);
+    return;
+  }
+  if (w == kFlusher) {
+    // staging ring -> grid (last block) or this block's sweep buffer
+    double* dst = last_block ? p.a : p.gbuf + (long long)b * p.n;
+    for (int k = 0; k < nch; ++k) {
+      done(nw - 1, k);
+      const int lo = max(0, k * kCH - kShiftLane31), hi = min(n, (k + 1) * kCH - kShiftLane31);
+      for (int x = lo + lane; x < hi; x += 32) dst[x] = ring[kGsWarps][x & (kGsRing - 1)];
+      if (!last_block) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_gpu(p.gprog + b, hi);
+      }
+      signal(kFlusher, k);
+    }
+    return;
   }
 
+  // ---- compute warps: lane k of warp w runs sweep 32 * (b * kGsWarps + w) + k ----
+  if (w >= nw) return;
+  const bool to_staging = w == nw - 1;
+  const int wlane = last_block && to_staging ? (int)((p.sweeps - 1) % 32) : 31;  // emits this warp's sweep
+  const int wlag = kGsLag * (wlane + 1);
+  const int lane_off = kGsLag * (lane + 1);
+  const double* rin = ring[w];
+  double* rout = to_staging ? ring[kGsWarps] : ring[w + 1];
+  const bool writer = lane == wlane;
+  double L = bnd, u0 = bnd, u1 = bnd, out = bnd;
+
   for (int ch = 0; ch < nch; ++ch) {
-    const int jb = ch * 32;
+    const int jb0 = ch * kCH;
+    // inputs: positions < min(n, jb0 + kCH - 1)
     if (w == 0) {
-      load_chunk(ch + kGsPrefetch);  // (chunks past n just store bnd)
-      asm volatile("cp.async.wait_group %0;\n" ::"n"(kGsPrefetch));  // chunk ch landed
-      __syncwarp();
+      done(kLoader, ch);
     } else {
-      const int need = min(jb + 31, n);
-      SpinGuard sg;
-      while (ld_acquire_cta(&prod[w]) < need) sg.tick();
+      const int need = min(n, jb0 + kCH - 1);
+      done(w - 1, (need + kShiftLane31 + kCH - 1) / kCH - 1);
     }
-    {  // ring space in the consumer of my lane-31 stream: positions up to jb-65
-      const int lim = jb - 65 - kGsRing;
-      SpinGuard sg;
-      while (ld_acquire_cta(&cons[w + 1]) <= lim) sg.tick();
+    // ring space for the positions this chunk writes
+    if (to_staging) {
+      if (ch >= kWar - 1) done(kFlusher, ch - (kWar - 1));
+    } else if (ch >= kWar) {
+      done(w + 1, ch - kWar);
     }
-    // steady chunk: every lane real and every position of the chunk inside
-    // [0, n) — no selects on the DMUL->DADD->DADD chain
-    const bool steady = warp_real && jb - kGsLag * 32 >= 0 && jb + 31 - kGsLag < n;
-    if (steady && MASK == 7u) {
-      // full 3-tap stencil: the products w1*C and w2*R are formed as soon as
-      // their operands arrive, so the loop-carried chain is exactly
-      // L -> DMUL -> DADD -> DADD (bit-identical: same products, same adds)
-      double pa = __dmul_rn(p.w1, u0), pb = __dmul_rn(p.w2, u1);
+#pragma unroll 1
+    for (int sub = 0; sub < kSub; ++sub) {
+      const int jb = jb0 + sub * 32;
+      // steady sub-chunk: every position of the chunk inside [0, n) — no
+      // selects on the DMUL->DADD->DADD chain
+      const bool steady = jb - kGsLag * 32 >= 0 && jb + 31 - kGsLag < n;
+      if (steady && MASK == 7u) {
+        // full 3-tap stencil: the products w1*C and w2*R are formed as soon as
+        // their operands arrive, so the loop-carried chain is exactly
+        // L -> DMUL -> DADD -> DADD (bit-identical: same products, same adds)
+        double pa = __dmul_rn(p.w1, u0), pb = __dmul_rn(p.w2, u1);
 #pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        const int j = jb + u;
-        const double sh = __shfl_up_sync(0xffffffffu, out, 1);
-        const double rv = rin[(j - 1) & (kGsRing - 1)];  // same address for all lanes: broadcast
-        const double sv = lane == 0 ? rv : sh;
-        out = __dadd_rn(pb, __dadd_rn(pa, __dmul_rn(p.w0, L)));
-        pa = __dmul_rn(p.w1, u1);  // next iteration's C is this iteration's R
-        pb = __dmul_rn(p.w2, sv);  // next iteration's R just arrived
-        L = out;
-        u0 = u1;
-        u1 = sv;
-        const int po = j - kGsLag * 32;
-        if (writer) rout[po & (kGsRing - 1)] = out;
-      }
-    } else if (steady) {
+        for (int u = 0; u < 32; ++u) {
+          const int j = jb + u;
+          const double sh = __shfl_up_sync(0xffffffffu, out, 1);
+          const double rv = rin[(j - 1) & (kGsRing - 1)];  // same address for all lanes: broadcast
+          const double sv = lane == 0 ? rv : sh;
+          out = __dadd_rn(pb, __dadd_rn(pa, __dmul_rn(p.w0, L)));
+          pa = __dmul_rn(p.w1, u1);  // next iteration's C is this iteration's R
+          pb = __dmul_rn(p.w2, sv);  // next iteration's R just arrived
+          L = out;
+          u0 = u1;
+          u1 = sv;
+          if (writer) rout[(j - wlag) & (kGsRing - 1)] = out;
+        }
+      } else if (steady) {
 #pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        const int j = jb + u;
-        const double sh = __shfl_up_sync(0xffffffffu, out, 1);
-        const double rv = rin[(j - 1) & (kGsRing - 1)];  // same address for all lanes: broadcast
-        const double sv = lane == 0 ? rv : sh;
-        out = gs_taps<MASK>(L, u0, u1, p.w0, p.w1, p.w2);
-        L = out;
-        u0 = u1;
-        u1 = sv;
-        const int po = j - kGsLag * 32;
-        if (writer) rout[po & (kGsRing - 1)] = out;
-      }
-    } else {
+        for (int u = 0; u < 32; ++u) {
+          const int j = jb + u;
+          const double sh = __shfl_up_sync(0xffffffffu, out, 1);
+          const double rv = rin[(j - 1) & (kGsRing - 1)];
+          const double sv = lane == 0 ? rv : sh;
+          out = gs_taps<MASK>(L, u0, u1, p.w0, p.w1, p.w2);
+          L = out;
+          u0 = u1;
+          u1 = sv;
+          if (writer) rout[(j - wlag) & (kGsRing - 1)] = out;
+        }
+      } else {
 #pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        const int j = jb + u;
-        const double sh = __shfl_up_sync(0xffffffffu, out, 1);
-        const int pos = j - 1;
-        const double rv = rin[pos & (kGsRing - 1)];
-        const double up = (unsigned)pos < (unsigned)n ? rv : bnd;
-        const double sv = lane == 0 ? up : sh;
-        const int i = j - lane_off;
-        const double v = gs_taps<MASK>(L, u0, u1, p.w0, p.w1, p.w2);
-        out = (unsigned)i < (unsigned)n ? (real ? v : u0) : bnd;
-        L = out;
-        u0 = u1;
-        u1 = sv;
-        const int po = j - kGsLag * 32;
-        if (writer && (unsigned)po < (unsigned)n) rout[po & (kGsRing - 1)] = out;
-      }
-    }
-    __syncwarp();
-    if (writer && w + 1 < kGsWarps) st_release_cta(&prod[w + 1], max(0, min(jb + 32 - kGsLag * 32, n)));
-    if (lane == 0 && w > 0) st_release_cta(&cons[w], jb + 31);
-    if (w == kGsWarps - 1) {
-      const int pc = ch - kGsLag;  // position chunk completed by lane 31
-      if (pc >= 0 && pc * 32 < n) {
-        const int x = pc * 32 + lane;
-        if (x < n) odst[x] = rout[x & (kGsRing - 1)];
-        __syncwarp();
-        if (lane == 0) st_release_cta(&cons[kGsWarps], x + 1 - lane);  // staging slots consumed
-        const bool batch_end = ((pc + 1) % kGsPubChunks == 0) || (pc + 1) * 32 >= n;
-        if (!last_block && batch_end) {
-          __threadfence();
-          __syncwarp();
-          if (lane == 0) st_release_gpu(p.gprog + b, min((pc + 1) * 32, n));
+        for (int u = 0; u < 32; ++u) {
+          const int j = jb + u;
+          const double sh = __shfl_up_sync(0xffffffffu, out, 1);
+          const int pos = j - 1;
+          const double rv = rin[pos & (kGsRing - 1)];
+          const double up = (unsigned)pos < (unsigned)n ? rv : bnd;
+          const double sv = lane == 0 ? up : sh;
+          const int i = j - lane_off;
+          const double v = gs_taps<MASK>(L, u0, u1, p.w0, p.w1, p.w2);
+          out = (unsigned)i < (unsigned)n ? v : bnd;
+          L = out;
+          u0 = u1;
+          u1 = sv;
+          const int po = j - wlag;
+          if (writer && (unsigned)po < (unsigned)n) rout[po & (kGsRing - 1)] = out;
         }
       }
-      __syncwarp();
     }
+    signal(w, ch);
   }
 }
 
@@ -255,8 +284,8 @@ int gs1d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, in
   if (n >= (1ll << 30)) return fail(TVS_ERR_UNSUPPORTED, "gs1d_pipeline: N >= 2^30");
   static const int warps = [] {
     const char* e = getenv("TVS_GS1D_WARPS");
-    const int v = e ? atoi(e) : 4;
-    return (v == 1 || v == 2 || v == 4) ? v : 4;
+    const int v = e ? atoi(e) : 2;  // measured: 2 compute warps/block >= 4 (config 2)
+    return (v == 1 || v == 2 || v == 4) ? v : 2;
   }();
   const long long per_launch = (long long)kGsMaxBlocks * warps * 32;
   const int max_blocks = (int)std::min<long long>((steps + warps * 32 - 1) / (warps * 32), kGsMaxBlocks);
@@ -278,13 +307,13 @@ int gs1d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, in
   auto launch = [&](auto warps_tag) {
     constexpr int W = decltype(warps_tag)::value;
     switch (mask) {
-      case 1: gs1d_kernel<1, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
-      case 2: gs1d_kernel<2, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
-      case 3: gs1d_kernel<3, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
-      case 4: gs1d_kernel<4, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
-      case 5: gs1d_kernel<5, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
-      case 6: gs1d_kernel<6, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
-      default: gs1d_kernel<7, W><<<a.nblocks, W * 32, 0, s>>>(a); break;
+      case 1: gs1d_kernel<1, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
+      case 2: gs1d_kernel<2, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
+      case 3: gs1d_kernel<3, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
+      case 4: gs1d_kernel<4, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
+      case 5: gs1d_kernel<5, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
+      case 6: gs1d_kernel<6, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
+      default: gs1d_kernel<7, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
     }
   };
   for (long long done = 0; done < steps; done += per_launch) {

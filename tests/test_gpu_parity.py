@@ -89,6 +89,19 @@ def test_gs1d_pipeline_sizes(cuda_ready, n, steps):
         assert np.array_equal(got.interior, want.interior), (kernel, n, steps)
 
 
+@pytest.mark.parametrize("n,steps", [(1, 1), (2, 33), (95, 31), (96, 32), (97, 127), (128, 128), (129, 129),
+                                     (383, 97), (384, 1), (385, 159), (511, 256), (512, 385), (513, 1000),
+                                     (1000, 64 * 4 * 32 + 5), (4099, 100)])
+def test_gs1d_chunk_and_writer_lane_edges(cuda_ready, n, steps):
+    """Sizes around the 128-position chunk / 512-position ring and sweep counts
+    that leave the last block with a partial warp (writer lane (T-1) % 32)."""
+    g = Grid.random((n,), seed=7 * n + steps, boundary=0.5 if n % 3 else -1.25)
+    spec = spec_for("gs1d_w343", g.boundary)
+    want = cref.scalar_reference(spec, g, steps)
+    got = execute(spec, g, steps)
+    assert np.array_equal(got.interior, want.interior), (n, steps)
+
+
 def test_gs1d_many_blocks_and_passes(cuda_ready):
     """> 64 blocks of 128 sweeps: exercises multi-launch passes and identity lanes."""
     g = Grid.random((300,), seed=9)

@@ -9,13 +9,14 @@
 // (min_space_stride = 2, model.py:171-193).  Here a lane *is* a sweep:
 //
 //   lane k of global warp g runs sweep q = 32*g + k and, at local step j,
-//   updates position i = j - 3*(k+1)   (lag 3 = min stride 2 + 1, so the
-//   value received by __shfl_up is consumed one step later and the 24-cycle
-//   shuffle stays off the critical path).
+//   updates position i = j - 4*(k+1)   (lag 4 = min stride 2 + 2: the value
+//   received by __shfl_up is old(i+3), first used as a product operand two
+//   steps later, so the 24-cycle shuffle can never land on the chain
+//   whatever order the compiler issues the step in).
 //
 // Per step each lane does one update (its new left neighbour is its own
 // previous result — the serial GS dependence — and its two old values are
-// what lane k-1 produced two and one steps earlier).  The only critical
+// what lane k-1 produced three and two steps earlier).  The only critical
 // path is DMUL->DADD->DADD = 3 x 8 cycles per position, so one sweep's worth
 // of positions streams through all T lanes with an (N + ~4T) step latency.
 //
@@ -31,19 +32,18 @@
 // Everything advances in chunks of kCH = 128 positions.  Completion of chunk
 // k by warp X is phase k / kNB of mbarrier bar[X][k % kNB] (hardware-suspended
 // waits; no fences or acquire spins on the compute warps).  Ring bounds
-// (R = 4 chunks of positions per ring):
+// (R = 4 chunks of positions per ring; lane 31 lags S = 128 positions):
 //   compute w at chunk c needs positions < min(n, (c+1)*kCH - 1), complete
-//     once warp w-1 (lane 31 lags 96 positions) finished chunk
-//     ceil((need + 96) / kCH) - 1 <= c + 1;
-//   writing positions up to (c+1)*kCH - 97 into a ring overwrites position
-//     p - R, consumed once the reader finished chunk c - 4  (4 * 128 < R + 96);
+//     once warp w-1 finished chunk ceil((need + S) / kCH) - 1 <= c + 1;
+//   writing positions up to (c+1)*kCH - 1 - S into a ring overwrites position
+//     p - R, consumed once the reader finished chunk c - 4  (4 * 128 < R + S);
 //   the loader's chunk k overwrites chunk k - 4, consumed once warp 0 finished
 //     chunk k - 3.
 // A waiter is never more than 5 chunks away from the phase it waits for, so
 // kNB = 8 barrier slots never alias.  Blocks take tickets in start order and
 // only wait on lower tickets, so the launch is deadlock-free for any grid
 // size.  The last block runs only as many warps as it has sweeps, and its last
-// warp emits sweep T from lane (T-1) % 32 (lag 3 * (lane+1) <= 96, so every
+// warp emits sweep T from lane (T-1) % 32 (lag 4 * (lane+1) <= S, so every
 // bound above stays conservative; its staging writes are reused once the
 // flusher finished chunk c - 3).  No lane ever selects between sweep and
 // identity, so the loop-carried chain is the same in every warp.
@@ -55,7 +55,7 @@
 
 namespace tvs {
 
-constexpr int kGsLag = 3;                 // position lag between adjacent lanes
+constexpr int kGsLag = 4;                 // position lag between adjacent lanes
 constexpr int kCH = 128;                  // positions per chunk
 constexpr int kSub = kCH / 32;            // 32-position unrolled sub-chunks per chunk
 constexpr int kRingCh = 4;                // ring = 4 chunks
@@ -63,7 +63,7 @@ constexpr int kGsRing = kCH * kRingCh;    // ring positions (power of two)
 constexpr int kNB = 8;                    // mbarrier ring per warp
 constexpr int kWar = 4;                   // ring reuse: reader finished chunk c - kWar
 constexpr int kGsMaxBlocks = 64;          // sweeps per launch <= 64 * 32 * kGsWarps
-constexpr int kShiftLane31 = kGsLag * 32; // lane 31's position lag (96)
+constexpr int kShiftLane31 = kGsLag * 32; // lane 31's position lag S (128)
 static_assert((kGsRing & (kGsRing - 1)) == 0, "ring must be a power of two");
 static_assert(kWar * kCH < kGsRing + kShiftLane31, "ring reuse bound");
 static_assert(kCH >= kShiftLane31, "consumer waits at most one chunk ahead");
@@ -123,6 +123,9 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
   const int nch = (n + kShiftLane31 + kCH - 1) / kCH;  // lane 31 finishes position n-1 in chunk nch-1
   // compute warps with sweeps in this block; the last one feeds the flusher
   const int nw = last_block ? (int)((p.sweeps - (long long)b * kGsWarps * 32 + 31) / 32) : kGsWarps;
+  // the staging ring stores position x at (x + soff) & (R-1) so that the
+  // emitting lane's 32 stores per sub-chunk never wrap (constant offsets)
+  const int soff = last_block ? (kGsLag * ((int)((p.sweeps - 1) % 32) + 1)) & 31 : 0;
   auto done = [&](int x, int k) { mbar_wait_uniform(&bar[x][k % kNB], (unsigned)(k / kNB) & 1u); };
   auto signal = [&](int x, int k) {  // all lanes past their work on chunk k
     __syncwarp();
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
     for (int k = 0; k < nch; ++k) {
       done(nw - 1, k);
       const int lo = max(0, k * kCH - kShiftLane31), hi = min(n, (k + 1) * kCH - kShiftLane31);
-      for (int x = lo + lane; x < hi; x += 32) dst[x] = ring[kGsWarps][x & (kGsRing - 1)];
+      for (int x = lo + lane; x < hi; x += 32) dst[x] = ring[kGsWarps][(x + soff) & (kGsRing - 1)];
       if (!last_block) {
         __threadfence();
         __syncwarp();
@@ -182,8 +185,11 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
   const int lane_off = kGsLag * (lane + 1);
   const double* rin = ring[w];
   double* rout = to_staging ? ring[kGsWarps] : ring[w + 1];
+  const int woff = to_staging ? soff : 0;  // (wlag - woff) % 32 == 0
   const bool writer = lane == wlane;
-  double L = bnd, u0 = bnd, u1 = bnd, out = bnd;
+  // L: own previous result (new value at i-1); u0, u1, u2: old values at
+  // i, i+1, i+2 (C, R, and next step's R); out: this step's result
+  double L = bnd, u0 = bnd, u1 = bnd, u2 = bnd, out = bnd;
 
   for (int ch = 0; ch < nch; ++ch) {
     const int jb0 = ch * kCH;
@@ -203,40 +209,45 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
 #pragma unroll 1
     for (int sub = 0; sub < kSub; ++sub) {
       const int jb = jb0 + sub * 32;
-      // steady sub-chunk: every position of the chunk inside [0, n) — no
-      // selects on the DMUL->DADD->DADD chain
-      const bool steady = jb - kGsLag * 32 >= 0 && jb + 31 - kGsLag < n;
+      // steady sub-chunk: every lane's position (j - 4*(lane+1)) inside
+      // [0, n) for the whole sub-chunk — no selects on the chain
+      const bool steady = jb - kShiftLane31 >= 0 && jb + 31 - kGsLag < n;
+      // sub-chunk bases: lane 0 reads position j-1 (only u = 0 can wrap), the
+      // emitting lane writes position j - wlag (never wraps, see woff)
+      const double r0v = rin[(jb - 1) & (kGsRing - 1)];
+      const double* rb = rin + (jb & (kGsRing - 1)) - 1;
+      double* wb = rout + ((jb - wlag + woff) & (kGsRing - 1));
       if (steady && MASK == 7u) {
-        // full 3-tap stencil: the products w1*C and w2*R are formed as soon as
-        // their operands arrive, so the loop-carried chain is exactly
-        // L -> DMUL -> DADD -> DADD (bit-identical: same products, same adds)
+        // full 3-tap stencil: products w1*C and w2*R are formed a step ahead
+        // from values already in registers, so the loop-carried chain is
+        // exactly L -> DMUL -> DADD -> DADD (same products, same adds)
         double pa = __dmul_rn(p.w1, u0), pb = __dmul_rn(p.w2, u1);
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
-          const int j = jb + u;
           const double sh = __shfl_up_sync(0xffffffffu, out, 1);
-          const double rv = rin[(j - 1) & (kGsRing - 1)];  // same address for all lanes: broadcast
-          const double sv = lane == 0 ? rv : sh;
+          const double rv = u == 0 ? r0v : rb[u];  // same address for all lanes: broadcast
+          const double sv = lane == 0 ? rv : sh;    // old(i+3)
           out = __dadd_rn(pb, __dadd_rn(pa, __dmul_rn(p.w0, L)));
-          pa = __dmul_rn(p.w1, u1);  // next iteration's C is this iteration's R
-          pb = __dmul_rn(p.w2, sv);  // next iteration's R just arrived
+          pa = __dmul_rn(p.w1, u1);  // next step's C
+          pb = __dmul_rn(p.w2, u2);  // next step's R
           L = out;
           u0 = u1;
-          u1 = sv;
-          if (writer) rout[(j - wlag) & (kGsRing - 1)] = out;
+          u1 = u2;
+          u2 = sv;
+          if (writer) wb[u] = out;
         }
       } else if (steady) {
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
-          const int j = jb + u;
           const double sh = __shfl_up_sync(0xffffffffu, out, 1);
-          const double rv = rin[(j - 1) & (kGsRing - 1)];
+          const double rv = u == 0 ? r0v : rb[u];
           const double sv = lane == 0 ? rv : sh;
           out = gs_taps<MASK>(L, u0, u1, p.w0, p.w1, p.w2);
           L = out;
           u0 = u1;
-          u1 = sv;
-          if (writer) rout[(j - wlag) & (kGsRing - 1)] = out;
+          u1 = u2;
+          u2 = sv;
+          if (writer) wb[u] = out;
         }
       } else {
 #pragma unroll
@@ -252,9 +263,10 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
           out = (unsigned)i < (unsigned)n ? v : bnd;
           L = out;
           u0 = u1;
-          u1 = sv;
+          u1 = u2;
+          u2 = sv;
           const int po = j - wlag;
-          if (writer && (unsigned)po < (unsigned)n) rout[po & (kGsRing - 1)] = out;
+          if (writer && (unsigned)po < (unsigned)n) rout[(po + woff) & (kGsRing - 1)] = out;
         }
       }
     }

@@ -29,14 +29,14 @@
 //   * a FLUSHER warp copies the staging ring to global memory and publishes
 //     progress (GPU-scope release) for block b+1's loader.
 //
-// Everything advances in chunks of kCH = 128 positions.  Completion of chunk
+// Everything advances in chunks of kCH = 256 positions.  Completion of chunk
 // k by warp X is phase k / kNB of mbarrier bar[X][k % kNB] (hardware-suspended
 // waits; no fences or acquire spins on the compute warps).  Ring bounds
 // (R = 4 chunks of positions per ring; lane 31 lags S = 128 positions):
 //   compute w at chunk c needs positions < min(n, (c+1)*kCH - 1), complete
 //     once warp w-1 finished chunk ceil((need + S) / kCH) - 1 <= c + 1;
 //   writing positions up to (c+1)*kCH - 1 - S into a ring overwrites position
-//     p - R, consumed once the reader finished chunk c - 4  (4 * 128 < R + S);
+//     p - R, consumed once the reader finished chunk c - 4  (4 * kCH < R + S);
 //   the loader's chunk k overwrites chunk k - 4, consumed once warp 0 finished
 //     chunk k - 3.
 // A waiter is never more than 5 chunks away from the phase it waits for, so
@@ -56,7 +56,10 @@
 namespace tvs {
 
 constexpr int kGsLag = 4;                 // position lag between adjacent lanes
-constexpr int kCH = 128;                  // positions per chunk
+#ifndef GS1D_CH
+#define GS1D_CH 256
+#endif
+constexpr int kCH = GS1D_CH;              // positions per chunk
 constexpr int kSub = kCH / 32;            // 32-position unrolled sub-chunks per chunk
 constexpr int kRingCh = 4;                // ring = 4 chunks
 constexpr int kGsRing = kCH * kRingCh;    // ring positions (power of two)
@@ -67,6 +70,7 @@ constexpr int kShiftLane31 = kGsLag * 32; // lane 31's position lag S (128)
 static_assert((kGsRing & (kGsRing - 1)) == 0, "ring must be a power of two");
 static_assert(kWar * kCH < kGsRing + kShiftLane31, "ring reuse bound");
 static_assert(kCH >= kShiftLane31, "consumer waits at most one chunk ahead");
+static_assert((kWar - 1) * kCH < kGsRing + 1, "staging reuse bound (writer lag >= 0)");
 
 __device__ __forceinline__ long long ld_acquire_gpu(const long long* p) {
   long long v;
@@ -206,15 +210,19 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
     } else if (ch >= kWar) {
       done(w + 1, ch - kWar);
     }
+    // first input of the next sub-chunk, loaded a sub-chunk ahead (inside the
+    // chunk only: position jb0 + kCH - 1 is not yet guaranteed)
+    double r0n = rin[(jb0 - 1) & (kGsRing - 1)];
 #pragma unroll 1
     for (int sub = 0; sub < kSub; ++sub) {
       const int jb = jb0 + sub * 32;
+      const double r0v = r0n;
+      if (sub + 1 < kSub) r0n = rin[(jb + 31) & (kGsRing - 1)];
       // steady sub-chunk: every lane's position (j - 4*(lane+1)) inside
       // [0, n) for the whole sub-chunk — no selects on the chain
       const bool steady = jb - kShiftLane31 >= 0 && jb + 31 - kGsLag < n;
       // sub-chunk bases: lane 0 reads position j-1 (only u = 0 can wrap), the
       // emitting lane writes position j - wlag (never wraps, see woff)
-      const double r0v = rin[(jb - 1) & (kGsRing - 1)];
       const double* rb = rin + (jb & (kGsRing - 1)) - 1;
       double* wb = rout + ((jb - wlag + woff) & (kGsRing - 1));
       if (steady && MASK == 7u) {

@@ -78,17 +78,20 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(smaddr(b)) : "memory");
 }
 __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
+  // no suspend-time hint: a bare TRYWAIT suspends in hardware until the phase
+  // completes or a system time limit passes (a hint expands to a
+  // NANOSLEEP.SYNCS loop that every mbarrier event in the CTA wakes up)
   unsigned ok;
-  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
-               : "=r"(ok) : "r"(smaddr(b)), "r"(parity), "r"(20000u) : "memory");
+  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(ok) : "r"(smaddr(b)), "r"(parity) : "memory");
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  unsigned n = 0;
+  if (mbar_try(b, parity)) return;
+  const long long t0 = clock64();
   while (!mbar_try(b, parity))
-    if (++n > (1u << 18)) __trap();  // watchdog (~5 s of suspended waits)
+    if (clock64() - t0 > (1ll << 34)) __trap();  // watchdog (~9 s)
 }
-
 __device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
   asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(smaddr(b)), "r"(bytes)
                : "memory");
@@ -106,11 +109,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // divergence analysis still sees warp-uniform code (keeps shuffles free of
 // BRA.DIV scaffolding).  `leader`: only that thread issues.
 __device__ __forceinline__ void mbar_wait_uniform(unsigned long long* b, unsigned parity) {
-  // watchdog: trap after ~2^34 cycles (~9 s) without the phase completing
+  // hardware-suspending TRYWAIT loop (no hint, see mbar_try); the watchdog
+  // clock is read once per 8 tries: trap after ~2^34 cycles (~9 s)
   asm volatile(
       "{ .reg .pred p; .reg .u64 t0, t1; mov.u64 t0, %%clock64;\n"
-      "TVS_WAIT: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
-      "@p bra TVS_DONE; mov.u64 t1, %%clock64; sub.u64 t1, t1, t0; setp.lt.u64 p, t1, 17179869184;\n"
+      "TVS_WAIT: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @p bra TVS_DONE;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @p bra TVS_DONE;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @p bra TVS_DONE;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @p bra TVS_DONE;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @p bra TVS_DONE;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @p bra TVS_DONE;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @p bra TVS_DONE;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @p bra TVS_DONE;\n"
+      "mov.u64 t1, %%clock64; sub.u64 t1, t1, t0; setp.lt.u64 p, t1, 17179869184;\n"
       "@p bra TVS_WAIT; trap;\n"
       "TVS_DONE: }" ::"r"(smaddr(b)), "r"(parity) : "memory");
 }

@@ -36,6 +36,7 @@
 // sweep of row d - 127 back to the grid in place.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -71,10 +72,15 @@ constexpr int kLam = 2;              // column lag lane t-1 -> t
 constexpr int kMu = 3;               // extra lag warp w-1 -> w (>= kC + 1 - kLam)
 constexpr int kBig = 5;              // lag group g-1 -> g (>= kC + 1)
 constexpr int kBase = 10;            // every producer starts left of column 0 (>= kLam + kBig + 2)
-constexpr int kRG = 256;             // global ring depth (iterations)
-constexpr int kK = 256;              // global ring slots (boundaries in flight)
+// Global ring between clusters (blocks when CS = 1): rg iterations per
+// boundary, kslots boundaries in flight — both sized at launch.  With G chain
+// units resident, the oldest can run at most G * rg iterations ahead of the
+// first unit not yet resident, and must reach c_end to retire, so the host
+// makes G * rg >= 2 * c_end (no back-pressure deadlock for any width).
 constexpr int kPub = 4;              // IO warps publish up/downstream every kPub chunks
 constexpr int kComputeWarps = kG * kWarpsG;
+constexpr int kPhLag = kBig * kG / kC;  // phantom chunk kl = producer chunk kl + kPhLag
+static_assert(kBig * kG % kC == 0, "phantom lag must be whole chunks");
 constexpr int kThreads = (kComputeWarps + 2) * 32;  // + loader warp + drainer warp
 constexpr int kRows = kR + kC;       // ring rows incl. kC mirror rows (chunk reads never wrap)
 constexpr size_t kSmem = sizeof(double) * (size_t)(kG + 1) * kRows * kSlots;
@@ -88,7 +94,9 @@ struct Gs2pArgs {
   int sweeps;                // real sweeps this pass (<= 128)
   int nctas;
   int c_end;                 // iterations per warp (multiple of kC)
-  double* gring;             // kK * kRG * 128
+  double* gring;             // kslots * rg * 128
+  int rg;                    // global ring depth (iterations, power of two)
+  int kslots;                // global ring slots (boundaries in flight)
   unsigned long long* gprod; // kK tagged counters: (boundary+1) << 32 | iterations written
   unsigned long long* gcons; // kK tagged counters: (boundary+1) << 32 | iterations consumed
   int* ticket;
@@ -127,6 +135,48 @@ __device__ __forceinline__ void st_rel_gpu(unsigned long long* p, unsigned long 
 // order; completion of chunk m is phase (m >> 3) of barrier bar[X][m & 7].
 // Every waiter is at most 5 chunks behind / 3 ahead of the warp it waits on
 // (RAW/WAR bounds), so a slot never wraps under a waiter (no ABA).
+// ---- thread-block cluster helpers (distributed shared memory) ----
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release;\nbarrier.cluster.wait.acquire;" ::: "memory");
+}
+// shared::cta address -> the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ unsigned mapa(const void* local, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smaddr(local)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void remote_arrive(unsigned rbar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
+}
+__device__ __forceinline__ void remote_arrive_tx(unsigned rbar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(rbar), "r"(bytes)
+               : "memory");
+}
+// local shared memory -> shared memory of another CTA in the cluster, completion
+// counted as transaction bytes on that CTA's mbarrier
+__device__ __forceinline__ void push_s2s(unsigned rdst, const void* src, unsigned bytes, unsigned rbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(rdst), "r"(smaddr(src)), "r"(bytes), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* b, unsigned parity) {
+  // acquire at cluster scope: the phase was completed by another CTA
+  auto try1 = [&] {
+    unsigned ok;
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok) : "r"(smaddr(b)), "r"(parity) : "memory");
+    return ok != 0;
+  };
+  if (try1()) return;
+  const long long t0 = clock64();
+  while (!try1())
+    if (clock64() - t0 > (1ll << 34)) __trap();
+}
+
 // Wait until a shared-memory progress counter reaches `v`; back off so the
 // spinning warps do not starve the IO warp of issue slots.
 __device__ __forceinline__ void wait_ge(const int* p, int v) {
@@ -155,7 +205,16 @@ __device__ __forceinline__ double gs9(const double* w, double nw, double n, doub
   return acc;
 }
 
-template <unsigned MASK>
+// CS > 1: consecutive blocks of the chain form a thread-block cluster; block
+// r+1 of a cluster receives block r's last group through distributed shared
+// memory (one bulk copy per chunk pushed by block r's drainer straight into
+// block r+1's phantom ring, completing on block r+1's mbarrier) instead of the
+// global ring — no GPU-scope fence on those hops.  Only the first block of a
+// cluster reads the global ring.  WAR: block r+1's loader returns a credit
+// (remote arrive) for phantom chunk kl once its group 0 finished chunk kl - 5;
+// credit kl also tells block r that its chunk kl push completed, which lets
+// block r's last group reuse those ring rows (pushed[]).
+template <unsigned MASK, int CS>
 __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p) {
   using namespace gs2p;
   extern __shared__ __align__(16) double smem[];
@@ -168,22 +227,40 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
   auto mirror_of = [&](double* p_row_elem, int it) -> double* { return (it & (kR - 1)) < kC ? p_row_elem + (size_t)kR * kSlots : nullptr; };
   constexpr int kLoader = kComputeWarps, kDrainer = kComputeWarps + 1;
   __shared__ unsigned long long bar[kComputeWarps + 2][8];
+  // cluster hand-off: pbar = phantom chunk arrived (pushed by block r-1 or
+  // filled by my loader), cbar = credits from block r+1, pushed = my chunk's
+  // push to block r+1 complete
+  __shared__ unsigned long long pbar[8], cbar[8], pushed[8];
   __shared__ int s_ticket;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const unsigned crank = CS > 1 ? cluster_rank() : 0u;
   if (threadIdx.x == 0) {
-    s_ticket = atomicAdd(p.ticket, 1);
+    if (crank == 0) s_ticket = atomicAdd(p.ticket, 1) * CS;
     for (int x = 0; x < kComputeWarps + 2; ++x)
       for (int q = 0; q < 8; ++q) mbar_init(&bar[x][q], x == kLoader ? 32u : 1u);
+    for (int q = 0; q < 8; ++q) {
+      mbar_init(&pbar[q], 1u);
+      mbar_init(&cbar[q], 1u);
+      mbar_init(&pushed[q], 1u);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
+  int n;  // block index along the chain
+  if constexpr (CS > 1) {
+    cluster_sync_all();  // every block's barriers initialised before any remote access
+    int t0;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(t0) : "r"(mapa(&s_ticket, 0)) : "memory");
+    n = t0 + (int)crank;
+  } else {
+    __syncthreads();
+    n = s_ticket;
+  }
   // "warp x completed chunk m" / "I completed chunk m"
   auto wait_chunk = [&](int x, int m) {
 #ifndef GS2P_NOWAIT
     if (m >= 0) mbar_wait(&bar[x][m & 7], (unsigned)(m >> 3) & 1u);
 #endif
   };
-  const int n = s_ticket;           // block index along the chain
   if (threadIdx.x == 0) TRACE(n, 0);
   const int d0 = n * kG;            // first group (diagonal) of this block
   const int nch = p.c_end / kC;
@@ -191,9 +268,16 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
   const int e0 = p.e0, e1 = p.e1;
 
   const bool has_up = n > 0, has_down = n + 1 < p.nctas;
-  const int up_slot = (n + kK - 1) % kK, dn_slot = n % kK;
-  const unsigned long long up_tag = (unsigned long long)n << 32;        // boundary n-1 -> tag n
-  const unsigned long long dn_tag = (unsigned long long)(n + 1) << 32;  // boundary n -> tag n+1
+  const bool up_cl = CS > 1 && crank > 0;                 // phantom pushed by block n-1 (same cluster)
+  const bool dn_cl = CS > 1 && crank + 1 < CS && has_down;  // push to block n+1 (same cluster)
+  const bool up_gl = has_up && !up_cl, dn_gl = has_down && !dn_cl;
+  auto ring_row = [&](int gi, int r) -> double* { return &smem[((size_t)gi * kRows + r) * kSlots]; };
+  // global boundaries are between clusters: bd after my cluster, bd - 1 before
+  const int kK = p.kslots, kRG = p.rg;
+  const int bd = n / CS;
+  const int up_slot = (bd - 1 + kK) % kK, dn_slot = bd % kK;
+  const unsigned long long up_tag = (unsigned long long)bd << 32;        // boundary bd-1 -> tag bd
+  const unsigned long long dn_tag = (unsigned long long)(bd + 1) << 32;  // boundary bd -> tag bd+1
   if (wi == kComputeWarps) {
     // ============ loader warp: grid rows (slot 0) + previous block's last group ============
     const double* up_ring = p.gring + (size_t)up_slot * kRG * kLanes;
@@ -212,8 +296,9 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
       // every group's warp 0 -> slot 0) finished chunk kl-5 (ring chunk kl-8 reusable)
       for (int q = 0; q < kWarpsG; ++q) wait_chunk(q, kl - 5);
       for (int g = 1; g < kG; ++g) wait_chunk(g * kWarpsG, kl - 5);
+      if (up_cl && lane == 0) remote_arrive(mapa(&cbar[kl & 7], crank - 1));  // credit: phantom chunk kl writable
       // upstream data for producer iterations up to it_hi + Lambda*G
-      if (has_up) {
+      if (up_gl) {
         const int up_need = min(it_hi + kBig * kG, p.c_end);
         SpinGuard guard;
         while ((up_seen >> 32) != (up_tag >> 32) || (up_seen & 0xffffffffull) < (unsigned long long)up_need) {
@@ -228,6 +313,8 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
       lw += clock64() - lws;
 #endif
       // slot 0 of rings -1..G-1: grid row d0+g+1 at column it + lam - Lambda*g - base
+      // (also for a pushed phantom ring: the push carries only the lane slots,
+      // block n-1's own slot 0 of those rows is reloaded by its loader)
       if (lane < (kG + 1) * kC) {
         const int g = lane / kC - 1, it = it_lo + lane % kC;
         const int row = d0 + g + 1, col = it + kLam - kBig * g - kBase;
@@ -239,32 +326,41 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
       }
       // phantom lanes: 4 iterations x 64 pairs, 16-byte copies (L2 only: the
       // global ring is rewritten every kRG iterations)
+      if (!up_cl) {
 #pragma unroll
-      for (int q = 0; q < kC * kLanes / 64; ++q) {
-        const int e = lane + 32 * q;  // pair index
-        const int it = it_lo + e / (kLanes / 2), t = 2 * (e % (kLanes / 2));
-        const int pit = it + kBig * kG;
-        double* dst = ring_lane0(0, it) + t;
-        double* mir = mirror_of(dst, it);
-        const double* src = (has_up && pit < p.c_end) ? up_ring + (size_t)(pit % kRG) * kLanes + t : bndsrc;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smaddr(dst)), "l"(src));
-        if (mir) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smaddr(mir)), "l"(src));
+        for (int q = 0; q < kC * kLanes / 64; ++q) {
+          const int e = lane + 32 * q;  // pair index
+          const int it = it_lo + e / (kLanes / 2), t = 2 * (e % (kLanes / 2));
+          const int pit = it + kBig * kG;
+          double* dst = ring_lane0(0, it) + t;
+          double* mir = mirror_of(dst, it);
+          const double* src = (has_up && pit < p.c_end) ? up_ring + (size_t)(pit & (kRG - 1)) * kLanes + t : bndsrc;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smaddr(dst)), "l"(src));
+          if (mir) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smaddr(mir)), "l"(src));
+        }
+      } else if (it_hi + kBig * kG > p.c_end) {
+        // block n-1 has no iterations left for these phantom rows: boundary
+        for (int e = lane; e < kC * kLanes; e += 32) {
+          const int r = (it_lo & (kR - 1)) + e / kLanes;
+          ring_row(0, r)[2 + e % kLanes] = bnd;
+          if (r < kC) ring_row(0, r + kR)[2 + e % kLanes] = bnd;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pbar[kl & 7]);
       }
       // the chunk's barrier phase completes when every lane's copies landed
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smaddr(&bar[kLoader][kl & 7])) : "memory");
-      if (has_up && ((kl + 1) % kPub == 0 || kl + 1 == nch)) {
+      if (up_gl && ((kl + 1) % kPub == 0 || kl + 1 == nch)) {
         // producer iterations below it_hi + Lambda*G are no longer read from
         // the global ring once this chunk's copies completed
         wait_chunk(kLoader, kl);
         if (lane == 0) st_rel_gpu(p.gcons + up_slot, up_tag | (unsigned long long)min(it_hi + kBig * kG, p.c_end));
       }
     }
-    return;
-  }
-  if (wi == kComputeWarps + 1) {
+  } else if (wi == kComputeWarps + 1) {
     // ============ drainer warp: last group -> next block (global ring) ============
     double* dn_ring = p.gring + (size_t)dn_slot * kRG * kLanes;
-    bool slot_ok = !has_down || n < kK;
+    bool slot_ok = !dn_gl || bd < kK;
     unsigned long long dn_cons_seen = 0;
     SpinGuard guard;
 #ifdef GS2P_TRACE
@@ -282,13 +378,13 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
       for (int g = 0; g + 1 < kG; ++g) wait_chunk(g * kWarpsG + kWarpsG - 1, ks);
       for (;;) {
         bool ok = true;
-        if (ok && has_down && !slot_ok) {  // previous user of this global slot fully consumed
+        if (ok && dn_gl && !slot_ok) {  // previous user of this global slot fully consumed
           unsigned long long v = lane == 0 ? ld_acq_gpu(p.gcons + dn_slot) : 0ull;
           v = __shfl_sync(0xffffffffu, v, 0);
-          slot_ok = v >= (((unsigned long long)(n + 1 - kK) << 32) | (unsigned long long)p.c_end);
+          slot_ok = v >= (((unsigned long long)(bd + 1 - kK) << 32) | (unsigned long long)p.c_end);
           ok = slot_ok;
         }
-        if (ok && has_down && lo + kC > kRG) {  // global back-pressure
+        if (ok && dn_gl && lo + kC > kRG) {  // global back-pressure
           const unsigned long long need = dn_tag | (unsigned long long)(lo + kC - kRG);
           if (dn_cons_seen < need) {
             unsigned long long v = lane == 0 ? ld_acq_gpu(p.gcons + dn_slot) : 0ull;
@@ -303,14 +399,35 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
 #ifdef GS2P_TRACE
       dw += clock64() - dws;
 #endif
+      if (dn_cl && ks >= kPhLag) {
+        // my chunk ks -> phantom chunk kl = ks - kPhLag of block n+1 (pit = it + kBig * kG)
+        const int kl = ks - kPhLag;
+        mbar_wait_cluster(&cbar[kl & 7], (unsigned)(kl >> 3) & 1u);  // block n+1 freed those rows
+        if (lane == 0) {
+          mbar_arrive(&pushed[kl & 7]);  // credit kl => my chunk kl push completed
+          fence_proxy_async_smem();      // compute warps' ring writes -> async-proxy read
+          // lane slots only: slot 0 of these rows is refilled by my loader
+          // as soon as my compute warps are done with them
+          const unsigned rb = mapa(&pbar[kl & 7], crank + 1);
+          const int rdst = (kl * kC) & (kR - 1), rsrc = lo & (kR - 1);
+          const unsigned bytes = (unsigned)(kLanes * sizeof(double));
+          remote_arrive_tx(rb, (rdst < kC ? 2u : 1u) * kC * bytes);
+#pragma unroll
+          for (int u = 0; u < kC; ++u) {
+            const double* src = ring_row(kG, rsrc + u) + 2;
+            push_s2s(mapa(ring_row(0, rdst + u) + 2, crank + 1), src, bytes, rb);
+            if (rdst < kC) push_s2s(mapa(ring_row(0, rdst + kR + u) + 2, crank + 1), src, bytes, rb);
+          }
+        }
+      }
 #ifndef GS2P_NODRAIN
-      if (has_down) {
+      if (dn_gl) {
 #pragma unroll
         for (int q = 0; q < kC * kLanes / 64; ++q) {
           const int e = lane + 32 * q;
           const int it = lo + e / (kLanes / 2), t = 2 * (e % (kLanes / 2));
           const double2 v = *reinterpret_cast<const double2*>(ring_lane0(kG, it) + t);
-          *reinterpret_cast<double2*>(dn_ring + (size_t)(it % kRG) * kLanes + t) = v;
+          *reinterpret_cast<double2*>(dn_ring + (size_t)(it & (kRG - 1)) * kLanes + t) = v;
         }
       }
       if (lane < kG * kC) {  // final outputs: lane 127 of group g = row d_g - 127
@@ -322,15 +439,14 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
 #endif
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar[kDrainer][ks & 7]);
-      if (has_down && ((ks + 1) % kPub == 0 || ks + 1 == nch)) {
+      if (dn_gl && ((ks + 1) % kPub == 0 || ks + 1 == nch)) {
         __threadfence();
         __syncwarp();
         if (lane == 0) st_rel_gpu(p.gprod + dn_slot, dn_tag | (unsigned long long)(lo + kC));
         if (lane == 0 && ks + 1 == kPub) TRACE(n, 4);
       }
     }
-    return;
-  }
+  } else {
 
   // ======================= compute warps =======================
   const int g = wi / kWarpsG, w = wi % kWarpsG;
@@ -372,6 +488,7 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
     const int cb = k * kC;
     if (lane == 0 && w == 0 && g == 0 && (k == 0 || k == 100)) TRACE(n, k == 0 ? 1 : 2);
     if (lane == 0 && w == kWarpsG - 1 && g == kG - 1 && k == 100) TRACE(n, 3);
+    if (lane == 0 && w == kWarpsG - 1 && g == kG - 1 && k == nch - 1) TRACE(n, 5);
 #ifdef GS2P_TRACE
     const long long tw0 = clock64();
     if (k == 0) t_start = tw0;
@@ -382,6 +499,8 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
     if (dep_prev2 >= 0) wait_chunk(dep_prev2, k - 1);
     if (dep_left >= 0) wait_chunk(dep_left, k - 1);
     if (needs_io) wait_chunk(kLoader, k);
+    if (up_cl && g == 0) mbar_wait_cluster(&pbar[k & 7], (unsigned)(k >> 3) & 1u);
+    if (dn_cl && g == kG - 1 && k >= 8) mbar_wait(&pushed[(k - 8) & 7], (unsigned)((k - 8) >> 3) & 1u);
     wait_chunk(war0, k - 5);
     if (war1 >= 0) wait_chunk(war1, k - 5);
     wait_chunk(war2, k - 5);
@@ -462,6 +581,17 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
     __syncwarp();
     if (lane == 0) mbar_arrive(&bar[wi][k & 7]);
   }
+  }  // compute warps
+  // no block of a cluster leaves while a peer may still push into / credit it
+  if constexpr (CS > 1) cluster_sync_all();
+#ifdef GS2P_TRACE
+  if (threadIdx.x == 0) {
+    TRACE(n, 6);
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (n < 4096) g_trace[n][7] = smid;
+  }
+#endif
 }
 
 static unsigned gs_mask2d(const tvs_stencil& st, double w[9]) {
@@ -503,14 +633,6 @@ int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, in
   a.c_end = ((a.e1 + 2 + kBase + skew + kBig * kG + kC - 1) / kC) * kC;
   for (int k = 0; k < 9; ++k) a.w[k] = w[k];
   a.bnd = st.boundary;
-  const size_t ring_bytes = sizeof(double) * (size_t)kK * kRG * kLanes;
-  const size_t ctrl_bytes = sizeof(unsigned long long) * 2 * kK + 64;
-  a.gring = static_cast<double*>(scratch(ring_bytes, 0));
-  char* ctrl = static_cast<char*>(scratch(ctrl_bytes, 1));
-  if (!a.gring || !ctrl) return fail(TVS_ERR_CUDA, "gs2d_pipeline: scratch");
-  a.gprod = reinterpret_cast<unsigned long long*>(ctrl);
-  a.gcons = a.gprod + kK;
-  a.ticket = reinterpret_cast<int*>(a.gcons + kK);
   double* bndpad = static_cast<double*>(scratch(sizeof(double) * 32, 2));
   if (!bndpad) return fail(TVS_ERR_CUDA, "gs2d_pipeline: scratch");
   {
@@ -519,15 +641,77 @@ int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, in
     TVS_CUDA(cudaMemcpyAsync(bndpad, h, sizeof(h), cudaMemcpyHostToDevice, s));
   }
   a.bndpad = bndpad;
-  auto kern = mask == 0x1FFu ? gs2d_pipe_kernel<0x1FFu> : gs2d_pipe_kernel<kStar>;
-  TVS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
-  for (int64_t done = 0; done < steps; done += kLanes) {
-    a.sweeps = (int)std::min<int64_t>(kLanes, steps - done);
-    TVS_CUDA(cudaMemsetAsync(ctrl, 0, ctrl_bytes, s));
-    kern<<<a.nctas, kThreads, kSmem, s>>>(a);
-    TVS_LAUNCHED("gs2d_pipe_kernel");
-  }
-  return TVS_OK;
+  // Cluster size.  Consecutive blocks of a cluster hand off through
+  // distributed shared memory, which shortens the block->block chain (the
+  // bound for narrow grids: 8192x2048 T=100 29.3 ms at 1, 20.2 ms at 8) but
+  // couples the blocks tightly and leaves SMs idle at cluster granularity,
+  // which costs wide grids whose time is set by per-block speed (8192x8192:
+  // 31.4 ms at 1, 48.7 at 8).  Measured crossover: a block's iteration count
+  // c_end ~ 148 x 50.  TVS_GS2D_CLUSTER = 1, 2, 4 or 8 overrides.
+  static const int cs_env = [] {
+    const char* e = getenv("TVS_GS2D_CLUSTER");
+    const int v = e ? atoi(e) : 0;
+    return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 0;
+  }();
+  const int cs_req = cs_env ? cs_env : (a.c_end < 148 * 50 ? 8 : 1);
+  auto launch = [&](auto cs_tag) -> int {
+    constexpr int CS = decltype(cs_tag)::value;
+    auto kern = mask == 0x1FFu ? gs2d_pipe_kernel<0x1FFu, CS> : gs2d_pipe_kernel<kStar, CS>;
+    TVS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+    Gs2pArgs b = a;
+    b.nctas = (a.nctas + CS - 1) / CS * CS;  // tail blocks hold only out-of-grid rows
+    cudaLaunchConfig_t lc{};
+    cudaLaunchAttribute attr[1];
+    lc.gridDim = dim3((unsigned)b.nctas);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = kSmem;
+    lc.stream = s;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    // resident chain units: clusters (CS > 1) or blocks
+    int units = 0;
+    if (CS > 1) {
+      if (cudaOccupancyMaxActiveClusters(&units, kern, &lc) != cudaSuccess || units < 1) {
+        cudaGetLastError();
+        return TVS_ERR_UNSUPPORTED;  // caller retries with CS = 1
+      }
+    } else {
+      int per_sm = 0, dev = 0, sms = 0;
+      TVS_CUDA(cudaGetDevice(&dev));
+      TVS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      TVS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, kSmem));
+      units = std::max(1, per_sm * sms);
+    }
+    int rg = 256;
+    while ((long long)rg * units < 2ll * b.c_end + 64) rg *= 2;
+    b.rg = rg;
+    b.kslots = units + 2;
+    const size_t ring_bytes = sizeof(double) * (size_t)b.kslots * rg * kLanes;
+    const size_t ctrl_bytes = sizeof(unsigned long long) * 2 * b.kslots + 64;
+    b.gring = static_cast<double*>(scratch(ring_bytes, 0));
+    char* ctrl = static_cast<char*>(scratch(ctrl_bytes, 1));
+    if (!b.gring || !ctrl) return fail(TVS_ERR_CUDA, "gs2d_pipeline: scratch");
+    b.gprod = reinterpret_cast<unsigned long long*>(ctrl);
+    b.gcons = b.gprod + b.kslots;
+    b.ticket = reinterpret_cast<int*>(b.gcons + b.kslots);
+    for (int64_t done = 0; done < steps; done += kLanes) {
+      b.sweeps = (int)std::min<int64_t>(kLanes, steps - done);
+      TVS_CUDA(cudaMemsetAsync(ctrl, 0, ctrl_bytes, s));
+      TVS_CUDA(cudaLaunchKernelEx(&lc, kern, b));
+      TVS_LAUNCHED("gs2d_pipe_kernel");
+    }
+    return TVS_OK;
+  };
+  int rc = TVS_ERR_UNSUPPORTED;
+  if (cs_req == 8) rc = launch(std::integral_constant<int, 8>{});
+  else if (cs_req == 4) rc = launch(std::integral_constant<int, 4>{});
+  else if (cs_req == 2) rc = launch(std::integral_constant<int, 2>{});
+  if (rc == TVS_ERR_UNSUPPORTED) rc = launch(std::integral_constant<int, 1>{});
+  return rc;
 }
 
 }  // namespace tvs

@@ -4,6 +4,7 @@ the reference's own outputs (golden) and the oracle, bit-exact."""
 from __future__ import annotations
 
 import dataclasses
+import os
 
 import numpy as np
 import pytest
@@ -262,3 +263,18 @@ def test_cli_bench_and_verify(cuda_ready, tmp_path):
     want = cref.scalar_reference(get("heat2d").spec, Grid.random((200, 150), seed=0), 9)
     assert fields[11] == f"{fnv1a64(want.dump_bytes()):016x}"
     assert cli.main(["--mode", "verify", "--kernel", "gs2d9p", "--cells", "3"]) == 0
+
+
+@pytest.mark.parametrize("cluster", [1, 2, 4, 8])
+def test_gs2d_pipeline_cluster_sizes(cuda_ready, cluster):
+    """Lexicographic GS-2D pipeline with consecutive blocks handing off through
+    distributed shared memory (cluster > 1) or the global ring (cluster 1):
+    several clusters, partial last cluster, multi-pass sweeps, narrow grids
+    (phantom tail filled by the loader) — bit-exact against the oracle."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, TVS_GS2D_CLUSTER=str(cluster))
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "gs2d_cluster_check.py")],
+                       env=env, capture_output=True, text=True, timeout=180)
+    assert r.returncode == 0, r.stdout + r.stderr

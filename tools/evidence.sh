@@ -9,4 +9,6 @@ done
 python tools/profile_run.py --config 3 --T 8 --reps 1 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:jacobi2d -c 1 -o gpurun_out/full_c3 python tools/profile_run.py --config 3 --T 8 --reps 1 > /dev/null 2>&1
 python tools/profile_run.py --config 5 --T 1 --reps 1 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:jacobi3d -c 1 -o gpurun_out/full_c5 python tools/profile_run.py --config 5 --T 1 --reps 1 > /dev/null 2>&1
 python tools/profile_run.py --config 1 --reps 1 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:jacobi1d -s 2 -c 1 -o gpurun_out/full_c1 python tools/profile_run.py --config 1 --reps 1 > /dev/null 2>&1
+python tools/profile_run.py --config 2 --reps 1 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:gs1d -c 1 -o gpurun_out/full_c2 python tools/profile_run.py --config 2 --reps 1 > /dev/null 2>&1
+python tools/profile_run.py --config 4 --reps 1 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:gs2d -c 1 -o gpurun_out/full_c4 python tools/profile_run.py --config 4 --reps 1 > /dev/null 2>&1
 ls -la gpurun_out

@@ -1,0 +1,3 @@
+for i in 1 2 3; do for c in 2 4 8; do echo -n "CS=$c "; TVS_GS2D_CLUSTER=$c timeout 120 python tools/gs2d_case.py 700 12000 1; done; done
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "cluster_sizes or gauss_seidel_orders" -p no:cacheprovider 2>&1 | tail -2
+for c in 1 2 4 8; do for s in "8192 8192" "8192 2048"; do echo -n "CS=$c "; TVS_GS2D_CLUSTER=$c timeout 120 python tools/shape_run.py gs2d9p $s --T 100 2>&1 | tail -1; done; done

@@ -70,6 +70,9 @@ __device__ __forceinline__ double tap_next(double c, double v, double acc) {
 __device__ __forceinline__ double tap_first(double c, double v) { return __dmul_rn(c, v); }
 
 // ---- mbarriers and bulk (TMA) copies -------------------------------------
+#ifndef TVS_MBAR_SLEEP
+#define TVS_MBAR_SLEEP 0
+#endif
 __device__ __forceinline__ unsigned smaddr(const void* q) { return (unsigned)__cvta_generic_to_shared(q); }
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smaddr(b)), "r"(count) : "memory");
@@ -86,11 +89,36 @@ __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity)
                : "=r"(ok) : "r"(smaddr(b)), "r"(parity) : "memory");
   return ok != 0;
 }
+// address form (shared::cta address precomputed by the caller)
+__device__ __forceinline__ bool mbar_try_a(unsigned a, unsigned parity) {
+  unsigned ok;
+  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+  return ok != 0;
+}
+static __device__ __noinline__ void mbar_wait_slow(unsigned a, unsigned parity) {
+  const long long t0 = clock64();
+  for (unsigned n = 1;; ++n) {
+    if (mbar_try_a(a, parity)) return;
+    if ((n & 63u) == 0 && clock64() - t0 > (1ll << 34)) __trap();
+  }
+}
+__device__ __forceinline__ void mbar_wait_a(unsigned a, unsigned parity) {
+  if (!mbar_try_a(a, parity)) mbar_wait_slow(a, parity);
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
   if (mbar_try(b, parity)) return;
+  // retry loop kept lean: waiting warps share the SMSP with computing ones.
+  // Optional back-off (TVS_MBAR_SLEEP ns) frees issue slots while waiting;
+  // the watchdog reads the clock once per 64 tries (trap after ~2^34 cycles)
   const long long t0 = clock64();
-  while (!mbar_try(b, parity))
-    if (clock64() - t0 > (1ll << 34)) __trap();  // watchdog (~9 s)
+  for (unsigned n = 1;; ++n) {
+#if TVS_MBAR_SLEEP > 0
+    __nanosleep(TVS_MBAR_SLEEP);
+#endif
+    if (mbar_try(b, parity)) return;
+    if ((n & 63u) == 0 && clock64() - t0 > (1ll << 34)) __trap();
+  }
 }
 __device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
   asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(smaddr(b)), "r"(bytes)

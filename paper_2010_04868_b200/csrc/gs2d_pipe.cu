@@ -31,9 +31,9 @@
 //             only wait on lower tickets (plus bounded back-pressure), so the
 //             launch is deadlock-free.
 // "Virtual lane -1" of group g (ring slot 0) is grid row d_g + 1 at sweep
-// t0 - 1: lane 0 reads its old own row / row below from there.  Lanes past
-// the requested sweep count are identity lanes.  Lane 127 writes the final
-// sweep of row d - 127 back to the grid in place.
+// t0 - 1: lane 0 reads its old own row / row below from there.  Lane lf = T - 1 (the last
+// requested sweep of the pass) writes the final value of row d - lf back to
+// the grid in place; lanes past it compute values nothing reads.
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
@@ -64,7 +64,10 @@ __device__ unsigned long long g_wait[2][6][2];
 namespace gs2p {
 constexpr int kLanes = 128;          // sweeps per pass (4 warps)
 constexpr int kWarpsG = 4;
-constexpr int kG = 4;                // groups per block
+#ifndef GS2P_KG
+#define GS2P_KG 4
+#endif
+constexpr int kG = GS2P_KG;          // groups per block
 constexpr int kC = 4;                // iterations per chunk (sync granularity)
 constexpr int kR = 32;               // ring depth (iterations), power of two
 constexpr int kSlots = kLanes + 2;   // [0] virtual lane -1, [1] pad, [2 + t] lane t (16-B aligned pairs)
@@ -80,7 +83,7 @@ constexpr int kBase = 10;            // every producer starts left of column 0 (
 constexpr int kPub = 4;              // IO warps publish up/downstream every kPub chunks
 constexpr int kComputeWarps = kG * kWarpsG;
 constexpr int kPhLag = kBig * kG / kC;  // phantom chunk kl = producer chunk kl + kPhLag
-static_assert(kBig * kG % kC == 0, "phantom lag must be whole chunks");
+constexpr bool kClusterOK = kBig * kG % kC == 0;  // DSMEM push needs a whole-chunk phantom lag
 constexpr int kThreads = (kComputeWarps + 2) * 32;  // + loader warp + drainer warp
 constexpr int kRows = kR + kC;       // ring rows incl. kC mirror rows (chunk reads never wrap)
 constexpr size_t kSmem = sizeof(double) * (size_t)(kG + 1) * kRows * kSlots;
@@ -268,6 +271,11 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
   const int e0 = p.e0, e1 = p.e1;
 
   const bool has_up = n > 0, has_down = n + 1 < p.nctas;
+  // lane lf = sweeps - 1 runs the last requested sweep: group d's lane lf
+  // emits the final value of row d - lf.  Lanes past it compute values no
+  // real lane or output ever reads, so no lane selects between sweep and
+  // identity and every warp inside the grid runs the pure body.
+  const int lf = p.sweeps - 1, lf_warp = lf / 32;
   const bool up_cl = CS > 1 && crank > 0;                 // phantom pushed by block n-1 (same cluster)
   const bool dn_cl = CS > 1 && crank + 1 < CS && has_down;  // push to block n+1 (same cluster)
   const bool up_gl = has_up && !up_cl, dn_gl = has_down && !dn_cl;
@@ -372,10 +380,10 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
       const long long dws = clock64();
       if (ks == 100 && lane == 0) WAITACC(n, 5, (unsigned long long)dw, (unsigned long long)(dws - dt0));
 #endif
-      // the last group (forwarded downstream) and every group's warp 3
-      // (lane 127 = the final sweep, written back to the grid here)
+      // the last group (forwarded downstream) and every group's warp lf_warp
+      // (lane lf = the final sweep, written back to the grid here)
       for (int q = 0; q < kWarpsG; ++q) wait_chunk((kG - 1) * kWarpsG + q, ks);
-      for (int g = 0; g + 1 < kG; ++g) wait_chunk(g * kWarpsG + kWarpsG - 1, ks);
+      for (int g = 0; g + 1 < kG; ++g) wait_chunk(g * kWarpsG + lf_warp, ks);
       for (;;) {
         bool ok = true;
         if (ok && dn_gl && !slot_ok) {  // previous user of this global slot fully consumed
@@ -430,11 +438,11 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
           *reinterpret_cast<double2*>(dn_ring + (size_t)(it & (kRG - 1)) * kLanes + t) = v;
         }
       }
-      if (lane < kG * kC) {  // final outputs: lane 127 of group g = row d_g - 127
+      if (lane < kG * kC) {  // final outputs: lane lf of group g = row d_g - lf
         const int g = lane / kC, it = lo + lane % kC;
-        const int row = d0 + g - (kLanes - 1);
-        const int col = it - (kBase + kLam * (kLanes - 1) + kMu * (kWarpsG - 1) + kBig * g);
-        if (row >= 0 && row < e0 && col >= 0 && col < e1) p.a[(long long)row * p.s0 + col] = ring(g + 1, it, kLanes);
+        const int row = d0 + g - lf;
+        const int col = it - (kBase + kLam * lf + kMu * lf_warp + kBig * g);
+        if (row >= 0 && row < e0 && col >= 0 && col < e1) p.a[(long long)row * p.s0 + col] = ring(g + 1, it, lf + 1);
       }
 #endif
       __syncwarp();
@@ -454,9 +462,8 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
   const int d = d0 + g;                  // diagonal of this group
   const int row = d - t;
   const bool row_ok = row >= 0 && row < e0;
-  const bool real = t < p.sweeps;
-  // per-lane output mode: 0 compute, 1 identity (beyond the sweep count), 2 outside the grid
-  const int mode = row_ok ? (real ? 0 : 1) : 2;
+  // per-lane output mode: 0 compute, 2 outside the grid (emits the boundary)
+  const int mode = row_ok ? 0 : 2;
   const bool warp_pure = __all_sync(0xffffffffu, mode == 0);
   const int col_off = kBase + kLam * t + kMu * w + kBig * g;  // column = iteration - col_off
   const int offE = 1 - kLam - kBig - ((lane == 0 && w > 0) ? kMu : 0);
@@ -476,9 +483,21 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
   const bool needs_io = g == 0 || w == 0;
   const int war0 = g + 1 < kG ? (g + 1) * kWarpsG + w : kDrainer;
   const int war1 = (g + 1 < kG && w + 1 < kWarpsG) ? (g + 1) * kWarpsG + w + 1 : -1;
-  // warp 3's lane 127 is read by the drainer (final outputs), the others by warp w+1
+  // lane 31 of warp w is read by warp w+1 (warp 3's by the drainer, which
+  // forwards / writes it); lane lf by the drainer (war3 below)
   const int war2 = w + 1 < kWarpsG ? g * kWarpsG + w + 1 : kDrainer;
+  // the drainer also reads lane lf's slots (final outputs)
+  const int war3 = (w == lf_warp && w + 1 < kWarpsG) ? kDrainer : -1;
 
+  // shared::cta addresses of the chunk-completion rings this warp waits on
+  const unsigned a_prev = smaddr(&bar[g > 0 ? dep_prev : 0][0]);
+  const unsigned a_prev2 = smaddr(&bar[dep_prev2 >= 0 ? dep_prev2 : 0][0]);
+  const unsigned a_left = smaddr(&bar[dep_left >= 0 ? dep_left : 0][0]);
+  const unsigned a_loader = smaddr(&bar[kLoader][0]);
+  const unsigned a_war0 = smaddr(&bar[war0][0]);
+  const unsigned a_war1 = smaddr(&bar[war1 >= 0 ? war1 : 0][0]);
+  const unsigned a_war2 = smaddr(&bar[war2][0]);
+  const unsigned a_war3 = smaddr(&bar[war3 >= 0 ? war3 : 0][0]);
   double nw = bnd, nn = bnd, ne = bnd, cc = bnd, ee = bnd, sw = bnd, ss = bnd, se = bnd, ww = bnd, out = bnd;
 #ifdef GS2P_TRACE
   long long t_wait = 0, t_start = 0;
@@ -495,15 +514,28 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
 #endif
     // RAW: producers finished chunk k-1 (the loader: chunk k); WAR: readers
     // of my ring slots finished chunk k-5 (the ring holds 8 chunks)
-    if (g > 0) wait_chunk(dep_prev, k - 1);
-    if (dep_prev2 >= 0) wait_chunk(dep_prev2, k - 1);
-    if (dep_left >= 0) wait_chunk(dep_left, k - 1);
-    if (needs_io) wait_chunk(kLoader, k);
-    if (up_cl && g == 0) mbar_wait_cluster(&pbar[k & 7], (unsigned)(k >> 3) & 1u);
-    if (dn_cl && g == kG - 1 && k >= 8) mbar_wait(&pushed[(k - 8) & 7], (unsigned)((k - 8) >> 3) & 1u);
-    wait_chunk(war0, k - 5);
-    if (war1 >= 0) wait_chunk(war1, k - 5);
-    wait_chunk(war2, k - 5);
+#ifndef GS2P_NOWAIT
+    {
+      // slot offset / parity per chunk distance, barrier bases per warp (above)
+      const unsigned o1 = (unsigned)((k - 1) & 7) * 8u, q1 = (unsigned)((k - 1) >> 3) & 1u;
+      const unsigned o0 = (unsigned)(k & 7) * 8u, q0 = (unsigned)(k >> 3) & 1u;
+      const unsigned o5 = (unsigned)((k - 5) & 7) * 8u, q5 = (unsigned)((k - 5) >> 3) & 1u;
+      if (k >= 1) {
+        if (g > 0) mbar_wait_a(a_prev + o1, q1);
+        if (dep_prev2 >= 0) mbar_wait_a(a_prev2 + o1, q1);
+        if (dep_left >= 0) mbar_wait_a(a_left + o1, q1);
+      }
+      if (needs_io) mbar_wait_a(a_loader + o0, q0);
+      if (up_cl && g == 0) mbar_wait_cluster(&pbar[k & 7], q0);
+      if (dn_cl && g == kG - 1 && k >= 8) mbar_wait(&pushed[(k - 8) & 7], (unsigned)((k - 8) >> 3) & 1u);
+      if (k >= 5) {
+        mbar_wait_a(a_war0 + o5, q5);
+        if (war1 >= 0) mbar_wait_a(a_war1 + o5, q5);
+        mbar_wait_a(a_war2 + o5, q5);
+        if (war3 >= 0) mbar_wait_a(a_war3 + o5, q5);
+      }
+    }
+#endif
 #ifdef GS2P_TRACE
     t_wait += clock64() - tw0;
     if (k == 100 && lane == 0) {
@@ -524,15 +556,27 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
       double* pOut = base_cur + (cb & (kR - 1)) * kSlots + t + 2;
       const bool mirror = (cb & (kR - 1)) == 0;  // rows 0..kC-1 are mirrored at kR..kR+kC-1
       double outs[kC];
+      // every ring input of the chunk is loaded before the first ring store:
+      // the compiler cannot prove the stores do not alias the loads, so
+      // interleaved they would serialise each iteration's loads behind the
+      // previous iteration's whole accumulation chain.  (They do not alias:
+      // pNE/pE read group g-1's ring, pSE another warp's lane slot or the
+      // loader's slot 0, and everything read was published before this chunk.)
+      double in_ne[kC], in_e[kC], in_se[kC];
+#pragma unroll
+      for (int u = 0; u < kC; ++u) {
+        in_ne[u] = pNE[u * kSlots];
+        in_e[u] = pE[u * kSlots];
+        in_se[u] = pSE[u * kSlots];
+      }
       auto body = [&](auto pure_tag) {
         constexpr bool PURE = decltype(pure_tag)::value;
 #pragma unroll
         for (int u = 0; u < kC; ++u) {
-          const double ne_new = pNE[u * kSlots];
-          const double e_new = pE[u * kSlots];
+          const double ne_new = in_ne[u];
+          const double e_new = in_e[u];
           const double sh = __shfl_up_sync(0xffffffffu, out, 1);
-          const double sl = pSE[u * kSlots];
-          const double se_new = lane == 0 ? sl : sh;
+          const double se_new = lane == 0 ? in_se[u] : sh;
           nw = nn; nn = ne; ne = ne_new;
           cc = ee; ee = e_new;
           sw = ss; ss = se; se = se_new;
@@ -540,7 +584,7 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
           if constexpr (PURE) {
             out = v;
           } else {
-            out = mode == 0 ? v : (mode == 1 ? cc : bnd);
+            out = mode == 0 ? v : bnd;
           }
           ww = out;
           pOut[u * kSlots] = out;
@@ -571,7 +615,7 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
         sw = ss; ss = se; se = se_new;
         const double v = gs9<MASK>(wk, nw, nn, ne, ww, cc, ee, sw, ss, se);
         const bool inside = row_ok && j >= 0 && j < e1;
-        out = inside ? (real ? v : cc) : bnd;
+        out = inside ? v : bnd;
         ww = out;
         const int r = c & (kR - 1);
         base_cur[r * kSlots + t + 2] = out;
@@ -656,6 +700,9 @@ int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, in
   const int cs_req = cs_env ? cs_env : (a.c_end < 148 * 50 ? 8 : 1);
   auto launch = [&](auto cs_tag) -> int {
     constexpr int CS = decltype(cs_tag)::value;
+    if constexpr (CS > 1 && !kClusterOK) {
+      return TVS_ERR_UNSUPPORTED;  // cluster hand-off needs a whole-chunk phantom lag
+    } else {
     auto kern = mask == 0x1FFu ? gs2d_pipe_kernel<0x1FFu, CS> : gs2d_pipe_kernel<kStar, CS>;
     TVS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     Gs2pArgs b = a;
@@ -705,6 +752,7 @@ int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, in
       TVS_LAUNCHED("gs2d_pipe_kernel");
     }
     return TVS_OK;
+    }
   };
   int rc = TVS_ERR_UNSUPPORTED;
   if (cs_req == 8) rc = launch(std::integral_constant<int, 8>{});

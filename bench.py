@@ -121,7 +121,14 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, start):
+        """Host wall-clock bounds of the timed region (samples outside are dropped)."""
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
 
     def __exit__(self, *exc):
         if self.proc:
@@ -134,7 +141,10 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
+        t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", float("inf"))
+        for ts, line in self.lines:
+            if not t0 <= ts <= t1 + 0.05:
+                continue
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 6:
                 continue
@@ -156,7 +166,7 @@ def flush_l2(buf):
         buf.fill_(1.0)
 
 
-def device_time(cfg, K, W, sampler=None):
+def device_time(cfg, K, W, sampler=None, fma=None, min_timed_s=0.0):
     """Device-resident timing through the plan API: per-step ms (CUDA events
     on the plan stream) and launches per step.  Each step runs all T updates
     on the field left by the previous step (same work every step)."""
@@ -167,16 +177,24 @@ def device_time(cfg, K, W, sampler=None):
 
     spec = get(cfg["kernel"]).spec
     g = make_grid(cfg)
-    plan = _native.Plan(spec, cfg["extents"], config.current().native())
+    ex = config.current().native(**({"fma": fma} if fma else {}))
+    plan = _native.Plan(spec, cfg["extents"], ex)
     stream = torch.cuda.ExternalStream(plan.stream_handle())
     l2 = torch.empty(256 * 2 ** 20 // 8, dtype=torch.float64, device="cuda") if g.data.nbytes < 2 ** 30 else None
-    times, launches = [], 0
+    times, times_w, launches = [], [], 0
     plan.upload(g.data, g.offset)
     plan.synchronize()
     del g
-    for i in range(W + K):
+    if sampler is not None:
+        sampler.start()  # nvidia-smi needs ~0.1-0.5 s to start; samples are kept only inside the timed region
+    i = 0
+    while i < W + K:
+        if i == W and min_timed_s > 0 and times_w:
+            # short steps (configs 1-2: < 1 ms): time enough of them that the
+            # clock sampler sees the timed region
+            K = max(K, min(2000, int(min_timed_s * 1e3 / max(times_w[-1], 1e-3)) + 1))
         if i == W and sampler is not None:
-            sampler.start()
+            sampler.mark(True)
         if i >= W:
             flush_l2(l2)
         torch.cuda.synchronize()
@@ -188,7 +206,11 @@ def device_time(cfg, K, W, sampler=None):
         if i >= W:
             times.append(e0.elapsed_time(e1))
             launches = plan.last_launches()
+        else:
+            times_w.append(e0.elapsed_time(e1))
+        i += 1
     if sampler is not None:
+        sampler.mark(False)
         sampler.stop()
     plan.close()
     return times, launches
@@ -231,6 +253,7 @@ def cpu_sample(cfg, budget_s=12.0):
     gauss = spec.dependence_kind == "gauss_seidel"
     cores = 1 if gauss else (os.cpu_count() or 1)
     pts = int(np.prod(cfg["extents"]))
+    cref.scalar_reference(spec, g, 1, order="lexicographic", threads=cores)  # warm-up (first touch)
     t0 = time.perf_counter()
     cref.scalar_reference(spec, g, 1, order="lexicographic", threads=cores)
     one = time.perf_counter() - t0
@@ -244,17 +267,17 @@ def cpu_sample(cfg, budget_s=12.0):
     return rate, cores, desc
 
 
-def measure_config(cfg, K, W, with_e2e=True, with_cpu=True):
+def measure_config(cfg, K, W, with_e2e=True, with_cpu=True, min_timed_s=0.0):
     hbm_peak, peak_src = peaks()
     pts = int(np.prod(cfg["extents"]))
     updates = pts * cfg["T"]
     clk = ClockSampler()
-    times, launches = device_time(cfg, K, W, sampler=clk)
+    times, launches = device_time(cfg, K, W, sampler=clk, min_timed_s=min_timed_s)
     ms = statistics.mean(times)
     value = updates / (ms * 1e-3) / 1e9
     res = {
-        "value": value, "unit": "GStencil/s", "ms_per_step": ms, "ms_per_step_min": min(times), "steps": K,
-        "warmup": W, "gpu_launches": launches * K, "launches_per_step": launches, "clocks": clk.summary(),
+        "value": value, "unit": "GStencil/s", "ms_per_step": ms, "ms_per_step_min": min(times), "steps": len(times),
+        "warmup": W, "gpu_launches": launches * len(times), "launches_per_step": launches, "clocks": clk.summary(),
         "workload": f"{cfg['name']} {'x'.join(map(str, cfg['extents']))} T={cfg['T']}",
     }
     # per launch of the dominant kernel (every launch of a step is that kernel
@@ -417,10 +440,25 @@ def main():
                 continue
             try:
                 r = measure_config(c, max(2, min(args.steps, 3)), args.warmup, with_e2e=True,
-                                   with_cpu=not args.no_cpu)
+                                   with_cpu=not args.no_cpu, min_timed_s=0.25)
                 per[c["name"]] = {k: r[k] for k in ("value", "unit", "ms_per_step", "steps", "workload", "roofline",
                                                      "fp64", "e2e", "cpu_baseline", "clocks", "launches_per_step")
                                   if k in r}
+                if c["name"] == "3d27p_jacobi":
+                    # north_star tolerance mode: fused multiply-add (<= 1e-12 max relative
+                    # error vs the oracle, tests/test_gpu_parity.py::test_fma_policies);
+                    # `value` above stays the bit-exact default of the public API
+                    clk = ClockSampler()
+                    ft, _ = device_time(c, max(2, min(args.steps, 3)), args.warmup, sampler=clk, fma="allow")
+                    fms = statistics.mean(ft)
+                    fv = int(np.prod(c["extents"])) * c["T"] / (fms * 1e-3) / 1e9
+                    hbm_peak, _ = peaks()
+                    per[c["name"]]["fma_allow"] = {
+                        "value": fv, "unit": "GStencil/s", "ms_per_step": fms, "clocks": clk.summary(),
+                        "roofline": {"bound": "hbm", "achieved": fv * BYTES_PER_UPDATE, "peak": hbm_peak,
+                                     "unit": "GB/s", "frac": fv * BYTES_PER_UPDATE / hbm_peak},
+                        "note": "fma='allow': 27 DFMA per update instead of 27 DMUL + 26 DADD; within the "
+                                "north_star 1e-12 relative tolerance, not bit-exact"}
             except Exception as exc:  # report, never hide
                 per[c["name"]] = {"error": repr(exc)}
         line["per_stencil"] = per

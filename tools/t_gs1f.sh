@@ -1,0 +1,2 @@
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "gs1d or golden or known" -p no:cacheprovider 2>&1 | tail -2
+for T in 32 1000 4096; do timeout 60 python tools/profile_run.py --config 2 --T $T --reps 2 | tail -1; done

@@ -1,7 +1,7 @@
 """Command-line harness mirroring the reference CLI (tvstencil/cli.py:73-286).
 
     python -m paper_2010_04868_b200.cli --mode bench --kernel heat2d --nx 16384 --ny 16384 --t 200 --reps 5
-    python -m paper_2010_04868_b200.cli --mode verify --kernel all --cells 8
+    python -m paper_2010_04868_b200.cli --mode verify --kernel all --cells 20
 
 Same flags, JSON ``--config`` defaults (explicit flags win), metric
 (GStencil/s = interior points x T / median seconds / 1e9, cli.py:228-231),
@@ -55,7 +55,7 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--csv", help="append benchmark rows to this file")
     p.add_argument("--dump", help="write the final grid dump (TSTN) here")
     p.add_argument("--seed", type=int, default=0)
-    p.add_argument("--cells", type=int, default=8, help="verify-mode cells per kernel")
+    p.add_argument("--cells", type=int, default=20, help="verify-mode cells per kernel (reference acceptance: 20)")
     p.add_argument("--config", help="JSON file with flag defaults")
     p.add_argument("--order", default="lexicographic", choices=("lexicographic", "reference"),
                    help="Gauss-Seidel update order (2D/3D)")

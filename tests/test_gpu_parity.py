@@ -13,7 +13,7 @@ from conftest import grid_from, spec_for
 from oracle import cref
 from oracle import oracle as npo
 from paper_2010_04868_b200 import Grid, _native, config
-from paper_2010_04868_b200.catalog import get
+from paper_2010_04868_b200.catalog import DEFAULT_CATALOG, get
 from paper_2010_04868_b200.kernels import KernelVariant, gs1d_temporal, gs2d_temporal, heat1d_temporal
 from paper_2010_04868_b200.kernels._common import execute
 from paper_2010_04868_b200.verify import default_matrix, equivalence_matrix, run_temporal
@@ -46,15 +46,30 @@ def test_known_answers_gpu(cuda_ready):
 
 
 def test_equivalence_matrix_gpu(cuda_ready):
-    """The reference's acceptance-matrix shape (verify.py:169-222), 8 cells
-    per kernel, GPU runner vs oracle.  GS in 2D/3D compares against the
+    """The reference's acceptance matrix (verify.py:169-222 with
+    test_acceptance.py:35's 20 cells per kernel) over every float64 catalog
+    kernel, GPU runner vs oracle.  GS in 2D/3D compares against the
     lexicographic oracle (the GPU default order)."""
-    cells = default_matrix(cells_per_kernel=8, master_seed=2024)
+    cells = default_matrix(cells_per_kernel=20, master_seed=2024)
 
     def reference(spec, grid, steps):
         return cref.scalar_reference(spec, grid, steps, order="lexicographic", threads=8)
 
     rep = equivalence_matrix(cells, reference)
+    assert rep.passed, rep.to_json()
+
+
+def test_equivalence_matrix_gpu_reference_order(cuda_ready):
+    """The same 20-cell matrix for the Gauss-Seidel kernels in the reference
+    oracle's own anti-diagonal order (baselines.py:83-107), GPU runner with
+    order="reference" vs the NumPy restatement of scalar_reference."""
+    gs = [k for k in ("gs2d", "gs2d9p", "gs3d") if k in DEFAULT_CATALOG]
+    cells = default_matrix(cells_per_kernel=20, master_seed=2024, kernels=gs)
+
+    def runner(kernel, grid, steps, variant):
+        return run_temporal(kernel, grid, steps, variant, order="reference")
+
+    rep = equivalence_matrix(cells, lambda spec, grid, steps: npo.scalar_reference(spec, grid, steps), runner)
     assert rep.passed, rep.to_json()
 
 

@@ -27,7 +27,7 @@
 
 namespace tvs {
 
-constexpr int kMaxD2 = 12;     // deepest temporal block instantiated (P = 4 up to D = 8, P = 2 above)
+constexpr int kMaxD2 = 12;     // deepest temporal block instantiated (P = 4 / 3 / 2 columns per lane, see launch2d_one)
 constexpr int kWarps2 = 1;     // warps per block (task = blockIdx.x: warp-uniform control flow)
 #ifndef J2D_SEG
 #define J2D_SEG 256
@@ -235,7 +235,7 @@ bool jacobi2d_blocked_supported(const tvs_stencil& st) {
 }
 
 int jacobi2d_max_depth() { return kMaxD2; }
-int jacobi2d_default_depth() { return 8; }  // measured best (config 3: D=4 1235, 6 1540, 8 1593 GSt/s)
+int jacobi2d_default_depth() { return 8; }  // measured best (config 3, P = 3: D = 6 1392, 7 1593, 8 1723, 10 1576 GSt/s)
 
 template <unsigned MASK, int D, int P>
 static void launch2d_d(bool fma, unsigned blocks, cudaStream_t s, const double* src, double* dst, const Geo& geo,
@@ -249,7 +249,10 @@ static void launch2d_d(bool fma, unsigned blocks, cudaStream_t s, const double* 
 template <unsigned MASK, int D>
 static void launch2d_one(bool fma, cudaStream_t s, const double* src, double* dst, const Geo& geo, int64_t origin,
                          const Coeff9& cf, double bnd) {
-  constexpr int P = D <= 8 ? 4 : 2;
+  // columns per lane: registers grow as 2 * P * D accumulators; P = 3 at
+  // D = 5..8 keeps 12 warps/SM at D = 8 (168 registers) where P = 4 held 9
+  // (config 3: D = 8 P = 4 1596, P = 3 1723 GSt/s; D > 8 at P = 3 is slower)
+  constexpr int P = D <= 4 ? 4 : (D <= 8 ? 3 : 2);
   const int64_t U = 32 * P - 2 * D;
   const int64_t ns = (geo.e1 + U - 1) / U;
   const int64_t nseg = (geo.e0 + kRowsSeg - 1) / kRowsSeg;

@@ -1,7 +1,7 @@
 // C-ABI entry points of libtvstencil.so (include/tvstencil.h).
 //
 // Dispatch:
-//   Jacobi 1D        -> jacobi1d_blocked   (register trapezoid, up to 64 steps/launch)
+//   Jacobi 1D        -> jacobi1d_blocked   (register trapezoid, default 64 steps/launch)
 //   Jacobi 2D star/box -> jacobi2d_blocked (warp strips, D levels per HBM pass)
 //   Jacobi 3D star/box -> jacobi3d_streaming (2.5D plane streaming, 1 step/launch)
 //   Jacobi other     -> jacobi_naive_step  (generic taps, 1 step/launch)
@@ -231,8 +231,8 @@ static int jacobi_device(const tvs_stencil& st, const tvs_geometry& g, double* s
     int rc;
     int step_now = 1;
     if (!naive && g.dim == 1 && jacobi1d_blocked_supported(st, g)) {
-      int depth = ex.temporal_depth > 0 ? ex.temporal_depth : 64;
-      step_now = (int)std::min<int64_t>(left, std::min(depth, 64));
+      int depth = ex.temporal_depth > 0 ? ex.temporal_depth : jacobi1d_default_depth();
+      step_now = (int)std::min<int64_t>(left, std::min(depth, jacobi1d_max_depth()));
       rc = jacobi1d_blocked(st, g, a, b, step_now, fma, s);
     } else if (!naive && g.dim == 2 && jacobi2d_blocked_supported(st)) {
       int depth = ex.temporal_depth > 0 ? ex.temporal_depth : jacobi2d_default_depth();

@@ -195,6 +195,8 @@ int jacobi_naive_step(const tvs_stencil& st, const tvs_geometry& g, const double
 bool jacobi1d_blocked_supported(const tvs_stencil& st, const tvs_geometry& g);
 int jacobi1d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
                      int depth, bool fma, cudaStream_t s);
+int jacobi1d_default_depth();
+int jacobi1d_max_depth();
 bool jacobi2d_blocked_supported(const tvs_stencil& st);
 int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
                      int depth, bool fma, cudaStream_t s);

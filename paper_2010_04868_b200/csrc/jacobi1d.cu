@@ -16,12 +16,21 @@
 // data (2^20 points = 8 MiB) stays L2-resident between launches, so the
 // kernel is FP64-issue bound: 5 DP ops / update unfused, 3 with the exact
 // power-of-two FMA form (heat1d: 0.25/0.5/0.25).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace tvs {
 
-constexpr int kP1 = 32;      // points per lane
-constexpr int kWarps1 = 8;   // warps per block
+#ifndef J1D_P
+#define J1D_P 32
+#endif
+#ifndef J1D_DEPTH
+#define J1D_DEPTH 64
+#endif
+constexpr int kP1 = J1D_P;          // points per lane
+constexpr int kMaxDepth1 = 2 * J1D_DEPTH;  // deepest block a launch accepts
+constexpr int kWarps1 = 8;          // warps per block
 
 template <unsigned MASK, bool FMA>
 __device__ __forceinline__ double upd1(double l, double c, double r, const double w[3]) {
@@ -107,6 +116,9 @@ static void launch1d(bool fma, unsigned blocks, cudaStream_t s, const double* sr
     jacobi1d_kernel<MASK, false><<<blocks, kWarps1 * 32, 0, s>>>(src, dst, n, depth, w[0], w[1], w[2], bnd);
 }
 
+int jacobi1d_default_depth() { return J1D_DEPTH; }
+int jacobi1d_max_depth() { return std::min(kMaxDepth1, 16 * kP1 - 1); }
+
 bool jacobi1d_blocked_supported(const tvs_stencil& st, const tvs_geometry& g) {
   double w[3];
   return slots1d(st, w) > 0 && g.axis0_offset == 0 && g.axis0_global == g.extents[0];
@@ -116,8 +128,8 @@ int jacobi1d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double*
                      bool fma, cudaStream_t s) {
   double w[3];
   const int mask = slots1d(st, w);
-  if (mask <= 0 || depth < 1 || depth > 64)
-    return fail(TVS_ERR_UNSUPPORTED, "jacobi1d_blocked: unsorted taps or depth outside 1..64");
+  if (mask <= 0 || depth < 1 || depth > kMaxDepth1 || 2 * depth >= 32 * kP1)
+    return fail(TVS_ERR_UNSUPPORTED, "jacobi1d_blocked: unsorted taps or depth out of range");
   const int64_t n = g.extents[0];
   const int64_t useful = 32 * kP1 - 2 * depth;
   const int64_t warps = (n + useful - 1) / useful;

@@ -1,0 +1,2 @@
+TVSTENCIL_LIB=build/var/lib_p2.so timeout 120 python tools/parity_quick.py heat2d | tail -1
+for d in 6 8 10 12; do echo -n "P2 "; TVSTENCIL_LIB=build/var/lib_p2.so timeout 60 python tools/profile_run.py --config 3 --depth $d --reps 3 | tail -1; done

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -272,6 +273,8 @@ struct RunCtx {
   int nbuf = 0;
   cudaStream_t stream = nullptr;
   tvs_geometry geo{};
+  std::vector<cudaStream_t> bands;  // pipelined 2D Jacobi: one stream per row band
+  std::vector<cudaEvent_t> events;  // pool (timing disabled)
   ~RunCtx() { release(); }
   void release() {
     if (device >= 0) {
@@ -281,6 +284,10 @@ struct RunCtx {
       for (auto& b : buf)
         if (b) cudaFree(b), b = nullptr;
       if (stream) cudaStreamDestroy(stream), stream = nullptr;
+      for (auto& b : bands) cudaStreamDestroy(b);
+      for (auto& e : events) cudaEventDestroy(e);
+      bands.clear();
+      events.clear();
       cudaSetDevice(cur);
     }
     device = -1;
@@ -308,6 +315,135 @@ static int ensure_ctx(RunCtx& c, int device, int dim, const int64_t* ext, int nb
     }
   }
   c.nbuf = nbuf;
+  return TVS_OK;
+}
+
+// ---- pipelined host -> device -> host path for 2D temporally blocked Jacobi --
+// tvs_run on host buffers: instead of upload-all / T steps / download-all,
+// rows are split into bands (512 rows).  Band b's launch k (depth D <= 12,
+// so its halo lies in bands b-1..b+1) depends only on launches k-1 of bands
+// b-1, b, b+1 — they write the rows it reads and read the rows it
+// overwrites in the other ping-pong buffer.  Every band has its own stream;
+// uploads run band by band on the copy stream, each band's launches wait on
+// its neighbours' events, and each band downloads as soon as its last launch
+// ends.  Measured (config 3, 16384^2 x 200, pinned host buffers): 108 ms
+// single-stream -> 94 ms with 512-row bands; the dependency cone (band b's
+// last launch needs bands b +- K uploaded) keeps the first download behind
+// most of the upload, so full three-way overlap would need overlapped tiling
+// (private per-band buffers with redundant halo rows) — not done.  Early bands therefore compute while later bands upload and download
+// while the tail computes (PCIe is full duplex).  Same kernels, same
+// arithmetic: bit-identical to the single-stream path.
+static int band_rows_default() {
+  static const int v = [] {
+    const char* e = getenv("TVS_E2E_BANDS");  // 0 disables the pipelined path
+    return e ? atoi(e) : 2 * jacobi2d_band_rows();  // 512 rows (256: 141 ms, 1024: 95 ms)
+  }();
+  return v;
+}
+
+static int copy_rows(const tvs_geometry& g, double* dev, const tvs_layout& lay, double* host, bool upload,
+                     int64_t r0, int64_t r1, cudaStream_t s) {
+  double* d0 = dev + g.origin + r0 * g.strides[0];
+  double* h0 = host + (lay.offset + r0) * lay.shape[1] + lay.offset;
+  const size_t hp = sizeof(double) * lay.shape[1], dp = sizeof(double) * g.strides[0];
+  const size_t w = sizeof(double) * g.extents[1];
+  if (upload)
+    TVS_CUDA(cudaMemcpy2DAsync(d0, dp, h0, hp, w, r1 - r0, cudaMemcpyHostToDevice, s));
+  else
+    TVS_CUDA(cudaMemcpy2DAsync(h0, hp, d0, dp, w, r1 - r0, cudaMemcpyDeviceToHost, s));
+  return TVS_OK;
+}
+
+static int jacobi2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, const double* in, double* out,
+                              int64_t steps, const tvs_exec& ex, RunCtx& c, int64_t band) {
+  const tvs_geometry& g = c.geo;
+  const int64_t rows = g.extents[0];
+  const int nb = (int)((rows + band - 1) / band);
+  int depth = ex.temporal_depth > 0 ? ex.temporal_depth : jacobi2d_default_depth();
+  depth = std::min(depth, jacobi2d_max_depth());
+  const int K = (int)((steps + depth - 1) / depth);
+  const bool fma = use_fma(st, ex);
+  while ((int)c.bands.size() < nb) {
+    cudaStream_t t;
+    TVS_CUDA(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+    c.bands.push_back(t);
+  }
+  auto bs = [&](int b) { return c.bands[b]; };
+  const size_t nev = (size_t)nb * (K + 1);
+  while (c.events.size() < nev) {
+    cudaEvent_t e;
+    TVS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.events.push_back(e);
+  }
+  auto up = [&](int b) { return c.events[b]; };                               // band b uploaded
+  auto done = [&](int b, int k) { return c.events[(size_t)nb * (k + 1) + b]; };  // launch k of band b ended
+  cudaStream_t cs = c.stream;
+  int rc;
+  // TVS_E2E_TRACE=1: stderr timeline (upload start/end, first and last download)
+  static const bool trace = getenv("TVS_E2E_TRACE") != nullptr;
+  cudaEvent_t tr[5] = {};
+  if (trace)
+    for (auto& e : tr) cudaEventCreate(&e);
+  if (trace) cudaEventRecord(tr[0], cs);
+  if ((rc = fill_halo(g, c.buf[0], st.boundary, cs))) return rc;
+  if ((rc = fill_halo(g, c.buf[1], st.boundary, cs))) return rc;
+  // Enqueue in wavefront order.  Streams share a few hardware queues
+  // (CUDA_DEVICE_MAX_CONNECTIONS, default 8), so an operation can end up
+  // queued behind unrelated work enqueued before it: issuing every upload
+  // first put band kernels behind the whole 2 GB upload.  At step t: upload
+  // band t, then every launch (b, k) whose inputs are then uploaded
+  // (b + k + 1 = t), then the download of the band whose last launch was
+  // just issued.  Every event waited on was recorded earlier in host order.
+  std::vector<int> dk(K);
+  {
+    int64_t left = steps;
+    for (int k = 0; k < K; ++k) {
+      dk[k] = (int)std::min<int64_t>(left, depth);
+      left -= dk[k];
+    }
+  }
+  double* result = c.buf[K & 1];
+  const auto h0 = std::chrono::steady_clock::now();
+  for (int t = 0; t <= nb + K; ++t) {
+    if (t < nb) {
+      if ((rc = copy_rows(g, c.buf[0], lay, const_cast<double*>(in), true, t * band, std::min(rows, (t + 1) * band), cs)))
+        return rc;
+      TVS_CUDA(cudaEventRecord(up(t), cs));
+      if (trace && t == nb - 1) cudaEventRecord(tr[1], cs);
+    }
+    for (int k = 0; k < K; ++k) {
+      const int b = t - 1 - k;  // (b, k) reads bands b-1..b+1 after launch k-1 (or their upload)
+      if (b < 0 || b >= nb) continue;
+      cudaStream_t sb = bs(b);
+      for (int nbr = b - 1; nbr <= b + 1; ++nbr) {
+        if (nbr < 0 || nbr >= nb) continue;
+        if (k == 0)
+          TVS_CUDA(cudaStreamWaitEvent(sb, up(nbr), 0));
+        else
+          TVS_CUDA(cudaStreamWaitEvent(sb, done(nbr, k - 1), 0));
+      }
+      if ((rc = jacobi2d_blocked(st, g, c.buf[k & 1], c.buf[(k + 1) & 1], dk[k], fma, sb, b * band,
+                                 std::min(rows, (b + 1) * band))))
+        return rc;
+      TVS_CUDA(cudaEventRecord(done(b, k), sb));
+    }
+    const int bd = t - K;  // its launch K-1 was issued in this step (t = bd + K)
+    if (bd >= 0 && bd < nb) {
+      if (trace && bd == 0) cudaEventRecord(tr[2], bs(0));
+      if ((rc = copy_rows(g, result, lay, out, false, bd * band, std::min(rows, (bd + 1) * band), bs(bd)))) return rc;
+      if (trace && bd == 0) cudaEventRecord(tr[3], bs(0));
+    }
+  }
+  const double host_up_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+  for (int b = 0; b < nb; ++b) TVS_CUDA(cudaStreamSynchronize(bs(b)));
+  if (trace) cudaEventRecord(tr[4], cs);
+  if (trace) {
+    float t[5] = {};
+    for (int i = 1; i < 5; ++i) cudaEventElapsedTime(&t[i], tr[0], tr[i]);
+    fprintf(stderr, "[e2e] bands %d x %lld rows, K %d: uploads done %.2f ms, band0 D2H %.2f-%.2f ms, last D2H end %.2f ms"
+            " (host enqueue %.2f ms)\n", nb, (long long)band, K, t[1], t[2], t[3], t[4], host_up_ms);
+    for (auto& e : tr) cudaEventDestroy(e);
+  }
   return TVS_OK;
 }
 
@@ -421,6 +557,12 @@ int tvs_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, doub
   if ((rc = ensure_ctx(g_run, ex->device, st->dim, lay->extents, gs ? 1 : 2))) return rc;
   RunCtx& c = g_run;
   cudaStream_t s = c.stream;
+  if (!gs) {
+    const int64_t band = band_rows_default();
+    if (band > 0 && st->dim == 2 && steps > 0 && ex->algo != TVS_ALGO_NAIVE && jacobi2d_blocked_supported(*st) &&
+        band % jacobi2d_band_rows() == 0 && c.geo.extents[0] >= 4 * band)
+      return jacobi2d_pipelined(*st, *lay, in, out, steps, *ex, c, band);
+  }
   if ((rc = fill_halo(c.geo, c.buf[0], st->boundary, s))) return rc;
   if ((rc = copy_interior(c.geo, c.buf[0], *lay, const_cast<double*>(in), true, s))) return rc;
   double* result = c.buf[0];

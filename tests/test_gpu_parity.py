@@ -293,3 +293,17 @@ def test_gs2d_pipeline_cluster_sizes(cuda_ready, cluster):
     r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "gs2d_cluster_check.py")],
                        env=env, capture_output=True, text=True, timeout=180)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("band", [0, 512, 1024, 2048])
+def test_jacobi2d_pipelined_e2e_bands(cuda_ready, band):
+    """tvs_run's pipelined 2D Jacobi path (row bands on their own streams,
+    uploads / launches / downloads overlapped by events) is bit-identical to
+    the oracle for several band sizes; band 0 = the single-stream path."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, TVS_E2E_BANDS=str(band))
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "e2e_band_check.py")],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr

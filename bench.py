@@ -166,7 +166,7 @@ def flush_l2(buf):
         buf.fill_(1.0)
 
 
-def device_time(cfg, K, W, sampler=None, fma=None, min_timed_s=0.0):
+def device_time(cfg, K, W, sampler=None, fma=None, min_timed_s=0.0, algo=None):
     """Device-resident timing through the plan API: per-step ms (CUDA events
     on the plan stream) and launches per step.  Each step runs all T updates
     on the field left by the previous step (same work every step)."""
@@ -177,7 +177,7 @@ def device_time(cfg, K, W, sampler=None, fma=None, min_timed_s=0.0):
 
     spec = get(cfg["kernel"]).spec
     g = make_grid(cfg)
-    ex = config.current().native(**({"fma": fma} if fma else {}))
+    ex = config.current().native(**({"fma": fma} if fma else {}), **({"algo": algo} if algo else {}))
     plan = _native.Plan(spec, cfg["extents"], ex)
     stream = torch.cuda.ExternalStream(plan.stream_handle())
     l2 = torch.empty(256 * 2 ** 20 // 8, dtype=torch.float64, device="cuda") if g.data.nbytes < 2 ** 30 else None
@@ -312,6 +312,33 @@ def measure_config(cfg, K, W, with_e2e=True, with_cpu=True, min_timed_s=0.0):
     return res
 
 
+def untiled_legs(args):
+    """North_star: "untiled kernels reach >= 70% of HBM peak".  The
+    single-step kernel (K1, algo='naive': one time step per HBM pass, no
+    temporal blocking) on the full config-3 grid, and config 5's own kernel,
+    which is single-step by construction (2.5D plane streaming).  Effective
+    bandwidth = 16 B x update rate; ncu DRAM bytes per launch in profiles/."""
+    hbm_peak, _ = peaks()
+    out = {}
+    for cid, algo, T in ((3, "naive", 20), (5, "auto", 10)):
+        c = dict(CONFIGS[cid], T=T)
+        try:
+            clk = ClockSampler()
+            t, launches = device_time(c, max(2, min(args.steps, 3)), args.warmup, sampler=clk, algo=algo)
+            ms = statistics.mean(t)
+            v = int(np.prod(c["extents"])) * T / (ms * 1e-3) / 1e9
+            out[c["name"]] = {
+                "kernel": "jacobi_naive_kernel" if algo == "naive" else "jacobi3d_kernel",
+                "value": v, "unit": "GStencil/s", "steps_per_run": T, "launches_per_run": launches,
+                "ms_per_run": ms, "clocks": clk.summary(),
+                "roofline": {"bound": "hbm", "achieved": v * BYTES_PER_UPDATE, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": v * BYTES_PER_UPDATE / hbm_peak},
+            }
+        except Exception as exc:  # report, never hide
+            out[c["name"]] = {"error": repr(exc)}
+    return out
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU path (oracle port) on the host."""
     rank = int(os.environ.get("RANK", "0"))
@@ -433,6 +460,7 @@ def main():
         "gpu_launches": head["gpu_launches"], "clocks": head["clocks"], "e2e": head.get("e2e"),
         "roofline": head["roofline"], "fp64": head["fp64"], "cpu_baseline": head.get("cpu_baseline"),
     }
+    line["untiled"] = untiled_legs(args)
     if not args.no_all:
         per = {}
         for cid, c in CONFIGS.items():

@@ -152,6 +152,40 @@ def test_jacobi3d_streaming(cuda_ready, kernel, ext):
         assert np.array_equal(got.interior, want.interior), algo
 
 
+@pytest.mark.parametrize("n", [1, 7, 255, 256, 2047, 2048, 2049, 4096 + 300, 20000])
+def test_naive_1d_tiles(cuda_ready, n):
+    """Single-step kernel: full 2048-element tiles and ragged tails."""
+    g = Grid.random((n,), seed=n, boundary=0.25)
+    for kernel in ("heat1d", "gs1d_w343"):
+        spec = dataclasses.replace(spec_for(kernel, 0.25), dependence_kind="jacobi")
+        want = cref.scalar_reference(spec, g, 7)
+        got = execute(spec, g, 7, algo="naive", fma="never")
+        assert np.array_equal(got.interior, want.interior), kernel
+
+
+@pytest.mark.parametrize("ext", [(64, 64, 64), (5, 67, 33), (3, 64, 31)])
+def test_naive_generic_taps(cuda_ready, ext):
+    """Single-step kernel with a tap count it does not specialise (runtime
+    tap loop): a 3D 10-tap stencil and a 2D 4-tap stencil."""
+    from paper_2010_04868_b200.model import StencilSpec
+
+    rng = np.random.default_rng(11)
+    offs3 = [(-1, 0, 0), (0, -1, 1), (0, 0, -1), (0, 0, 0), (0, 0, 1), (0, 1, -1), (1, -1, -1), (1, 0, 0),
+             (1, 1, 0), (1, 1, 1)]
+    spec3 = StencilSpec(name="t10", dim=3, radius=1, shape="box", dependence_kind="jacobi",
+                        coefficients={o: float(w) for o, w in zip(offs3, rng.uniform(0, 0.2, len(offs3)))})
+    g = Grid.random(ext, seed=3)
+    want = cref.scalar_reference(spec3, g, 4)
+    assert np.array_equal(execute(spec3, g, 4, algo="naive", fma="never").interior, want.interior)
+    assert np.array_equal(execute(spec3, g, 4, fma="never").interior, want.interior)
+    offs2 = [(-1, 1), (0, -1), (0, 0), (1, 1)]
+    spec2 = StencilSpec(name="t4", dim=2, radius=1, shape="box", dependence_kind="jacobi",
+                        coefficients={o: float(w) for o, w in zip(offs2, rng.uniform(0, 0.3, 4))})
+    g2 = Grid.random(ext[1:], seed=4)
+    want2 = cref.scalar_reference(spec2, g2, 5)
+    assert np.array_equal(execute(spec2, g2, 5, algo="naive", fma="never").interior, want2.interior)
+
+
 def test_fma_policies(cuda_ready):
     """exact: power-of-two weights fuse bit-identically; allow: tolerance."""
     g = Grid.random((300, 301), seed=2)
@@ -204,10 +238,12 @@ def test_plan_api_accumulates_steps(cuda_ready):
         plan.close()
 
 
-def test_slab_decomposition_emulated_ranks(cuda_ready):
+@pytest.mark.parametrize("algo", ["auto", "naive"])
+def test_slab_decomposition_emulated_ranks(cuda_ready, algo):
     """The sharded path's device side on one GPU: W emulated ranks, halos
     copied between their buffers (no cross-rank waiting), bit-identical to
-    the single-domain result for W in 1..4 and several depths."""
+    the single-domain result for W in 1..4 and several depths (blocked and
+    single-step kernels)."""
     import torch
 
     from paper_2010_04868_b200 import halo
@@ -243,7 +279,7 @@ def test_slab_decomposition_emulated_ranks(cuda_ready):
                         import ctypes as C
 
                         in_dst = C.c_int32(0)
-                        ex = _native.make_exec(temporal_depth=depth)
+                        ex = _native.make_exec(temporal_depth=depth, algo=_native.ALGO_NAIVE if algo == "naive" else _native.ALGO_AUTO)
                         _native.check(_native.lib().tvs_jacobi_device(
                             C.byref(st), C.byref(lay.geometry), C.c_void_p(pair[cur].data_ptr()),
                             C.c_void_p(pair[1 - cur].data_ptr()), k, C.byref(ex),

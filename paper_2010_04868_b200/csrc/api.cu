@@ -3,7 +3,7 @@
 // Dispatch:
 //   Jacobi 1D        -> jacobi1d_blocked   (register trapezoid, default 64 steps/launch)
 //   Jacobi 2D star/box -> jacobi2d_blocked (warp strips, D levels per HBM pass)
-//   Jacobi 3D star/box -> jacobi3d_streaming (2.5D plane streaming, 1 step/launch)
+//   Jacobi 3D star/box -> jacobi3d_blocked2 (2 levels/launch) + jacobi3d_streaming (2.5D, 1 step/launch)
 //   Jacobi other     -> jacobi_naive_step  (generic taps, 1 step/launch)
 //   Gauss-Seidel 1D  -> gs1d_pipeline      (time-skewed warp pipeline)
 //   Gauss-Seidel 2D lexicographic -> gs2d_pipeline (time-lane chain)
@@ -241,7 +241,14 @@ static int jacobi_device(const tvs_stencil& st, const tvs_geometry& g, double* s
       step_now = (int)std::min<int64_t>(left, depth);
       rc = jacobi2d_blocked(st, g, a, b, step_now, fma, s);
     } else if (!naive && g.dim == 3 && jacobi3d_streaming_supported(st)) {
-      rc = jacobi3d_streaming(st, g, a, b, fma, s);
+      int depth = ex.temporal_depth > 0 ? ex.temporal_depth : jacobi3d_default_depth();
+      depth = std::min(depth, jacobi3d_max_depth());
+      if (depth >= 2 && left >= 2) {
+        step_now = 2;
+        rc = jacobi3d_blocked2(st, g, a, b, fma, s);
+      } else {
+        rc = jacobi3d_streaming(st, g, a, b, fma, s);
+      }
     } else {
       rc = jacobi_naive_step(st, g, a, b, fma, s);
     }

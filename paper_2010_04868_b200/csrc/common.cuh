@@ -206,6 +206,10 @@ int jacobi2d_band_rows();
 int jacobi2d_max_depth();
 int jacobi2d_default_depth();
 bool jacobi3d_streaming_supported(const tvs_stencil& st);
+int jacobi3d_max_depth();
+int jacobi3d_default_depth();
+int jacobi3d_blocked2(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, bool fma,
+                      cudaStream_t s);
 int jacobi3d_streaming(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
                        bool fma, cudaStream_t s);
 int gs1d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s);

@@ -155,6 +155,154 @@ __global__ void __launch_bounds__(kThreads3) jacobi3d_kernel(const double* __res
   }
 }
 
+// ---- K4b: two time levels per HBM pass ---------------------------------
+//
+// Temporal blocking of K4 (north_star: "several time steps are advanced per
+// HBM round-trip").  A block owns a 64 x 32 frame of axis-2 x axis-1
+// positions (frame (i, j) = global (y0-1+i, x0-1+j)) and streams along axis
+// 0.  Per input plane p (staged once in shared memory by 16-byte cp.async,
+// 34 x 68 cells = the frame plus a 1-cell ring):
+//   level 1: every frame position takes the plane's 3x3 taps (finishing
+//            level-1 plane p-1, continuing p, starting p+1) — the K4 partial
+//            sums — and the finished plane p-1 is written to a shared level-1
+//            buffer (cells outside the domain pinned to the boundary, exactly
+//            what a single step reads from the memory halo);
+//   level 2: after one barrier, every frame position takes level-1 plane
+//            p-1's 3x3 taps, finishing level-2 plane p-2, which is stored for
+//            the inner 62 x 30 positions.
+// Both levels use K4's accumulation order (sorted taps: plane -1, 0, +1,
+// each row-major), so two levels equal two K4 launches bit for bit.  HBM
+// traffic per update ~ (8 B x 34*68/(62*30) + 8 B) / 2 ~ 9 B instead of 16.
+constexpr int kTBW = 64;               // frame width (2 columns per lane)
+constexpr int kTBH = 32;               // frame height (8 warps x kRY rows)
+constexpr int kTBOX = kTBW - 2;        // useful output columns per block
+constexpr int kTBOY = kTBH - 2;        // useful output rows per block
+constexpr int kTBP = 68;               // smem pitch (frame + ring, 16-byte rows)
+constexpr int kTBR = kTBH + 2;         // smem rows
+constexpr int kTBChunks = kTBR * (kTBP / 2);
+constexpr int kTBSlots = (kTBChunks + kThreads3 - 1) / kThreads3;
+constexpr int kTBPlanesSeg = 64;       // output planes per block
+constexpr size_t kTBSmem = (size_t)(3 + 2) * kTBR * kTBP * sizeof(double);
+
+template <unsigned MASK, bool FMA>
+__device__ __forceinline__ void tb_level(const double* __restrict__ plane, int w, int lane, double (&A)[2][kRY],
+                                         double (&B)[2][kRY], double (&out)[2][kRY], const double* c) {
+  constexpr bool G0 = has_plane<MASK>(0), G1 = has_plane<MASK>(1), G2 = has_plane<MASK>(2);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double v[kRY + 2][3];
+    const double* b = plane + (w * kRY) * kTBP + lane + 32 * h;
+#pragma unroll
+    for (int rr = 0; rr < kRY + 2; ++rr)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) v[rr][k] = b[rr * kTBP + k];
+    if constexpr (G2) add_plane<MASK, 2, !(G0 || G1), FMA>(B[h], v, c);
+#pragma unroll
+    for (int r = 0; r < kRY; ++r) out[h][r] = B[h][r];
+#pragma unroll
+    for (int r = 0; r < kRY; ++r) B[h][r] = A[h][r];
+    if constexpr (G1) add_plane<MASK, 1, !G0, FMA>(B[h], v, c);
+    if constexpr (G0) add_plane<MASK, 0, true, FMA>(A[h], v, c);
+  }
+}
+
+template <unsigned MASK, bool FMA>
+__global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double* __restrict__ src,
+                                                                   double* __restrict__ dst, Geo g, int64_t origin,
+                                                                   Coeff27 cf, double bnd) {
+  extern __shared__ __align__(16) double tb_smem[];
+  double* l0 = tb_smem;                       // 3 staged input planes
+  double* l1 = tb_smem + 3 * kTBR * kTBP;     // 2 level-1 planes (frame at +1,+1)
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const int tid = w * 32 + lane;
+  const int64_t x0 = (int64_t)blockIdx.x * kTBOX, y0 = (int64_t)blockIdx.y * kTBOY;
+  const int64_t p0 = (int64_t)blockIdx.z * kTBPlanesSeg;
+  const int64_t p1 = min(p0 + kTBPlanesSeg, g.e0);  // level-2 outputs [p0, p1)
+
+  // staging slots: smem cell (row i, col 2c) <- global (y0-2+i, x0-2+2c);
+  // rows/columns beyond the memory halo are never needed (their level-1
+  // positions are pinned) and are not read
+  int soff[kTBSlots];
+  int64_t goff[kTBSlots];
+  bool sval[kTBSlots];
+#pragma unroll
+  for (int k = 0; k < kTBSlots; ++k) {
+    const int e = tid + k * kThreads3;
+    const int i = e / (kTBP / 2), c2 = e % (kTBP / 2);
+    const int64_t y = y0 - 2 + i, x = x0 - 2 + 2 * c2;
+    soff[k] = i * kTBP + 2 * c2;
+    goff[k] = y * g.s1 + x;
+    sval[k] = e < kTBChunks && y >= -1 && y <= g.e1 && x <= g.e2;
+  }
+  const double* base = src + origin;
+  auto stage = [&](int64_t p) {
+    if (p >= -1 && p <= g.e0) {
+      const double* pb = base + p * g.s0;
+      double* tb = l0 + (int)((p - p0 + 3) % 3) * (kTBR * kTBP);
+#pragma unroll
+      for (int k = 0; k < kTBSlots; ++k)
+        if (sval[k]) cp_async16(tb + soff[k], pb + goff[k]);
+    }
+    cp_async_commit();
+  };
+
+  // per-thread frame positions: rows i = w*kRY + r, columns j = lane + 32h
+  unsigned in_dom = 0;   // bit (h*kRY + r): level-1 position inside the domain (axes 1, 2)
+  unsigned store_ok = 0; // bit (h*kRY + r): useful level-2 output
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int r = 0; r < kRY; ++r) {
+      const int i = w * kRY + r, j = lane + 32 * h;
+      const int64_t y = y0 - 1 + i, x = x0 - 1 + j;
+      const bool dom = y >= 0 && y < g.e1 && x >= 0 && x < g.e2;
+      in_dom |= (dom ? 1u : 0u) << (h * kRY + r);
+      store_ok |= (dom && i >= 1 && i < kTBH - 1 && j >= 1 && j < kTBW - 1 ? 1u : 0u) << (h * kRY + r);
+    }
+
+  double A1[2][kRY], B1[2][kRY], A2[2][kRY], B2[2][kRY], out[2][kRY];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int r = 0; r < kRY; ++r) A1[h][r] = B1[h][r] = A2[h][r] = B2[h][r] = 0.0;
+
+  stage(p0 - 2);
+  for (int64_t p = p0 - 2; p <= p1 + 1; ++p) {
+    stage(p + 1);  // empty group past the end keeps the wait count uniform
+    cp_async_wait<1>();
+    __syncthreads();  // plane p visible; iteration p-1 finished everywhere
+    // level 1: plane p -> finishes level-1 plane q1 = p-1
+    tb_level<MASK, FMA>(l0 + (int)((p - p0 + 3) % 3) * (kTBR * kTBP), w, lane, A1, B1, out, cf.c);
+    const int64_t q1 = p - 1;
+    const int64_t gq1 = q1 + g.a0_off;
+    const bool plane_pin = q1 < 0 || q1 >= g.e0 || gq1 < 0 || gq1 >= g.a0_glob;
+    double* l1b = l1 + (int)((q1 - p0 + 4) & 1) * (kTBR * kTBP);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int r = 0; r < kRY; ++r) {
+        const bool keep = !plane_pin && (in_dom >> (h * kRY + r) & 1u);
+        l1b[(w * kRY + r + 1) * kTBP + lane + 32 * h + 1] = keep ? out[h][r] : bnd;
+      }
+    __syncthreads();  // level-1 plane q1 visible
+    if (q1 >= p0 - 1) {
+      // level 2: level-1 plane q1 -> finishes level-2 plane q2 = q1-1
+      tb_level<MASK, FMA>(l1b, w, lane, A2, B2, out, cf.c);
+      const int64_t q2 = q1 - 1;
+      if (q2 >= p0 && q2 < p1) {
+        const int64_t gq2 = q2 + g.a0_off;
+        const bool pin = gq2 < 0 || gq2 >= g.a0_glob;
+        double* op = dst + origin + q2 * g.s0 + (y0 - 1 + w * kRY) * g.s1 + (x0 - 1 + lane);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int r = 0; r < kRY; ++r)
+            if (store_ok >> (h * kRY + r) & 1u) op[r * g.s1 + 32 * h] = pin ? bnd : out[h][r];
+      }
+    }
+  }
+}
+
 static unsigned slots3d(const tvs_stencil& st, Coeff27& cf) {
   unsigned mask = 0;
   int last = -1;
@@ -173,6 +321,38 @@ bool jacobi3d_streaming_supported(const tvs_stencil& st) {
   Coeff27 cf;
   const unsigned m = slots3d(st, cf);
   return m == kBox27 || m == kStar7;
+}
+
+int jacobi3d_max_depth() { return 2; }
+int jacobi3d_default_depth() { return 2; }
+
+template <unsigned MASK, bool FMA>
+static int launch_tb(const Geo& geo, const tvs_geometry& g, const double* src, double* dst, const Coeff27& cf,
+                     double bnd, cudaStream_t s) {
+  // per device context; a host-side attribute write, no synchronisation
+  TVS_CUDA(cudaFuncSetAttribute(jacobi3d_tb_kernel<MASK, FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kTBSmem));
+  const dim3 block(kTX3, kTYT);
+  const dim3 grid((unsigned)((geo.e2 + kTBOX - 1) / kTBOX), (unsigned)((geo.e1 + kTBOY - 1) / kTBOY),
+                  (unsigned)((geo.e0 + kTBPlanesSeg - 1) / kTBPlanesSeg));
+  jacobi3d_tb_kernel<MASK, FMA><<<grid, block, kTBSmem, s>>>(src, dst, geo, g.origin, cf, bnd);
+  TVS_LAUNCHED("jacobi3d_tb_kernel");
+  return TVS_OK;
+}
+
+// Two time levels in one pass (K4b): src -> dst after 2 steps.
+int jacobi3d_blocked2(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, bool fma,
+                      cudaStream_t s) {
+  Coeff27 cf;
+  const unsigned mask = slots3d(st, cf);
+  const Geo geo = make_geo(g);
+  if (mask == kBox27)
+    return fma ? launch_tb<kBox27, true>(geo, g, src, dst, cf, st.boundary, s)
+               : launch_tb<kBox27, false>(geo, g, src, dst, cf, st.boundary, s);
+  if (mask == kStar7)
+    return fma ? launch_tb<kStar7, true>(geo, g, src, dst, cf, st.boundary, s)
+               : launch_tb<kStar7, false>(geo, g, src, dst, cf, st.boundary, s);
+  return fail(TVS_ERR_UNSUPPORTED, "jacobi3d_blocked2: tap set");
 }
 
 int jacobi3d_streaming(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, bool fma,

@@ -152,6 +152,24 @@ def test_jacobi3d_streaming(cuda_ready, kernel, ext):
         assert np.array_equal(got.interior, want.interior), algo
 
 
+@pytest.mark.parametrize("kernel", ["heat3d", "jac3d27p"])
+@pytest.mark.parametrize("ext", [(1, 1, 1), (2, 30, 62), (70, 31, 63), (65, 61, 125), (131, 29, 200)])
+def test_jacobi3d_two_level_blocking(cuda_ready, kernel, ext):
+    """K4b (two time levels per pass) against the oracle and against K4
+    (depth 1) across frame edges (62 x 30 useful per block, 64-plane
+    segments), odd step counts (2-level launches + one single step) and both
+    FMA contracts."""
+    g = Grid.random(ext, seed=sum(ext), boundary=0.375)
+    spec = spec_for(kernel, 0.375)
+    want = cref.scalar_reference(spec, g, 7)
+    for depth in (0, 1, 2, 3):
+        got = execute(spec, g, 7, depth=depth, fma="never")
+        assert np.array_equal(got.interior, want.interior), depth
+    a = execute(spec, g, 6, depth=2, fma="allow")
+    b = execute(spec, g, 6, depth=1, fma="allow")
+    assert np.array_equal(a.interior, b.interior)
+
+
 @pytest.mark.parametrize("n", [1, 7, 255, 256, 2047, 2048, 2049, 4096 + 300, 20000])
 def test_naive_1d_tiles(cuda_ready, n):
     """Single-step kernel: full 2048-element tiles and ragged tails."""

@@ -32,7 +32,13 @@ constexpr int kWarps2 = 1;     // warps per block (task = blockIdx.x: warp-unifo
 #ifndef J2D_SEG
 #define J2D_SEG 256
 #endif
-constexpr int kRowsSeg = J2D_SEG;  // output rows per warp task
+constexpr int kRowsSeg = J2D_SEG;
+#ifndef J2D_RING
+#define J2D_RING 4  // > 0: cp.async row ring depth (0: register prefetch); 4 measured best (config 3: 0 1733, 4 1754-1793, 8 1754, 16 1741 GSt/s)
+#endif
+#ifndef J2D_PF
+#define J2D_PF 2
+#endif  // output rows per warp task
 
 constexpr unsigned kStar5 = (1u << 1) | (1u << 3) | (1u << 4) | (1u << 5) | (1u << 7);
 constexpr unsigned kBox9 = 0x1FFu;
@@ -88,7 +94,6 @@ __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __
                                                                 Coeff9 cf, double bnd, int64_t n_strips,
                                                                 int64_t n_tasks, int64_t seg0) {
   constexpr int U = 32 * kP2 - 2 * D;  // useful columns per strip
-  constexpr int PF = 2;                // rows prefetched ahead (registers)
   const double(&c)[9] = cf.c;          // constant-bank operands
 
   const int lane = threadIdx.x & 31;
@@ -179,6 +184,58 @@ __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __
 
   using T0 = std::true_type;
   using T1 = std::false_type;
+#if J2D_RING > 0
+  // rows staged NR-1 ahead by per-lane 8-byte cp.async into a per-warp shared
+  // ring ([slot][p][lane]: conflict-free); each lane reads back only what it
+  // copied itself, so cp.async.wait_group is the only synchronisation
+  constexpr int NR = J2D_RING;
+  static_assert((NR & (NR - 1)) == 0, "ring depth must be a power of two");
+  __shared__ double ring[NR][kP2][32];
+  auto row_ok_f = [&](int mm) { return mm >= 0 && mm < e0 && mm + a0 >= 0 && mm + a0 < ag; };
+  auto issue_row = [&](int mm) {
+    if (mm < m_end && row_ok_f(mm)) {
+      const double* rp = col_base + (int64_t)mm * g.s0;
+      const int slot = (mm - m_begin) & (NR - 1);
+#pragma unroll
+      for (int p = 0; p < kP2; ++p)
+        if (!(col_out >> p & 1u)) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(&ring[slot][p][lane]);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(rp + p));
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  auto read_row = [&](int mm, double (&r)[kP2]) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(NR - 1) : "memory");
+    const bool ok = row_ok_f(mm);
+    const int slot = (mm - m_begin) & (NR - 1);
+#pragma unroll
+    for (int p = 0; p < kP2; ++p) r[p] = (ok && !(col_out >> p & 1u)) ? ring[slot][p][lane] : bnd;
+  };
+#pragma unroll
+  for (int k = 0; k < NR - 1; ++k) issue_row(m_begin + k);
+  int m = m_begin;
+  for (; m + 2 <= m_end; m += 2) {
+    double row[kP2];
+    issue_row(m + NR - 1);
+    read_row(m, row);
+    step(m, row, T0{});
+    issue_row(m + NR);
+    read_row(m + 1, row);
+    step(m + 1, row, T1{});
+  }
+  if (m < m_end) {
+    double row[kP2];
+    issue_row(m + NR - 1);
+    read_row(m, row);
+    step(m, row, T0{});
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+#else
+  constexpr int PF = J2D_PF;  // rows prefetched ahead (registers, even)
+  static_assert(PF % 2 == 0, "role swap alternates per step");
   double pre[PF][kP2];
 #pragma unroll
   for (int k = 0; k < PF; ++k) load_row(m_begin + k, pre[k]);
@@ -211,6 +268,7 @@ __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __
       step(m, row, T1{});
   }
 }
+#endif
 
 // Coefficients by 3x3 position if the offsets are strictly sorted (the
 // kernel's fixed order); returns the tap mask or 0.

@@ -15,6 +15,8 @@
  *   baselines.py:43-49   jacobi_plane_update (one step)     -> tvs_jacobi_device(steps=1)
  *   cli.py:156-170       _bench_once (device-resident reps) -> tvs_plan_* API
  *   grid.py:127-133      fnv1a64                            -> tvs_fnv1a64
+ *   baselines.py:52-66   life_plane_update (int32 Life)     -> tvs_life_run / tvs_life_device
+ *   kernels/lcs.py:32-108 lcs_temporal(a, b) -> int          -> tvs_lcs / tvs_lcs_device
  *
  * Arithmetic contract (baselines.py:3-7, 43-49; vec.py:296-298): taps are
  * evaluated in the order given (the caller passes StencilSpec.offsets()
@@ -149,6 +151,35 @@ int tvs_gauss_seidel_device(const tvs_stencil* st, const tvs_geometry* g, double
 /* Host <-> device interior copies between the Grid layout and a geometry. */
 int tvs_upload(const tvs_geometry* g, double* dev, const tvs_layout* lay, const double* host, void* stream);
 int tvs_download(const tvs_geometry* g, const double* dev, const tvs_layout* lay, double* host, void* stream);
+
+/* ---- integer kernels ------------------------------
+ * Life-like automaton (StencilSpec.is_life, model.py): n = wrapping int32
+ * sum over `offsets` (StencilSpec.offsets(): the box neighbours, centre
+ * excluded); n in birth -> 1, else n in survive -> own state, else 0
+ * (baselines.py:52-66).  Masks: bit v set <=> count v in the set (v <= 8). */
+typedef struct tvs_life_rule {
+  int32_t dim;
+  int32_t ntaps; /* 1..26 */
+  int32_t offsets[26][3];
+  int32_t birth_mask;
+  int32_t survive_mask;
+  int32_t boundary; /* constant value of every non-interior cell */
+  int32_t pad_;
+} tvs_life_rule;
+/* one call: host int32 Grid in (reference layout), host Grid out */
+int tvs_life_run(const tvs_life_rule* r, const tvs_layout* lay, const int32_t* in, int32_t* out, int64_t steps,
+                 const tvs_exec* ex);
+/* caller-owned device blocks (geometry as for fp64, 4-byte cells); ping-pong
+ * like tvs_jacobi_device */
+int tvs_life_device(const tvs_life_rule* r, const tvs_geometry* g, int32_t* src, int32_t* dst, int64_t steps,
+                    const tvs_exec* ex, void* stream, int32_t* result_in_dst);
+int tvs_fill_halo_i32(const tvs_geometry* g, int32_t* dev, int32_t value, void* stream);
+int tvs_upload_i32(const tvs_geometry* g, int32_t* dev, const tvs_layout* lay, const int32_t* host, void* stream);
+int tvs_download_i32(const tvs_geometry* g, const int32_t* dev, const tvs_layout* lay, int32_t* host, void* stream);
+/* LCS length of int32 sequences a (na) and b (nb) (kernels/lcs.py:32). */
+int tvs_lcs(const int32_t* a, int64_t na, const int32_t* b, int64_t nb, const tvs_exec* ex, int64_t* length);
+/* device-resident form: a, b device pointers, *result written on `stream` */
+int tvs_lcs_device(const int32_t* a, int64_t na, const int32_t* b, int64_t nb, int32_t* result, void* stream);
 
 /* ---- misc -------------------------------------------------------------- */
 const char* tvs_last_error(void);

@@ -56,7 +56,12 @@ def _problem(spec, grid) -> Problem:
 
 
 def scalar_reference(spec, grid, steps, order="reference", threads=0):
-    """Same contract as oracle.scalar_reference, in C."""
+    """Same contract as oracle.scalar_reference, in C (Life-like int32 rules
+    delegate to the NumPy restatement)."""
+    if spec.is_life:
+        from . import oracle as _npo
+
+        return _npo.scalar_reference(spec, grid, steps)
     p = _problem(spec, grid)
     out = grid.copy()
     if spec.dependence_kind == "gauss_seidel":

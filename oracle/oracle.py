@@ -8,6 +8,10 @@ Follows tvstencil/baselines.py of the reference:
   gather all taps, then scatter);
 * ``scalar_reference``      <- baselines.py:110-125 (out of place; Jacobi
   ping-pongs two planes, GS sweeps one copy in place).
+* ``life_plane_update``    <- baselines.py:52-66 (int32 neighbour sum, the
+  B-then-S ``np.where`` decision tree);
+* ``lcs_length``           <- baselines.py:128-150 (full-table quadratic DP
+  swept along anti-diagonals).
 Added: ``gs_sweep_lexicographic`` (row-major in-place order, the loop of
 test_baselines.py:39-52 for any tap set), selected with
 ``scalar_reference(..., order="lexicographic")``.
@@ -31,6 +35,43 @@ def jacobi_plane_update(spec, src, dst, offset, extents):
     for off in taps[1:]:
         acc = spec.coefficients[off] * _window(src, offset, extents, off) + acc
     _window(dst, offset, extents, (0,) * len(extents))[...] = acc
+
+
+def life_plane_update(spec, src, dst, offset, extents):
+    """One Life-like step over the whole interior (baselines.py:52-66):
+    n = int32 sum of the ``offsets()`` neighbours (wrapping), then count in
+    birth -> 1, else count in survive (minus birth) -> own state, else 0."""
+    taps = spec.offsets()
+    n = _window(src, offset, extents, taps[0]) + _window(src, offset, extents, taps[1])
+    for off in taps[2:]:
+        n = n + _window(src, offset, extents, off)
+    alive = _window(src, offset, extents, (0,) * len(extents))
+    out = np.zeros_like(alive)
+    for b in sorted(spec.birth):
+        out = np.where(n == b, np.int32(1), out)
+    for sv in sorted(set(spec.survive) - set(spec.birth)):
+        out = np.where(n == sv, alive, out)
+    _window(dst, offset, extents, (0,) * len(extents))[...] = out
+
+
+def lcs_length(a, b) -> int:
+    """LCS length by the full-table DP along anti-diagonals
+    (baselines.py:128-150)."""
+    a = np.asarray(a, dtype=np.int32)
+    b = np.asarray(b, dtype=np.int32)
+    n, m = len(a), len(b)
+    if n == 0 or m == 0:
+        return 0
+    table = np.zeros((n + 1, m + 1), dtype=np.int32)
+    for d in range(2, n + m + 1):
+        i0, i1 = max(1, d - m), min(n, d - 1)
+        if i0 > i1:
+            continue
+        i = np.arange(i0, i1 + 1)
+        j = d - i
+        eq = a[i - 1] == b[j - 1]
+        table[i, j] = np.where(eq, table[i - 1, j - 1] + np.int32(1), np.maximum(table[i - 1, j], table[i, j - 1]))
+    return int(table[n, m])
 
 
 def gs_sweep_1d(spec, data, offset, n):
@@ -114,7 +155,8 @@ def scalar_reference(spec, grid, steps, order="reference"):
                 raise ValueError(order)
         return cur
     nxt = grid.alloc_like()
+    update = life_plane_update if spec.is_life else jacobi_plane_update
     for _ in range(steps):
-        jacobi_plane_update(spec, cur.data, nxt.data, cur.offset, cur.extents)
+        update(spec, cur.data, nxt.data, cur.offset, cur.extents)
         cur, nxt = nxt, cur
     return cur

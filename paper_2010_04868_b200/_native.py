@@ -53,6 +53,13 @@ class Geometry(C.Structure):
     ]
 
 
+class LifeRule(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int32), ("ntaps", C.c_int32), ("offsets", (C.c_int32 * 3) * 26),
+        ("birth_mask", C.c_int32), ("survive_mask", C.c_int32), ("boundary", C.c_int32), ("pad_", C.c_int32),
+    ]
+
+
 # exported symbols with their argtypes (checked by tests/test_native_abi.py
 # against include/tvstencil.h)
 _P = C.c_void_p
@@ -79,6 +86,14 @@ _SIGS = {
     "tvs_host_register": (C.c_int, [_P, C.c_size_t]),
     "tvs_host_unregister": (C.c_int, [_P]),
     "tvs_fnv1a64": (C.c_uint64, [_P, C.c_size_t, C.c_uint64]),
+    "tvs_life_run": (C.c_int, [C.POINTER(LifeRule), C.POINTER(Layout), _P, _P, C.c_int64, C.POINTER(Exec)]),
+    "tvs_life_device": (C.c_int, [C.POINTER(LifeRule), C.POINTER(Geometry), _P, _P, C.c_int64, C.POINTER(Exec), _P,
+                                  C.POINTER(C.c_int32)]),
+    "tvs_fill_halo_i32": (C.c_int, [C.POINTER(Geometry), _P, C.c_int32, _P]),
+    "tvs_upload_i32": (C.c_int, [C.POINTER(Geometry), _P, C.POINTER(Layout), _P, _P]),
+    "tvs_download_i32": (C.c_int, [C.POINTER(Geometry), _P, C.POINTER(Layout), _P, _P]),
+    "tvs_lcs": (C.c_int, [_P, C.c_int64, _P, C.c_int64, C.POINTER(Exec), C.POINTER(C.c_int64)]),
+    "tvs_lcs_device": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P]),
     "tvs_launch_counter": (C.c_int64, []),
     "tvs_version": (C.c_char_p, []),
 }
@@ -155,6 +170,45 @@ def make_stencil(spec) -> Stencil:
         st.coeffs[k] = float(spec.coefficients[off])
     st.boundary = float(spec.boundary)
     return st
+
+
+def make_life_rule(spec) -> LifeRule:
+    """Life-like StencilSpec (``is_life``) -> tvs_life_rule, neighbours in
+    ``spec.offsets()`` order (model.py: the box minus the centre)."""
+    if not spec.is_life:
+        raise UnsupportedError(f"{spec.name} is not a Life-like rule")
+    offs = spec.offsets()
+    if spec.radius != 1 or not 1 <= len(offs) <= 26:
+        raise UnsupportedError(f"{spec.name}: only radius-1 Life rules run on the GPU path")
+    r = LifeRule()
+    r.dim, r.ntaps = spec.dim, len(offs)
+    for k, off in enumerate(offs):
+        for d in range(3):
+            r.offsets[k][d] = off[d] if d < spec.dim else 0
+    r.birth_mask = sum(1 << int(v) for v in spec.birth)
+    r.survive_mask = sum(1 << int(v) for v in spec.survive)
+    r.boundary = int(spec.boundary)
+    return r
+
+
+def life_run(spec, src: np.ndarray, dst: np.ndarray, extents, offset: int, steps: int, ex: Exec) -> None:
+    """int32 host Grid data in -> host Grid data out."""
+    rule = make_life_rule(spec)
+    for a in (src, dst):
+        if a.dtype != np.int32 or not a.flags.c_contiguous:
+            raise ValueError("Life grid data must be a C-contiguous int32 array")
+    lay = make_layout(src, extents, offset)
+    check(lib().tvs_life_run(C.byref(rule), C.byref(lay), src.ctypes.data, dst.ctypes.data, int(steps), C.byref(ex)),
+          f"tvs_life_run({spec.name})")
+
+
+def lcs(a: np.ndarray, b: np.ndarray, ex: Exec) -> int:
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    b = np.ascontiguousarray(b, dtype=np.int32)
+    n = C.c_int64(0)
+    check(lib().tvs_lcs(a.ctypes.data if a.size else None, a.size, b.ctypes.data if b.size else None, b.size,
+                        C.byref(ex), C.byref(n)), "tvs_lcs")
+    return int(n.value)
 
 
 def make_layout(data: np.ndarray, extents, offset: int) -> Layout:

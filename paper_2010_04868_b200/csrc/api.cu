@@ -219,6 +219,13 @@ static int copy_interior(const tvs_geometry& g, double* dev, const tvs_layout& l
   return TVS_OK;
 }
 
+// non-static forms for the other translation units (integer.cu)
+int validate_exec_api(const tvs_exec* ex) { return validate_exec(ex); }
+int set_device_api(int dev) { return set_device(dev); }
+int geometry_init_api(int dim, const int64_t* ext, int64_t a0_off, int64_t a0_glob, tvs_geometry* g) {
+  return geometry_init(dim, ext, a0_off, a0_glob, g);
+}
+
 // ---- algorithm drivers -----------------------------------------------------
 static int jacobi_device(const tvs_stencil& st, const tvs_geometry& g, double* src, double* dst, int64_t steps,
                          const tvs_exec& ex, cudaStream_t s, int32_t* in_dst) {

@@ -185,6 +185,11 @@ void count_launch(int64_t n = 1);
     ::tvs::count_launch();                                          \
   } while (0)
 
+// api.cu helpers shared with integer.cu
+int validate_exec_api(const tvs_exec* ex);
+int set_device_api(int dev);
+int geometry_init_api(int dim, const int64_t* ext, int64_t a0_off, int64_t a0_glob, tvs_geometry* g);
+
 // Fused-multiply-add decision (TVS_FMA_EXACT: all coefficients 0 or +-2^k).
 bool coeffs_power_of_two(const tvs_stencil& st);
 bool use_fma(const tvs_stencil& st, const tvs_exec& ex);

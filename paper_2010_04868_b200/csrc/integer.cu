@@ -1,0 +1,497 @@
+// Integer kernels of the reference catalog: Life-like
+// cellular automata and the LCS dynamic programme, int32 throughout.
+//
+// K7 life_kernel — replaces life_plane_update (reference baselines.py:52-66)
+// behind jacobi2d_temporal(kernel="life") (verify.py:60): one time step per
+// launch over a padded int32 block (same geometry as the fp64 path, 4-byte
+// cells).  n = wrapping int32 sum of the radius-1 box neighbours (the
+// centre excluded, StencilSpec.offsets() for life, model.py); the
+// B-then-S rule: n in birth -> 1, else n in survive -> the cell's own
+// state, else 0.  Integer addition is exact mod 2^32, so any summation order
+// is bit-identical to the reference's.  A thread owns 8 outputs along the
+// slowest in-block axis and issues every neighbour load before the first
+// add (the K1 bandwidth layout): 4 B read + 4 B written per cell update.
+//
+// K8 lcs_kernel — replaces lcs_temporal (reference kernels/lcs.py:32-108)
+// and its oracle lcs_reference (baselines.py:128-150).  The paper's
+// time lanes on a GPU: the A index is time, lane k of warp w owns DP row
+// x = x0 + 32w + k + 1 and at step s updates column y = s + 1 - k, so
+//   up   = lcs[x-1][y]   = lane k-1's output one step earlier (__shfl_up),
+//   diag = lcs[x-1][y-1] = the `up` this lane received one step earlier,
+//   left = lcs[x][y-1]   = its own previous output,
+//   b[y-1] slides through the lanes one position per step (__shfl_up),
+// out = a[x-1] == b[y-1] ? diag + 1 : max(up, left).  Lane 0 reads row
+// x0 + 32w from a boundary row written by warp w-1's lane 31 (progress
+// published every 32 columns with a GPU-scope release); warps take tickets
+// in start order and only wait on lower tickets (deadlock-free).  Passes of
+// at most kLcsMaxWarps warps bound the boundary-row workspace.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace tvs {
+
+// ---------------------------------------------------------------- Life ----
+constexpr int kLifeNR = 8;
+
+struct LifeTaps {
+  int n;
+  int bmask, smask;  // bit v: count v in birth / survive
+  int bnd;
+  int64_t lin[26];
+};
+
+__device__ __forceinline__ int life_rule(unsigned n, int alive, const LifeTaps& t) {
+  if (n <= 26u && ((t.bmask >> n) & 1)) return 1;
+  if (n <= 26u && ((t.smask >> n) & 1)) return alive;
+  return 0;
+}
+
+template <int NT>
+__device__ __forceinline__ void life_points(const int* __restrict__ src, int64_t idx, int64_t rs, const LifeTaps& t,
+                                            int (&out)[kLifeNR]) {
+  unsigned n[kLifeNR];
+  int c[kLifeNR];
+#pragma unroll
+  for (int r = 0; r < kLifeNR; ++r) c[r] = __ldg(src + idx + r * rs);
+  if constexpr (NT > 0) {
+    int v[NT][kLifeNR];
+#pragma unroll
+    for (int k = 0; k < NT; ++k)
+#pragma unroll
+      for (int r = 0; r < kLifeNR; ++r) v[k][r] = __ldg(src + idx + r * rs + t.lin[k]);
+#pragma unroll
+    for (int r = 0; r < kLifeNR; ++r) {
+      n[r] = (unsigned)v[0][r];
+#pragma unroll
+      for (int k = 1; k < NT; ++k) n[r] += (unsigned)v[k][r];
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < kLifeNR; ++r) n[r] = 0u;
+    for (int k = 0; k < t.n; ++k) {
+      int v[kLifeNR];
+#pragma unroll
+      for (int r = 0; r < kLifeNR; ++r) v[r] = __ldg(src + idx + r * rs + t.lin[k]);
+#pragma unroll
+      for (int r = 0; r < kLifeNR; ++r) n[r] += (unsigned)v[r];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kLifeNR; ++r) out[r] = life_rule(n[r], c[r], t);
+}
+
+__device__ __forceinline__ int life_point(const int* __restrict__ src, int64_t idx, const LifeTaps& t) {
+  unsigned n = 0u;
+  for (int k = 0; k < t.n; ++k) n += (unsigned)__ldg(src + idx + t.lin[k]);
+  return life_rule(n, __ldg(src + idx), t);
+}
+
+// Block (32, 8), tiles as K1 (jacobi_naive.cu): 1D 2048 consecutive cells,
+// 2D/3D 32 columns x 64 rows (of plane blockIdx.z in 3D).
+template <int NT>
+__global__ void __launch_bounds__(256) life_kernel(const int* __restrict__ src, int* __restrict__ dst, Geo g,
+                                                   LifeTaps t, int64_t origin) {
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  int out[kLifeNR];
+  if (g.dim == 1) {
+    const int64_t i0 = (int64_t)blockIdx.x * (256 * kLifeNR) + ty * 32 + tx;
+    if (i0 + (kLifeNR - 1) * 256 < g.e0 && g.a0_off == 0 && g.a0_glob == g.e0) {
+      life_points<NT>(src, origin + i0, 256, t, out);
+#pragma unroll
+      for (int r = 0; r < kLifeNR; ++r) dst[origin + i0 + r * 256] = out[r];
+    } else {
+      for (int r = 0; r < kLifeNR; ++r) {
+        const int64_t i = i0 + r * 256;
+        if (i >= g.e0) break;
+        const int64_t gi = i + g.a0_off;
+        dst[origin + i] = (gi < 0 || gi >= g.a0_glob) ? t.bnd : life_point(src, origin + i, t);
+      }
+    }
+    return;
+  }
+  const bool d3 = g.dim == 3;
+  const int64_t rows = d3 ? g.e1 : g.e0, cols = d3 ? g.e2 : g.e1, rs = d3 ? g.s1 : g.s0;
+  const int64_t c = (int64_t)blockIdx.x * 32 + tx;
+  const int64_t r0 = (int64_t)blockIdx.y * (8 * kLifeNR) + ty * kLifeNR;
+  const int64_t p = d3 ? (int64_t)blockIdx.z : 0;
+  const int64_t base = origin + (d3 ? p * g.s0 : 0) + c;
+  if (c >= cols) return;
+  if (d3) {
+    const int64_t gp = p + g.a0_off;
+    if (gp < 0 || gp >= g.a0_glob) {
+      for (int r = 0; r < kLifeNR && r0 + r < rows; ++r) dst[base + (r0 + r) * rs] = t.bnd;
+      return;
+    }
+  }
+  const bool rows_ok = d3 || (r0 + g.a0_off >= 0 && r0 + kLifeNR - 1 + g.a0_off < g.a0_glob);
+  if (r0 + kLifeNR <= rows && rows_ok) {
+    life_points<NT>(src, base + r0 * rs, rs, t, out);
+#pragma unroll
+    for (int r = 0; r < kLifeNR; ++r) dst[base + (r0 + r) * rs] = out[r];
+  } else {
+    for (int r = 0; r < kLifeNR && r0 + r < rows; ++r) {
+      const int64_t idx = base + (r0 + r) * rs;
+      const int64_t gr = r0 + r + g.a0_off;
+      dst[idx] = (!d3 && (gr < 0 || gr >= g.a0_glob)) ? t.bnd : life_point(src, idx, t);
+    }
+  }
+}
+
+__global__ void fill_halo_i32_kernel(int* base, tvs_geometry g, int value) {
+  const int64_t n = g.alloc_elems;
+  const int64_t last_pitch = g.dim == 1 ? g.alloc_elems : g.strides[g.dim - 2];
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    bool interior;
+    if (g.dim == 1) {
+      const int64_t x = idx - kPadLast;
+      interior = x >= 0 && x < g.extents[0];
+    } else if (g.dim == 2) {
+      const int64_t r = idx / last_pitch - 1, c = idx % last_pitch - kPadLast;
+      interior = r >= 0 && r < g.extents[0] && c >= 0 && c < g.extents[1];
+    } else {
+      const int64_t p = idx / g.strides[0] - 1, rem = idx % g.strides[0];
+      const int64_t r = rem / g.strides[1] - 1, c = rem % g.strides[1] - kPadLast;
+      interior = p >= 0 && p < g.extents[0] && r >= 0 && r < g.extents[1] && c >= 0 && c < g.extents[2];
+    }
+    if (!interior) base[idx] = value;
+  }
+}
+
+static int fill_halo_i32(const tvs_geometry& g, int* dev, int value, cudaStream_t s) {
+  const int blocks = (int)std::min<int64_t>((g.alloc_elems + 255) / 256, 148 * 16);
+  fill_halo_i32_kernel<<<blocks, 256, 0, s>>>(dev, g, value);
+  TVS_LAUNCHED("fill_halo_i32_kernel");
+  return TVS_OK;
+}
+
+static int validate_life(const tvs_life_rule* r) {
+  if (!r) return fail(TVS_ERR_INVALID, "null life rule");
+  if (r->dim < 1 || r->dim > 3) return fail(TVS_ERR_INVALID, "dim must be 1..3");
+  if (r->ntaps < 1 || r->ntaps > 26) return fail(TVS_ERR_INVALID, "life: ntaps must be 1..26");
+  if ((r->birth_mask | r->survive_mask) & ~0x1FF) return fail(TVS_ERR_INVALID, "life rule sets must be subsets of 0..8");
+  for (int k = 0; k < r->ntaps; ++k)
+    for (int d = 0; d < 3; ++d) {
+      const int o = r->offsets[k][d];
+      if (o < -1 || o > 1) return fail(TVS_ERR_INVALID, "tap offset exceeds radius 1");
+      if (d >= r->dim && o != 0) return fail(TVS_ERR_INVALID, "tap offset on a missing axis");
+    }
+  return TVS_OK;
+}
+
+static int life_step(const tvs_life_rule& r, const tvs_geometry& g, const int* src, int* dst, cudaStream_t s) {
+  LifeTaps t{};
+  t.n = r.ntaps;
+  t.bmask = r.birth_mask;
+  t.smask = r.survive_mask;
+  t.bnd = r.boundary;
+  const int64_t s0 = g.strides[0], s1 = g.dim == 3 ? g.strides[1] : 1;
+  for (int k = 0; k < r.ntaps; ++k) {
+    const int* o = r.offsets[k];
+    t.lin[k] = g.dim == 1 ? o[0] : g.dim == 2 ? o[0] * s0 + o[1] : o[0] * s0 + o[1] * s1 + o[2];
+  }
+  const Geo geo = make_geo(g);
+  auto cdiv = [](int64_t a, int64_t b) { return (a + b - 1) / b; };
+  int64_t gx, gy = 1, gz = 1;
+  if (geo.dim == 1) {
+    gx = cdiv(geo.e0, 256 * kLifeNR);
+  } else if (geo.dim == 2) {
+    gx = cdiv(geo.e1, 32);
+    gy = cdiv(geo.e0, 8 * kLifeNR);
+  } else {
+    gx = cdiv(geo.e2, 32);
+    gy = cdiv(geo.e1, 8 * kLifeNR);
+    gz = geo.e0;
+  }
+  if (gx >= (1ll << 31) || gy > 65535 || gz > 65535) return fail(TVS_ERR_SIZE, "life: grid too large");
+  const dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)gz), block(32, 8);
+  if (r.ntaps == 8)
+    life_kernel<8><<<grid, block, 0, s>>>(src, dst, geo, t, g.origin);
+  else if (r.ntaps == 2)
+    life_kernel<2><<<grid, block, 0, s>>>(src, dst, geo, t, g.origin);
+  else
+    life_kernel<0><<<grid, block, 0, s>>>(src, dst, geo, t, g.origin);
+  TVS_LAUNCHED("life_kernel");
+  return TVS_OK;
+}
+
+static int life_device(const tvs_life_rule& r, const tvs_geometry& g, int* src, int* dst, int64_t steps,
+                       cudaStream_t s, int32_t* in_dst) {
+  int* a = src;
+  int* b = dst;
+  for (int64_t k = 0; k < steps; ++k) {
+    const int rc = life_step(r, g, a, b, s);
+    if (rc) return rc;
+    std::swap(a, b);
+  }
+  if (in_dst) *in_dst = a == dst ? 1 : 0;
+  return TVS_OK;
+}
+
+static int copy_interior_i32(const tvs_geometry& g, int* dev, const tvs_layout& lay, int* host, bool upload,
+                             cudaStream_t s) {
+  if (lay.dim != g.dim) return fail(TVS_ERR_SIZE, "layout/geometry dimension mismatch");
+  for (int d = 0; d < g.dim; ++d) {
+    if (lay.extents[d] != g.extents[d]) return fail(TVS_ERR_SIZE, "layout/geometry extents mismatch");
+    if (lay.offset + lay.extents[d] > lay.shape[d]) return fail(TVS_ERR_INVALID, "layout shape too small");
+  }
+  const size_t E = sizeof(int);
+  const auto kind = upload ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  int* d0 = dev + g.origin;
+  if (g.dim == 1) {
+    int* h0 = host + lay.offset;
+    TVS_CUDA(cudaMemcpyAsync(upload ? (void*)d0 : (void*)h0, upload ? (void*)h0 : (void*)d0, E * g.extents[0], kind, s));
+  } else if (g.dim == 2) {
+    int* h0 = host + lay.offset * lay.shape[1] + lay.offset;
+    const size_t hp = E * lay.shape[1], dp = E * g.strides[0], w = E * g.extents[1];
+    if (upload)
+      TVS_CUDA(cudaMemcpy2DAsync(d0, dp, h0, hp, w, g.extents[0], kind, s));
+    else
+      TVS_CUDA(cudaMemcpy2DAsync(h0, hp, d0, dp, w, g.extents[0], kind, s));
+  } else {
+    cudaMemcpy3DParms p;
+    std::memset(&p, 0, sizeof(p));
+    const cudaPitchedPtr hptr = make_cudaPitchedPtr(host, E * lay.shape[2], lay.shape[2], lay.shape[1]);
+    const cudaPitchedPtr dptr = make_cudaPitchedPtr(dev, E * g.strides[1], g.strides[1], g.strides[0] / g.strides[1]);
+    const cudaPos hpos = make_cudaPos(E * lay.offset, lay.offset, lay.offset);
+    const cudaPos dpos = make_cudaPos(E * kPadLast, 1, 1);
+    p.extent = make_cudaExtent(E * g.extents[2], g.extents[1], g.extents[0]);
+    if (upload) {
+      p.srcPtr = hptr; p.srcPos = hpos; p.dstPtr = dptr; p.dstPos = dpos;
+    } else {
+      p.srcPtr = dptr; p.srcPos = dpos; p.dstPtr = hptr; p.dstPos = hpos;
+    }
+    p.kind = kind;
+    TVS_CUDA(cudaMemcpy3DAsync(&p, s));
+  }
+  return TVS_OK;
+}
+
+// ----------------------------------------------------------------- LCS ----
+constexpr int kLcsMaxWarps = 4096;  // warps (32 DP rows each) per pass
+
+struct LcsArgs {
+  const int* a;   // device, na
+  const int* b;   // device, nb
+  int na, nb;
+  int x0;         // DP rows x0+1 .. handled by this pass
+  int nwarps;
+  int* rows;      // (nwarps + 1) x (nb + 1): row w = lcs[x0 + 32w][*]
+  int* prog;      // nwarps + 1 progress counters (columns of row w published)
+  int* ticket;
+  int* result;    // lcs[na][nb]
+};
+
+__device__ __forceinline__ int ld_acquire_i32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_i32(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(32) lcs_kernel(LcsArgs p) {
+  __shared__ int s_w;
+  const int lane = threadIdx.x;
+  if (lane == 0) s_w = atomicAdd(p.ticket, 1);
+  __syncwarp();
+  const int w = s_w;
+  if (w >= p.nwarps) return;
+  const int nb = p.nb;
+  const int x = p.x0 + 32 * w + lane + 1;  // DP row of this lane
+  const int av = x <= p.na ? p.a[x - 1] : 0;
+  const int* rin = p.rows + (size_t)w * (nb + 1);
+  int* rout = p.rows + (size_t)(w + 1) * (nb + 1);
+  const bool last_lane_real = p.x0 + 32 * w + 32 <= p.na;
+  int out = 0, prev_up = 0, bwin = 0;
+  int c_up = 0, c_b = 0;
+  SpinGuard guard;
+  for (int s = 0; s < nb + 31; ++s) {
+    const int ph = s & 31;
+    if (ph == 0) {
+      // columns s+1 .. s+32 of the row above this warp, and b[s .. s+31]
+      const int need = min(s + 32, nb);
+      while (ld_acquire_i32(p.prog + w) < need) guard.tick();
+      const int y = s + 1 + lane;
+      c_up = y <= nb ? rin[y] : 0;
+      c_b = s + lane < nb ? p.b[s + lane] : 0;
+    }
+    const int up_sh = __shfl_up_sync(0xffffffffu, out, 1);
+    const int b_sh = __shfl_up_sync(0xffffffffu, bwin, 1);
+    const int up0 = __shfl_sync(0xffffffffu, c_up, ph);
+    const int b0 = __shfl_sync(0xffffffffu, c_b, ph);
+    const int up = lane == 0 ? up0 : up_sh;
+    bwin = lane == 0 ? b0 : b_sh;
+    const int y = s + 1 - lane;
+    int v = av == bwin ? prev_up + 1 : max(up, out);
+    if (y < 1) v = 0;  // lcs[x][0] = 0 before the lane's first column
+    prev_up = up;
+    out = v;
+    if (y >= 1 && y <= nb) {
+      if (lane == 31) rout[y] = out;
+      if (x == p.na && y == nb) *p.result = out;
+    }
+    if (lane == 31 && last_lane_real && y >= 1 && ((y & 31) == 0 || y == nb)) st_release_i32(p.prog + w + 1, y);
+  }
+}
+
+struct LcsWork {
+  int device = -1;
+  int* buf = nullptr;
+  size_t bytes = 0;
+  ~LcsWork() {
+    if (buf) cudaFree(buf);
+  }
+};
+static thread_local LcsWork g_lcs;
+
+static int lcs_device(const int* a, int na, const int* b, int nb, int* result_dev, cudaStream_t s) {
+  if (na == 0 || nb == 0) {
+    TVS_CUDA(cudaMemsetAsync(result_dev, 0, sizeof(int), s));
+    return TVS_OK;
+  }
+  const int total_warps = (na + 31) / 32;
+  // workspace budget ~256 MB of boundary rows
+  const int64_t row_bytes = (int64_t)(nb + 1) * sizeof(int);
+  const int cap = (int)std::max<int64_t>(1, std::min<int64_t>(kLcsMaxWarps, (256ll << 20) / row_bytes - 1));
+  const int per = std::min(total_warps, cap);
+  const size_t need = (size_t)(per + 1) * row_bytes + (size_t)(per + 2) * sizeof(int) + 256;
+  int dev;
+  TVS_CUDA(cudaGetDevice(&dev));
+  if (g_lcs.bytes < need || g_lcs.device != dev) {
+    if (g_lcs.buf) cudaFree(g_lcs.buf);
+    g_lcs.buf = nullptr;
+    g_lcs.bytes = 0;
+    TVS_CUDA(cudaMalloc(&g_lcs.buf, need));
+    g_lcs.bytes = need;
+    g_lcs.device = dev;
+  }
+  int* rows = g_lcs.buf;
+  int* prog = rows + (size_t)(per + 1) * (nb + 1);
+  int* ticket = prog + per + 1;
+  TVS_CUDA(cudaMemsetAsync(rows, 0, row_bytes, s));  // lcs[0][*] = 0
+  for (int x0 = 0, first = 1; x0 < na; x0 += 32 * per, first = 0) {
+    const int nw = std::min(per, (na - x0 + 31) / 32);
+    if (!first) TVS_CUDA(cudaMemcpyAsync(rows, rows + (size_t)per * (nb + 1), row_bytes, cudaMemcpyDeviceToDevice, s));
+    TVS_CUDA(cudaMemsetAsync(prog, 0, (size_t)(per + 2) * sizeof(int), s));
+    TVS_CUDA(cudaMemcpyAsync(prog, &nb, sizeof(int), cudaMemcpyHostToDevice, s));  // row 0 complete
+    LcsArgs p{a, b, na, nb, x0, nw, rows, prog, ticket, result_dev};
+    lcs_kernel<<<nw, 32, 0, s>>>(p);
+    TVS_LAUNCHED("lcs_kernel");
+    // next pass reads row `per` (the last warp of a full pass has 32 real rows)
+    if (nw < per) break;
+  }
+  return TVS_OK;
+}
+
+}  // namespace tvs
+
+using namespace tvs;
+
+extern "C" {
+
+int tvs_fill_halo_i32(const tvs_geometry* g, int32_t* dev, int32_t value, void* stream) {
+  if (!g || !dev) return fail(TVS_ERR_INVALID, "null argument");
+  return fill_halo_i32(*g, dev, value, (cudaStream_t)stream);
+}
+
+int tvs_upload_i32(const tvs_geometry* g, int32_t* dev, const tvs_layout* lay, const int32_t* host, void* stream) {
+  if (!g || !dev || !lay || !host) return fail(TVS_ERR_INVALID, "null argument");
+  return copy_interior_i32(*g, dev, *lay, const_cast<int*>(host), true, (cudaStream_t)stream);
+}
+
+int tvs_download_i32(const tvs_geometry* g, const int32_t* dev, const tvs_layout* lay, int32_t* host, void* stream) {
+  if (!g || !dev || !lay || !host) return fail(TVS_ERR_INVALID, "null argument");
+  return copy_interior_i32(*g, const_cast<int*>(dev), *lay, host, false, (cudaStream_t)stream);
+}
+
+int tvs_life_device(const tvs_life_rule* r, const tvs_geometry* g, int32_t* src, int32_t* dst, int64_t steps,
+                    const tvs_exec* ex, void* stream, int32_t* result_in_dst) {
+  int rc = validate_life(r);
+  if (rc) return rc;
+  if ((rc = validate_exec_api(ex))) return rc;
+  if (!g || !src || !dst) return fail(TVS_ERR_INVALID, "null argument");
+  if (g->dim != r->dim) return fail(TVS_ERR_SIZE, "grid/rule dimension mismatch");
+  if (steps < 0) return fail(TVS_ERR_INVALID, "steps must be >= 0");
+  return life_device(*r, *g, src, dst, steps, (cudaStream_t)stream, result_in_dst);
+}
+
+int tvs_life_run(const tvs_life_rule* r, const tvs_layout* lay, const int32_t* in, int32_t* out, int64_t steps,
+                 const tvs_exec* ex) {
+  int rc = validate_life(r);
+  if (rc) return rc;
+  if ((rc = validate_exec_api(ex))) return rc;
+  if (!lay || !in || !out) return fail(TVS_ERR_INVALID, "null argument");
+  if (lay->dim != r->dim) return fail(TVS_ERR_SIZE, "grid/rule dimension mismatch");
+  if (steps < 0) return fail(TVS_ERR_INVALID, "steps must be >= 0");
+  if ((rc = set_device_api(ex->device))) return rc;
+  tvs_geometry g;
+  if ((rc = geometry_init_api(r->dim, lay->extents, 0, lay->extents[0], &g))) return rc;
+  int* buf[2] = {nullptr, nullptr};
+  cudaStream_t s;
+  TVS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  auto done = [&](int code) {
+    for (int* b : buf)
+      if (b) cudaFreeAsync(b, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    return code;
+  };
+  for (int k = 0; k < 2; ++k) {
+    if (cudaMallocAsync(&buf[k], sizeof(int) * g.alloc_elems, s) != cudaSuccess)
+      return done(cuda_fail(cudaGetLastError(), "cudaMallocAsync"));
+    if ((rc = fill_halo_i32(g, buf[k], r->boundary, s))) return done(rc);
+  }
+  if ((rc = copy_interior_i32(g, buf[0], *lay, const_cast<int*>(in), true, s))) return done(rc);
+  int32_t in_dst = 0;
+  if ((rc = life_device(*r, g, buf[0], buf[1], steps, s, &in_dst))) return done(rc);
+  if ((rc = copy_interior_i32(g, in_dst ? buf[1] : buf[0], *lay, out, false, s))) return done(rc);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return done(cuda_fail(e, "tvs_life_run"));
+  return done(TVS_OK);
+}
+
+int tvs_lcs_device(const int32_t* a, int64_t na, const int32_t* b, int64_t nb, int32_t* result, void* stream) {
+  if (na < 0 || nb < 0) return fail(TVS_ERR_INVALID, "negative length");
+  if (na > INT32_MAX - 64 || nb > INT32_MAX - 64) return fail(TVS_ERR_SIZE, "lcs: sequence too long");
+  if (!result || (na > 0 && !a) || (nb > 0 && !b)) return fail(TVS_ERR_INVALID, "null argument");
+  return lcs_device(a, (int)na, b, (int)nb, result, (cudaStream_t)stream);
+}
+
+int tvs_lcs(const int32_t* a, int64_t na, const int32_t* b, int64_t nb, const tvs_exec* ex, int64_t* length) {
+  int rc = validate_exec_api(ex);
+  if (rc) return rc;
+  if (!length || na < 0 || nb < 0 || (na > 0 && !a) || (nb > 0 && !b)) return fail(TVS_ERR_INVALID, "bad argument");
+  if (na > INT32_MAX - 64 || nb > INT32_MAX - 64) return fail(TVS_ERR_SIZE, "lcs: sequence too long");
+  *length = 0;
+  if (na == 0 || nb == 0) return TVS_OK;
+  if ((rc = set_device_api(ex->device))) return rc;
+  cudaStream_t s;
+  TVS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  int* d = nullptr;
+  auto done = [&](int code) {
+    if (d) cudaFreeAsync(d, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    return code;
+  };
+  const size_t bytes = sizeof(int) * (size_t)(na + nb + 1);
+  if (cudaMallocAsync(&d, bytes, s) != cudaSuccess) return done(cuda_fail(cudaGetLastError(), "cudaMallocAsync"));
+  if (cudaMemcpyAsync(d, a, sizeof(int) * na, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(d + na, b, sizeof(int) * nb, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return done(cuda_fail(cudaGetLastError(), "tvs_lcs upload"));
+  if ((rc = lcs_device(d, (int)na, d + na, (int)nb, d + na + nb, s))) return done(rc);
+  int res = 0;
+  if (cudaMemcpyAsync(&res, d + na + nb, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return done(cuda_fail(cudaGetLastError(), "tvs_lcs download"));
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return done(cuda_fail(e, "tvs_lcs"));
+  *length = res;
+  return done(TVS_OK);
+}
+
+}  // extern "C"

@@ -23,7 +23,10 @@ def execute(spec, grid: Grid, steps: int, *, order: str = "lexicographic", out: 
     steps = int(steps)
     if steps < 0:
         raise ValueError("steps must be >= 0")
-    if grid.element_kind != "float64":
+    if spec.is_life:
+        if grid.element_kind != "int32":
+            raise UnsupportedError(f"{spec.name}: Life rules run on int32 grids")
+    elif grid.element_kind != "float64":
         raise UnsupportedError(f"{spec.name}: {grid.element_kind} grids are not on the GPU path")
     if out is None:
         out = grid.copy()
@@ -35,5 +38,8 @@ def execute(spec, grid: Grid, steps: int, *, order: str = "lexicographic", out: 
     if steps == 0:
         return out
     ex = config.current().native(order=order, fma=fma, depth=depth, algo=algo)
-    _native.run(spec, grid.data, out.data, grid.extents, grid.offset, steps, ex)
+    if spec.is_life:
+        _native.life_run(spec, grid.data, out.data, grid.extents, grid.offset, steps, ex)
+    else:
+        _native.run(spec, grid.data, out.data, grid.extents, grid.offset, steps, ex)
     return out

@@ -29,6 +29,35 @@ def load_golden():
     return meta, arrays
 
 
+def load_golden_int():
+    with open(os.path.join(GOLDEN, "reference_int.json")) as fh:
+        meta = json.load(fh)
+    return meta, np.load(os.path.join(GOLDEN, "reference_int.npz"))
+
+
+def life_spec(case):
+    """Life-like StencilSpec of a reference_int.json case."""
+    import dataclasses
+
+    from paper_2010_04868_b200.catalog import get
+
+    return dataclasses.replace(get("life").spec, name=case["name"], dim=case["dim"], boundary=case["boundary"],
+                               birth=frozenset(case["birth"]), survive=frozenset(case["survive"]))
+
+
+def int_grid(interior, boundary=0):
+    from paper_2010_04868_b200 import Grid
+
+    g = Grid(interior.shape, 1, boundary=boundary, element_kind="int32")
+    g.set_interior(interior)
+    return g
+
+
+@pytest.fixture(scope="session")
+def golden_int():
+    return load_golden_int()
+
+
 @pytest.fixture(scope="session")
 def golden():
     return load_golden()

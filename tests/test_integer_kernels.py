@@ -1,0 +1,108 @@
+"""Integer kernels: Life-like rules
+(baselines.py:52-66) and LCS (kernels/lcs.py:32, baselines.py:128-150).
+
+CPU: the NumPy oracle and the int32 Grid generator pinned to the REAL
+reference's outputs (tests/golden/make_golden_int.py).  GPU: the CUDA
+kernels through the drop-in functions / C ABI against the same goldens and
+the oracle, bit-exact (integer results)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import int_grid, life_spec
+from oracle import oracle as npo
+from paper_2010_04868_b200 import Grid
+from paper_2010_04868_b200.catalog import get
+
+
+def test_int_grid_random_reproduces_reference_inputs(golden_int):
+    meta, arrays = golden_int
+    for c in meta["life"]:
+        g = Grid.random(tuple(c["extents"]), seed=c["seed"], boundary=c["boundary"], element_kind="int32")
+        assert np.array_equal(g.interior, arrays[c["key"] + "_in"]), c["key"]
+
+
+def test_oracle_life_matches_reference(golden_int):
+    meta, arrays = golden_int
+    for c in meta["life"]:
+        got = npo.scalar_reference(life_spec(c), int_grid(arrays[c["key"] + "_in"], c["boundary"]), c["steps"])
+        assert np.array_equal(got.interior, arrays[c["key"] + "_out"]), c
+
+
+def test_oracle_lcs_matches_reference(golden_int):
+    meta, arrays = golden_int
+    for c in meta["lcs"]:
+        assert npo.lcs_length(arrays[c["key"] + "_a"], arrays[c["key"] + "_b"]) == c["length"], c
+
+
+# ---------------------------------------------------------------- GPU ----
+
+@pytest.mark.gpu
+def test_life_golden_gpu(cuda_ready, golden_int):
+    from paper_2010_04868_b200.kernels._common import execute
+
+    meta, arrays = golden_int
+    for c in meta["life"]:
+        g = int_grid(arrays[c["key"] + "_in"], c["boundary"])
+        got = execute(life_spec(c), g, c["steps"])
+        assert np.array_equal(got.interior, arrays[c["key"] + "_out"]), c
+        assert np.array_equal(g.interior, arrays[c["key"] + "_in"])  # input untouched
+        assert (got.data[0] == c["boundary"]).all()
+
+
+@pytest.mark.gpu
+def test_life_drop_in_dispatch(cuda_ready):
+    """run_temporal("life") -> jacobi2d_temporal(kernel="life") as in the
+    reference dispatcher (verify.py:60)."""
+    from paper_2010_04868_b200.verify import run_temporal
+
+    g = Grid.random((300, 257), seed=4, element_kind="int32")
+    want = npo.scalar_reference(get("life").spec, g, 40)
+    assert np.array_equal(run_temporal("life", g, 40).interior, want.interior)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ext", [(1,), (2047,), (2048,), (70001,), (63, 65), (64, 31), (129, 1000), (9, 10, 11),
+                                 (3, 65, 40)])
+def test_life_tiles_and_wrapping_sums(cuda_ready, ext):
+    """Tile edges of the 8-outputs-per-thread layout, and arbitrary int32
+    cell values (the neighbour sum wraps mod 2^32 exactly like NumPy)."""
+    import dataclasses
+
+    from paper_2010_04868_b200.kernels._common import execute
+
+    rng = np.random.default_rng(len(ext) * 1000 + ext[0])
+    spec = dataclasses.replace(get("life").spec, dim=len(ext), boundary=-3, birth=frozenset({0, 3}),
+                               survive=frozenset({2, 3, 8}))
+    g = Grid(ext, 1, boundary=-3, element_kind="int32")
+    vals = rng.integers(0, 2, ext, dtype=np.int32)
+    vals[rng.random(ext) < 0.05] = np.int32(2 ** 31 - 1)
+    vals[rng.random(ext) < 0.05] = np.int32(-(2 ** 31))
+    g.set_interior(vals)
+    want = npo.scalar_reference(spec, g, 6)
+    assert np.array_equal(execute(spec, g, 6).interior, want.interior)
+
+
+@pytest.mark.gpu
+def test_lcs_golden_gpu(cuda_ready, golden_int):
+    from paper_2010_04868_b200.kernels import lcs_temporal
+
+    meta, arrays = golden_int
+    for c in meta["lcs"]:
+        assert lcs_temporal(arrays[c["key"] + "_a"], arrays[c["key"] + "_b"]) == c["length"], c
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("na,nb,alpha", [(5000, 4000, 4), (777, 12345, 2), (12000, 31, 3), (140000, 40, 4)])
+def test_lcs_sizes_gpu(cuda_ready, na, nb, alpha):
+    """Many warps in the chain, short and long rows, and (140000 rows) more
+    than one pass of kLcsMaxWarps warps."""
+    from paper_2010_04868_b200.kernels import lcs_temporal
+
+    rng = np.random.default_rng(na + nb)
+    a = rng.integers(0, alpha, na).astype(np.int32)
+    b = rng.integers(0, alpha, nb).astype(np.int32)
+    assert lcs_temporal(a, b) == npo.lcs_length(a, b)
+    assert lcs_temporal(a, a[: nb]) == min(na, nb) if nb <= na else True

@@ -39,6 +39,7 @@ def test_struct_layouts_match_c():
 int main(void) {
   printf("%zu %zu %zu %zu\n", sizeof(tvs_stencil), sizeof(tvs_layout), sizeof(tvs_exec), sizeof(tvs_geometry));
   printf("%zu %zu %zu\n", offsetof(tvs_stencil, coeffs), offsetof(tvs_stencil, boundary), offsetof(tvs_geometry, origin));
+  printf("%zu %zu %zu\n", sizeof(tvs_life_rule), offsetof(tvs_life_rule, birth_mask), offsetof(tvs_life_rule, boundary));
   return 0;
 }
 '''
@@ -51,8 +52,10 @@ int main(void) {
     sizes = [int(x) for x in out]
     assert sizes[:4] == [ctypes.sizeof(_native.Stencil), ctypes.sizeof(_native.Layout),
                          ctypes.sizeof(_native.Exec), ctypes.sizeof(_native.Geometry)]
-    assert sizes[4:] == [_native.Stencil.coeffs.offset, _native.Stencil.boundary.offset,
-                         _native.Geometry.origin.offset]
+    assert sizes[4:7] == [_native.Stencil.coeffs.offset, _native.Stencil.boundary.offset,
+                          _native.Geometry.origin.offset]
+    assert sizes[7:] == [ctypes.sizeof(_native.LifeRule), _native.LifeRule.birth_mask.offset,
+                         _native.LifeRule.boundary.offset]
 
 
 def test_host_only_entry_points():

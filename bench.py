@@ -339,6 +339,89 @@ def untiled_legs(args):
     return out
 
 
+def integer_legs(args):
+    """SURVEY §8f rank 4 kernels, device-resident (torch buffers, CUDA events
+    on the launching stream): Life B2S23 (reference catalog "life") on a
+    16384^2 int32 grid, 4 B read + 4 B written per cell update; LCS length of
+    two seeded 65536-long sequences (4-letter alphabet), DP cells/s."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2010_04868_b200 import _native
+    from paper_2010_04868_b200.catalog import get
+
+    hbm_peak, _ = peaks()
+    out = {}
+    K = max(2, min(args.steps, 3))
+    try:
+        ext, T = (16384, 16384), 20
+        spec = get("life").spec
+        rule = _native.make_life_rule(spec)
+        geo = _native.geometry(2, ext)
+        n = int(geo.alloc_elems)
+        bufs = [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(2)]
+        s = torch.cuda.current_stream()
+        for b in bufs:
+            _native.check(_native.lib().tvs_fill_halo_i32(C.byref(geo), C.c_void_p(b.data_ptr()), 0,
+                                                          C.c_void_p(s.cuda_stream)))
+        view = bufs[0].as_strided(ext, (int(geo.strides[0]), 1), int(geo.origin))
+        g = torch.Generator(device="cuda").manual_seed(0)
+        view.copy_(torch.randint(0, 2, ext, generator=g, device="cuda", dtype=torch.int32))
+        ex = _native.make_exec()
+        res = C.c_int32(0)
+
+        def run():
+            _native.check(_native.lib().tvs_life_device(
+                C.byref(rule), C.byref(geo), C.c_void_p(bufs[0].data_ptr()), C.c_void_p(bufs[1].data_ptr()), T,
+                C.byref(ex), C.c_void_p(s.cuda_stream), C.byref(res)))
+
+        times = []
+        for i in range(args.warmup + K):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            run()
+            e1.record(s)
+            e1.synchronize()
+            if i >= args.warmup:
+                times.append(e0.elapsed_time(e1))
+        ms = statistics.mean(times)
+        v = ext[0] * ext[1] * T / (ms * 1e-3) / 1e9
+        out["life_b2s23_2d"] = {
+            "kernel": "life_kernel", "workload": f"life B2S23 {ext[0]}x{ext[1]} int32 T={T}", "value": v,
+            "unit": "GCellUpdates/s", "ms_per_run": ms, "launches_per_run": T,
+            "roofline": {"bound": "hbm", "achieved": v * 8, "peak": hbm_peak, "unit": "GB/s", "frac": v * 8 / hbm_peak,
+                         "note": "algorithmic 4 B read + 4 B written per cell update"}}
+        del bufs
+    except Exception as exc:  # report, never hide
+        out["life_b2s23_2d"] = {"error": repr(exc)}
+    try:
+        na = nb = 65536
+        rng = np.random.default_rng(12)
+        a = torch.from_numpy(rng.integers(0, 4, na).astype(np.int32)).cuda()
+        b = torch.from_numpy(rng.integers(0, 4, nb).astype(np.int32)).cuda()
+        r = torch.zeros(1, dtype=torch.int32, device="cuda")
+        s = torch.cuda.current_stream()
+        times = []
+        for i in range(args.warmup + K):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            _native.check(_native.lib().tvs_lcs_device(C.c_void_p(a.data_ptr()), na, C.c_void_p(b.data_ptr()), nb,
+                                                       C.c_void_p(r.data_ptr()), C.c_void_p(s.cuda_stream)))
+            e1.record(s)
+            e1.synchronize()
+            if i >= args.warmup:
+                times.append(e0.elapsed_time(e1))
+        ms = statistics.mean(times)
+        out["lcs"] = {"kernel": "lcs_kernel", "workload": f"lcs {na}x{nb} alphabet 4", "value": na * nb / (ms * 1e-3) / 1e9,
+                      "unit": "GCells/s", "ms_per_run": ms, "length": int(r.item())}
+    except Exception as exc:  # report, never hide
+        out["lcs"] = {"error": repr(exc)}
+    return out
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU path (oracle port) on the host."""
     rank = int(os.environ.get("RANK", "0"))
@@ -461,6 +544,7 @@ def main():
         "roofline": head["roofline"], "fp64": head["fp64"], "cpu_baseline": head.get("cpu_baseline"),
     }
     line["untiled"] = untiled_legs(args)
+    line["integer"] = integer_legs(args)
     if not args.no_all:
         per = {}
         for cid, c in CONFIGS.items():

@@ -141,6 +141,42 @@ __global__ void __launch_bounds__(256) life_kernel(const int* __restrict__ src, 
   }
 }
 
+// 2D, all 8 box neighbours (the catalog's Life): a thread owns column c and
+// kLifeNR rows; it loads the (kLifeNR + 2) x 3 window once (every load issued
+// before the first add; the side columns hit L1) and forms
+// n = rowsum(r-1) + rowsum(r) + rowsum(r+1) - centre, exact mod 2^32 like
+// the reference's wrapping int32 sum in any order.
+__global__ void __launch_bounds__(256) life2d_box_kernel(const int* __restrict__ src, int* __restrict__ dst, Geo g,
+                                                         LifeTaps t, int64_t origin) {
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * 32 + tx;
+  const int64_t r0 = (int64_t)blockIdx.y * (8 * kLifeNR) + ty * kLifeNR;
+  if (c >= g.e1) return;
+  const int64_t base = origin + c;
+  const bool full = r0 + kLifeNR <= g.e0 && r0 + g.a0_off >= 0 && r0 + kLifeNR - 1 + g.a0_off < g.a0_glob;
+  if (full) {
+    unsigned v[kLifeNR + 2][3];
+#pragma unroll
+    for (int r = 0; r < kLifeNR + 2; ++r)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) v[r][k] = (unsigned)__ldg(src + base + (r0 + r - 1) * g.s0 + (k - 1));
+    unsigned h[kLifeNR + 2];
+#pragma unroll
+    for (int r = 0; r < kLifeNR + 2; ++r) h[r] = v[r][0] + v[r][1] + v[r][2];
+#pragma unroll
+    for (int r = 0; r < kLifeNR; ++r) {
+      const unsigned n = h[r] + h[r + 1] + h[r + 2] - v[r + 1][1];
+      dst[base + (r0 + r) * g.s0] = life_rule(n, (int)v[r + 1][1], t);
+    }
+  } else {
+    for (int r = 0; r < kLifeNR && r0 + r < g.e0; ++r) {
+      const int64_t idx = base + (r0 + r) * g.s0;
+      const int64_t gr = r0 + r + g.a0_off;
+      dst[idx] = (gr < 0 || gr >= g.a0_glob) ? t.bnd : life_point(src, idx, t);
+    }
+  }
+}
+
 __global__ void fill_halo_i32_kernel(int* base, tvs_geometry g, int value) {
   const int64_t n = g.alloc_elems;
   const int64_t last_pitch = g.dim == 1 ? g.alloc_elems : g.strides[g.dim - 2];
@@ -208,6 +244,13 @@ static int life_step(const tvs_life_rule& r, const tvs_geometry& g, const int* s
   }
   if (gx >= (1ll << 31) || gy > 65535 || gz > 65535) return fail(TVS_ERR_SIZE, "life: grid too large");
   const dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)gz), block(32, 8);
+  unsigned ring = 0;  // 3x3 positions named by the taps
+  for (int k = 0; k < r.ntaps; ++k) ring |= 1u << ((r.offsets[k][0] + 1) * 3 + (r.offsets[k][1] + 1));
+  if (geo.dim == 2 && r.ntaps == 8 && ring == 0x1EFu) {  // exactly the 8 box neighbours
+    life2d_box_kernel<<<grid, block, 0, s>>>(src, dst, geo, t, g.origin);
+    TVS_LAUNCHED("life2d_box_kernel");
+    return TVS_OK;
+  }
   if (r.ntaps == 8)
     life_kernel<8><<<grid, block, 0, s>>>(src, dst, geo, t, g.origin);
   else if (r.ntaps == 2)

@@ -17,6 +17,8 @@
  *   grid.py:127-133      fnv1a64                            -> tvs_fnv1a64
  *   baselines.py:52-66   life_plane_update (int32 Life)     -> tvs_life_run / tvs_life_device
  *   kernels/lcs.py:32-108 lcs_temporal(a, b) -> int          -> tvs_lcs / tvs_lcs_device
+ *   tiling.py:347-371    execute_parallel(kernel, grid, sched) -> tvs_tiled_run / tvs_tiled_life
+ *   tiling.py:374-406    lcs_blocked(a, b, sched)           -> tvs_lcs_tiled
  *
  * Arithmetic contract (baselines.py:3-7, 43-49; vec.py:296-298): taps are
  * evaluated in the order given (the caller passes StencilSpec.offsets()
@@ -180,6 +182,26 @@ int tvs_download_i32(const tvs_geometry* g, const int32_t* dev, const tvs_layout
 int tvs_lcs(const int32_t* a, int64_t na, const int32_t* b, int64_t nb, const tvs_exec* ex, int64_t* length);
 /* device-resident form: a, b device pointers, *result written on `stream` */
 int tvs_lcs_device(const int32_t* a, int64_t na, const int32_t* b, int64_t nb, int32_t* result, void* stream);
+
+/* ---- tile-schedule executor ----------------------
+ * One tile of a schedule (tiling.py Tile): time levels [t0, t1); axis d at
+ * time t covers [lo[d] + slope_lo[d]*(t-t0), hi[d] + slope_hi[d]*(t-t0))
+ * clipped to the grid.  Tiles are listed wave by wave; wave w is
+ * tiles[wave_start[w] .. wave_start[w+1]).  Every wave is one launch (one
+ * CTA per tile) over a full time history in device memory; Gauss-Seidel
+ * uses the lexicographic in-place semantics. */
+typedef struct tvs_tile {
+  int32_t t0, t1;
+  int32_t lo[3], hi[3];
+  int32_t slope_lo[3], slope_hi[3];
+} tvs_tile;
+int tvs_tiled_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, double* out, int64_t steps,
+                  const tvs_tile* tiles, const int64_t* wave_start, int64_t nwaves, const tvs_exec* ex);
+int tvs_tiled_life(const tvs_life_rule* r, const tvs_layout* lay, const int32_t* in, int32_t* out, int64_t steps,
+                   const tvs_tile* tiles, const int64_t* wave_start, int64_t nwaves, const tvs_exec* ex);
+/* LCS over rectangle tiles: time = A index (t -> row t+1), axis 0 = B index */
+int tvs_lcs_tiled(const int32_t* a, int64_t na, const int32_t* b, int64_t nb, const tvs_tile* tiles,
+                  const int64_t* wave_start, int64_t nwaves, const tvs_exec* ex, int64_t* length);
 
 /* ---- misc -------------------------------------------------------------- */
 const char* tvs_last_error(void);

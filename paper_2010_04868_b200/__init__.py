@@ -16,6 +16,7 @@ from .model import (
     ScheduleParams,
     StencilSpec,
     dependences,
+    lcs_dependences,
     gs_hyperplane,
     gs_new_taps,
     min_space_stride,
@@ -32,6 +33,7 @@ __all__ = [
     "StencilSpec",
     "UnsupportedError",
     "dependences",
+    "lcs_dependences",
     "fnv1a64",
     "gs_hyperplane",
     "gs_new_taps",

@@ -60,6 +60,13 @@ class LifeRule(C.Structure):
     ]
 
 
+class TileDesc(C.Structure):
+    _fields_ = [
+        ("t0", C.c_int32), ("t1", C.c_int32), ("lo", C.c_int32 * 3), ("hi", C.c_int32 * 3),
+        ("slope_lo", C.c_int32 * 3), ("slope_hi", C.c_int32 * 3),
+    ]
+
+
 # exported symbols with their argtypes (checked by tests/test_native_abi.py
 # against include/tvstencil.h)
 _P = C.c_void_p
@@ -94,6 +101,12 @@ _SIGS = {
     "tvs_download_i32": (C.c_int, [C.POINTER(Geometry), _P, C.POINTER(Layout), _P, _P]),
     "tvs_lcs": (C.c_int, [_P, C.c_int64, _P, C.c_int64, C.POINTER(Exec), C.POINTER(C.c_int64)]),
     "tvs_lcs_device": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P]),
+    "tvs_tiled_run": (C.c_int, [C.POINTER(Stencil), C.POINTER(Layout), _P, _P, C.c_int64, C.POINTER(TileDesc),
+                                C.POINTER(C.c_int64), C.c_int64, C.POINTER(Exec)]),
+    "tvs_tiled_life": (C.c_int, [C.POINTER(LifeRule), C.POINTER(Layout), _P, _P, C.c_int64, C.POINTER(TileDesc),
+                                 C.POINTER(C.c_int64), C.c_int64, C.POINTER(Exec)]),
+    "tvs_lcs_tiled": (C.c_int, [_P, C.c_int64, _P, C.c_int64, C.POINTER(TileDesc), C.POINTER(C.c_int64), C.c_int64,
+                                C.POINTER(Exec), C.POINTER(C.c_int64)]),
     "tvs_launch_counter": (C.c_int64, []),
     "tvs_version": (C.c_char_p, []),
 }

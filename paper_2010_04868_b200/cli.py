@@ -9,7 +9,11 @@ median of ``--reps`` after one warm-up, and CSV schema
 ``kernel,variant,dim,nx,ny,nz,t,threads,tile,reps,gstencils_per_s,checksum``
 (cli.py:39) with the FNV-1a checksum of the final grid's TSTN dump — so a
 GPU row and a reference CPU row of the same run carry the same checksum.
-Appended columns: ``backend,device_ms,depth``.
+Appended columns: ``backend,device_ms,depth``.  ``--tile WxH[xD]:T`` and
+``--threads a[..b]`` select the tile-schedule executor (tiling.py: one GPU
+launch per wave, one CTA per tile) as in the reference (cli.py:57-70,
+156-170); ``life`` (int32) and ``lcs`` (LCS length of two seeded
+sequences, cells = na x nb) are benchmarked like the reference does.
 
 ``--mode verify`` runs on the GPU only (the product never embeds the CPU
 oracle): the reference's known-answer vectors (test_baselines.py:17-36) and,
@@ -33,12 +37,50 @@ from . import _native, config
 from .catalog import DEFAULT_CATALOG, get as catalog_get
 from .grid import Grid, fnv1a64
 from .kernels import KernelVariant
+from .kernels import lcs_temporal
+from .tiling import build_schedule, execute_parallel, lcs_blocked
 from .verify import default_matrix, run_temporal
 
 CSV_HEADER = "kernel,variant,dim,nx,ny,nz,t,threads,tile,reps,gstencils_per_s,checksum"
 CSV_EXTRA = "backend,device_ms,depth"
 DEFAULT_SIZES = {1: (1_000_000,), 2: (512, 512), 3: (64, 64, 64)}
-GPU_KERNELS = [k for k, e in DEFAULT_CATALOG.items() if e.spec.element_kind == "float64"]
+GPU_KERNELS = list(DEFAULT_CATALOG) + ["lcs"]
+FP_KERNELS = [k for k, e in DEFAULT_CATALOG.items() if e.spec.element_kind == "float64"]
+DEFAULT_TILES = {  # reference cli.py:44-53 (used when --threads > 1 without --tile)
+    "heat1d": ((16384,), 128), "heat2d": ((256, 256), 64), "jac2d9p": ((256, 256), 64),
+    "heat3d": ((32, 32, 32), 8), "life": ((256, 256), 32), "gs1d": ((2048,), 64), "gs2d": ((128, 128), 32),
+    "gs3d": ((32, 32, 32), 32), "lcs": ((4096,), 4096),
+}
+
+
+def _parse_tile(text):
+    """'WxHxD:T' -> (space extents, time height) (reference cli.py:57-63)."""
+    space, _, t = text.partition(":")
+    if not t:
+        raise argparse.ArgumentTypeError("tile needs a :T time height")
+    return tuple(int(p) for p in space.split("x")), int(t)
+
+
+def _parse_threads(text):
+    if ".." in text:
+        lo, hi = text.split("..")
+        return list(range(int(lo), int(hi) + 1))
+    return [int(text)]
+
+
+def _fit_tile(tile, extents, entry):
+    """Shrink a tile request by powers of two until it fits the grid (the
+    reference's rule, cli.py:253-265)."""
+    space, height = tile
+    space = list(space[: len(extents)]) + [space[-1]] * (len(extents) - len(space))
+    floor = 4 * entry.s * entry.vl
+    for i, (w, n) in enumerate(zip(space, extents)):
+        while w > n and (i > 0 or w // 2 >= floor):
+            w //= 2
+        space[i] = min(w, n) if i > 0 else w
+    while height > entry.vl and height > min(space[1:] or [height]):
+        height //= 2
+    return tuple(space), max(entry.vl, height // entry.vl * entry.vl)
 
 
 def build_parser() -> argparse.ArgumentParser:
@@ -51,6 +93,9 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--ny", type=int)
     p.add_argument("--nz", type=int)
     p.add_argument("--t", type=int, dest="steps")
+    p.add_argument("--tile", type=_parse_tile, help="tile-schedule executor: WxHxD:T (space tile : time height)")
+    p.add_argument("--threads", type=_parse_threads, default=None,
+                   help="reference worker counts (a or a..b); on the GPU every tile of a wave is a CTA")
     p.add_argument("--reps", type=int, default=5)
     p.add_argument("--csv", help="append benchmark rows to this file")
     p.add_argument("--dump", help="write the final grid dump (TSTN) here")
@@ -74,6 +119,10 @@ def _apply_config(args, argv):
         attr = "steps" if key == "t" else key.replace("-", "_")
         if key in passed or attr in passed or not hasattr(args, attr):
             continue
+        if attr == "tile" and isinstance(value, str):
+            value = _parse_tile(value)
+        if attr == "threads" and isinstance(value, (str, int)):
+            value = _parse_threads(str(value))
         setattr(args, attr, value)
     return args
 
@@ -94,46 +143,77 @@ def _grid_size(args, dim):
     return tuple(size)
 
 
+def _timed(fn, reps):
+    fn()  # warm-up
+    times, out = [], None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = fn()
+        times.append(time.perf_counter() - t0)
+    return statistics.median(times), out
+
+
 def _bench(args) -> int:
     rows = []
     scheme = args.variant.replace("-", "_")
+    tile_txt = ("x".join(map(str, args.tile[0])) + f":{args.tile[1]}") if args.tile else ""
     for kernel in _kernels(args.kernel):
-        entry = catalog_get(kernel)
-        dim = entry.spec.dim
-        size = _grid_size(args, dim)
-        steps = args.steps or 64
-        grid = Grid.random(size, seed=args.seed)
-        opts = {"order": args.order} if entry.spec.dependence_kind == "gauss_seidel" and dim > 1 else {}
-        with config.using(fma=args.fma, depth=args.depth):
-            # device-resident time (plan API) for the device_ms column
-            plan = _native.Plan(entry.spec, size, config.current().native(order=args.order))
-            plan.upload(grid.data, grid.offset)
-            plan.run(steps)
-            plan.synchronize()
-            dev = []
-            for _ in range(args.reps):
-                plan.upload(grid.data, grid.offset)
-                plan.run(steps)
-                dev.append(plan.last_ms())
-            plan.close()
-            run_temporal(kernel, grid, steps, KernelVariant(scheme, entry.spec.dependence_kind != "jacobi"), **opts)
-            times = []
-            out = None
-            for _ in range(args.reps):
-                t0 = time.perf_counter()
-                out = run_temporal(kernel, grid, steps,
-                                   KernelVariant(scheme, entry.spec.dependence_kind != "jacobi"), **opts)
-                times.append(time.perf_counter() - t0)
-        pts = int(np.prod(size))
-        rate = pts * steps / statistics.median(times) / 1e9
-        check = fnv1a64(out.dump_bytes())
-        if args.dump:
-            out.dump(args.dump)
-        s3 = tuple(size) + (0, 0)
-        row = (f"{kernel},{args.variant},{dim},{s3[0]},{s3[1] or ''},{s3[2] or ''},{steps},1,,{args.reps},"
-               f"{rate:.6f},{check:016x},cuda-sm100a,{statistics.median(dev):.3f},{args.depth}")
-        rows.append(row)
-        print(row)
+        for threads in args.threads or [1]:
+            dev_ms = ""
+            if kernel == "lcs":
+                rng = np.random.default_rng(args.seed)
+                na = args.nx or 20000
+                nb = args.ny or na
+                a = rng.integers(0, 4, na, dtype=np.int32)
+                b = rng.integers(0, 4, nb, dtype=np.int32)
+                steps, dim, s3 = na, 2, (na, nb, 0)
+                if args.tile or threads > 1:
+                    tile = args.tile or DEFAULT_TILES["lcs"]
+                    sched = build_schedule("lcs", (nb,), na, tile[0], tile[1])
+                    med, val = _timed(lambda: lcs_blocked(a, b, sched, workers=threads), args.reps)
+                else:
+                    med, val = _timed(lambda: lcs_temporal(a, b), args.reps)
+                rate = na * nb / med / 1e9
+                check = val & 0xFFFFFFFFFFFFFFFF
+            else:
+                entry = catalog_get(kernel)
+                dim = entry.spec.dim
+                size = _grid_size(args, dim)
+                steps = args.steps or 64
+                grid = Grid.random(size, seed=args.seed, element_kind=entry.spec.element_kind, vl=entry.vl)
+                gauss = entry.spec.dependence_kind == "gauss_seidel"
+                opts = {"order": args.order} if gauss and dim > 1 else {}
+                tile = args.tile or (DEFAULT_TILES[kernel] if threads > 1 else None)
+                with config.using(fma=args.fma, depth=args.depth):
+                    if tile:
+                        tile = _fit_tile(tile, grid.extents, entry)
+                        sched = build_schedule(kernel, grid.extents, steps, tile[0], tile[1])
+                        med, out = _timed(lambda: execute_parallel(kernel, grid, sched, workers=threads), args.reps)
+                    else:
+                        if entry.spec.element_kind == "float64":
+                            # device-resident time (plan API) for the device_ms column
+                            plan = _native.Plan(entry.spec, size, config.current().native(order=args.order))
+                            plan.upload(grid.data, grid.offset)
+                            plan.run(steps)
+                            plan.synchronize()
+                            dev = []
+                            for _ in range(args.reps):
+                                plan.upload(grid.data, grid.offset)
+                                plan.run(steps)
+                                dev.append(plan.last_ms())
+                            plan.close()
+                            dev_ms = f"{statistics.median(dev):.3f}"
+                        var = KernelVariant(scheme, gauss)
+                        med, out = _timed(lambda: run_temporal(kernel, grid, steps, var, **opts), args.reps)
+                rate = int(np.prod(size)) * steps / med / 1e9
+                check = fnv1a64(out.dump_bytes())
+                if args.dump:
+                    out.dump(args.dump)
+                s3 = tuple(size) + (0, 0)
+            row = (f"{kernel},{args.variant},{dim},{s3[0]},{s3[1] or ''},{s3[2] or ''},{steps},{threads},{tile_txt},"
+                   f"{args.reps},{rate:.6f},{check:016x},cuda-sm100a,{dev_ms},{args.depth}")
+            rows.append(row)
+            print(row)
     if args.csv:
         try:
             new = not open(args.csv).read(1)
@@ -161,7 +241,7 @@ def _verify(args) -> int:
         good = got == want
         ok &= good
         print(f"  {'PASS' if good else 'FAIL'} known answer {kernel}: {got}")
-    cells = default_matrix(cells_per_kernel=args.cells, kernels=_kernels(args.kernel))
+    cells = default_matrix(cells_per_kernel=args.cells, kernels=[k for k in _kernels(args.kernel) if k in FP_KERNELS])
     t0 = time.time()
     bad = 0
     for cell in cells:

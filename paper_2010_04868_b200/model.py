@@ -133,6 +133,13 @@ def dependences(spec: StencilSpec) -> frozenset[Dependence]:
     return frozenset(out)
 
 
+def lcs_dependences() -> frozenset[Dependence]:
+    """The LCS recurrence with the A index as time (reference
+    ``model.py:163-168``): lcs[x][y] reads lcs[x-1][y], lcs[x-1][y-1] and
+    lcs[x][y-1]."""
+    return frozenset({Dependence(1, (0,)), Dependence(1, (-1,)), Dependence(0, (-1,))})
+
+
 def min_space_stride(deps: frozenset[Dependence]) -> int:
     """Smallest integer s > max{dx0/dt : dt >= 1, dx0 > 0}; 1 if none.
     (reference ``model.py:171-193``).  On the GPU this is the minimum lane lag

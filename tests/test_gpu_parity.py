@@ -334,6 +334,34 @@ def test_cli_bench_and_verify(cuda_ready, tmp_path):
     assert cli.main(["--mode", "verify", "--kernel", "gs2d9p", "--cells", "3"]) == 0
 
 
+def test_cli_tiles_threads_life_lcs(cuda_ready, tmp_path):
+    """--tile / --threads route through the tile-schedule executor with the
+    same checksum as the unblocked run; life and lcs rows as the reference
+    CLI writes them (cli.py:156-240)."""
+    from oracle import oracle as npo
+    from paper_2010_04868_b200 import cli
+    from paper_2010_04868_b200.grid import fnv1a64
+
+    csv = tmp_path / "rows.csv"
+    assert cli.main(["--mode", "bench", "--kernel", "heat2d", "--nx", "96", "--ny", "80", "--t", "12",
+                     "--tile", "64x32:8", "--threads", "1..2", "--reps", "1", "--csv", str(csv)]) == 0
+    assert cli.main(["--mode", "bench", "--kernel", "life", "--nx", "96", "--ny", "80", "--t", "12",
+                     "--reps", "1", "--csv", str(csv)]) == 0
+    assert cli.main(["--mode", "bench", "--kernel", "lcs", "--nx", "300", "--ny", "200", "--reps", "1",
+                     "--csv", str(csv)]) == 0
+    assert cli.main(["--mode", "bench", "--kernel", "lcs", "--nx", "300", "--ny", "200", "--reps", "1",
+                     "--tile", "64:32", "--csv", str(csv)]) == 0
+    rows = [r.split(",") for r in csv.read_text().strip().splitlines()[1:]]
+    want = cref.scalar_reference(get("heat2d").spec, Grid.random((96, 80), seed=0), 12)
+    assert rows[0][7] == "1" and rows[1][7] == "2" and rows[0][8] == "64x32:8"
+    assert rows[0][11] == rows[1][11] == f"{fnv1a64(want.dump_bytes()):016x}"
+    wl = npo.scalar_reference(get("life").spec, Grid.random((96, 80), seed=0, element_kind="int32"), 12)
+    assert rows[2][11] == f"{fnv1a64(wl.dump_bytes()):016x}"
+    rng = np.random.default_rng(0)
+    a, b = rng.integers(0, 4, 300, dtype=np.int32), rng.integers(0, 4, 200, dtype=np.int32)
+    assert int(rows[3][11], 16) == int(rows[4][11], 16) == npo.lcs_length(a, b)
+
+
 @pytest.mark.parametrize("cluster", [1, 2, 4, 8])
 def test_gs2d_pipeline_cluster_sizes(cuda_ready, cluster):
     """Lexicographic GS-2D pipeline with consecutive blocks handing off through

@@ -350,7 +350,8 @@ static int ensure_ctx(RunCtx& c, int device, int dim, const int64_t* ext, int nb
 static int band_rows_default() {
   static const int v = [] {
     const char* e = getenv("TVS_E2E_BANDS");  // 0 disables the pipelined path
-    return e ? atoi(e) : 2 * jacobi2d_band_rows();  // 512 rows (256: 141 ms, 1024: 95 ms)
+    // config 3 e2e (skewed bands, 32-row segments): 128 58.1, 256 55.5, 512 56.4, 1024 59.6 ms
+    return e ? atoi(e) : 256;
   }();
   return v;
 }
@@ -368,94 +369,105 @@ static int copy_rows(const tvs_geometry& g, double* dev, const tvs_layout& lay, 
   return TVS_OK;
 }
 
+// Drop-in path for 2D Jacobi with host Grids: uploads, temporally blocked
+// passes and downloads overlap over row bands.  Band b of pass k covers rows
+// [b*band - S_k, (b+1)*band - S_k) (clipped), S_k = levels of passes < k:
+// every pass shifts the bands up by its own depth, so pass k of band b reads
+// only rows that pass k-1 of bands b and b-1 wrote (a parallelogram in
+// (rows, time)).  Band b therefore runs all its passes as soon as band b+1's
+// first rows are uploaded and band b-1 has kept pace, and its final rows go
+// back to the host while later bands are still uploading: H2D, compute and
+// D2H all overlap (PCIe is full duplex).  One stream per band; pass k of band
+// b waits on pass k-1 of band b-1 (same-stream order covers band b itself).
+// WAR is safe: the only later writer of rows that pass k of band b reads is
+// pass k+2 of band b+1, which depends on pass k+1 of band b.
 static int jacobi2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, const double* in, double* out,
                               int64_t steps, const tvs_exec& ex, RunCtx& c, int64_t band) {
   const tvs_geometry& g = c.geo;
   const int64_t rows = g.extents[0];
-  const int nb = (int)((rows + band - 1) / band);
   int depth = ex.temporal_depth > 0 ? ex.temporal_depth : jacobi2d_default_depth();
   depth = std::min(depth, jacobi2d_max_depth());
   const int K = (int)((steps + depth - 1) / depth);
   const bool fma = use_fma(st, ex);
+  // shorter row segments than the device-resident default: a band's pass is
+  // then a shorter dependent chain, which is what the pipeline's tail waits on
+  static const int seg = [] {
+    const char* e = getenv("TVS_E2E_SEG");  // config 3 e2e at 256-row bands: 32 55.5, 64 60.1, 256 64.0 ms
+    return e ? atoi(e) : 32;
+  }();
+  std::vector<int> dk(K);
+  std::vector<int64_t> S(K + 1, 0);
+  {
+    int64_t left = steps;
+    for (int k = 0; k < K; ++k) {
+      dk[k] = (int)std::min<int64_t>(left, depth);
+      left -= dk[k];
+      S[k + 1] = S[k] + dk[k];
+    }
+  }
+  if (band < 2 * depth) return fail(TVS_ERR_INVALID, "pipelined band shorter than two temporal blocks");
+  // enough bands that the last one still reaches the top row after every shift
+  const int nb = (int)((rows + S[K] + band - 1) / band);
   while ((int)c.bands.size() < nb) {
     cudaStream_t t;
     TVS_CUDA(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
     c.bands.push_back(t);
   }
-  auto bs = [&](int b) { return c.bands[b]; };
   const size_t nev = (size_t)nb * (K + 1);
   while (c.events.size() < nev) {
     cudaEvent_t e;
     TVS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c.events.push_back(e);
   }
-  auto up = [&](int b) { return c.events[b]; };                               // band b uploaded
-  auto done = [&](int b, int k) { return c.events[(size_t)nb * (k + 1) + b]; };  // launch k of band b ended
+  auto up = [&](int b) { return c.events[b]; };                               // upload of rows [b*band, (b+1)*band)
+  auto done = [&](int b, int k) { return c.events[(size_t)nb * (k + 1) + b]; };  // pass k of band b ended
+  auto lo_of = [&](int b, int k) { return std::max<int64_t>(0, (int64_t)b * band - S[k]); };
+  auto hi_of = [&](int b, int k) { return std::min<int64_t>(rows, (int64_t)(b + 1) * band - S[k]); };
   cudaStream_t cs = c.stream;
   int rc;
-  // TVS_E2E_TRACE=1: stderr timeline (upload start/end, first and last download)
   static const bool trace = getenv("TVS_E2E_TRACE") != nullptr;
-  cudaEvent_t tr[5] = {};
-  if (trace)
+  cudaEvent_t tr[4] = {};
+  if (trace) {
     for (auto& e : tr) cudaEventCreate(&e);
-  if (trace) cudaEventRecord(tr[0], cs);
+    cudaEventRecord(tr[0], cs);
+  }
   if ((rc = fill_halo(g, c.buf[0], st.boundary, cs))) return rc;
   if ((rc = fill_halo(g, c.buf[1], st.boundary, cs))) return rc;
-  // Enqueue in wavefront order.  Streams share a few hardware queues
-  // (CUDA_DEVICE_MAX_CONNECTIONS, default 8), so an operation can end up
-  // queued behind unrelated work enqueued before it: issuing every upload
-  // first put band kernels behind the whole 2 GB upload.  At step t: upload
-  // band t, then every launch (b, k) whose inputs are then uploaded
-  // (b + k + 1 = t), then the download of the band whose last launch was
-  // just issued.  Every event waited on was recorded earlier in host order.
-  std::vector<int> dk(K);
-  {
-    int64_t left = steps;
-    for (int k = 0; k < K; ++k) {
-      dk[k] = (int)std::min<int64_t>(left, depth);
-      left -= dk[k];
-    }
-  }
+  const int nup = (int)((rows + band - 1) / band);
   double* result = c.buf[K & 1];
-  const auto h0 = std::chrono::steady_clock::now();
-  for (int t = 0; t <= nb + K; ++t) {
-    if (t < nb) {
-      if ((rc = copy_rows(g, c.buf[0], lay, const_cast<double*>(in), true, t * band, std::min(rows, (t + 1) * band), cs)))
+  int uploaded = 0;
+  for (int b = 0; b < nb; ++b) {
+    // uploads stay one band ahead of the band whose passes are enqueued next
+    for (; uploaded < nup && uploaded <= b + 1; ++uploaded) {
+      if ((rc = copy_rows(g, c.buf[0], lay, const_cast<double*>(in), true, (int64_t)uploaded * band,
+                          std::min(rows, (int64_t)(uploaded + 1) * band), cs)))
         return rc;
-      TVS_CUDA(cudaEventRecord(up(t), cs));
-      if (trace && t == nb - 1) cudaEventRecord(tr[1], cs);
+      TVS_CUDA(cudaEventRecord(up(uploaded), cs));
+      if (trace && uploaded == nup - 1) cudaEventRecord(tr[1], cs);
     }
+    cudaStream_t sb = c.bands[b];
+    // pass 0 reads rows [b*band - d, (b+1)*band + d): uploads b-1 .. b+1
+    for (int u = b - 1; u <= b + 1; ++u)
+      if (u >= 0 && u < nup) TVS_CUDA(cudaStreamWaitEvent(sb, up(u), 0));
     for (int k = 0; k < K; ++k) {
-      const int b = t - 1 - k;  // (b, k) reads bands b-1..b+1 after launch k-1 (or their upload)
-      if (b < 0 || b >= nb) continue;
-      cudaStream_t sb = bs(b);
-      for (int nbr = b - 1; nbr <= b + 1; ++nbr) {
-        if (nbr < 0 || nbr >= nb) continue;
-        if (k == 0)
-          TVS_CUDA(cudaStreamWaitEvent(sb, up(nbr), 0));
-        else
-          TVS_CUDA(cudaStreamWaitEvent(sb, done(nbr, k - 1), 0));
-      }
-      if ((rc = jacobi2d_blocked(st, g, c.buf[k & 1], c.buf[(k + 1) & 1], dk[k], fma, sb, b * band,
-                                 std::min(rows, (b + 1) * band))))
+      if (k > 0 && b > 0) TVS_CUDA(cudaStreamWaitEvent(sb, done(b - 1, k - 1), 0));
+      const int64_t lo = lo_of(b, k), hi = hi_of(b, k);
+      if (hi > lo && (rc = jacobi2d_blocked(st, g, c.buf[k & 1], c.buf[(k + 1) & 1], dk[k], fma, sb, lo, hi, seg)))
         return rc;
       TVS_CUDA(cudaEventRecord(done(b, k), sb));
     }
-    const int bd = t - K;  // its launch K-1 was issued in this step (t = bd + K)
-    if (bd >= 0 && bd < nb) {
-      if (trace && bd == 0) cudaEventRecord(tr[2], bs(0));
-      if ((rc = copy_rows(g, result, lay, out, false, bd * band, std::min(rows, (bd + 1) * band), bs(bd)))) return rc;
-      if (trace && bd == 0) cudaEventRecord(tr[3], bs(0));
-    }
+    const int64_t lo = lo_of(b, K), hi = hi_of(b, K);
+    if (hi > lo && (rc = copy_rows(g, result, lay, out, false, lo, hi, sb))) return rc;
+    if (trace && b == 0) cudaEventRecord(tr[2], sb);
   }
-  const double host_up_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
-  for (int b = 0; b < nb; ++b) TVS_CUDA(cudaStreamSynchronize(bs(b)));
-  if (trace) cudaEventRecord(tr[4], cs);
+  for (int b = 0; b < nb; ++b) TVS_CUDA(cudaStreamSynchronize(c.bands[b]));
   if (trace) {
-    float t[5] = {};
-    for (int i = 1; i < 5; ++i) cudaEventElapsedTime(&t[i], tr[0], tr[i]);
-    fprintf(stderr, "[e2e] bands %d x %lld rows, K %d: uploads done %.2f ms, band0 D2H %.2f-%.2f ms, last D2H end %.2f ms"
-            " (host enqueue %.2f ms)\n", nb, (long long)band, K, t[1], t[2], t[3], t[4], host_up_ms);
+    cudaEventRecord(tr[3], cs);
+    cudaStreamSynchronize(cs);
+    float t[4] = {};
+    for (int i = 1; i < 4; ++i) cudaEventElapsedTime(&t[i], tr[0], tr[i]);
+    fprintf(stderr, "[e2e] bands %d x %lld rows, K %d: uploads done %.2f ms, band0 final D2H %.2f ms, end %.2f ms\n",
+            nb, (long long)band, K, t[1], t[2], t[3]);
     for (auto& e : tr) cudaEventDestroy(e);
   }
   return TVS_OK;
@@ -574,7 +586,7 @@ int tvs_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, doub
   if (!gs) {
     const int64_t band = band_rows_default();
     if (band > 0 && st->dim == 2 && steps > 0 && ex->algo != TVS_ALGO_NAIVE && jacobi2d_blocked_supported(*st) &&
-        band % jacobi2d_band_rows() == 0 && c.geo.extents[0] >= 4 * band)
+        c.geo.extents[0] >= 4 * band)
       return jacobi2d_pipelined(*st, *lay, in, out, steps, *ex, c, band);
   }
   if ((rc = fill_halo(c.geo, c.buf[0], st->boundary, s))) return rc;

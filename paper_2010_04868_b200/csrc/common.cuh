@@ -203,10 +203,11 @@ int jacobi1d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double*
 int jacobi1d_default_depth();
 int jacobi1d_max_depth();
 bool jacobi2d_blocked_supported(const tvs_stencil& st);
-// rows [row_lo, row_hi) only when given (row_lo a multiple of the kernel's
-// 256-row segment): one band of the pipelined host path
+// rows [row_lo, row_hi) only when given (any band): one band of the
+// pipelined host path
 int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
-                     int depth, bool fma, cudaStream_t s, int64_t row_lo = 0, int64_t row_hi = -1);
+                     int depth, bool fma, cudaStream_t s, int64_t row_lo = 0, int64_t row_hi = -1,
+                     int seg_rows = 0);
 int jacobi2d_band_rows();
 int jacobi2d_max_depth();
 int jacobi2d_default_depth();

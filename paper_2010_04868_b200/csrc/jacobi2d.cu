@@ -92,18 +92,18 @@ template <unsigned MASK, int D, bool FMA, int kP2>
 __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __restrict__ src,
                                                                 double* __restrict__ dst, Geo g, int64_t origin,
                                                                 Coeff9 cf, double bnd, int64_t n_strips,
-                                                                int64_t n_tasks, int64_t seg0) {
+                                                                int64_t n_tasks, int64_t row_lo, int64_t row_hi, int seg_rows) {
   constexpr int U = 32 * kP2 - 2 * D;  // useful columns per strip
   const double(&c)[9] = cf.c;          // constant-bank operands
 
   const int lane = threadIdx.x & 31;
   const int64_t task = kWarps2 == 1 ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * kWarps2 + (threadIdx.x >> 5);
   if (task >= n_tasks) return;
-  const int64_t strip = task % n_strips, seg = seg0 + task / n_strips;
+  const int64_t strip = task % n_strips, seg = task / n_strips;
   const int col0 = (int)(-D + strip * U);  // first column of the strip
   const int cl = col0 + lane * kP2;        // this lane's first column
-  const int r0 = (int)(seg * kRowsSeg);    // first output row
-  const int r1 = (int)(r0 + kRowsSeg < g.e0 ? r0 + kRowsSeg : g.e0);
+  const int r0 = (int)(row_lo + seg * seg_rows);  // first output row
+  const int r1 = (int)(r0 + seg_rows < row_hi ? r0 + seg_rows : row_hi);
   const int e0 = (int)g.e0, e1 = (int)g.e1;
   const int a0 = (int)g.a0_off, ag = (int)g.a0_glob;
 
@@ -297,66 +297,67 @@ int jacobi2d_default_depth() { return 8; }  // measured best (config 3, P = 3: D
 
 template <unsigned MASK, int D, int P>
 static void launch2d_d(bool fma, unsigned blocks, cudaStream_t s, const double* src, double* dst, const Geo& geo,
-                       int64_t origin, const Coeff9& cf, double bnd, int64_t ns, int64_t nt, int64_t seg0) {
+                       int64_t origin, const Coeff9& cf, double bnd, int64_t ns, int64_t nt, int64_t lo, int64_t hi,
+                       int seg_rows) {
   if (fma)
-    jacobi2d_kernel<MASK, D, true, P><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, seg0);
+    jacobi2d_kernel<MASK, D, true, P><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows);
   else
-    jacobi2d_kernel<MASK, D, false, P><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, seg0);
+    jacobi2d_kernel<MASK, D, false, P><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows);
 }
 
-// rows [row_lo, row_hi) of the grid (row_lo a multiple of kRowsSeg; the
+// rows [row_lo, row_hi) of the grid (any band; the
 // whole grid by default): one row band of the pipelined host path
 template <unsigned MASK, int D>
 static void launch2d_one(bool fma, cudaStream_t s, const double* src, double* dst, const Geo& geo, int64_t origin,
-                         const Coeff9& cf, double bnd, int64_t row_lo, int64_t row_hi) {
+                         const Coeff9& cf, double bnd, int64_t row_lo, int64_t row_hi, int seg_rows) {
   // columns per lane: registers grow as 2 * P * D accumulators; P = 3 at
   // D = 5..8 keeps 12 warps/SM at D = 8 (168 registers) where P = 4 held 9
   // (config 3: D = 8 P = 4 1596, P = 3 1723 GSt/s; D > 8 at P = 3 is slower)
   constexpr int P = D <= 4 ? 4 : (D <= 8 ? 3 : 2);
   const int64_t U = 32 * P - 2 * D;
   const int64_t ns = (geo.e1 + U - 1) / U;
-  const int64_t seg0 = row_lo / kRowsSeg;
-  const int64_t nseg = (row_hi + kRowsSeg - 1) / kRowsSeg - seg0;
+  const int64_t nseg = (row_hi - row_lo + seg_rows - 1) / seg_rows;
   const int64_t nt = ns * nseg;
   const unsigned blocks = (unsigned)((nt + kWarps2 - 1) / kWarps2);
-  launch2d_d<MASK, D, P>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt, seg0);
+  launch2d_d<MASK, D, P>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt, row_lo, row_hi, seg_rows);
 }
 
 template <unsigned MASK>
 static void launch2d(int depth, bool fma, cudaStream_t s, const double* src, double* dst, const Geo& geo,
-                     int64_t origin, const Coeff9& cf, double bnd, int64_t lo, int64_t hi) {
+                     int64_t origin, const Coeff9& cf, double bnd, int64_t lo, int64_t hi, int seg) {
   switch (depth) {
-    case 1: launch2d_one<MASK, 1>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi); break;
-    case 2: launch2d_one<MASK, 2>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi); break;
-    case 3: launch2d_one<MASK, 3>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi); break;
-    case 4: launch2d_one<MASK, 4>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi); break;
-    case 5: launch2d_one<MASK, 5>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi); break;
-    case 6: launch2d_one<MASK, 6>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi); break;
-    case 7: launch2d_one<MASK, 7>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi); break;
-    case 8: launch2d_one<MASK, 8>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi); break;
-    case 9: launch2d_one<MASK, 9>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi); break;
-    case 10: launch2d_one<MASK, 10>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi); break;
-    case 11: launch2d_one<MASK, 11>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi); break;
-    default: launch2d_one<MASK, 12>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi); break;
+    case 1: launch2d_one<MASK, 1>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
+    case 2: launch2d_one<MASK, 2>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
+    case 3: launch2d_one<MASK, 3>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
+    case 4: launch2d_one<MASK, 4>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
+    case 5: launch2d_one<MASK, 5>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
+    case 6: launch2d_one<MASK, 6>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
+    case 7: launch2d_one<MASK, 7>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
+    case 8: launch2d_one<MASK, 8>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
+    case 9: launch2d_one<MASK, 9>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
+    case 10: launch2d_one<MASK, 10>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
+    case 11: launch2d_one<MASK, 11>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
+    default: launch2d_one<MASK, 12>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
   }
 }
 
 int jacobi2d_band_rows() { return kRowsSeg; }
 
 int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, int depth,
-                     bool fma, cudaStream_t s, int64_t row_lo, int64_t row_hi) {
+                     bool fma, cudaStream_t s, int64_t row_lo, int64_t row_hi, int seg_rows) {
   Coeff9 cf;
   const unsigned mask = slots2d(st, cf);
   if ((mask != kStar5 && mask != kBox9) || depth < 1 || depth > kMaxD2)
     return fail(TVS_ERR_UNSUPPORTED, "jacobi2d_blocked: tap set or depth");
   if (row_hi < 0) row_hi = g.extents[0];
-  if (row_lo < 0 || row_lo % kRowsSeg != 0 || row_hi > g.extents[0] || row_lo >= row_hi)
+  if (seg_rows <= 0) seg_rows = kRowsSeg;
+  if (row_lo < 0 || row_hi > g.extents[0] || row_lo >= row_hi)
     return fail(TVS_ERR_INVALID, "jacobi2d_blocked: row band");
   const Geo geo = make_geo(g);
   if (mask == kStar5)
-    launch2d<kStar5>(depth, fma, s, src, dst, geo, g.origin, cf, st.boundary, row_lo, row_hi);
+    launch2d<kStar5>(depth, fma, s, src, dst, geo, g.origin, cf, st.boundary, row_lo, row_hi, seg_rows);
   else
-    launch2d<kBox9>(depth, fma, s, src, dst, geo, g.origin, cf, st.boundary, row_lo, row_hi);
+    launch2d<kBox9>(depth, fma, s, src, dst, geo, g.origin, cf, st.boundary, row_lo, row_hi, seg_rows);
   TVS_LAUNCHED("jacobi2d_kernel");
   return TVS_OK;
 }

@@ -16,9 +16,11 @@ from paper_2010_04868_b200 import Grid, config  # noqa: E402
 from paper_2010_04868_b200.catalog import get  # noqa: E402
 from paper_2010_04868_b200.kernels._common import execute  # noqa: E402
 
-# (rows, cols, steps, depth): >= 4 bands of 512 / 1024 rows, ragged last band,
+# (rows, cols, steps, depth): >= 4 bands, ragged last band, bands shifted by the
+# levels of every pass (skewed pipeline),
 # T not a multiple of the depth, 1-step runs, both P regimes (D <= 4, D 5..8)
-CASES = [(4100, 130, 19, 0), (4096, 333, 8, 0), (5000, 64, 1, 0), (9000, 50, 33, 5), (4608, 97, 12, 3)]
+CASES = [(4100, 130, 19, 0), (4096, 333, 8, 0), (5000, 64, 1, 0), (9000, 50, 33, 5), (4608, 97, 12, 3),
+         (4096, 40, 700, 0)]  # total band shift (700 rows) beyond one band: empty / clipped bands
 bad = 0
 for kernel in ("heat2d", "jac2d9p"):
     for rows, cols, steps, depth in CASES:

@@ -377,7 +377,7 @@ def test_gs2d_pipeline_cluster_sizes(cuda_ready, cluster):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("band", [0, 512, 1024, 2048])
+@pytest.mark.parametrize("band", [0, 300, 512, 777, 1024])
 def test_jacobi2d_pipelined_e2e_bands(cuda_ready, band):
     """tvs_run's pipelined 2D Jacobi path (row bands on their own streams,
     uploads / launches / downloads overlapped by events) is bit-identical to

@@ -473,6 +473,106 @@ static int jacobi2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
   return TVS_OK;
 }
 
+// 3D Jacobi drop-in path: the same skewed pipeline over axis-0 slabs (planes
+// [b*slab - S_k, (b+1)*slab - S_k) in pass k, S_k = levels of passes < k),
+// two levels per pass (K4b; a single-step last pass when T is odd).  Every
+// slab-pass reads only planes that pass k-1 of slabs b and b-1 wrote.
+static int copy_planes(const tvs_geometry& g, double* dev, const tvs_layout& lay, double* host, bool upload,
+                       int64_t p0, int64_t p1, cudaStream_t s) {
+  cudaMemcpy3DParms p;
+  std::memset(&p, 0, sizeof(p));
+  const cudaPitchedPtr hptr = make_cudaPitchedPtr(host, sizeof(double) * lay.shape[2], lay.shape[2], lay.shape[1]);
+  const cudaPitchedPtr dptr = make_cudaPitchedPtr(dev, sizeof(double) * g.strides[1], g.strides[1],
+                                                  g.strides[0] / g.strides[1]);
+  const cudaPos hpos = make_cudaPos(sizeof(double) * lay.offset, lay.offset, lay.offset + p0);
+  const cudaPos dpos = make_cudaPos(sizeof(double) * kPadLast, 1, 1 + p0);
+  p.extent = make_cudaExtent(sizeof(double) * g.extents[2], g.extents[1], p1 - p0);
+  if (upload) {
+    p.srcPtr = hptr; p.srcPos = hpos; p.dstPtr = dptr; p.dstPos = dpos; p.kind = cudaMemcpyHostToDevice;
+  } else {
+    p.srcPtr = dptr; p.srcPos = dpos; p.dstPtr = hptr; p.dstPos = hpos; p.kind = cudaMemcpyDeviceToHost;
+  }
+  TVS_CUDA(cudaMemcpy3DAsync(&p, s));
+  return TVS_OK;
+}
+
+static int slab_planes_default() {
+  static const int v = [] {
+    const char* e = getenv("TVS_E2E_SLAB");  // 0 disables the pipelined 3D path
+    return e ? atoi(e) : 32;
+  }();
+  return v;
+}
+
+static int jacobi3d_pipelined(const tvs_stencil& st, const tvs_layout& lay, const double* in, double* out,
+                              int64_t steps, const tvs_exec& ex, RunCtx& c, int64_t slab) {
+  const tvs_geometry& g = c.geo;
+  const int64_t planes = g.extents[0];
+  int depth = ex.temporal_depth > 0 ? ex.temporal_depth : jacobi3d_default_depth();
+  depth = std::max(1, std::min(depth, jacobi3d_max_depth()));
+  const int K = (int)((steps + depth - 1) / depth);
+  const bool fma = use_fma(st, ex);
+  std::vector<int> dk(K);
+  std::vector<int64_t> S(K + 1, 0);
+  {
+    int64_t left = steps;
+    for (int k = 0; k < K; ++k) {
+      dk[k] = (int)std::min<int64_t>(left, depth);
+      left -= dk[k];
+      S[k + 1] = S[k] + dk[k];
+    }
+  }
+  if (slab < 4 * depth) return fail(TVS_ERR_INVALID, "pipelined slab thinner than four temporal blocks");
+  const int nb = (int)((planes + S[K] + slab - 1) / slab);
+  while ((int)c.bands.size() < nb) {
+    cudaStream_t t;
+    TVS_CUDA(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+    c.bands.push_back(t);
+  }
+  const size_t nev = (size_t)nb * (K + 1);
+  while (c.events.size() < nev) {
+    cudaEvent_t e;
+    TVS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.events.push_back(e);
+  }
+  auto up = [&](int b) { return c.events[b]; };
+  auto done = [&](int b, int k) { return c.events[(size_t)nb * (k + 1) + b]; };
+  auto lo_of = [&](int b, int k) { return std::max<int64_t>(0, (int64_t)b * slab - S[k]); };
+  auto hi_of = [&](int b, int k) { return std::min<int64_t>(planes, (int64_t)(b + 1) * slab - S[k]); };
+  cudaStream_t cs = c.stream;
+  int rc;
+  if ((rc = fill_halo(g, c.buf[0], st.boundary, cs))) return rc;
+  if ((rc = fill_halo(g, c.buf[1], st.boundary, cs))) return rc;
+  const int nup = (int)((planes + slab - 1) / slab);
+  double* result = c.buf[K & 1];
+  int uploaded = 0;
+  for (int b = 0; b < nb; ++b) {
+    for (; uploaded < nup && uploaded <= b + 1; ++uploaded) {
+      if ((rc = copy_planes(g, c.buf[0], lay, const_cast<double*>(in), true, (int64_t)uploaded * slab,
+                            std::min(planes, (int64_t)(uploaded + 1) * slab), cs)))
+        return rc;
+      TVS_CUDA(cudaEventRecord(up(uploaded), cs));
+    }
+    cudaStream_t sb = c.bands[b];
+    for (int u = b - 1; u <= b + 1; ++u)
+      if (u >= 0 && u < nup) TVS_CUDA(cudaStreamWaitEvent(sb, up(u), 0));
+    for (int k = 0; k < K; ++k) {
+      if (k > 0 && b > 0) TVS_CUDA(cudaStreamWaitEvent(sb, done(b - 1, k - 1), 0));
+      const int64_t lo = lo_of(b, k), hi = hi_of(b, k);
+      if (hi > lo) {
+        rc = dk[k] == 2 ? jacobi3d_blocked2(st, g, c.buf[k & 1], c.buf[(k + 1) & 1], fma, sb, lo, hi, (int)slab)
+                        : jacobi3d_streaming(st, g, c.buf[k & 1], c.buf[(k + 1) & 1], fma, sb, lo, hi, (int)slab);
+        if (rc) return rc;
+      }
+      TVS_CUDA(cudaEventRecord(done(b, k), sb));
+    }
+    const int64_t lo = lo_of(b, K), hi = hi_of(b, K);
+    if (hi > lo && (rc = copy_planes(g, result, lay, out, false, lo, hi, sb))) return rc;
+  }
+  for (int b = 0; b < nb; ++b) TVS_CUDA(cudaStreamSynchronize(c.bands[b]));
+  return TVS_OK;
+}
+
 }  // namespace tvs
 
 using namespace tvs;
@@ -588,6 +688,10 @@ int tvs_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, doub
     if (band > 0 && st->dim == 2 && steps > 0 && ex->algo != TVS_ALGO_NAIVE && jacobi2d_blocked_supported(*st) &&
         c.geo.extents[0] >= 4 * band)
       return jacobi2d_pipelined(*st, *lay, in, out, steps, *ex, c, band);
+    const int64_t slab = slab_planes_default();
+    if (slab > 0 && st->dim == 3 && steps > 0 && ex->algo != TVS_ALGO_NAIVE && jacobi3d_streaming_supported(*st) &&
+        c.geo.extents[0] >= 4 * slab)
+      return jacobi3d_pipelined(*st, *lay, in, out, steps, *ex, c, slab);
   }
   if ((rc = fill_halo(c.geo, c.buf[0], st->boundary, s))) return rc;
   if ((rc = copy_interior(c.geo, c.buf[0], *lay, const_cast<double*>(in), true, s))) return rc;

@@ -214,10 +214,11 @@ int jacobi2d_default_depth();
 bool jacobi3d_streaming_supported(const tvs_stencil& st);
 int jacobi3d_max_depth();
 int jacobi3d_default_depth();
+// axis-0 planes [plo, phi) only when given, `seg` output planes per block
 int jacobi3d_blocked2(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, bool fma,
-                      cudaStream_t s);
-int jacobi3d_streaming(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
-                       bool fma, cudaStream_t s);
+                      cudaStream_t s, int64_t plo = 0, int64_t phi = -1, int seg = 0);
+int jacobi3d_streaming(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, bool fma,
+                       cudaStream_t s, int64_t plo = 0, int64_t phi = -1, int seg = 0);
 int gs1d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s);
 bool gs2d_pipe_supported(const tvs_stencil& st);
 int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s);

@@ -76,14 +76,15 @@ __device__ __forceinline__ constexpr bool has_plane(int G) {
 template <unsigned MASK, bool FMA>
 __global__ void __launch_bounds__(kThreads3) jacobi3d_kernel(const double* __restrict__ src,
                                                             double* __restrict__ dst, Geo g, int64_t origin,
-                                                            Coeff27 cf, double bnd) {
+                                                            Coeff27 cf, double bnd, int64_t plo, int64_t phi,
+                                                            int seg) {
   constexpr bool G0 = has_plane<MASK>(0), G1 = has_plane<MASK>(1), G2 = has_plane<MASK>(2);
   __shared__ __align__(16) double tile[kBufs3][kSH][kSW];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * kTX3 + tx;
   const int64_t x0 = (int64_t)blockIdx.x * kTX3, y0 = (int64_t)blockIdx.y * kTY3;
-  const int64_t p0 = (int64_t)blockIdx.z * kPlanesSeg;
-  const int64_t p1 = min(p0 + kPlanesSeg, g.e0);  // outputs [p0, p1)
+  const int64_t p0 = plo + (int64_t)blockIdx.z * seg;
+  const int64_t p1 = min(p0 + seg, phi);  // outputs [p0, p1)
 
   // per-thread staging slots, fixed for every plane: smem offset + global
   // offset relative to the plane base; rows beyond the halo are not read
@@ -209,15 +210,16 @@ __device__ __forceinline__ void tb_level(const double* __restrict__ plane, int w
 template <unsigned MASK, bool FMA>
 __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double* __restrict__ src,
                                                                    double* __restrict__ dst, Geo g, int64_t origin,
-                                                                   Coeff27 cf, double bnd) {
+                                                                   Coeff27 cf, double bnd, int64_t plo,
+                                                                   int64_t phi, int seg) {
   extern __shared__ __align__(16) double tb_smem[];
   double* l0 = tb_smem;                       // 3 staged input planes
   double* l1 = tb_smem + 3 * kTBR * kTBP;     // 2 level-1 planes (frame at +1,+1)
   const int lane = threadIdx.x, w = threadIdx.y;
   const int tid = w * 32 + lane;
   const int64_t x0 = (int64_t)blockIdx.x * kTBOX, y0 = (int64_t)blockIdx.y * kTBOY;
-  const int64_t p0 = (int64_t)blockIdx.z * kTBPlanesSeg;
-  const int64_t p1 = min(p0 + kTBPlanesSeg, g.e0);  // level-2 outputs [p0, p1)
+  const int64_t p0 = plo + (int64_t)blockIdx.z * seg;
+  const int64_t p1 = min(p0 + seg, phi);  // level-2 outputs [p0, p1)
 
   // staging slots: smem cell (row i, col 2c) <- global (y0-2+i, x0-2+2c);
   // rows/columns beyond the memory halo are never needed (their level-1
@@ -328,52 +330,58 @@ int jacobi3d_default_depth() { return 2; }
 
 template <unsigned MASK, bool FMA>
 static int launch_tb(const Geo& geo, const tvs_geometry& g, const double* src, double* dst, const Coeff27& cf,
-                     double bnd, cudaStream_t s) {
+                     double bnd, cudaStream_t s, int64_t plo, int64_t phi, int seg) {
   // per device context; a host-side attribute write, no synchronisation
   TVS_CUDA(cudaFuncSetAttribute(jacobi3d_tb_kernel<MASK, FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kTBSmem));
   const dim3 block(kTX3, kTYT);
   const dim3 grid((unsigned)((geo.e2 + kTBOX - 1) / kTBOX), (unsigned)((geo.e1 + kTBOY - 1) / kTBOY),
-                  (unsigned)((geo.e0 + kTBPlanesSeg - 1) / kTBPlanesSeg));
-  jacobi3d_tb_kernel<MASK, FMA><<<grid, block, kTBSmem, s>>>(src, dst, geo, g.origin, cf, bnd);
+                  (unsigned)((phi - plo + seg - 1) / seg));
+  jacobi3d_tb_kernel<MASK, FMA><<<grid, block, kTBSmem, s>>>(src, dst, geo, g.origin, cf, bnd, plo, phi, seg);
   TVS_LAUNCHED("jacobi3d_tb_kernel");
   return TVS_OK;
 }
 
 // Two time levels in one pass (K4b): src -> dst after 2 steps.
 int jacobi3d_blocked2(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, bool fma,
-                      cudaStream_t s) {
+                      cudaStream_t s, int64_t plo, int64_t phi, int seg) {
   Coeff27 cf;
   const unsigned mask = slots3d(st, cf);
   const Geo geo = make_geo(g);
+  if (phi < 0) phi = geo.e0;
+  if (seg <= 0) seg = kTBPlanesSeg;
+  if (plo < 0 || phi > geo.e0 || plo >= phi) return fail(TVS_ERR_INVALID, "jacobi3d_blocked2: plane range");
   if (mask == kBox27)
-    return fma ? launch_tb<kBox27, true>(geo, g, src, dst, cf, st.boundary, s)
-               : launch_tb<kBox27, false>(geo, g, src, dst, cf, st.boundary, s);
+    return fma ? launch_tb<kBox27, true>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg)
+               : launch_tb<kBox27, false>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg);
   if (mask == kStar7)
-    return fma ? launch_tb<kStar7, true>(geo, g, src, dst, cf, st.boundary, s)
-               : launch_tb<kStar7, false>(geo, g, src, dst, cf, st.boundary, s);
+    return fma ? launch_tb<kStar7, true>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg)
+               : launch_tb<kStar7, false>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg);
   return fail(TVS_ERR_UNSUPPORTED, "jacobi3d_blocked2: tap set");
 }
 
 int jacobi3d_streaming(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, bool fma,
-                       cudaStream_t s) {
+                       cudaStream_t s, int64_t plo, int64_t phi, int seg) {
   Coeff27 cf;
   const unsigned mask = slots3d(st, cf);
   if (mask != kBox27 && mask != kStar7) return fail(TVS_ERR_UNSUPPORTED, "jacobi3d_streaming: tap set");
   const Geo geo = make_geo(g);
+  if (phi < 0) phi = geo.e0;
+  if (seg <= 0) seg = kPlanesSeg;
+  if (plo < 0 || phi > geo.e0 || plo >= phi) return fail(TVS_ERR_INVALID, "jacobi3d_streaming: plane range");
   const dim3 block(kTX3, kTYT);
   const dim3 grid((unsigned)((geo.e2 + kTX3 - 1) / kTX3), (unsigned)((geo.e1 + kTY3 - 1) / kTY3),
-                  (unsigned)((geo.e0 + kPlanesSeg - 1) / kPlanesSeg));
+                  (unsigned)((phi - plo + seg - 1) / seg));
   if (mask == kBox27) {
     if (fma)
-      jacobi3d_kernel<kBox27, true><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary);
+      jacobi3d_kernel<kBox27, true><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary, plo, phi, seg);
     else
-      jacobi3d_kernel<kBox27, false><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary);
+      jacobi3d_kernel<kBox27, false><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary, plo, phi, seg);
   } else {
     if (fma)
-      jacobi3d_kernel<kStar7, true><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary);
+      jacobi3d_kernel<kStar7, true><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary, plo, phi, seg);
     else
-      jacobi3d_kernel<kStar7, false><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary);
+      jacobi3d_kernel<kStar7, false><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary, plo, phi, seg);
   }
   TVS_LAUNCHED("jacobi3d_kernel");
   return TVS_OK;

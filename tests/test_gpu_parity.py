@@ -377,6 +377,20 @@ def test_gs2d_pipeline_cluster_sizes(cuda_ready, cluster):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+@pytest.mark.parametrize("slab", [0, 8, 12, 32])
+def test_jacobi3d_pipelined_e2e_slabs(cuda_ready, slab):
+    """tvs_run's pipelined 3D Jacobi path (skewed axis-0 slabs on their own
+    streams, two levels per pass) is bit-identical to the oracle; slab 0 =
+    the single-stream path."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, TVS_E2E_SLAB=str(slab))
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "e2e_slab_check.py")],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 @pytest.mark.parametrize("band", [0, 300, 512, 777, 1024])
 def test_jacobi2d_pipelined_e2e_bands(cuda_ready, band):
     """tvs_run's pipelined 2D Jacobi path (row bands on their own streams,

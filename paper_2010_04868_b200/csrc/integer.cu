@@ -14,14 +14,16 @@
 //
 // K8 lcs_kernel — replaces lcs_temporal (reference kernels/lcs.py:32-108)
 // and its oracle lcs_reference (baselines.py:128-150).  The paper's
-// time lanes on a GPU: the A index is time, lane k of warp w owns DP row
-// x = x0 + 32w + k + 1 and at step s updates column y = s + 1 - k, so
-//   up   = lcs[x-1][y]   = lane k-1's output one step earlier (__shfl_up),
-//   diag = lcs[x-1][y-1] = the `up` this lane received one step earlier,
-//   left = lcs[x][y-1]   = its own previous output,
-//   b[y-1] slides through the lanes one position per step (__shfl_up),
-// out = a[x-1] == b[y-1] ? diag + 1 : max(up, left).  Lane 0 reads row
-// x0 + 32w from a boundary row written by warp w-1's lane 31 (progress
+// time lanes on a GPU: the A index is time; each lane owns 4 consecutive DP
+// rows skewed by one column each (a 4-row time-lane vector in registers) and
+// the 32 lanes of a warp continue the skew, so at every step
+//   up   = lcs[x-1][y]   = the row above's output one step earlier,
+//   diag = lcs[x-1][y-1] = its output two steps earlier,
+//   left = lcs[x][y-1]   = the row's own previous output,
+//   b[y-1] slides through the rows and lanes one position per step,
+// out = a[x-1] == b[y-1] ? diag + 1 : max(up, left); only the lane's first
+// row takes a shuffle (from lane k-1's last row).  Lane 0 reads row
+// x0 + 128w from a boundary row written by warp w-1's lane 31 (progress
 // published every 32 columns with a GPU-scope release); warps take tickets
 // in start order and only wait on lower tickets (deadlock-free).  Passes of
 // at most kLcsMaxWarps warps bound the boundary-row workspace.
@@ -314,7 +316,7 @@ static int copy_interior_i32(const tvs_geometry& g, int* dev, const tvs_layout& 
 }
 
 // ----------------------------------------------------------------- LCS ----
-constexpr int kLcsMaxWarps = 4096;  // warps (32 DP rows each) per pass
+constexpr int kLcsMaxWarps = 4096;  // warps (128 DP rows each) per pass
 
 struct LcsArgs {
   const int* a;   // device, na
@@ -322,8 +324,7 @@ struct LcsArgs {
   int na, nb;
   int x0;         // DP rows x0+1 .. handled by this pass
   int nwarps;
-  int* rows;      // (nwarps + 1) x (nb + 1): row w = lcs[x0 + 32w][*]
-  int* prog;      // nwarps + 1 progress counters (columns of row w published)
+  unsigned long long* rows;  // (nwarps + 1) x (nb + 1): row w = lcs[x0 + 128w][*], (y + 1) << 32 | value
   int* ticket;
   int* result;    // lcs[na][nb]
 };
@@ -337,6 +338,37 @@ __device__ __forceinline__ void st_release_i32(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Lane k owns kLcsRPL consecutive DP rows x_j = x0 + 32*kLcsRPL*w +
+// kLcsRPL*k + j + 1; at step s its row j updates column c - j with
+// c = s + 1 - kLcsRPL*k.  Every input of a step was produced in an earlier
+// step: up_j / diag_j of row j > 0 are row j-1's outputs one / two steps
+// back (registers), row 0's come from lane k-1's last row (one shuffle);
+// the B window shifts through the rows and lanes the same way.  So the
+// kLcsRPL updates of a step are independent and the loop-carried path is one
+// shuffle plus one select per step.
+constexpr int kLcsRPL = 4;
+constexpr int kLcsWarpRows = 32 * kLcsRPL;
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* q) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(q) : "memory");
+  return v;
+}
+// predicated inside the asm: no branch, so the warp never diverges around the
+// shuffles (a divergent region compiles them to the slow collective form)
+__device__ __forceinline__ void st_relaxed_u64_if(bool pred, unsigned long long* q, unsigned long long v) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.relaxed.gpu.global.b64 [%0], %1; }"
+               ::"l"(q), "l"(v), "r"((unsigned)pred) : "memory");
+}
+__device__ __forceinline__ void st_i32_if(bool pred, int* q, int v) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.global.b32 [%0], %1; }"
+               ::"l"(q), "r"(v), "r"((unsigned)pred) : "memory");
+}
+
+// Boundary rows carry (column + 1) in the high word of every 64-bit entry:
+// one single-copy-atomic store publishes a value together with its own
+// validity tag, so the hand-off needs no fence and no progress counter; the
+// consumer re-reads an entry until its tag matches.
 __global__ void __launch_bounds__(32) lcs_kernel(LcsArgs p) {
   __shared__ int s_w;
   const int lane = threadIdx.x;
@@ -345,41 +377,78 @@ __global__ void __launch_bounds__(32) lcs_kernel(LcsArgs p) {
   const int w = s_w;
   if (w >= p.nwarps) return;
   const int nb = p.nb;
-  const int x = p.x0 + 32 * w + lane + 1;  // DP row of this lane
-  const int av = x <= p.na ? p.a[x - 1] : 0;
-  const int* rin = p.rows + (size_t)w * (nb + 1);
-  int* rout = p.rows + (size_t)(w + 1) * (nb + 1);
-  const bool last_lane_real = p.x0 + 32 * w + 32 <= p.na;
-  int out = 0, prev_up = 0, bwin = 0;
-  int c_up = 0, c_b = 0;
+  const int xb = p.x0 + kLcsWarpRows * w + kLcsRPL * lane;  // row j of this lane is xb + j + 1
+  int av[kLcsRPL];
+#pragma unroll
+  for (int j = 0; j < kLcsRPL; ++j) av[j] = xb + j + 1 <= p.na ? p.a[xb + j] : 0;
+  const unsigned long long* rin = p.rows + (size_t)w * (nb + 1);
+  unsigned long long* rout = p.rows + (size_t)(w + 1) * (nb + 1);
+  int out[kLcsRPL], prev[kLcsRPL], bw[kLcsRPL];  // prev: outputs one step older than out
+#pragma unroll
+  for (int j = 0; j < kLcsRPL; ++j) out[j] = prev[j] = bw[j] = 0;
+  int up0_prev = 0;  // row-0 `up` of the previous step = row-0 diag now
+  // lane 0's inputs come in chunks of 32 columns, read half a chunk ahead and
+  // validated (re-read until the tag matches) when the chunk starts
+  int c_up = 0, c_b = 0, n_b = 0;
+  unsigned long long n_raw = 0;
   SpinGuard guard;
-  for (int s = 0; s < nb + 31; ++s) {
+  const int nsteps = nb + kLcsWarpRows - 1;
+  for (int s = 0; s < nsteps; ++s) {
     const int ph = s & 31;
     if (ph == 0) {
-      // columns s+1 .. s+32 of the row above this warp, and b[s .. s+31]
-      const int need = min(s + 32, nb);
-      while (ld_acquire_i32(p.prog + w) < need) guard.tick();
       const int y = s + 1 + lane;
-      c_up = y <= nb ? rin[y] : 0;
-      c_b = s + lane < nb ? p.b[s + lane] : 0;
+      unsigned long long raw = s == 0 && y <= nb ? ld_relaxed_u64(rin + y) : n_raw;
+      if (s == 0) n_b = lane < nb ? p.b[lane] : 0;
+      // warp-uniform retry loop (lanes whose entry is not tagged yet re-read)
+      bool bad = y <= nb && (int)(raw >> 32) != y + 1;
+      while (__any_sync(0xffffffffu, bad)) {
+        if (bad) raw = ld_relaxed_u64(rin + y);
+        bad = y <= nb && (int)(raw >> 32) != y + 1;
+        guard.tick();
+      }
+      c_up = y <= nb ? (int)(unsigned)raw : 0;
+      c_b = n_b;
+    } else if (ph == 16 && s + 16 < nsteps) {
+      const int y = s + 17 + lane;  // next chunk
+      n_raw = y <= nb ? ld_relaxed_u64(rin + y) : 0ull;
+      n_b = s + 16 + lane < nb ? p.b[s + 16 + lane] : 0;
     }
-    const int up_sh = __shfl_up_sync(0xffffffffu, out, 1);
-    const int b_sh = __shfl_up_sync(0xffffffffu, bwin, 1);
-    const int up0 = __shfl_sync(0xffffffffu, c_up, ph);
-    const int b0 = __shfl_sync(0xffffffffu, c_b, ph);
-    const int up = lane == 0 ? up0 : up_sh;
-    bwin = lane == 0 ? b0 : b_sh;
-    const int y = s + 1 - lane;
-    int v = av == bwin ? prev_up + 1 : max(up, out);
-    if (y < 1) v = 0;  // lcs[x][0] = 0 before the lane's first column
-    prev_up = up;
-    out = v;
-    if (y >= 1 && y <= nb) {
-      if (lane == 31) rout[y] = out;
-      if (x == p.na && y == nb) *p.result = out;
+    // from lane k-1: its last row's output and its oldest B value (previous step)
+    const int up_sh = __shfl_up_sync(0xffffffffu, out[kLcsRPL - 1], 1);
+    const int b_sh = __shfl_up_sync(0xffffffffu, bw[kLcsRPL - 1], 1);
+    const int up0_in = __shfl_sync(0xffffffffu, c_up, ph);
+    const int b0_in = __shfl_sync(0xffffffffu, c_b, ph);
+    const int up0 = lane == 0 ? up0_in : up_sh;
+    const int c = s + 1 - kLcsRPL * lane;
+    int nw[kLcsRPL];
+#pragma unroll
+    for (int j = kLcsRPL - 1; j >= 0; --j) {
+      const int bj = j == 0 ? (lane == 0 ? b0_in : b_sh) : bw[j - 1];
+      const int up = j == 0 ? up0 : out[j - 1];
+      const int dg = j == 0 ? up0_prev : prev[j - 1];
+      int v = av[j] == bj ? dg + 1 : max(up, out[j]);
+      if (c - j < 1) v = 0;  // lcs[x][0] = 0 before the row's first column
+      nw[j] = v;
+      bw[j] = bj;
     }
-    if (lane == 31 && last_lane_real && y >= 1 && ((y & 31) == 0 || y == nb)) st_release_i32(p.prog + w + 1, y);
+    up0_prev = up0;
+#pragma unroll
+    for (int j = 0; j < kLcsRPL; ++j) {
+      prev[j] = out[j];
+      out[j] = nw[j];
+    }
+    const int ylast = c - (kLcsRPL - 1);  // column of this lane's last row
+    st_relaxed_u64_if(lane == 31 && ylast >= 1 && ylast <= nb, rout + ylast,
+                      ((unsigned long long)(ylast + 1) << 32) | (unsigned)out[kLcsRPL - 1]);
+#pragma unroll
+    for (int j = 0; j < kLcsRPL; ++j) st_i32_if(xb + j + 1 == p.na && c - j == nb, p.result, out[j]);
   }
+}
+
+// row 0 of the first pass: lcs[0][y] = 0 for every column, tagged
+__global__ void lcs_row0_kernel(unsigned long long* row, int nb) {
+  for (int y = blockIdx.x * blockDim.x + threadIdx.x; y <= nb; y += gridDim.x * blockDim.x)
+    row[y] = (unsigned long long)(y + 1) << 32;
 }
 
 struct LcsWork {
@@ -397,12 +466,12 @@ static int lcs_device(const int* a, int na, const int* b, int nb, int* result_de
     TVS_CUDA(cudaMemsetAsync(result_dev, 0, sizeof(int), s));
     return TVS_OK;
   }
-  const int total_warps = (na + 31) / 32;
-  // workspace budget ~256 MB of boundary rows
-  const int64_t row_bytes = (int64_t)(nb + 1) * sizeof(int);
-  const int cap = (int)std::max<int64_t>(1, std::min<int64_t>(kLcsMaxWarps, (256ll << 20) / row_bytes - 1));
+  const int total_warps = (na + kLcsWarpRows - 1) / kLcsWarpRows;
+  // workspace budget ~512 MB of tagged boundary rows
+  const int64_t row_bytes = (int64_t)(nb + 1) * sizeof(unsigned long long);
+  const int cap = (int)std::max<int64_t>(1, std::min<int64_t>(kLcsMaxWarps, (512ll << 20) / row_bytes - 1));
   const int per = std::min(total_warps, cap);
-  const size_t need = (size_t)(per + 1) * row_bytes + (size_t)(per + 2) * sizeof(int) + 256;
+  const size_t need = (size_t)(per + 1) * row_bytes + 256;
   int dev;
   TVS_CUDA(cudaGetDevice(&dev));
   if (g_lcs.bytes < need || g_lcs.device != dev) {
@@ -413,19 +482,20 @@ static int lcs_device(const int* a, int na, const int* b, int nb, int* result_de
     g_lcs.bytes = need;
     g_lcs.device = dev;
   }
-  int* rows = g_lcs.buf;
-  int* prog = rows + (size_t)(per + 1) * (nb + 1);
-  int* ticket = prog + per + 1;
-  TVS_CUDA(cudaMemsetAsync(rows, 0, row_bytes, s));  // lcs[0][*] = 0
-  for (int x0 = 0, first = 1; x0 < na; x0 += 32 * per, first = 0) {
-    const int nw = std::min(per, (na - x0 + 31) / 32);
-    if (!first) TVS_CUDA(cudaMemcpyAsync(rows, rows + (size_t)per * (nb + 1), row_bytes, cudaMemcpyDeviceToDevice, s));
-    TVS_CUDA(cudaMemsetAsync(prog, 0, (size_t)(per + 2) * sizeof(int), s));
-    TVS_CUDA(cudaMemcpyAsync(prog, &nb, sizeof(int), cudaMemcpyHostToDevice, s));  // row 0 complete
-    LcsArgs p{a, b, na, nb, x0, nw, rows, prog, ticket, result_dev};
+  unsigned long long* rows = reinterpret_cast<unsigned long long*>(g_lcs.buf);
+  int* ticket = reinterpret_cast<int*>(rows + (size_t)(per + 1) * (nb + 1));
+  lcs_row0_kernel<<<64, 256, 0, s>>>(rows, nb);
+  TVS_LAUNCHED("lcs_row0_kernel");
+  for (int x0 = 0, first = 1; x0 < na; x0 += kLcsWarpRows * per, first = 0) {
+    const int nw = std::min(per, (na - x0 + kLcsWarpRows - 1) / kLcsWarpRows);
+    if (!first)  // the previous pass's last row (tags intact) becomes row 0
+      TVS_CUDA(cudaMemcpyAsync(rows, rows + (size_t)per * (nb + 1), row_bytes, cudaMemcpyDeviceToDevice, s));
+    // stale tags of the previous pass must not validate: clear rows 1..nw
+    TVS_CUDA(cudaMemsetAsync(rows + (nb + 1), 0, (size_t)nw * row_bytes, s));
+    TVS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), s));
+    LcsArgs p{a, b, na, nb, x0, nw, rows, ticket, result_dev};
     lcs_kernel<<<nw, 32, 0, s>>>(p);
     TVS_LAUNCHED("lcs_kernel");
-    // next pass reads row `per` (the last warp of a full pass has 32 real rows)
     if (nw < per) break;
   }
   return TVS_OK;

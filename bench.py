@@ -481,24 +481,56 @@ def run_sharded(args):
         cfg = CONFIGS[HEADLINE]
     spec = get(cfg["kernel"]).spec
     full = make_grid(cfg).interior
-    sj = ShardedJacobi(spec, cfg["extents"], dist, depth=8, device=torch.device("cuda", local))
-    times = []
-    for i in range(args.warmup + args.steps):
-        sj.cur = 0
-        sj.load_global(full)
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        sj.run(cfg["T"])
-        e1.record()
-        torch.cuda.synchronize()
-        dist.barrier()
-        if i >= args.warmup:
-            t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            times.append(float(t.item()))
-    ms = statistics.mean(times)
+    from paper_2010_04868_b200 import _native
+
+    depth = 8 if len(cfg["extents"]) == 2 else 2
+    sj = ShardedJacobi(spec, cfg["extents"], dist, depth=depth, device=torch.device("cuda", local))
+    lay = sj.layout
+    # e2e: this rank's rows (+ ghosts) from pinned host memory in, owned rows out
+    lo, hi = max(lay.r0 - lay.ghost, 0), min(lay.r1 + lay.ghost, int(lay.geometry.axis0_global))
+    h_in = torch.from_numpy(np.ascontiguousarray(full[lo:hi])).pin_memory()
+    h_out = torch.empty(tuple(sj.owned().shape), dtype=torch.float64).pin_memory()
+    in_view = sj.interior_view
+    clk = ClockSampler(local) if rank == 0 else None
+
+    def timed(e2e):
+        times, launches = [], 0
+        for i in range(args.warmup + args.steps):
+            sj.cur = 0
+            if not e2e:
+                sj.load_global(full)
+            dist.barrier()
+            torch.cuda.synchronize()
+            if i == args.warmup and clk is not None and not e2e:
+                clk.start()
+                clk.mark(True)
+            _native.launch_counter()  # reset
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            if e2e:
+                v = in_view(0)
+                v[lo - (lay.r0 - lay.ghost): hi - (lay.r0 - lay.ghost)].copy_(h_in, non_blocking=True)
+            sj.run(cfg["T"])
+            if e2e:
+                h_out.copy_(sj.owned(), non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            n = _native.launch_counter()
+            dist.barrier()
+            if i >= args.warmup:
+                t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                c = torch.tensor([n], device="cuda", dtype=torch.int64)
+                dist.all_reduce(c, op=dist.ReduceOp.SUM)
+                times.append(float(t.item()))
+                launches += int(c.item())
+        if clk is not None and not e2e:
+            clk.mark(False)
+            clk.stop()
+        return statistics.mean(times), launches
+
+    ms, launches = timed(False)
+    ems, _ = timed(True)
     updates = int(np.prod(cfg["extents"])) * cfg["T"]
     if rank == 0:
         hbm_peak, peak_src = peaks()
@@ -508,9 +540,13 @@ def run_sharded(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE seeds)",
             "config": {"workload": f"{cfg['name']} {'x'.join(map(str, cfg['extents']))} T={cfg['T']}",
-                       "parallelism": f"slab{world} (axis-0 rows, NCCL halo depth 8)"},
+                       "parallelism": f"slab{world} (axis-0 slabs, NCCL halo depth {depth})",
+                       "l2": "inputs larger than L2"},
+            "gpu_launches": launches, "clocks": clk.summary() if clk else None,
+            "e2e": {"value": updates / (ems * 1e-3) / 1e9, "unit": "GStencil/s", "ms_per_step": ems,
+                    "h2d_bytes_per_step": int(h_in.numel() * 8 * world), "d2h_bytes_per_step": int(updates / cfg["T"] * 8)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": None, "per": "GPU"},
+                         "frac": achieved / hbm_peak, "traffic": None, "per": "GPU", "peak_source": peak_src},
         }))
     dist.destroy_process_group()
     return 0
@@ -530,7 +566,9 @@ def main():
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":
         return run_reference(args)
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or os.environ.get("TVS_FORCE_SHARDED"):
+        # TVS_FORCE_SHARDED=1 under torchrun --nproc-per-node 1: the sharded
+        # path with one rank (exercises the halo-exchange plumbing on one GPU)
         return run_sharded(args)
     cfg = CONFIGS[args.config]
     head = measure_config(cfg, args.steps, args.warmup, with_e2e=True, with_cpu=not args.no_cpu)

@@ -182,7 +182,10 @@ constexpr int kTBP = 68;               // smem pitch (frame + ring, 16-byte rows
 constexpr int kTBR = kTBH + 2;         // smem rows
 constexpr int kTBChunks = kTBR * (kTBP / 2);
 constexpr int kTBSlots = (kTBChunks + kThreads3 - 1) / kThreads3;
-constexpr int kTBPlanesSeg = 64;       // output planes per block
+#ifndef J3D_TBSEG
+#define J3D_TBSEG 128  // measured (1024^3, T=20): 32 225 / 318, 64 235 / 332, 128 237 / 342, 256 232 / 339 GSt/s (exact / fma)
+#endif
+constexpr int kTBPlanesSeg = J3D_TBSEG;  // output planes per block
 constexpr size_t kTBSmem = (size_t)(3 + 2) * kTBR * kTBP * sizeof(double);
 
 template <unsigned MASK, bool FMA>

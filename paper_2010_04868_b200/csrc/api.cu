@@ -573,6 +573,88 @@ static int jacobi3d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
   return TVS_OK;
 }
 
+// 2D Gauss-Seidel drop-in path (lexicographic pipeline, one pass of <= 128
+// sweeps): row bands are uploaded while the kernel runs — its loader warps
+// wait on a rows-uploaded counter the copy stream advances with
+// cuStreamWriteValue32 — and downloaded while it runs: the kernel publishes
+// finished blocks in ticket order, and the download stream waits with
+// cuStreamWaitValue32 for the block that writes a band's last final row.
+// Every upload is enqueued before the kernel, so the kernel can never wait on
+// a copy queued behind it.
+typedef int (*StreamValueFn)(cudaStream_t, unsigned long long, unsigned, unsigned);
+static bool stream_value_fns(StreamValueFn* wait, StreamValueFn* write) {
+  static StreamValueFn w = nullptr, r = nullptr;
+  static const bool ok = [] {
+    void* f1 = nullptr;
+    void* f2 = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    // the v2 entry points (CUDA >= 12: stream memory operations need no opt-in)
+    if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &f1, 12000, cudaEnableDefault, &q1) != cudaSuccess ||
+        cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &f2, 12000, cudaEnableDefault, &q2) != cudaSuccess ||
+        q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !f1 || !f2) {
+      cudaGetLastError();
+      return false;
+    }
+    w = reinterpret_cast<StreamValueFn>(f1);
+    r = reinterpret_cast<StreamValueFn>(f2);
+    return true;
+  }();
+  *wait = w;
+  *write = r;
+  return ok;
+}
+
+static int gs2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, const double* in, double* out,
+                          int64_t steps, RunCtx& c, int64_t band) {
+  StreamValueFn wait_value, write_value;
+  if (!stream_value_fns(&wait_value, &write_value)) return TVS_ERR_UNSUPPORTED;
+  const tvs_geometry& g = c.geo;
+  const int64_t rows = g.extents[0];
+  const int nbands = (int)((rows + band - 1) / band);
+  unsigned* ctr = static_cast<unsigned*>(scratch(128, 3));  // [0] rows uploaded, [16] blocks done (64 B apart)
+  if (!ctr) return fail(TVS_ERR_CUDA, "gs2d_pipelined: scratch");
+  while ((int)c.bands.size() < 2) {
+    cudaStream_t t;
+    TVS_CUDA(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+    c.bands.push_back(t);
+  }
+  if (c.events.empty()) {
+    cudaEvent_t e;
+    TVS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.events.push_back(e);
+  }
+  cudaStream_t cs = c.stream, ks = c.bands[0], ds = c.bands[1];
+  int rc;
+  TVS_CUDA(cudaMemsetAsync(ctr, 0, 128, cs));
+  if ((rc = fill_halo(g, c.buf[0], st.boundary, cs))) return rc;
+  TVS_CUDA(cudaEventRecord(c.events[0], cs));
+  const unsigned long long rows_ready = reinterpret_cast<unsigned long long>(ctr);
+  const unsigned long long blocks_done = reinterpret_cast<unsigned long long>(ctr + 16);
+  for (int u = 0; u < nbands; ++u) {
+    const int64_t r1 = std::min(rows, (int64_t)(u + 1) * band);
+    if ((rc = copy_rows(g, c.buf[0], lay, const_cast<double*>(in), true, (int64_t)u * band, r1, cs))) return rc;
+    const int wrc = write_value(cs, rows_ready, (unsigned)r1, 0);
+    if (wrc != 0) return fail(TVS_ERR_CUDA, "cuStreamWriteValue32 failed (CUresult " + std::to_string(wrc) + ")");
+  }
+  TVS_CUDA(cudaStreamWaitEvent(ks, c.events[0], 0));
+  TVS_CUDA(cudaStreamWaitEvent(ds, c.events[0], 0));  // counters reset before any wait reads them
+  if ((rc = gs2d_pipeline(st, g, c.buf[0], steps, ks, ctr, ctr + 16))) return rc;
+  // row r's final value is written by the block holding group r + steps - 1
+  constexpr int kGroupsPerBlock = 4;  // gs2p::kG
+  const int64_t nblocks = (rows + 128 - 1 + kGroupsPerBlock - 1) / kGroupsPerBlock;
+  for (int u = 0; u < nbands; ++u) {
+    const int64_t r0 = (int64_t)u * band, r1 = std::min(rows, r0 + band);
+    const int64_t need = std::min<int64_t>(nblocks, (r1 - 1 + steps - 1) / kGroupsPerBlock + 1);
+    const int wrc = wait_value(ds, blocks_done, (unsigned)need, 0 /* CU_STREAM_WAIT_VALUE_GEQ */);
+    if (wrc != 0) return fail(TVS_ERR_CUDA, "cuStreamWaitValue32 failed (CUresult " + std::to_string(wrc) + ")");
+    if ((rc = copy_rows(g, c.buf[0], lay, out, false, r0, r1, ds))) return rc;
+  }
+  TVS_CUDA(cudaStreamSynchronize(ds));
+  TVS_CUDA(cudaStreamSynchronize(ks));
+  TVS_CUDA(cudaStreamSynchronize(cs));
+  return TVS_OK;
+}
+
 }  // namespace tvs
 
 using namespace tvs;
@@ -692,6 +774,14 @@ int tvs_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, doub
     if (slab > 0 && st->dim == 3 && steps > 0 && ex->algo != TVS_ALGO_NAIVE && jacobi3d_streaming_supported(*st) &&
         c.geo.extents[0] >= 4 * slab)
       return jacobi3d_pipelined(*st, *lay, in, out, steps, *ex, c, slab);
+  }
+  if (gs) {
+    const int64_t band = band_rows_default();
+    if (band > 0 && st->dim == 2 && steps > 0 && steps <= 128 && ex->algo != TVS_ALGO_NAIVE &&
+        ex->gs_order == TVS_GS_LEXICOGRAPHIC && gs2d_pipe_supported(*st) && c.geo.extents[0] >= 4 * band) {
+      rc = gs2d_pipelined(*st, *lay, in, out, steps, c, band);
+      if (rc != TVS_ERR_UNSUPPORTED) return rc;  // no stream memory operations: plain path below
+    }
   }
   if ((rc = fill_halo(c.geo, c.buf[0], st->boundary, s))) return rc;
   if ((rc = copy_interior(c.geo, c.buf[0], *lay, const_cast<double*>(in), true, s))) return rc;

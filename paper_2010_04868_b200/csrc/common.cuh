@@ -221,7 +221,9 @@ int jacobi3d_streaming(const tvs_stencil& st, const tvs_geometry& g, const doubl
                        cudaStream_t s, int64_t plo = 0, int64_t phi = -1, int seg = 0);
 int gs1d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s);
 bool gs2d_pipe_supported(const tvs_stencil& st);
-int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s);
+// rows_ready / blocks_done: drop-in pipeline hooks (see api.cu), single pass only
+int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s,
+                  const unsigned* rows_ready = nullptr, unsigned* blocks_done = nullptr);
 int gs_wavefront(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, int order,
                  cudaStream_t s);
 

@@ -104,6 +104,8 @@ struct Gs2pArgs {
   unsigned long long* gcons; // kK tagged counters: (boundary+1) << 32 | iterations consumed
   int* ticket;
   const double* bndpad;       // 32 copies of the boundary value
+  const unsigned* rows_ready; // drop-in pipeline: grid rows uploaded so far (nullptr: all resident)
+  unsigned* blocks_done;      // drop-in pipeline: blocks finished, published in ticket order (or nullptr)
   double w[9];
   double bnd;
 };
@@ -294,6 +296,19 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
     long long lw = 0, lt0 = clock64();
 #endif
     const double* bndsrc = p.bndpad;  // 32 copies of the boundary value (cp.async source)
+    if (p.rows_ready) {
+      // the drop-in path uploads row bands while this kernel runs: the only
+      // grid rows a block reads are rows d0 .. d0 + kG (slot 0 of its rings)
+      const unsigned need = (unsigned)min(e0, d0 + kG + 1);
+      SpinGuard sg;
+      unsigned have;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(have) : "l"(p.rows_ready) : "memory");
+        if (have >= need) break;
+        __nanosleep(256);
+        sg.tick();
+      }
+    }
     for (int kl = 0; kl < nch; ++kl) {
 #ifdef GS2P_TRACE
       const long long lws = clock64();
@@ -628,6 +643,23 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
   }  // compute warps
   // no block of a cluster leaves while a peer may still push into / credit it
   if constexpr (CS > 1) cluster_sync_all();
+  if (p.blocks_done) {
+    // publish "blocks 0..n done" in ticket order (block n-1 is resident and
+    // never waits on n, so this cannot deadlock); the drop-in path's download
+    // stream waits on this count for the rows whose final values are written
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      SpinGuard sg;
+      unsigned seen;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.blocks_done) : "memory");
+        if (seen >= (unsigned)n) break;
+        sg.tick();
+      }
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.blocks_done), "r"((unsigned)n + 1u) : "memory");
+    }
+  }
 #ifdef GS2P_TRACE
   if (threadIdx.x == 0) {
     TRACE(n, 6);
@@ -659,7 +691,8 @@ bool gs2d_pipe_supported(const tvs_stencil& st) {
   return m == 0x1FFu || m == kStar;
 }
 
-int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s) {
+int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s,
+                  const unsigned* rows_ready, unsigned* blocks_done) {
   using namespace gs2p;
   double w[9];
   const unsigned mask = gs_mask2d(st, w);
@@ -685,6 +718,8 @@ int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, in
     TVS_CUDA(cudaMemcpyAsync(bndpad, h, sizeof(h), cudaMemcpyHostToDevice, s));
   }
   a.bndpad = bndpad;
+  a.rows_ready = rows_ready;
+  a.blocks_done = blocks_done;
   // Cluster size.  Consecutive blocks of a cluster hand off through
   // distributed shared memory, which shortens the block->block chain (the
   // bound for narrow grids: 8192x2048 T=100 29.3 ms at 1, 20.2 ms at 8) but

@@ -377,6 +377,20 @@ def test_gs2d_pipeline_cluster_sizes(cuda_ready, cluster):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+@pytest.mark.parametrize("band", [0, 256, 300])
+def test_gs2d_pipelined_e2e_bands(cuda_ready, band):
+    """tvs_run's overlapped 2D Gauss-Seidel path (uploads gated into the
+    running kernel, downloads gated on published blocks) is bit-identical to
+    the lexicographic oracle; band 0 = the plain path."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, TVS_E2E_BANDS=str(band))
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "e2e_gs2d_check.py")],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 @pytest.mark.parametrize("slab", [0, 8, 12, 32])
 def test_jacobi3d_pipelined_e2e_slabs(cuda_ready, slab):
     """tvs_run's pipelined 3D Jacobi path (skewed axis-0 slabs on their own

@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -393,26 +394,28 @@ __global__ void __launch_bounds__(32) lcs_kernel(LcsArgs p) {
   unsigned long long n_raw = 0;
   SpinGuard guard;
   const int nsteps = nb + kLcsWarpRows - 1;
-  for (int s = 0; s < nsteps; ++s) {
-    const int ph = s & 31;
-    if (ph == 0) {
-      const int y = s + 1 + lane;
-      unsigned long long raw = s == 0 && y <= nb ? ld_relaxed_u64(rin + y) : n_raw;
-      if (s == 0) n_b = lane < nb ? p.b[lane] : 0;
-      // warp-uniform retry loop (lanes whose entry is not tagged yet re-read)
-      bool bad = y <= nb && (int)(raw >> 32) != y + 1;
-      while (__any_sync(0xffffffffu, bad)) {
-        if (bad) raw = ld_relaxed_u64(rin + y);
-        bad = y <= nb && (int)(raw >> 32) != y + 1;
-        guard.tick();
-      }
-      c_up = y <= nb ? (int)(unsigned)raw : 0;
-      c_b = n_b;
-    } else if (ph == 16 && s + 16 < nsteps) {
-      const int y = s + 17 + lane;  // next chunk
-      n_raw = y <= nb ? ld_relaxed_u64(rin + y) : 0ull;
-      n_b = s + 16 + lane < nb ? p.b[s + 16 + lane] : 0;
+  // the lane/row holding DP row na (if any) meets column nb at step rstep
+  const int rj = p.na - 1 - xb;
+  const bool has_res = rj >= 0 && rj < kLcsRPL;
+  const int rstep = has_res ? nb - 1 + kLcsRPL * lane + rj : -1;
+  int res = 0;
+  auto chunk_start = [&](int s) {
+    const int y = s + 1 + lane;
+    unsigned long long raw = s == 0 && y <= nb ? ld_relaxed_u64(rin + y) : n_raw;
+    if (s == 0) n_b = lane < nb ? p.b[lane] : 0;
+    // warp-uniform retry loop (lanes whose entry is not tagged yet re-read)
+    bool bad = y <= nb && (int)(raw >> 32) != y + 1;
+    while (__any_sync(0xffffffffu, bad)) {
+      if (bad) raw = ld_relaxed_u64(rin + y);
+      bad = y <= nb && (int)(raw >> 32) != y + 1;
+      guard.tick();
     }
+    c_up = y <= nb ? (int)(unsigned)raw : 0;
+    c_b = n_b;
+  };
+  // one step; WARM: rows may still be left of column 1 (first 128 steps)
+  auto step = [&](int s, int ph, auto warm_tag) {
+    constexpr bool WARM = decltype(warm_tag)::value;
     // from lane k-1: its last row's output and its oldest B value (previous step)
     const int up_sh = __shfl_up_sync(0xffffffffu, out[kLcsRPL - 1], 1);
     const int b_sh = __shfl_up_sync(0xffffffffu, bw[kLcsRPL - 1], 1);
@@ -427,7 +430,7 @@ __global__ void __launch_bounds__(32) lcs_kernel(LcsArgs p) {
       const int up = j == 0 ? up0 : out[j - 1];
       const int dg = j == 0 ? up0_prev : prev[j - 1];
       int v = av[j] == bj ? dg + 1 : max(up, out[j]);
-      if (c - j < 1) v = 0;  // lcs[x][0] = 0 before the row's first column
+      if (WARM && c - j < 1) v = 0;  // lcs[x][0] = 0 before the row's first column
       nw[j] = v;
       bw[j] = bj;
     }
@@ -440,9 +443,43 @@ __global__ void __launch_bounds__(32) lcs_kernel(LcsArgs p) {
     const int ylast = c - (kLcsRPL - 1);  // column of this lane's last row
     st_relaxed_u64_if(lane == 31 && ylast >= 1 && ylast <= nb, rout + ylast,
                       ((unsigned long long)(ylast + 1) << 32) | (unsigned)out[kLcsRPL - 1]);
+    if (s == rstep) res = rj == 0 ? out[0] : rj == 1 ? out[1] : rj == 2 ? out[2] : out[kLcsRPL - 1];
+  };
+  // chunks of 32 steps, the body unrolled so the chunk bookkeeping (start,
+  // next-chunk prefetch at ph 16) costs no per-step branches
+  const int nfull = nsteps / 32;
+  for (int q = 0; q < nfull; ++q) {
+    const int s0 = q * 32;
+    chunk_start(s0);
+    const bool pre = s0 + 32 < nsteps;
+    if (s0 < kLcsWarpRows) {
 #pragma unroll
-    for (int j = 0; j < kLcsRPL; ++j) st_i32_if(xb + j + 1 == p.na && c - j == nb, p.result, out[j]);
+      for (int ph = 0; ph < 32; ++ph) {
+        if (ph == 16 && pre) {
+          const int y = s0 + 33 + lane;  // next chunk
+          n_raw = y <= nb ? ld_relaxed_u64(rin + y) : 0ull;
+          n_b = s0 + 32 + lane < nb ? p.b[s0 + 32 + lane] : 0;
+        }
+        step(s0 + ph, ph, std::true_type{});
+      }
+    } else {
+#pragma unroll
+      for (int ph = 0; ph < 32; ++ph) {
+        if (ph == 16 && pre) {
+          const int y = s0 + 33 + lane;
+          n_raw = y <= nb ? ld_relaxed_u64(rin + y) : 0ull;
+          n_b = s0 + 32 + lane < nb ? p.b[s0 + 32 + lane] : 0;
+        }
+        step(s0 + ph, ph, std::false_type{});
+      }
+    }
   }
+  if (nfull * 32 < nsteps) {  // ragged last chunk
+    const int s0 = nfull * 32;
+    chunk_start(s0);
+    for (int ph = 0; s0 + ph < nsteps; ++ph) step(s0 + ph, ph, std::true_type{});
+  }
+  st_i32_if(has_res, p.result, res);
 }
 
 // row 0 of the first pass: lcs[0][y] = 0 for every column, tagged

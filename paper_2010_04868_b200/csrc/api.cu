@@ -473,6 +473,79 @@ static int jacobi2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
   return TVS_OK;
 }
 
+// 1D Jacobi drop-in path: the same skewed pipeline over position bands
+// (64 levels per pass in registers, K2), contiguous copies.
+static int jacobi1d_pipelined(const tvs_stencil& st, const tvs_layout& lay, const double* in, double* out,
+                              int64_t steps, const tvs_exec& ex, RunCtx& c, int64_t band) {
+  const tvs_geometry& g = c.geo;
+  const int64_t n = g.extents[0];
+  int depth = ex.temporal_depth > 0 ? ex.temporal_depth : jacobi1d_default_depth();
+  depth = std::max(1, std::min(depth, jacobi1d_max_depth()));
+  const int K = (int)((steps + depth - 1) / depth);
+  const bool fma = use_fma(st, ex);
+  std::vector<int> dk(K);
+  std::vector<int64_t> S(K + 1, 0);
+  {
+    int64_t left = steps;
+    for (int k = 0; k < K; ++k) {
+      dk[k] = (int)std::min<int64_t>(left, depth);
+      left -= dk[k];
+      S[k + 1] = S[k] + dk[k];
+    }
+  }
+  if (band < 4 * depth) return fail(TVS_ERR_INVALID, "pipelined band shorter than four temporal blocks");
+  const int nb = (int)((n + S[K] + band - 1) / band);
+  while ((int)c.bands.size() < nb) {
+    cudaStream_t t;
+    TVS_CUDA(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+    c.bands.push_back(t);
+  }
+  const size_t nev = (size_t)nb * (K + 1);
+  while (c.events.size() < nev) {
+    cudaEvent_t e;
+    TVS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.events.push_back(e);
+  }
+  auto up = [&](int b) { return c.events[b]; };
+  auto done = [&](int b, int k) { return c.events[(size_t)nb * (k + 1) + b]; };
+  auto lo_of = [&](int b, int k) { return std::max<int64_t>(0, (int64_t)b * band - S[k]); };
+  auto hi_of = [&](int b, int k) { return std::min<int64_t>(n, (int64_t)(b + 1) * band - S[k]); };
+  auto copy = [&](double* dev, double* host, bool upload, int64_t p0, int64_t p1, cudaStream_t s) {
+    double* d = dev + g.origin + p0;
+    double* h = host + lay.offset + p0;
+    return cudaMemcpyAsync(upload ? (void*)d : (void*)h, upload ? (void*)h : (void*)d, sizeof(double) * (p1 - p0),
+                           upload ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s);
+  };
+  cudaStream_t cs = c.stream;
+  int rc;
+  if ((rc = fill_halo(g, c.buf[0], st.boundary, cs))) return rc;
+  if ((rc = fill_halo(g, c.buf[1], st.boundary, cs))) return rc;
+  const int nup = (int)((n + band - 1) / band);
+  double* result = c.buf[K & 1];
+  int uploaded = 0;
+  for (int b = 0; b < nb; ++b) {
+    for (; uploaded < nup && uploaded <= b + 1; ++uploaded) {
+      TVS_CUDA(copy(c.buf[0], const_cast<double*>(in), true, (int64_t)uploaded * band,
+                    std::min(n, (int64_t)(uploaded + 1) * band), cs));
+      TVS_CUDA(cudaEventRecord(up(uploaded), cs));
+    }
+    cudaStream_t sb = c.bands[b];
+    for (int u = b - 1; u <= b + 1; ++u)
+      if (u >= 0 && u < nup) TVS_CUDA(cudaStreamWaitEvent(sb, up(u), 0));
+    for (int k = 0; k < K; ++k) {
+      if (k > 0 && b > 0) TVS_CUDA(cudaStreamWaitEvent(sb, done(b - 1, k - 1), 0));
+      const int64_t lo = lo_of(b, k), hi = hi_of(b, k);
+      if (hi > lo && (rc = jacobi1d_blocked(st, g, c.buf[k & 1], c.buf[(k + 1) & 1], dk[k], fma, sb, lo, hi)))
+        return rc;
+      TVS_CUDA(cudaEventRecord(done(b, k), sb));
+    }
+    const int64_t lo = lo_of(b, K), hi = hi_of(b, K);
+    if (hi > lo) TVS_CUDA(copy(result, out, false, lo, hi, sb));
+  }
+  for (int b = 0; b < nb; ++b) TVS_CUDA(cudaStreamSynchronize(c.bands[b]));
+  return TVS_OK;
+}
+
 // 3D Jacobi drop-in path: the same skewed pipeline over axis-0 slabs (planes
 // [b*slab - S_k, (b+1)*slab - S_k) in pass k, S_k = levels of passes < k),
 // two levels per pass (K4b; a single-step last pass when T is odd).  Every
@@ -770,6 +843,13 @@ int tvs_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, doub
     if (band > 0 && st->dim == 2 && steps > 0 && ex->algo != TVS_ALGO_NAIVE && jacobi2d_blocked_supported(*st) &&
         c.geo.extents[0] >= 4 * band)
       return jacobi2d_pipelined(*st, *lay, in, out, steps, *ex, c, band);
+    static const int64_t band1 = [] {
+      const char* e = getenv("TVS_E2E_BAND1");  // 0 disables the pipelined 1D path
+      return e ? atoll(e) : 262144ll;  // config 1 e2e: 65536 1.56, 131072 1.01, 262144 0.80 ms (plain 0.86)
+    }();
+    if (band1 > 0 && st->dim == 1 && steps > 0 && ex->algo != TVS_ALGO_NAIVE && jacobi1d_blocked_supported(*st, c.geo) &&
+        c.geo.extents[0] >= 4 * band1)
+      return jacobi1d_pipelined(*st, *lay, in, out, steps, *ex, c, band1);
     const int64_t slab = slab_planes_default();
     if (slab > 0 && st->dim == 3 && steps > 0 && ex->algo != TVS_ALGO_NAIVE && jacobi3d_streaming_supported(*st) &&
         c.geo.extents[0] >= 4 * slab)

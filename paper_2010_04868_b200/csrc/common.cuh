@@ -199,7 +199,7 @@ int jacobi_naive_step(const tvs_stencil& st, const tvs_geometry& g, const double
                       bool fma, cudaStream_t s);
 bool jacobi1d_blocked_supported(const tvs_stencil& st, const tvs_geometry& g);
 int jacobi1d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
-                     int depth, bool fma, cudaStream_t s);
+                     int depth, bool fma, cudaStream_t s, int64_t rlo = 0, int64_t rhi = -1);
 int jacobi1d_default_depth();
 int jacobi1d_max_depth();
 bool jacobi2d_blocked_supported(const tvs_stencil& st);

@@ -45,13 +45,14 @@ __device__ __forceinline__ double upd1(double l, double c, double r, const doubl
 template <unsigned MASK, bool FMA>
 __global__ void __launch_bounds__(kWarps1 * 32) jacobi1d_kernel(const double* __restrict__ src,
                                                                 double* __restrict__ dst, int64_t n, int depth,
-                                                                double w0, double w1, double w2, double bnd) {
+                                                                double w0, double w1, double w2, double bnd,
+                                                                int64_t rlo, int64_t rhi) {
   const double w[3] = {w0, w1, w2};
   const int lane = threadIdx.x & 31;
   const int64_t warp = (int64_t)blockIdx.x * kWarps1 + (threadIdx.x >> 5);
   const int64_t useful = 32 * kP1 - 2 * depth;
-  const int64_t x0 = -depth + warp * useful;  // first point of the warp tile
-  if (x0 + depth >= n) return;               // whole warp beyond the domain
+  const int64_t x0 = rlo - depth + warp * useful;  // first point of the warp tile (outputs [rlo, rhi))
+  if (x0 + depth >= rhi) return;                  // whole warp beyond the range
   const int64_t xl = x0 + lane * kP1;         // this lane's first point
 
   double v[kP1];
@@ -87,7 +88,7 @@ __global__ void __launch_bounds__(kWarps1 * 32) jacobi1d_kernel(const double* __
 #pragma unroll
   for (int m = 0; m < kP1; ++m) {
     const int64_t x = xl + m;
-    if (x >= lo && x < hi && x >= 0 && x < n) dst[x] = v[m];
+    if (x >= lo && x < hi && x >= rlo && x < rhi) dst[x] = v[m];
   }
 }
 
@@ -109,11 +110,11 @@ static int slots1d(const tvs_stencil& st, double w[3]) {
 
 template <unsigned MASK>
 static void launch1d(bool fma, unsigned blocks, cudaStream_t s, const double* src, double* dst, int64_t n, int depth,
-                     const double w[3], double bnd) {
+                     const double w[3], double bnd, int64_t rlo, int64_t rhi) {
   if (fma)
-    jacobi1d_kernel<MASK, true><<<blocks, kWarps1 * 32, 0, s>>>(src, dst, n, depth, w[0], w[1], w[2], bnd);
+    jacobi1d_kernel<MASK, true><<<blocks, kWarps1 * 32, 0, s>>>(src, dst, n, depth, w[0], w[1], w[2], bnd, rlo, rhi);
   else
-    jacobi1d_kernel<MASK, false><<<blocks, kWarps1 * 32, 0, s>>>(src, dst, n, depth, w[0], w[1], w[2], bnd);
+    jacobi1d_kernel<MASK, false><<<blocks, kWarps1 * 32, 0, s>>>(src, dst, n, depth, w[0], w[1], w[2], bnd, rlo, rhi);
 }
 
 int jacobi1d_default_depth() { return J1D_DEPTH; }
@@ -125,25 +126,27 @@ bool jacobi1d_blocked_supported(const tvs_stencil& st, const tvs_geometry& g) {
 }
 
 int jacobi1d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, int depth,
-                     bool fma, cudaStream_t s) {
+                     bool fma, cudaStream_t s, int64_t rlo, int64_t rhi) {
   double w[3];
   const int mask = slots1d(st, w);
   if (mask <= 0 || depth < 1 || depth > kMaxDepth1 || 2 * depth >= 32 * kP1)
     return fail(TVS_ERR_UNSUPPORTED, "jacobi1d_blocked: unsorted taps or depth out of range");
   const int64_t n = g.extents[0];
+  if (rhi < 0) rhi = n;
+  if (rlo < 0 || rhi > n || rlo >= rhi) return fail(TVS_ERR_INVALID, "jacobi1d_blocked: range");
   const int64_t useful = 32 * kP1 - 2 * depth;
-  const int64_t warps = (n + useful - 1) / useful;
+  const int64_t warps = (rhi - rlo + useful - 1) / useful;
   const unsigned blocks = (unsigned)((warps + kWarps1 - 1) / kWarps1);
   const double* s0 = src + g.origin;
   double* d0 = dst + g.origin;
   switch (mask) {
-    case 1: launch1d<1>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
-    case 2: launch1d<2>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
-    case 3: launch1d<3>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
-    case 4: launch1d<4>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
-    case 5: launch1d<5>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
-    case 6: launch1d<6>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
-    default: launch1d<7>(fma, blocks, s, s0, d0, n, depth, w, st.boundary); break;
+    case 1: launch1d<1>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
+    case 2: launch1d<2>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
+    case 3: launch1d<3>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
+    case 4: launch1d<4>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
+    case 5: launch1d<5>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
+    case 6: launch1d<6>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
+    default: launch1d<7>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
   }
   TVS_LAUNCHED("jacobi1d_kernel");
   return TVS_OK;

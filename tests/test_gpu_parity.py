@@ -377,6 +377,19 @@ def test_gs2d_pipeline_cluster_sizes(cuda_ready, cluster):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+@pytest.mark.parametrize("band", [0, 1024, 1500])
+def test_jacobi1d_pipelined_e2e_bands(cuda_ready, band):
+    """tvs_run's pipelined 1D Jacobi path (skewed position bands) is
+    bit-identical to the oracle; band 0 = the plain path."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, TVS_E2E_BAND1=str(band))
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "e2e_band1_check.py")],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 @pytest.mark.parametrize("band", [0, 256, 300])
 def test_gs2d_pipelined_e2e_bands(cuda_ready, band):
     """tvs_run's overlapped 2D Gauss-Seidel path (uploads gated into the

@@ -180,6 +180,105 @@ __global__ void __launch_bounds__(256) life2d_box_kernel(const int* __restrict__
   }
 }
 
+// K7b: 2D box Life, D time levels per HBM pass (the K3 scheme in int32).
+// One warp per block owns a strip of 32*kLP columns (kLP per lane) and
+// streams a segment of rows; level l works one row behind level l-1.  Per
+// level and column a lane keeps F = rowsum(q-1) + rowsum(q), M = rowsum(q)
+// and the centre of row q; when row q+1 of level l-1 arrives (its edge
+// columns by __shfl_up / __shfl_down) the count of row q is
+// F + rowsum(q+1) - centre (exact mod 2^32) and the rule gives the level-l
+// value of row q, which is what level l+1 consumes next.  Rows / columns
+// outside the domain are pinned to the boundary at every level.  The outer
+// D columns of a strip and D rows of a segment are recomputed by the
+// neighbouring tasks, so each level of a task is exactly one Life step of
+// its output cells: bit-identical to D single steps.
+constexpr int kLP = 4;           // columns per lane
+constexpr int kLifeSeg = 256;    // output rows per task
+
+__device__ __forceinline__ int life_rule_u(unsigned n, int centre, unsigned bmask, unsigned smask) {
+  const bool in = n < 27u;
+  const bool born = in && ((bmask >> n) & 1u);
+  const bool keep = in && ((smask >> n) & 1u);
+  return born ? 1 : (keep ? centre : 0);
+}
+
+template <int D>
+__global__ void __launch_bounds__(32) life2d_tb_kernel(const int* __restrict__ src, int* __restrict__ dst, Geo g,
+                                                       int64_t origin, unsigned bmask, unsigned smask, int bnd,
+                                                       int64_t n_strips, int64_t n_tasks) {
+  constexpr int U = 32 * kLP - 2 * D;  // useful columns per strip
+  const int lane = threadIdx.x;
+  const int64_t task = blockIdx.x;
+  if (task >= n_tasks) return;
+  const int64_t strip = task % n_strips, seg = task / n_strips;
+  const int col0 = (int)(-D + strip * U);
+  const int cl = col0 + lane * kLP;
+  const int r0 = (int)(seg * kLifeSeg);
+  const int r1 = (int)min((int64_t)r0 + kLifeSeg, g.e0);
+  const int e0 = (int)g.e0, e1 = (int)g.e1;
+  const int a0 = (int)g.a0_off, ag = (int)g.a0_glob;
+  unsigned col_out = 0, store_mask = 0;
+#pragma unroll
+  for (int p = 0; p < kLP; ++p) {
+    const int x = cl + p;
+    col_out |= (x < 0 || x >= e1 ? 1u : 0u) << p;
+    store_mask |= (x >= col0 + D && x < col0 + D + U && x >= 0 && x < e1 ? 1u : 0u) << p;
+  }
+  unsigned F[D][kLP], M[D][kLP];
+  int C[D][kLP];
+#pragma unroll
+  for (int l = 0; l < D; ++l)
+#pragma unroll
+    for (int p = 0; p < kLP; ++p) F[l][p] = M[l][p] = 0u, C[l][p] = bnd;
+  const int* col_base = src + origin + cl;
+  auto load_row = [&](int m, int (&r)[kLP]) {
+    const bool row_ok = m >= 0 && m < e0 && m + a0 >= 0 && m + a0 < ag;
+    const int* rp = col_base + (int64_t)m * g.s0;
+#pragma unroll
+    for (int p = 0; p < kLP; ++p) r[p] = (row_ok && !(col_out >> p & 1u)) ? __ldg(rp + p) : bnd;
+  };
+  const int m_begin = r0 - D, m_end = r1 + D;
+  int pre[2][kLP];
+  load_row(m_begin, pre[0]);
+  load_row(m_begin + 1, pre[1]);
+  for (int m = m_begin; m < m_end; ++m) {
+    int in[kLP + 2];
+#pragma unroll
+    for (int p = 0; p < kLP; ++p) in[p + 1] = pre[0][p];
+#pragma unroll
+    for (int p = 0; p < kLP; ++p) pre[0][p] = pre[1][p];
+    load_row(m + 2, pre[1]);
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+      // row m - l of level l (its input) arrived: finish row m - l - 1 of level l+1
+      in[0] = __shfl_up_sync(0xffffffffu, in[kLP], 1);
+      in[kLP + 1] = __shfl_down_sync(0xffffffffu, in[1], 1);
+      const int q = m - l - 1;  // row finished at level l+1
+      const bool pin_row = q + a0 < 0 || q + a0 >= ag;
+      int out[kLP];
+#pragma unroll
+      for (int p = 0; p < kLP; ++p) {
+        const unsigned rs = (unsigned)in[p] + (unsigned)in[p + 1] + (unsigned)in[p + 2];
+        const unsigned nsum = F[l][p] + rs - (unsigned)C[l][p];
+        const int v = life_rule_u(nsum, C[l][p], bmask, smask);
+        out[p] = (pin_row || (col_out >> p & 1u)) ? bnd : v;
+        F[l][p] = M[l][p] + rs;
+        M[l][p] = rs;
+        C[l][p] = in[p + 1];
+      }
+#pragma unroll
+      for (int p = 0; p < kLP; ++p) in[p + 1] = out[p];
+    }
+    const int q = m - D;  // level-D row leaving
+    if (q >= r0 && q < r1) {
+      int* wp = dst + origin + (int64_t)q * g.s0 + cl;
+#pragma unroll
+      for (int p = 0; p < kLP; ++p)
+        if (store_mask >> p & 1u) wp[p] = in[p + 1];
+    }
+  }
+}
+
 __global__ void fill_halo_i32_kernel(int* base, tvs_geometry g, int value) {
   const int64_t n = g.alloc_elems;
   const int64_t last_pitch = g.dim == 1 ? g.alloc_elems : g.strides[g.dim - 2];
@@ -264,14 +363,46 @@ static int life_step(const tvs_life_rule& r, const tvs_geometry& g, const int* s
   return TVS_OK;
 }
 
+template <int D>
+static int life2d_tb_launch(const tvs_life_rule& r, const tvs_geometry& g, const int* src, int* dst, cudaStream_t s) {
+  const Geo geo = make_geo(g);
+  constexpr int U = 32 * kLP - 2 * D;
+  const int64_t ns = (geo.e1 + U - 1) / U;
+  const int64_t nt = ns * ((geo.e0 + kLifeSeg - 1) / kLifeSeg);
+  life2d_tb_kernel<D><<<(unsigned)nt, 32, 0, s>>>(src, dst, geo, g.origin, (unsigned)r.birth_mask,
+                                                  (unsigned)r.survive_mask, r.boundary, ns, nt);
+  TVS_LAUNCHED("life2d_tb_kernel");
+  return TVS_OK;
+}
+
+static bool life_is_box2d(const tvs_life_rule& r) {
+  unsigned ring = 0;
+  for (int k = 0; k < r.ntaps; ++k) ring |= 1u << ((r.offsets[k][0] + 1) * 3 + (r.offsets[k][1] + 1));
+  return r.dim == 2 && r.ntaps == 8 && ring == 0x1EFu;
+}
+
 static int life_device(const tvs_life_rule& r, const tvs_geometry& g, int* src, int* dst, int64_t steps,
-                       cudaStream_t s, int32_t* in_dst) {
+                       cudaStream_t s, int32_t* in_dst, int depth = 0) {
   int* a = src;
   int* b = dst;
-  for (int64_t k = 0; k < steps; ++k) {
-    const int rc = life_step(r, g, a, b, s);
+  static const int env_depth = [] {
+    const char* e = getenv("TVS_LIFE_DEPTH");  // 16384^2 B2S23: 1 597, 2 903, 4 1058, 8 1027 (spills) GCellUpd/s
+    return e ? atoi(e) : 4;
+  }();
+  const int D = depth > 0 ? depth : env_depth;
+  const bool box2d = life_is_box2d(r);
+  const int cap = D >= 8 ? 8 : (D >= 4 ? 4 : (D >= 2 ? 2 : 1));
+  for (int64_t k = 0; k < steps;) {
+    const int64_t left = steps - k;
+    int done = box2d ? cap : 1;
+    while (done > left) done >>= 1;  // 8, 4, 2 or 1 levels this pass
+    const int rc = done == 8   ? life2d_tb_launch<8>(r, g, a, b, s)
+                   : done == 4 ? life2d_tb_launch<4>(r, g, a, b, s)
+                   : done == 2 ? life2d_tb_launch<2>(r, g, a, b, s)
+                               : life_step(r, g, a, b, s);
     if (rc) return rc;
     std::swap(a, b);
+    k += done;
   }
   if (in_dst) *in_dst = a == dst ? 1 : 0;
   return TVS_OK;
@@ -567,7 +698,7 @@ int tvs_life_device(const tvs_life_rule* r, const tvs_geometry* g, int32_t* src,
   if (!g || !src || !dst) return fail(TVS_ERR_INVALID, "null argument");
   if (g->dim != r->dim) return fail(TVS_ERR_SIZE, "grid/rule dimension mismatch");
   if (steps < 0) return fail(TVS_ERR_INVALID, "steps must be >= 0");
-  return life_device(*r, *g, src, dst, steps, (cudaStream_t)stream, result_in_dst);
+  return life_device(*r, *g, src, dst, steps, (cudaStream_t)stream, result_in_dst, ex->temporal_depth);
 }
 
 int tvs_life_run(const tvs_life_rule* r, const tvs_layout* lay, const int32_t* in, int32_t* out, int64_t steps,
@@ -598,7 +729,7 @@ int tvs_life_run(const tvs_life_rule* r, const tvs_layout* lay, const int32_t* i
   }
   if ((rc = copy_interior_i32(g, buf[0], *lay, const_cast<int*>(in), true, s))) return done(rc);
   int32_t in_dst = 0;
-  if ((rc = life_device(*r, g, buf[0], buf[1], steps, s, &in_dst))) return done(rc);
+  if ((rc = life_device(*r, g, buf[0], buf[1], steps, s, &in_dst, ex->temporal_depth))) return done(rc);
   if ((rc = copy_interior_i32(g, in_dst ? buf[1] : buf[0], *lay, out, false, s))) return done(rc);
   const cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return done(cuda_fail(e, "tvs_life_run"));

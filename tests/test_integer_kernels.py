@@ -86,6 +86,26 @@ def test_life_tiles_and_wrapping_sums(cuda_ready, ext):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("ext", [(300, 257), (1000, 130), (70, 2000), (257, 300)])
+def test_life_temporal_blocking_depths(cuda_ready, ext):
+    """K7b (D levels per pass) for D = 1, 2, 4, 8 and step counts that are
+    not multiples of D, against the oracle; a non-zero boundary and a
+    non-Conway rule."""
+    import dataclasses
+
+    from paper_2010_04868_b200 import config
+    from paper_2010_04868_b200.kernels._common import execute
+
+    spec = dataclasses.replace(get("life").spec, boundary=1, birth=frozenset({3, 6}), survive=frozenset({2, 3}))
+    g = Grid(ext, 1, boundary=1, element_kind="int32")
+    g.set_interior(np.random.default_rng(ext[0]).integers(0, 2, ext, dtype=np.int32))
+    want = npo.scalar_reference(spec, g, 23)
+    for depth in (1, 2, 4, 8):
+        with config.using(depth=depth):
+            assert np.array_equal(execute(spec, g, 23).interior, want.interior), depth
+
+
+@pytest.mark.gpu
 def test_lcs_golden_gpu(cuda_ready, golden_int):
     from paper_2010_04868_b200.kernels import lcs_temporal
 

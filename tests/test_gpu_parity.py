@@ -220,6 +220,40 @@ def test_fma_policies(cuda_ready):
     assert np.array_equal(_run("jac3d27p", g3, 6, fma="exact").interior, want3.interior)
 
 
+def test_concurrent_drop_in_calls(cuda_ready):
+    """The reference runs kernels from a ThreadPoolExecutor (tiling.py:365):
+    the C ABI is re-entrant (per-thread device context, streams, scratch,
+    error string), so concurrent calls of every family — including the
+    pipelined 1D/2D/3D Jacobi, the stream-gated 2D Gauss-Seidel path, Life
+    and LCS — each return their own oracle result."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as npo
+    from paper_2010_04868_b200.kernels import lcs_temporal
+
+    jobs = [("heat2d", (1100, 200), 21), ("jac3d27p", (140, 20, 24), 9), ("gs2d9p", (1100, 150), 17),
+            ("heat1d", (1 << 20,), 70), ("gs1d_w343", (3000,), 40), ("life", (300, 260), 13)]
+
+    def one(job):
+        kernel, ext, steps = job
+        spec = get(kernel).spec
+        g = Grid.random(ext, seed=len(ext) + steps, element_kind=spec.element_kind)
+        got = execute(spec, g, steps)
+        want = (npo.scalar_reference(spec, g, steps) if spec.is_life
+                else cref.scalar_reference(spec, g, steps, order="lexicographic", threads=2))
+        return np.array_equal(got.interior, want.interior)
+
+    def lcs_job(seed):
+        rng = np.random.default_rng(seed)
+        a, b = rng.integers(0, 4, 3000, dtype=np.int32), rng.integers(0, 4, 2500, dtype=np.int32)
+        return lcs_temporal(a, b) == npo.lcs_length(a, b)
+
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        futs = [pool.submit(one, j) for j in jobs * 2] + [pool.submit(lcs_job, s) for s in range(3)]
+        results = [f.result() for f in futs]
+    assert all(results), results
+
+
 def test_drop_in_signatures_and_immutability(cuda_ready):
     g = Grid.random((512,), seed=8)
     before = g.data.copy()

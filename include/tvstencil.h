@@ -147,6 +147,11 @@ int tvs_fill_halo(const tvs_geometry* g, double* dev, double value, void* stream
  * one cell per step (callers exchange `steps` ghost rows first). */
 int tvs_jacobi_device(const tvs_stencil* st, const tvs_geometry* g, double* src, double* dst, int64_t steps,
                       const tvs_exec* ex, void* stream, int32_t* result_in_dst);
+/* One temporally blocked pass (`steps` <= the kernel's depth: 2D <= 12, 3D
+ * <= 2) writing only axis-0 rows [row_lo, row_hi) of dst: the interior /
+ * edge split that lets a halo exchange overlap the interior compute. */
+int tvs_jacobi_device_rows(const tvs_stencil* st, const tvs_geometry* g, const double* src, double* dst,
+                           int64_t steps, const tvs_exec* ex, void* stream, int64_t row_lo, int64_t row_hi);
 /* Gauss-Seidel in place on one device block (single GPU, no ghosts). */
 int tvs_gauss_seidel_device(const tvs_stencil* st, const tvs_geometry* g, double* grid, int64_t steps,
                             const tvs_exec* ex, void* stream);

@@ -85,6 +85,8 @@ _SIGS = {
     "tvs_fill_halo": (C.c_int, [C.POINTER(Geometry), _P, C.c_double, _P]),
     "tvs_jacobi_device": (C.c_int, [C.POINTER(Stencil), C.POINTER(Geometry), _P, _P, C.c_int64, C.POINTER(Exec), _P,
                                     C.POINTER(C.c_int32)]),
+    "tvs_jacobi_device_rows": (C.c_int, [C.POINTER(Stencil), C.POINTER(Geometry), _P, _P, C.c_int64, C.POINTER(Exec), _P,
+                                         C.c_int64, C.c_int64]),
     "tvs_gauss_seidel_device": (C.c_int, [C.POINTER(Stencil), C.POINTER(Geometry), _P, C.c_int64, C.POINTER(Exec), _P]),
     "tvs_upload": (C.c_int, [C.POINTER(Geometry), _P, C.POINTER(Layout), _P, _P]),
     "tvs_download": (C.c_int, [C.POINTER(Geometry), _P, C.POINTER(Layout), _P, _P]),

@@ -813,6 +813,26 @@ int tvs_jacobi_device(const tvs_stencil* st, const tvs_geometry* g, double* src,
   return jacobi_device(*st, *g, src, dst, steps, *ex, (cudaStream_t)stream, result_in_dst);
 }
 
+int tvs_jacobi_device_rows(const tvs_stencil* st, const tvs_geometry* g, const double* src, double* dst,
+                           int64_t steps, const tvs_exec* ex, void* stream, int64_t row_lo, int64_t row_hi) {
+  int rc = validate(st);
+  if (rc) return rc;
+  if ((rc = validate_exec(ex))) return rc;
+  if (!g || !src || !dst) return fail(TVS_ERR_INVALID, "null argument");
+  if (st->kind != TVS_JACOBI) return fail(TVS_ERR_INVALID, "tvs_jacobi_device_rows needs a Jacobi stencil");
+  if (st->dim != g->dim) return fail(TVS_ERR_SIZE, "stencil/geometry dimension mismatch");
+  if (steps < 1) return fail(TVS_ERR_INVALID, "steps must be >= 1");
+  if (row_lo < 0 || row_hi > g->extents[0] || row_lo >= row_hi) return fail(TVS_ERR_INVALID, "row range");
+  const bool fma = use_fma(*st, *ex);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (g->dim == 2 && jacobi2d_blocked_supported(*st) && steps <= jacobi2d_max_depth())
+    return jacobi2d_blocked(*st, *g, src, dst, (int)steps, fma, s, row_lo, row_hi);
+  if (g->dim == 3 && jacobi3d_streaming_supported(*st) && steps <= 2)
+    return steps == 2 ? jacobi3d_blocked2(*st, *g, src, dst, fma, s, row_lo, row_hi)
+                      : jacobi3d_streaming(*st, *g, src, dst, fma, s, row_lo, row_hi);
+  return fail(TVS_ERR_UNSUPPORTED, "tvs_jacobi_device_rows: one blocked 2D/3D launch of at most its depth");
+}
+
 int tvs_gauss_seidel_device(const tvs_stencil* st, const tvs_geometry* g, double* grid, int64_t steps,
                             const tvs_exec* ex, void* stream) {
   int rc = validate(st);

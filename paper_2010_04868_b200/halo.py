@@ -72,11 +72,13 @@ def make_layout(global_extents, world: int, rank: int, ghost: int) -> SlabLayout
     return SlabLayout(rank, world, r0, r1, ghost, ext, geo)
 
 
-def exchange(lay: SlabLayout, buf, dist, group=None) -> None:
+def exchange(lay: SlabLayout, buf, dist, group=None, wait: bool = True):
     """Swap halos: my first `ghost` owned rows -> rank-1's bottom ghosts,
-    my last `ghost` owned rows -> rank+1's top ghosts (one grouped batch)."""
+    my last `ghost` owned rows -> rank+1's top ghosts (one grouped batch).
+    ``wait=False`` returns the outstanding requests instead of waiting (the
+    overlapped pass waits after launching the interior rows)."""
     if lay.world == 1 or lay.ghost == 0:
-        return
+        return []
     g, n = lay.ghost, lay.n_own
     ops = []
     if lay.rank > 0:
@@ -85,8 +87,12 @@ def exchange(lay: SlabLayout, buf, dist, group=None) -> None:
     if lay.rank < lay.world - 1:
         ops.append(dist.P2POp(dist.isend, buf[lay.row_slice(n, g)], lay.rank + 1, group))
         ops.append(dist.P2POp(dist.irecv, buf[lay.row_slice(n + g, g)], lay.rank + 1, group))
-    for req in dist.batch_isend_irecv(ops):
+    reqs = dist.batch_isend_irecv(ops)
+    if not wait:
+        return reqs
+    for req in reqs:
         req.wait()
+    return []
 
 
 class ShardedJacobi:
@@ -94,7 +100,7 @@ class ShardedJacobi:
     steps src -> dst (default: the CUDA library on torch device tensors)."""
 
     def __init__(self, spec, global_extents, dist, depth: int = 8, device=None, step_fn=None, group=None,
-                 dtype=None):
+                 dtype=None, rows_fn=None, overlap: bool = True):
         import torch
 
         self.spec = spec
@@ -110,6 +116,10 @@ class ShardedJacobi:
                      for _ in range(2)]
         self.cur = 0
         self.step_fn = step_fn or self._cuda_step
+        # rows_fn(lay, src, dst, k, lo, hi): one k-step pass writing only local
+        # axis-0 rows [lo, hi) — lets the halo exchange overlap the interior
+        self.rows_fn = rows_fn if rows_fn is not None else (self._cuda_rows if step_fn is None else None)
+        self.overlap = overlap
         self._st = _native.make_stencil(spec) if step_fn is None else None
         self.launches = 0
 
@@ -153,15 +163,45 @@ class ShardedJacobi:
             int(k), C.byref(ex), C.c_void_p(stream), C.byref(in_dst)), "tvs_jacobi_device")
         return bool(in_dst.value)
 
+    def _cuda_rows(self, lay, src, dst, k, lo, hi):
+        import torch
+
+        ex = _native.make_exec(device=src.device.index or 0)
+        stream = torch.cuda.current_stream(src.device).cuda_stream
+        _native.check(_native.lib().tvs_jacobi_device_rows(
+            C.byref(self._st), C.byref(lay.geometry), C.c_void_p(src.data_ptr()), C.c_void_p(dst.data_ptr()),
+            int(k), C.byref(ex), C.c_void_p(stream), int(lo), int(hi)), "tvs_jacobi_device_rows")
+
+    def _max_pass(self) -> int:
+        """Levels one ranged launch can advance (2D kernel depth, 3D two)."""
+        return 12 if self.layout.geometry.dim == 2 else 2
+
     def run(self, steps: int) -> None:
+        lay = self.layout
+        g, n = lay.ghost, lay.n_own
         done = 0
         while done < steps:
             k = min(self.depth, steps - done)
-            exchange(self.layout, self.bufs[self.cur], self.dist, self.group)
             src, dst = self.bufs[self.cur], self.bufs[1 - self.cur]
-            in_dst = self.step_fn(self.layout, src, dst, k)
-            if in_dst:
+            if self.overlap and self.rows_fn is not None and lay.world > 1 and k <= min(g, self._max_pass()):
+                # owned rows are local [g, g+n); rows [g+k, g+n-k) read only
+                # owned rows, so they run while the halos are in flight; the
+                # k rows at each edge run once the new ghosts have landed.
+                # Ghost rows are not recomputed: the next exchange refills them.
+                reqs = exchange(lay, src, self.dist, self.group, wait=False)
+                if n - 2 * k > 0:
+                    self.rows_fn(lay, src, dst, k, g + k, g + n - k)
+                for req in reqs:
+                    req.wait()
+                edges = [(g, g + min(k, n))] + ([(g + max(n - k, k), g + n)] if n > k else [])
+                for lo, hi in edges:
+                    self.rows_fn(lay, src, dst, k, lo, hi)
                 self.cur = 1 - self.cur
+            else:
+                exchange(lay, src, self.dist, self.group)
+                in_dst = self.step_fn(lay, src, dst, k)
+                if in_dst:
+                    self.cur = 1 - self.cur
             done += k
 
     def gather(self):

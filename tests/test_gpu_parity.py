@@ -220,6 +220,49 @@ def test_fma_policies(cuda_ready):
     assert np.array_equal(_run("jac3d27p", g3, 6, fma="exact").interior, want3.interior)
 
 
+def test_ranged_passes_compose_to_full_pass(cuda_ready):
+    """tvs_jacobi_device_rows (the overlapped halo path's interior / edge
+    passes): ranged passes covering a slab's owned rows equal one full pass
+    there, bit-exact, for 2D depths up to 12 and 3D depths 1-2, on a
+    mid-domain slab (ghost rows on both sides)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2010_04868_b200 import halo
+
+    for kernel, ext, depths in (("heat2d", (300, 130), (1, 3, 8, 12)), ("jac2d9p", (200, 70), (2, 5)),
+                                ("jac3d27p", (60, 20, 36), (1, 2)), ("heat3d", (50, 17, 40), (2,))):
+        spec = get(kernel).spec
+        st = _native.make_stencil(spec)
+        g = Grid.random(ext, seed=3)
+        for k in depths:
+            lay = halo.make_layout(ext, 3, 1, max(k, 2))
+            n, gh = lay.n_own, lay.ghost
+            nel = int(lay.geometry.alloc_elems)
+            src = torch.full((nel,), 0.0, dtype=torch.float64, device="cuda")
+            view = src.as_strided(tuple(lay.extents), tuple(int(lay.geometry.strides[d]) for d in range(len(ext))),
+                                  int(lay.geometry.origin))
+            view.copy_(torch.from_numpy(g.interior[lay.r0 - gh: lay.r1 + gh].copy()))
+            full = torch.zeros_like(src)
+            part = torch.zeros_like(src)
+            ex = _native.make_exec(temporal_depth=k)  # the full pass is one launch of k levels too
+            stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+            in_dst = C.c_int32(0)
+            _native.check(_native.lib().tvs_jacobi_device(C.byref(st), C.byref(lay.geometry), C.c_void_p(src.data_ptr()),
+                                                          C.c_void_p(full.data_ptr()), k, C.byref(ex), stream,
+                                                          C.byref(in_dst)))
+            assert in_dst.value == 1
+            for lo, hi in ((gh + k, gh + n - k), (gh, gh + k), (gh + n - k, gh + n)):
+                _native.check(_native.lib().tvs_jacobi_device_rows(
+                    C.byref(st), C.byref(lay.geometry), C.c_void_p(src.data_ptr()), C.c_void_p(part.data_ptr()), k,
+                    C.byref(ex), stream, lo, hi))
+            torch.cuda.synchronize()
+            s0 = int(lay.geometry.strides[0])
+            own = slice((gh + 1) * s0, (gh + n + 1) * s0)
+            assert torch.equal(full[own], part[own]), (kernel, k)
+
+
 def test_concurrent_drop_in_calls(cuda_ready):
     """The reference runs kernels from a ThreadPoolExecutor (tiling.py:365):
     the C ABI is re-entrant (per-thread device context, streams, scratch,

@@ -55,7 +55,28 @@ def numpy_step(spec):
     return step
 
 
-def _worker(rank, world, port, kernel, ext, steps, depth, expect):
+def numpy_rows(spec):
+    """Ranged pass (stand-in for tvs_jacobi_device_rows): k steps writing only
+    local rows [lo, hi) of dst.  Rows outside [lo - k, hi + k) are poisoned
+    with NaN in the working copy, so a range the k-step cone does not cover
+    (or halos used before they land) shows up as NaN in the result."""
+    step = numpy_step(spec)
+
+    def rows(lay, src, dst, k, lo, hi):
+        g = lay.geometry
+        s0 = int(g.strides[0])
+        work = src.clone()
+        tmp = src.clone()  # pads / memory halo keep the boundary value
+        for r in range(-1, int(g.extents[0]) + 1):
+            if not lo - k <= r < hi + k:
+                work[(r + 1) * s0:(r + 2) * s0] = float("nan")
+        res = tmp if step(lay, work, tmp, k) else work
+        dst[(lo + 1) * s0:(hi + 1) * s0] = res[(lo + 1) * s0:(hi + 1) * s0]
+
+    return rows
+
+
+def _worker(rank, world, port, kernel, ext, steps, depth, expect, overlap=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -63,7 +84,8 @@ def _worker(rank, world, port, kernel, ext, steps, depth, expect):
 
         spec = get(kernel).spec
         full = np.random.default_rng(7).uniform(0, 1, ext)
-        sj = halo.ShardedJacobi(spec, ext, dist, depth=depth, device=torch.device("cpu"), step_fn=numpy_step(spec))
+        sj = halo.ShardedJacobi(spec, ext, dist, depth=depth, device=torch.device("cpu"), step_fn=numpy_step(spec),
+                                rows_fn=numpy_rows(spec) if overlap else None, overlap=overlap)
         sj.load_global(full)
         sj.run(steps)
         got = sj.gather().numpy()
@@ -74,10 +96,13 @@ def _worker(rank, world, port, kernel, ext, steps, depth, expect):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("overlap", [False, True])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("kernel,ext,steps,depth", [("heat2d", (23, 17), 11, 4), ("jac2d9p", (30, 9), 7, 3),
                                                      ("jac3d27p", (13, 6, 7), 5, 2)])
-def test_sharded_equals_single_domain(world, kernel, ext, steps, depth):
+def test_sharded_equals_single_domain(world, kernel, ext, steps, depth, overlap):
+    """Blocking exchange, and the overlapped pass (interior rows launched
+    while the halos are in flight, edge rows after they land)."""
     from oracle import oracle as npo
     from paper_2010_04868_b200 import Grid
     from paper_2010_04868_b200.catalog import get
@@ -85,7 +110,7 @@ def test_sharded_equals_single_domain(world, kernel, ext, steps, depth):
     g = Grid(ext, 1)
     g.set_interior(np.random.default_rng(7).uniform(0, 1, ext))
     expect = npo.scalar_reference(get(kernel).spec, g, steps).interior.copy()
-    mp.spawn(_worker, args=(world, _free_port(), kernel, ext, steps, depth, expect), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), kernel, ext, steps, depth, expect, overlap), nprocs=world, join=True)
 
 
 def test_split_rows_balanced():

@@ -23,15 +23,14 @@
 //   b[y-1] slides through the rows and lanes one position per step,
 // out = a[x-1] == b[y-1] ? diag + 1 : max(up, left); only the lane's first
 // row takes a shuffle (from lane k-1's last row).  Lane 0 reads row
-// x0 + 128w from a boundary row written by warp w-1's lane 31 (progress
-// published every 32 columns with a GPU-scope release); warps take tickets
-// in start order and only wait on lower tickets (deadlock-free).  Passes of
-// at most kLcsMaxWarps warps bound the boundary-row workspace.
+// x0 + 128w from a boundary row written by warp w-1's lane 31, whose 64-bit
+// entries carry their own column tag (value and validity in one
+// single-copy-atomic store: no fences, no progress counters); warps take
+// tickets in start order and only wait on lower tickets (deadlock-free).
+// Passes of at most kLcsMaxWarps warps bound the boundary-row workspace.
 #include <algorithm>
 #include <cstring>
-#include <mutex>
 #include <type_traits>
-#include <vector>
 
 #include "common.cuh"
 
@@ -460,15 +459,6 @@ struct LcsArgs {
   int* ticket;
   int* result;    // lcs[na][nb]
 };
-
-__device__ __forceinline__ int ld_acquire_i32(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_i32(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 // Lane k owns kLcsRPL consecutive DP rows x_j = x0 + 32*kLcsRPL*w +
 // kLcsRPL*k + j + 1; at step s its row j updates column c - j with

@@ -80,7 +80,10 @@ constexpr int kBase = 10;            // every producer starts left of column 0 (
 // units resident, the oldest can run at most G * rg iterations ahead of the
 // first unit not yet resident, and must reach c_end to retire, so the host
 // makes G * rg >= 2 * c_end (no back-pressure deadlock for any width).
-constexpr int kPub = 4;              // IO warps publish up/downstream every kPub chunks
+#ifndef GS2P_PUB
+#define GS2P_PUB 4  // 8192^2 T=100: 1 55.5, 2 35.7, 4 31.7, 6 34.7, 8 39.6 ms
+#endif
+constexpr int kPub = GS2P_PUB;       // IO warps publish up/downstream every kPub chunks
 constexpr int kComputeWarps = kG * kWarpsG;
 constexpr int kPhLag = kBig * kG / kC;  // phantom chunk kl = producer chunk kl + kPhLag
 constexpr bool kClusterOK = kBig * kG % kC == 0;  // DSMEM push needs a whole-chunk phantom lag

@@ -96,12 +96,31 @@ def _bits(value) -> str:
     return f"0x{np.float64(value).view(np.uint64):016x}"
 
 
-def equivalence_matrix(cells, reference, runner=None) -> MatrixReport:
+def equivalence_matrix(cells, reference, runner=None, lcs_reference=None) -> MatrixReport:
     """Run every cell through ``runner`` (default: the GPU drop-ins) and
-    compare bit-exactly with ``reference(spec, grid, steps)``."""
+    compare bit-exactly with ``reference(spec, grid, steps)``; ``lcs`` cells
+    (reference verify.py:136-145: two seeded 4-letter sequences) compare
+    ``lcs_temporal`` with ``lcs_reference(a, b)``."""
     runner = runner or run_temporal
     report = MatrixReport()
     for idx, cell in enumerate(cells):
+        if cell.kernel == "lcs":
+            from .kernels import lcs_temporal
+
+            if lcs_reference is None:
+                raise ValueError("lcs cells need an lcs_reference callable")
+            rng = np.random.default_rng(cell.seed)
+            a = rng.integers(0, 4, size=cell.size[0], dtype=np.int32)
+            b = rng.integers(0, 4, size=cell.size[1], dtype=np.int32)
+            got, want = lcs_temporal(a, b), int(lcs_reference(a, b))
+            res = CellResult(cell, got == want)
+            if not res.ok:
+                res.position = ()
+                res.got_bits, res.want_bits = f"{got:08x}", f"{want:08x}"
+            report.results.append(res)
+            if not res.ok and report.first_divergence is None:
+                report.first_divergence = idx
+            continue
         entry = catalog_get(cell.kernel)
         grid = Grid.random(cell.size, seed=cell.seed, element_kind=entry.spec.element_kind, vl=entry.vl)
         got = runner(cell.kernel, grid, cell.steps, KernelVariant(cell.scheme, cell.single_array))
@@ -121,13 +140,19 @@ def equivalence_matrix(cells, reference, runner=None) -> MatrixReport:
 
 def default_matrix(cells_per_kernel: int = 20, master_seed: int = 2024, kernels=None) -> list:
     """Acceptance matrix in the reference's shape (verify.py:169-222): random
-    cells per float64 catalog kernel with the size remainder classes
+    cells per float64 catalog kernel (or the given ``kernels``, which may
+    include ``life`` and ``lcs``) with the size remainder classes
     {0, 1, vl-1} mod 4*s*vl and every steps-mod-vl class."""
     rng = np.random.default_rng(master_seed)
     caps = {1: 4096, 2: 256, 3: 64}
     out = []
     names = kernels or [k for k, e in DEFAULT_CATALOG.items() if e.spec.element_kind == "float64"]
     for kernel in names:
+        if kernel == "lcs":  # reference verify.py:184-192: one 2000x2000 cell, the rest below 800
+            sizes = [(2000, 2000)] + [(int(rng.integers(1, 800)), int(rng.integers(1, 800)))
+                                      for _ in range(cells_per_kernel - 1)]
+            out.extend(Cell("lcs", "base", False, size, int(rng.integers(1 << 30)), size[0]) for size in sizes)
+            continue
         entry = catalog_get(kernel)
         vl, s, dim = entry.vl, entry.s, entry.spec.dim
         lo = vl * (s + 1) + entry.sl + 1

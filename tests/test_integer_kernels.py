@@ -126,3 +126,58 @@ def test_lcs_sizes_gpu(cuda_ready, na, nb, alpha):
     b = rng.integers(0, alpha, nb).astype(np.int32)
     assert lcs_temporal(a, b) == npo.lcs_length(a, b)
     assert lcs_temporal(a, a[: nb]) == min(na, nb) if nb <= na else True
+
+
+@pytest.mark.gpu
+def test_integer_acceptance_matrix_gpu(cuda_ready):
+    """The reference's acceptance matrix for its integer kernels
+    (verify.py:130-222: 20 life cells, 20 lcs cells incl. one 2000x2000)."""
+    from paper_2010_04868_b200.verify import default_matrix, equivalence_matrix
+
+    cells = default_matrix(cells_per_kernel=20, master_seed=2024, kernels=["life", "lcs"])
+    rep = equivalence_matrix(cells, npo.scalar_reference, lcs_reference=npo.lcs_length)
+    assert len(rep.results) == 40 and rep.passed, rep.to_json()
+
+
+def test_reference_known_lcs_and_life_properties_cpu():
+    """Oracle-side known answers the reference tests use (test_lcs.py:11-26,
+    test_kernels_nd.py:57-78): identical strings, disjoint alphabets, empty
+    inputs; a 2x2 block is a still life under B3/S23; an empty board stays
+    empty."""
+    import dataclasses
+
+    x = np.arange(50, dtype=np.int32) % 7
+    assert npo.lcs_length(x, x) == 50
+    assert npo.lcs_length(np.zeros(9, np.int32), np.ones(5, np.int32)) == 0
+    assert npo.lcs_length(np.zeros(0, np.int32), x) == 0
+    conway = dataclasses.replace(get("life").spec, birth=frozenset({3}), survive=frozenset({2, 3}))
+    g = Grid((10, 10), 1, element_kind="int32")
+    blk = np.zeros((10, 10), np.int32)
+    blk[4:6, 4:6] = 1
+    g.set_interior(blk)
+    assert np.array_equal(npo.scalar_reference(conway, g, 5).interior, blk)
+
+
+@pytest.mark.gpu
+def test_reference_known_lcs_and_life_properties_gpu(cuda_ready):
+    """The same known answers through the GPU drop-ins."""
+    import dataclasses
+
+    from paper_2010_04868_b200.kernels import lcs_temporal
+    from paper_2010_04868_b200.kernels._common import execute
+
+    x = np.arange(5000, dtype=np.int32) % 7
+    assert lcs_temporal(x, x) == 5000
+    assert lcs_temporal(np.zeros(900, np.int32), np.ones(700, np.int32)) == 0
+    assert lcs_temporal([], x) == 0 and lcs_temporal(x, []) == 0
+    for n in range(1, 10):  # short sequences (the reference's scalar path)
+        a, b = np.arange(n, dtype=np.int32) % 3, np.arange(n + 2, dtype=np.int32) % 2
+        assert lcs_temporal(a, b) == npo.lcs_length(a, b)
+    conway = dataclasses.replace(get("life").spec, birth=frozenset({3}), survive=frozenset({2, 3}))
+    g = Grid((300, 200), 1, element_kind="int32")
+    blk = np.zeros((300, 200), np.int32)
+    blk[100:102, 50:52] = 1
+    g.set_interior(blk)
+    assert np.array_equal(execute(conway, g, 17).interior, blk)
+    empty = Grid((300, 200), 1, element_kind="int32")
+    assert not execute(get("life").spec, empty, 9).interior.any()

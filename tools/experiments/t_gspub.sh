@@ -1,5 +1,5 @@
 # GS-2D: global-ring publication interval (hop latency vs fence count)
-for v in base p6 p8; do
+for v in base kg5; do
   L=build/var/$v/libtvstencil.so; [ $v = base ] && L=paper_2010_04868_b200/libtvstencil.so
   TVSTENCIL_LIB=$L timeout 300 python tools/parity_quick.py gs2d9p | tail -1
   TVSTENCIL_LIB=$L timeout 120 python tools/shape_run.py gs2d9p 8192 8192 --T 100 --reps 3 | sed "s/^/$v /"

@@ -241,7 +241,8 @@ def _verify(args) -> int:
         good = got == want
         ok &= good
         print(f"  {'PASS' if good else 'FAIL'} known answer {kernel}: {got}")
-    cells = default_matrix(cells_per_kernel=args.cells, kernels=[k for k in _kernels(args.kernel) if k in FP_KERNELS])
+    fp_names = [k for k in _kernels(args.kernel) if k in FP_KERNELS]
+    cells = default_matrix(cells_per_kernel=args.cells, kernels=fp_names) if fp_names else []
     t0 = time.time()
     bad = 0
     for cell in cells:
@@ -257,6 +258,34 @@ def _verify(args) -> int:
     ok &= bad == 0
     print(f"equivalence (blocked vs naive, GPU): {len(cells)} cells, {'PASS' if bad == 0 else 'FAIL'} "
           f"({time.time() - t0:.1f}s)")
+    # integer kernels: two independent GPU algorithms each (Life: 4 levels per
+    # pass vs single steps; LCS: time-lane pipeline vs tiled anti-diagonal waves)
+    ints = [k for k in _kernels(args.kernel) if k in ("life", "lcs")]
+    if ints:
+        t0 = time.time()
+        icells = default_matrix(cells_per_kernel=args.cells, kernels=ints)
+        ibad = 0
+        for cell in icells:
+            if cell.kernel == "lcs":
+                rng = np.random.default_rng(cell.seed)
+                a = rng.integers(0, 4, size=cell.size[0], dtype=np.int32)
+                b = rng.integers(0, 4, size=cell.size[1], dtype=np.int32)
+                sched = build_schedule("lcs", (len(b),), len(a), (128,), 64)
+                same = lcs_temporal(a, b) == lcs_blocked(a, b, sched)
+            else:
+                spec = catalog_get(cell.kernel).spec
+                g = Grid.random(cell.size, seed=cell.seed, element_kind="int32")
+                with config.using(depth=4):
+                    fast = execute(spec, g, cell.steps)
+                with config.using(depth=1):
+                    slow = execute(spec, g, cell.steps)
+                same = np.array_equal(fast.interior, slow.interior)
+            if not same:
+                ibad += 1
+                print(f"  FAIL {cell.describe()}")
+        ok &= ibad == 0
+        print(f"equivalence (integer kernels, GPU): {len(icells)} cells, {'PASS' if ibad == 0 else 'FAIL'} "
+              f"({time.time() - t0:.1f}s)")
     print("verify:", "PASS" if ok else "FAIL")
     return 0 if ok else 1
 

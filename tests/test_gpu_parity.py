@@ -409,6 +409,8 @@ def test_cli_bench_and_verify(cuda_ready, tmp_path):
     want = cref.scalar_reference(get("heat2d").spec, Grid.random((200, 150), seed=0), 9)
     assert fields[11] == f"{fnv1a64(want.dump_bytes()):016x}"
     assert cli.main(["--mode", "verify", "--kernel", "gs2d9p", "--cells", "3"]) == 0
+    assert cli.main(["--mode", "verify", "--kernel", "life", "--cells", "4"]) == 0
+    assert cli.main(["--mode", "verify", "--kernel", "lcs", "--cells", "3"]) == 0
 
 
 def test_cli_tiles_threads_life_lcs(cuda_ready, tmp_path):

@@ -123,6 +123,13 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append((time.time(), line.strip()))
 
+    def wait_ready(self, timeout=3.0):
+        """Block until nvidia-smi has produced its first sample (it needs
+        0.1-0.5 s to start), so a short timed region is still covered."""
+        t0 = time.time()
+        while self.proc is not None and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.01)
+
     def mark(self, start):
         """Host wall-clock bounds of the timed region (samples outside are dropped)."""
         if start:
@@ -187,6 +194,7 @@ def device_time(cfg, K, W, sampler=None, fma=None, min_timed_s=0.0, algo=None):
     del g
     if sampler is not None:
         sampler.start()  # nvidia-smi needs ~0.1-0.5 s to start; samples are kept only inside the timed region
+        sampler.wait_ready()
     i = 0
     while i < W + K:
         if i == W and min_timed_s > 0 and times_w:
@@ -503,6 +511,7 @@ def run_sharded(args):
             torch.cuda.synchronize()
             if i == args.warmup and clk is not None and not e2e:
                 clk.start()
+                clk.wait_ready()
                 clk.mark(True)
             _native.launch_counter()  # reset
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

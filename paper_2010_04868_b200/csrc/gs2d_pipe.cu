@@ -87,7 +87,14 @@ constexpr int kPub = GS2P_PUB;       // IO warps publish up/downstream every kPu
 constexpr int kComputeWarps = kG * kWarpsG;
 constexpr int kPhLag = kBig * kG / kC;  // phantom chunk kl = producer chunk kl + kPhLag
 constexpr bool kClusterOK = kBig * kG % kC == 0;  // DSMEM push needs a whole-chunk phantom lag
-constexpr int kThreads = (kComputeWarps + 2) * 32;  // + loader warp + drainer warp
+#ifndef GS2P_PUBLISHER
+#define GS2P_PUBLISHER 1  // 1: a publisher warp takes the GPU-scope fence + progress store off the drainer
+#endif
+#ifndef GS2P_PUBP
+#define GS2P_PUBP 2       // publisher: chunks per publication
+#endif
+constexpr int kPubP = GS2P_PUBP;
+constexpr int kThreads = (kComputeWarps + 2 + GS2P_PUBLISHER) * 32;  // + loader, drainer (+ publisher)
 constexpr int kRows = kR + kC;       // ring rows incl. kC mirror rows (chunk reads never wrap)
 constexpr size_t kSmem = sizeof(double) * (size_t)(kG + 1) * kRows * kSlots;
 static_assert(kMu >= kC + 1 - kLam && kBig >= kC + 1, "lags too small for chunked sync");
@@ -240,6 +247,7 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
   // push to block r+1 complete
   __shared__ unsigned long long pbar[8], cbar[8], pushed[8];
   __shared__ int s_ticket;
+  __shared__ int s_drained;  // chunks the drainer has finished (publisher warp)
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   const unsigned crank = CS > 1 ? cluster_rank() : 0u;
   if (threadIdx.x == 0) {
@@ -251,6 +259,7 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
       mbar_init(&cbar[q], 1u);
       mbar_init(&pushed[q], 1u);
     }
+    s_drained = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   int n;  // block index along the chain
@@ -465,13 +474,42 @@ __global__ void __launch_bounds__(gs2p::kThreads, 1) gs2d_pipe_kernel(Gs2pArgs p
 #endif
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar[kDrainer][ks & 7]);
+#if GS2P_PUBLISHER
+      if (lane == 0) st_rel_cta(&s_drained, ks + 1);  // monotone count for the publisher warp
+#else
       if (dn_gl && ((ks + 1) % kPub == 0 || ks + 1 == nch)) {
         __threadfence();
         __syncwarp();
         if (lane == 0) st_rel_gpu(p.gprod + dn_slot, dn_tag | (unsigned long long)(lo + kC));
         if (lane == 0 && ks + 1 == kPub) TRACE(n, 4);
       }
+#endif
     }
+#if GS2P_PUBLISHER
+  } else if (wi == kComputeWarps + 2) {
+    // ============ publisher warp: GPU-scope progress for the next block ============
+    // Waits for the drainer's chunks (its global-ring writes are then visible
+    // here at CTA scope through the mbarrier's release/acquire), fences once
+    // per kPubP chunks and stores the progress with release semantics: the
+    // fence is cumulative over the drainer's writes, and the drainer never
+    // stalls on it.  Lagging behind only delays (never advances) a publication.
+    if (dn_gl) {
+      int published = 0;
+      SpinGuard guard;
+      while (published < nch) {
+        const int c = ld_acq_cta(&s_drained);  // chunks the drainer finished (monotone)
+        if (c >= published + kPubP || (c == nch && c > published)) {
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) st_rel_gpu(p.gprod + dn_slot, dn_tag | (unsigned long long)(c * kC));
+          published = c;
+        } else {
+          __nanosleep(32);
+          guard.tick();
+        }
+      }
+    }
+#endif
   } else {
 
   // ======================= compute warps =======================

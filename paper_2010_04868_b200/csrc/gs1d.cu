@@ -60,7 +60,15 @@ constexpr int kGsLag = 4;                 // position lag between adjacent lanes
 #define GS1D_CH 256
 #endif
 constexpr int kCH = GS1D_CH;              // positions per chunk
-constexpr int kSub = kCH / 32;            // 32-position unrolled sub-chunks per chunk
+#ifndef GS1D_SUB
+#define GS1D_SUB 128  // measured (config 2): 32 -> 58.0, 64 -> 62.6, 128 -> 65.5 GSt/s
+#endif
+constexpr int kSubLen = GS1D_SUB;          // positions per unrolled sub-chunk
+constexpr int kSub = kCH / kSubLen;       // unrolled sub-chunks per chunk
+static_assert(kSubLen % 32 == 0 && kCH % kSubLen == 0, "sub-chunk length");
+// the emitting lane's stores stay inside the ring only while (wlag - woff) is a
+// multiple of kSubLen; wlag of a full block is kGsLag * 32 = 128
+static_assert(kSubLen <= 128, "sub-chunk longer than the emitting lane's lag");
 constexpr int kRingCh = 4;                // ring = 4 chunks
 constexpr int kGsRing = kCH * kRingCh;    // ring positions (power of two)
 constexpr int kNB = 8;                    // mbarrier ring per warp
@@ -107,7 +115,9 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
   constexpr int kLoader = kGsWarps, kFlusher = kGsWarps + 1;
   // ring[w]: input positions of compute warp w; ring[kGsWarps]: staging of
   // the last compute warp's sweep before the flusher writes it out.
-  __shared__ __align__(16) double ring[kGsWarps + 1][kGsRing];
+  // (dynamic: (kGsWarps + 1) * kGsRing doubles, over 48 KB for long chunks)
+  extern __shared__ __align__(16) double gs_dyn[];
+  double(*ring)[kGsRing] = reinterpret_cast<double(*)[kGsRing]>(gs_dyn);
   // bar[x][k % kNB]: chunk k done by compute warp x (x < kGsWarps), loaded
   // (x = kLoader) or flushed (x = kFlusher)
   __shared__ __align__(8) unsigned long long bar[kGsWarps + 2][kNB];
@@ -128,8 +138,8 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
   // compute warps with sweeps in this block; the last one feeds the flusher
   const int nw = last_block ? (int)((p.sweeps - (long long)b * kGsWarps * 32 + 31) / 32) : kGsWarps;
   // the staging ring stores position x at (x + soff) & (R-1) so that the
-  // emitting lane's 32 stores per sub-chunk never wrap (constant offsets)
-  const int soff = last_block ? (kGsLag * ((int)((p.sweeps - 1) % 32) + 1)) & 31 : 0;
+  // emitting lane's kSubLen stores per sub-chunk never wrap (constant offsets)
+  const int soff = last_block ? (kGsLag * ((int)((p.sweeps - 1) % 32) + 1)) & (kSubLen - 1) : 0;
   auto done = [&](int x, int k) { mbar_wait_uniform(&bar[x][k % kNB], (unsigned)(k / kNB) & 1u); };
   auto signal = [&](int x, int k) {  // all lanes past their work on chunk k
     __syncwarp();
@@ -152,14 +162,14 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
         }
         __syncwarp();
       }
-      double v[kSub];
+      double v[kCH / 32];
 #pragma unroll
-      for (int s = 0; s < kSub; ++s) {
+      for (int s = 0; s < kCH / 32; ++s) {
         const int x = lo + s * 32 + lane;
         v[s] = x < hi ? __ldcg(src + x) : bnd;
       }
 #pragma unroll
-      for (int s = 0; s < kSub; ++s) ring[0][(lo + s * 32 + lane) & (kGsRing - 1)] = v[s];
+      for (int s = 0; s < kCH / 32; ++s) ring[0][(lo + s * 32 + lane) & (kGsRing - 1)] = v[s];
       signal(kLoader, k);
     }
     return;
@@ -189,7 +199,7 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
   const int lane_off = kGsLag * (lane + 1);
   const double* rin = ring[w];
   double* rout = to_staging ? ring[kGsWarps] : ring[w + 1];
-  const int woff = to_staging ? soff : 0;  // (wlag - woff) % 32 == 0
+  const int woff = to_staging ? soff : 0;  // (wlag - woff) % kSubLen == 0
   const bool writer = lane == wlane;
   // L: own previous result (new value at i-1); u0, u1, u2: old values at
   // i, i+1, i+2 (C, R, and next step's R); out: this step's result
@@ -215,12 +225,12 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
     double r0n = rin[(jb0 - 1) & (kGsRing - 1)];
 #pragma unroll 1
     for (int sub = 0; sub < kSub; ++sub) {
-      const int jb = jb0 + sub * 32;
+      const int jb = jb0 + sub * kSubLen;
       const double r0v = r0n;
-      if (sub + 1 < kSub) r0n = rin[(jb + 31) & (kGsRing - 1)];
+      if (sub + 1 < kSub) r0n = rin[(jb + kSubLen - 1) & (kGsRing - 1)];
       // steady sub-chunk: every lane's position (j - 4*(lane+1)) inside
       // [0, n) for the whole sub-chunk — no selects on the chain
-      const bool steady = jb - kShiftLane31 >= 0 && jb + 31 - kGsLag < n;
+      const bool steady = jb - kShiftLane31 >= 0 && jb + kSubLen - 1 - kGsLag < n;
       // sub-chunk bases: lane 0 reads position j-1 (only u = 0 can wrap), the
       // emitting lane writes position j - wlag (never wraps, see woff)
       const double* rb = rin + (jb & (kGsRing - 1)) - 1;
@@ -231,7 +241,7 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
         // exactly L -> DMUL -> DADD -> DADD (same products, same adds)
         double pa = __dmul_rn(p.w1, u0), pb = __dmul_rn(p.w2, u1);
 #pragma unroll
-        for (int u = 0; u < 32; ++u) {
+        for (int u = 0; u < kSubLen; ++u) {
           const double sh = __shfl_up_sync(0xffffffffu, out, 1);
           const double rv = u == 0 ? r0v : rb[u];  // same address for all lanes: broadcast
           const double sv = lane == 0 ? rv : sh;    // old(i+3)
@@ -245,8 +255,8 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
           if (writer) wb[u] = out;
         }
       } else if (steady) {
-#pragma unroll
-        for (int u = 0; u < 32; ++u) {
+#pragma unroll 32
+        for (int u = 0; u < kSubLen; ++u) {
           const double sh = __shfl_up_sync(0xffffffffu, out, 1);
           const double rv = u == 0 ? r0v : rb[u];
           const double sv = lane == 0 ? rv : sh;
@@ -258,8 +268,8 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
           if (writer) wb[u] = out;
         }
       } else {
-#pragma unroll
-        for (int u = 0; u < 32; ++u) {
+#pragma unroll 32
+        for (int u = 0; u < kSubLen; ++u) {
           const int j = jb + u;
           const double sh = __shfl_up_sync(0xffffffffu, out, 1);
           const int pos = j - 1;
@@ -326,14 +336,20 @@ int gs1d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, in
   a.bnd = st.boundary;
   auto launch = [&](auto warps_tag) {
     constexpr int W = decltype(warps_tag)::value;
+    constexpr size_t smem = sizeof(double) * (W + 1) * kGsRing;
+    auto go = [&](auto kern) {
+      // (over 48 KB with the static barriers included)
+      if (smem > 40 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kern<<<a.nblocks, (W + 2) * 32, smem, s>>>(a);
+    };
     switch (mask) {
-      case 1: gs1d_kernel<1, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
-      case 2: gs1d_kernel<2, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
-      case 3: gs1d_kernel<3, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
-      case 4: gs1d_kernel<4, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
-      case 5: gs1d_kernel<5, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
-      case 6: gs1d_kernel<6, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
-      default: gs1d_kernel<7, W><<<a.nblocks, (W + 2) * 32, 0, s>>>(a); break;
+      case 1: go(gs1d_kernel<1, W>); break;
+      case 2: go(gs1d_kernel<2, W>); break;
+      case 3: go(gs1d_kernel<3, W>); break;
+      case 4: go(gs1d_kernel<4, W>); break;
+      case 5: go(gs1d_kernel<5, W>); break;
+      case 6: go(gs1d_kernel<6, W>); break;
+      default: go(gs1d_kernel<7, W>); break;
     }
   };
   for (long long done = 0; done < steps; done += per_launch) {

@@ -10,7 +10,7 @@ from paper_2010_04868_b200.catalog import get
 from paper_2010_04868_b200.kernels._common import execute
 
 cases = {"gs2d9p": [((40, 37), 5), ((65, 130), 11), ((300, 257), 100), ((9, 300), 3), ((1000, 700), 130)],
-         "gs1d_w343": [((5000,), 257), ((70000,), 140), ((4096,), 1000)],
+         "gs1d_w343": [((5000,), 257), ((70000,), 140), ((4096,), 1000), ((3001,), 33), ((777,), 70), ((20000,), 95)],
          "heat2d": [((300, 301), 12), ((1000, 999), 48)],
          "heat1d": [((4096,), 100), ((100003,), 1000), ((2 ** 20,), 130)]}
 fam = sys.argv[1] if len(sys.argv) > 1 else "gs2d9p"

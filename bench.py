@@ -226,12 +226,21 @@ def device_time(cfg, K, W, sampler=None, fma=None, min_timed_s=0.0, algo=None):
 
 def e2e_time(cfg, K, W):
     """Public drop-in call, pinned host buffers, H2D + D2H inside the timing."""
-    from paper_2010_04868_b200 import _native, kernels
+    from paper_2010_04868_b200 import Grid, _native, kernels
 
-    g = make_grid(cfg)
+    src = make_grid(cfg)
+    # page-locked Grid storage from the library (tvs_host_alloc); registering
+    # numpy pages instead costs ~15% of duplex PCIe rate (tools/pinned_probe.py)
+    host = os.environ.get("TVS_BENCH_HOST", "alloc")
+    g = src.copy() if host == "register" else Grid(src.extents, src.halo, src.boundary, src.element_kind,
+                                                   src.vl, pinned=True)
+    if host != "register":
+        np.copyto(g.data, src.data)
+    del src
     out = g.copy()
-    _native.host_register(g.data)
-    _native.host_register(out.data)
+    if host == "register":
+        _native.host_register(g.data)
+        _native.host_register(out.data)
     fn = getattr(kernels, cfg["fn"])
     kw = {"kernel": cfg["kernel"]}
     try:
@@ -243,8 +252,9 @@ def e2e_time(cfg, K, W):
             if i >= W:
                 times.append((t1 - t0) * 1e3)
     finally:
-        _native.host_unregister(g.data)
-        _native.host_unregister(out.data)
+        if host == "register":
+            _native.host_unregister(g.data)
+            _native.host_unregister(out.data)
     nbytes = int(np.prod(cfg["extents"])) * 8
     return times, nbytes, out
 

@@ -94,6 +94,8 @@ _SIGS = {
     "tvs_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
     "tvs_host_register": (C.c_int, [_P, C.c_size_t]),
     "tvs_host_unregister": (C.c_int, [_P]),
+    "tvs_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    "tvs_host_free": (C.c_int, [_P]),
     "tvs_fnv1a64": (C.c_uint64, [_P, C.c_size_t, C.c_uint64]),
     "tvs_life_run": (C.c_int, [C.POINTER(LifeRule), C.POINTER(Layout), _P, _P, C.c_int64, C.POINTER(Exec)]),
     "tvs_life_device": (C.c_int, [C.POINTER(LifeRule), C.POINTER(Geometry), _P, _P, C.c_int64, C.POINTER(Exec), _P,
@@ -331,6 +333,38 @@ def host_register(a: np.ndarray):
 
 def host_unregister(a: np.ndarray):
     check(lib().tvs_host_unregister(a.ctypes.data), "tvs_host_unregister")
+
+
+class _HostAlloc:
+    """Owner of one tvs_host_alloc block; freed when the last array view of
+    it is collected."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        check(lib().tvs_host_alloc(nbytes, C.byref(p)), "tvs_host_alloc")
+        self.ptr, self.nbytes = p.value, nbytes
+        self._free = lib().tvs_host_free
+
+    def __del__(self):
+        if self.ptr:
+            self._free(self.ptr)
+            self.ptr = None
+
+
+def host_empty(shape, dtype=np.float64) -> np.ndarray:
+    """Uninitialised page-locked (cudaHostAlloc) numpy array."""
+    shape = tuple(int(x) for x in np.atleast_1d(shape))
+    dt = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dt.itemsize
+    owner = _HostAlloc(nbytes)
+    raw = (C.c_char * max(nbytes, 1)).from_address(owner.ptr)
+    raw._tvs_owner = owner  # the array's base keeps the allocation alive
+    return np.frombuffer(raw, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+
+
+def host_array(n: int) -> np.ndarray:
+    """1-D page-locked float64 array of n elements (tools/pinned_probe.py)."""
+    return host_empty((n,))
 
 
 def launch_counter() -> int:

@@ -150,31 +150,48 @@ static int geometry_init(int dim, const int64_t* ext, int64_t a0_off, int64_t a0
   return TVS_OK;
 }
 
+// Halo fill that touches only non-interior cells: one block per line of the
+// last axis (row) — a halo line is filled whole, an interior line only in its
+// two pads.  (The earlier element-wise version evaluated 64-bit div/mod for
+// every cell of the allocation, ~1.5 ms per 2 GB buffer ahead of the first
+// upload of the drop-in pipeline.)
 __global__ void fill_halo_kernel(double* base, tvs_geometry g, double value) {
-  const int64_t n = g.alloc_elems;
-  const int64_t last_pitch = g.dim == 1 ? g.alloc_elems : g.strides[g.dim - 2];
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    bool interior;
-    if (g.dim == 1) {
-      int64_t x = idx - kPadLast;
-      interior = x >= 0 && x < g.extents[0];
-    } else if (g.dim == 2) {
-      int64_t r = idx / last_pitch - 1, c = idx % last_pitch - kPadLast;
-      interior = r >= 0 && r < g.extents[0] && c >= 0 && c < g.extents[1];
+  if (g.dim == 1) {
+    const int64_t n = g.extents[0], pads = g.alloc_elems - n;  // kPadLast before, the rest after
+    for (int64_t c = threadIdx.x; c < pads; c += blockDim.x) base[c < kPadLast ? c : c + n] = value;
+    return;
+  }
+  const int64_t pitch = g.strides[g.dim - 2];
+  const int64_t lines = g.alloc_elems / pitch;
+  const int64_t ncols = g.extents[g.dim - 1];
+  for (int64_t l = blockIdx.x; l < lines; l += gridDim.x) {
+    bool inner;
+    if (g.dim == 2) {
+      const int64_t r = l - 1;
+      inner = r >= 0 && r < g.extents[0];
     } else {
-      int64_t p = idx / g.strides[0] - 1;
-      int64_t rem = idx % g.strides[0];
-      int64_t r = rem / g.strides[1] - 1, c = rem % g.strides[1] - kPadLast;
-      interior = p >= 0 && p < g.extents[0] && r >= 0 && r < g.extents[1] && c >= 0 && c < g.extents[2];
+      const int64_t per = g.extents[1] + 2;
+      const int64_t p = l / per - 1, r = l % per - 1;
+      inner = p >= 0 && p < g.extents[0] && r >= 0 && r < g.extents[1];
     }
-    if (!interior) base[idx] = value;
+    double* line = base + l * pitch;
+    if (!inner) {
+      for (int64_t c = threadIdx.x; c < pitch; c += blockDim.x) line[c] = value;
+    } else {
+      const int64_t right = pitch - kPadLast - ncols;
+      for (int64_t c = threadIdx.x; c < kPadLast + right; c += blockDim.x)
+        line[c < kPadLast ? c : c + ncols] = value;
+    }
   }
 }
 
 static int fill_halo(const tvs_geometry& g, double* dev, double value, cudaStream_t s) {
-  int blocks = (int)std::min<int64_t>((g.alloc_elems + 255) / 256, 148 * 16);
-  fill_halo_kernel<<<blocks, 256, 0, s>>>(dev, g, value);
+  if (g.dim == 1) {
+    fill_halo_kernel<<<1, 256, 0, s>>>(dev, g, value);
+  } else {
+    const int64_t lines = g.alloc_elems / g.strides[g.dim - 2];
+    fill_halo_kernel<<<(int)std::min<int64_t>(lines, 148 * 32), 64, 0, s>>>(dev, g, value);
+  }
   TVS_LAUNCHED("fill_halo_kernel");
   return TVS_OK;
 }
@@ -436,8 +453,16 @@ static int jacobi2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
   int rc;
   static const bool trace = getenv("TVS_E2E_TRACE") != nullptr;
   cudaEvent_t tr[4] = {};
+  std::vector<cudaEvent_t> tup, tdn;  // per-band upload / download completion (trace only)
+  std::vector<double> thost;            // host clock when band b's work was enqueued (trace only)
+  const auto h0 = std::chrono::steady_clock::now();
+  auto host_ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count(); };
   if (trace) {
     for (auto& e : tr) cudaEventCreate(&e);
+    tup.resize((rows + band - 1) / band);
+    tdn.resize(nb);
+    for (auto& e : tup) cudaEventCreate(&e);
+    for (auto& e : tdn) cudaEventCreate(&e);
     cudaEventRecord(tr[0], cs);
   }
   if ((rc = fill_halo(g, c.buf[0], st.boundary, cs))) return rc;
@@ -448,11 +473,11 @@ static int jacobi2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
   for (int b = 0; b < nb; ++b) {
     // uploads stay one band ahead of the band whose passes are enqueued next
     for (; uploaded < nup && uploaded <= b + 1; ++uploaded) {
-      if ((rc = copy_rows(g, c.buf[0], lay, const_cast<double*>(in), true, (int64_t)uploaded * band,
-                          std::min(rows, (int64_t)(uploaded + 1) * band), cs)))
-        return rc;
+      const int64_t r0 = (int64_t)uploaded * band, r1 = std::min(rows, (int64_t)(uploaded + 1) * band);
+      if ((rc = copy_rows(g, c.buf[0], lay, const_cast<double*>(in), true, r0, r1, cs))) return rc;
       TVS_CUDA(cudaEventRecord(up(uploaded), cs));
       if (trace && uploaded == nup - 1) cudaEventRecord(tr[1], cs);
+      if (trace) cudaEventRecord(tup[uploaded], cs);
     }
     cudaStream_t sb = c.bands[b];
     // pass 0 reads rows [b*band - d, (b+1)*band + d): uploads b-1 .. b+1
@@ -468,8 +493,10 @@ static int jacobi2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
     const int64_t lo = lo_of(b, K), hi = hi_of(b, K);
     if (hi > lo && (rc = copy_rows(g, result, lay, out, false, lo, hi, sb))) return rc;
     if (trace && b == 0) cudaEventRecord(tr[2], sb);
+    if (trace) cudaEventRecord(tdn[b], sb), thost.push_back(host_ms());
   }
   for (int b = 0; b < nb; ++b) TVS_CUDA(cudaStreamSynchronize(c.bands[b]));
+  const double t_sync = host_ms();
   if (trace) {
     cudaEventRecord(tr[3], cs);
     cudaStreamSynchronize(cs);
@@ -477,7 +504,16 @@ static int jacobi2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
     for (int i = 1; i < 4; ++i) cudaEventElapsedTime(&t[i], tr[0], tr[i]);
     fprintf(stderr, "[e2e] bands %d x %lld rows, K %d: uploads done %.2f ms, band0 final D2H %.2f ms, end %.2f ms\n",
             nb, (long long)band, K, t[1], t[2], t[3]);
+    for (size_t b = 0; b < tdn.size(); b += 4) {
+      float u = 0, d = 0;
+      if (b < tup.size()) cudaEventElapsedTime(&u, tr[0], tup[b]);
+      cudaEventElapsedTime(&d, tr[0], tdn[b]);
+      fprintf(stderr, "  band %3zu: up %7.2f  down %7.2f ms  (host enqueued %7.2f)\n", b, u, d, thost[b]);
+    }
+    fprintf(stderr, "  host: enqueue done %.2f ms, synchronized %.2f ms\n", thost.back(), t_sync);
     for (auto& e : tr) cudaEventDestroy(e);
+    for (auto& e : tup) cudaEventDestroy(e);
+    for (auto& e : tdn) cudaEventDestroy(e);
   }
   return TVS_OK;
 }
@@ -846,6 +882,16 @@ int tvs_host_register(void* ptr, size_t bytes) {
 }
 int tvs_host_unregister(void* ptr) {
   TVS_CUDA(cudaHostUnregister(ptr));
+  return TVS_OK;
+}
+int tvs_host_alloc(size_t bytes, void** ptr) {
+  if (!ptr) return fail(TVS_ERR_INVALID, "null argument");
+  *ptr = nullptr;
+  TVS_CUDA(cudaHostAlloc(ptr, bytes ? bytes : 1, cudaHostAllocPortable));
+  return TVS_OK;
+}
+int tvs_host_free(void* ptr) {
+  TVS_CUDA(cudaFreeHost(ptr));
   return TVS_OK;
 }
 

@@ -314,6 +314,27 @@ def test_drop_in_signatures_and_immutability(cuda_ready):
     assert r.extents == (20, 20, 20)
 
 
+@pytest.mark.parametrize("kernel,ext,steps", [("heat1d", (300001,), 40), ("heat2d", (1100, 257), 19),
+                                                ("gs2d9p", (600, 130), 7), ("heat3d", (70, 33, 40), 5)])
+def test_pinned_grids_drop_in(cuda_ready, kernel, ext, steps):
+    """Grids on tvs_host_alloc storage (page-locked) through every drop-in
+    pipeline: same results as pageable Grids, pinned outputs, halo intact."""
+    src = Grid.random(ext, seed=sum(ext) + steps)
+    g = Grid(ext, 1, pinned=True)
+    np.copyto(g.data, src.data)
+    assert g.pinned and g.copy().pinned and g.alloc_like().pinned
+    out = g.alloc_like()
+    spec = get(kernel).spec
+    execute(spec, g, steps, out=out)
+    want = cref.scalar_reference(spec, src, steps, order="lexicographic", threads=8)
+    assert np.array_equal(out.interior, want.interior)
+    assert np.all(out.data[: out.offset] == 0.0)
+    assert np.array_equal(g.data, src.data)
+    e = _native.host_empty((3, 5), np.int32)
+    e[...] = 7
+    assert e.shape == (3, 5) and int(e.sum()) == 105
+
+
 def test_plan_api_accumulates_steps(cuda_ready):
     for kernel, ext in (("heat2d", (200, 333)), ("gs1d_w343", (5000,)), ("gs2d9p", (50, 60)),
                         ("jac3d27p", (30, 20, 40))):

@@ -12,11 +12,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2010_04868_b200 import Grid, _native  # noqa: E402
 
 ext = (16384, 16384)
-g = Grid(ext, 1)
+# PINNED=1: Grids on tvs_host_alloc storage; else numpy pages + cudaHostRegister
+pinned = os.environ.get("PINNED") == "1"
+g = Grid(ext, 1, pinned=pinned)
 g.data[...] = 1.0
 o = g.alloc_like()
-_native.host_register(g.data)
-_native.host_register(o.data)
+if not pinned:
+    _native.host_register(g.data)
+    _native.host_register(o.data)
+print("pinned" if pinned else "registered")
 geo = _native.geometry(2, ext)
 n = int(geo.alloc_elems)
 d1 = torch.empty(n, dtype=torch.float64, device="cuda")

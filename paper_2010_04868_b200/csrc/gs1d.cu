@@ -61,14 +61,17 @@ constexpr int kGsLag = 4;                 // position lag between adjacent lanes
 #endif
 constexpr int kCH = GS1D_CH;              // positions per chunk
 #ifndef GS1D_SUB
-#define GS1D_SUB 128  // measured (config 2): 32 -> 58.0, 64 -> 62.6, 128 -> 65.5 GSt/s
+#define GS1D_SUB 128  // measured (config 2): 32 -> 58.0, 64 -> 62.6, 128 -> 65.5, 256 -> 58.5 GSt/s
 #endif
 constexpr int kSubLen = GS1D_SUB;          // positions per unrolled sub-chunk
 constexpr int kSub = kCH / kSubLen;       // unrolled sub-chunks per chunk
 static_assert(kSubLen % 32 == 0 && kCH % kSubLen == 0, "sub-chunk length");
-// the emitting lane's stores stay inside the ring only while (wlag - woff) is a
-// multiple of kSubLen; wlag of a full block is kGsLag * 32 = 128
-static_assert(kSubLen <= 128, "sub-chunk longer than the emitting lane's lag");
+// the emitting lane's stores use one base per 128 positions of a sub-chunk:
+// (wlag - woff) is a multiple of 128 (wlag of a full block is kGsLag * 32),
+// so each 128-store run stays inside the ring (constant offsets)
+constexpr int kWRun = kSubLen < 128 ? kSubLen : 128;
+constexpr int kWRuns = kSubLen / kWRun;
+static_assert(kSubLen <= 128 || kSubLen % 128 == 0, "sub-chunk length");
 constexpr int kRingCh = 4;                // ring = 4 chunks
 constexpr int kGsRing = kCH * kRingCh;    // ring positions (power of two)
 constexpr int kNB = 8;                    // mbarrier ring per warp
@@ -138,8 +141,8 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
   // compute warps with sweeps in this block; the last one feeds the flusher
   const int nw = last_block ? (int)((p.sweeps - (long long)b * kGsWarps * 32 + 31) / 32) : kGsWarps;
   // the staging ring stores position x at (x + soff) & (R-1) so that the
-  // emitting lane's kSubLen stores per sub-chunk never wrap (constant offsets)
-  const int soff = last_block ? (kGsLag * ((int)((p.sweeps - 1) % 32) + 1)) & (kSubLen - 1) : 0;
+  // emitting lane's stores (runs of kWRun) never wrap (constant offsets)
+  const int soff = last_block ? (kGsLag * ((int)((p.sweeps - 1) % 32) + 1)) & (kWRun - 1) : 0;
   auto done = [&](int x, int k) { mbar_wait_uniform(&bar[x][k % kNB], (unsigned)(k / kNB) & 1u); };
   auto signal = [&](int x, int k) {  // all lanes past their work on chunk k
     __syncwarp();
@@ -199,7 +202,7 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
   const int lane_off = kGsLag * (lane + 1);
   const double* rin = ring[w];
   double* rout = to_staging ? ring[kGsWarps] : ring[w + 1];
-  const int woff = to_staging ? soff : 0;  // (wlag - woff) % kSubLen == 0
+  const int woff = to_staging ? soff : 0;  // (wlag - woff) % kWRun == 0
   const bool writer = lane == wlane;
   // L: own previous result (new value at i-1); u0, u1, u2: old values at
   // i, i+1, i+2 (C, R, and next step's R); out: this step's result
@@ -234,7 +237,9 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
       // sub-chunk bases: lane 0 reads position j-1 (only u = 0 can wrap), the
       // emitting lane writes position j - wlag (never wraps, see woff)
       const double* rb = rin + (jb & (kGsRing - 1)) - 1;
-      double* wb = rout + ((jb - wlag + woff) & (kGsRing - 1));
+      double* wb[kWRuns];
+#pragma unroll
+      for (int r = 0; r < kWRuns; ++r) wb[r] = rout + ((jb + r * kWRun - wlag + woff) & (kGsRing - 1));
       if (steady && MASK == 7u) {
         // full 3-tap stencil: products w1*C and w2*R are formed a step ahead
         // from values already in registers, so the loop-carried chain is
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
           u0 = u1;
           u1 = u2;
           u2 = sv;
-          if (writer) wb[u] = out;
+          if (writer) wb[u / kWRun][u % kWRun] = out;
         }
       } else if (steady) {
 #pragma unroll 32
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
           u0 = u1;
           u1 = u2;
           u2 = sv;
-          if (writer) wb[u] = out;
+          if (writer) rout[(jb + u - wlag + woff) & (kGsRing - 1)] = out;
         }
       } else {
 #pragma unroll 32

@@ -230,77 +230,111 @@ __global__ void __launch_bounds__(32) life2d_tb_kernel(const int* __restrict__ s
 #pragma unroll
     for (int p = 0; p < kLP; ++p) F[l][p] = M[l][p] = 0u, C[l][p] = bnd;
   const int* col_base = src + origin + cl;
-  auto load_row = [&](int m, int (&r)[kLP]) {
-    const bool row_ok = m >= 0 && m < e0 && m + a0 >= 0 && m + a0 < ag;
-    const int* rp = col_base + (int64_t)m * g.s0;
-#pragma unroll
-    for (int p = 0; p < kLP; ++p) r[p] = (row_ok && !(col_out >> p & 1u)) ? __ldg(rp + p) : bnd;
-  };
   const int m_begin = r0 - D, m_end = r1 + D;
-  int pre[2][kLP];
-  load_row(m_begin, pre[0]);
-  load_row(m_begin + 1, pre[1]);
-  for (int m = m_begin; m < m_end; ++m) {
-    int in[kLP + 2];
+  // interior warp (no column outside, every loaded row and every produced
+  // level row inside the local and global range): no per-row checks or
+  // boundary selects (the same split as the fp64 2D kernel)
+  const bool any_col_out = __any_sync(0xffffffffu, col_out != 0);
+  const bool interior = !any_col_out && m_begin >= 0 && m_end + 2 <= e0 && m_begin - D + a0 >= 0 &&
+                        m_end + 1 + a0 < ag;
+  auto run = [&](auto in_tag) {
+    constexpr bool IN = decltype(in_tag)::value;
+    auto load_row = [&](int m, int (&r)[kLP]) {
+      const int* rp = col_base + (int64_t)m * g.s0;
+      if constexpr (IN) {
 #pragma unroll
-    for (int p = 0; p < kLP; ++p) in[p + 1] = pre[0][p];
+        for (int p = 0; p < kLP; ++p) r[p] = __ldg(rp + p);
+      } else {
+        const bool row_ok = m >= 0 && m < e0 && m + a0 >= 0 && m + a0 < ag;
 #pragma unroll
-    for (int p = 0; p < kLP; ++p) pre[0][p] = pre[1][p];
-    load_row(m + 2, pre[1]);
-#pragma unroll
-    for (int l = 0; l < D; ++l) {
-      // row m - l of level l (its input) arrived: finish row m - l - 1 of level l+1
-      in[0] = __shfl_up_sync(0xffffffffu, in[kLP], 1);
-      in[kLP + 1] = __shfl_down_sync(0xffffffffu, in[1], 1);
-      const int q = m - l - 1;  // row finished at level l+1
-      const bool pin_row = q + a0 < 0 || q + a0 >= ag;
-      int out[kLP];
-#pragma unroll
-      for (int p = 0; p < kLP; ++p) {
-        const unsigned rs = (unsigned)in[p] + (unsigned)in[p + 1] + (unsigned)in[p + 2];
-        const unsigned nsum = F[l][p] + rs - (unsigned)C[l][p];
-        const int v = life_rule_u(nsum, C[l][p], bmask, smask);
-        out[p] = (pin_row || (col_out >> p & 1u)) ? bnd : v;
-        F[l][p] = M[l][p] + rs;
-        M[l][p] = rs;
-        C[l][p] = in[p + 1];
+        for (int p = 0; p < kLP; ++p) r[p] = (row_ok && !(col_out >> p & 1u)) ? __ldg(rp + p) : bnd;
       }
+    };
+    int pre[2][kLP];
+    load_row(m_begin, pre[0]);
+    load_row(m_begin + 1, pre[1]);
+    for (int m = m_begin; m < m_end; ++m) {
+      int in[kLP + 2];
 #pragma unroll
-      for (int p = 0; p < kLP; ++p) in[p + 1] = out[p];
-    }
-    const int q = m - D;  // level-D row leaving
-    if (q >= r0 && q < r1) {
-      int* wp = dst + origin + (int64_t)q * g.s0 + cl;
+      for (int p = 0; p < kLP; ++p) in[p + 1] = pre[0][p];
 #pragma unroll
-      for (int p = 0; p < kLP; ++p)
-        if (store_mask >> p & 1u) wp[p] = in[p + 1];
+      for (int p = 0; p < kLP; ++p) pre[0][p] = pre[1][p];
+      load_row(m + 2, pre[1]);
+#pragma unroll
+      for (int l = 0; l < D; ++l) {
+        // row m - l of level l (its input) arrived: finish row m - l - 1 of level l+1
+        in[0] = __shfl_up_sync(0xffffffffu, in[kLP], 1);
+        in[kLP + 1] = __shfl_down_sync(0xffffffffu, in[1], 1);
+        const int q = m - l - 1;  // row finished at level l+1
+        const bool pin_row = !IN && (q + a0 < 0 || q + a0 >= ag);
+        int out[kLP];
+#pragma unroll
+        for (int p = 0; p < kLP; ++p) {
+          const unsigned rs = (unsigned)in[p] + (unsigned)in[p + 1] + (unsigned)in[p + 2];
+          const unsigned nsum = F[l][p] + rs - (unsigned)C[l][p];
+          const int v = life_rule_u(nsum, C[l][p], bmask, smask);
+          if constexpr (IN)
+            out[p] = v;
+          else
+            out[p] = (pin_row || (col_out >> p & 1u)) ? bnd : v;
+          F[l][p] = M[l][p] + rs;
+          M[l][p] = rs;
+          C[l][p] = in[p + 1];
+        }
+#pragma unroll
+        for (int p = 0; p < kLP; ++p) in[p + 1] = out[p];
+      }
+      const int q = m - D;  // level-D row leaving
+      if (q >= r0 && q < r1) {
+        int* wp = dst + origin + (int64_t)q * g.s0 + cl;
+#pragma unroll
+        for (int p = 0; p < kLP; ++p)
+          if (store_mask >> p & 1u) wp[p] = in[p + 1];
+      }
     }
-  }
+  };
+  if (interior)
+    run(std::true_type{});
+  else
+    run(std::false_type{});
 }
 
+// halo fill touching only halo lines and pads (see fill_halo_kernel, api.cu)
 __global__ void fill_halo_i32_kernel(int* base, tvs_geometry g, int value) {
-  const int64_t n = g.alloc_elems;
-  const int64_t last_pitch = g.dim == 1 ? g.alloc_elems : g.strides[g.dim - 2];
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
-    bool interior;
-    if (g.dim == 1) {
-      const int64_t x = idx - kPadLast;
-      interior = x >= 0 && x < g.extents[0];
-    } else if (g.dim == 2) {
-      const int64_t r = idx / last_pitch - 1, c = idx % last_pitch - kPadLast;
-      interior = r >= 0 && r < g.extents[0] && c >= 0 && c < g.extents[1];
+  if (g.dim == 1) {
+    const int64_t n = g.extents[0], pads = g.alloc_elems - n;  // kPadLast before, the rest after
+    for (int64_t c = threadIdx.x; c < pads; c += blockDim.x) base[c < kPadLast ? c : c + n] = value;
+    return;
+  }
+  const int64_t pitch = g.strides[g.dim - 2];
+  const int64_t lines = g.alloc_elems / pitch;
+  const int64_t ncols = g.extents[g.dim - 1];
+  for (int64_t l = blockIdx.x; l < lines; l += gridDim.x) {
+    bool inner;
+    if (g.dim == 2) {
+      inner = l - 1 >= 0 && l - 1 < g.extents[0];
     } else {
-      const int64_t p = idx / g.strides[0] - 1, rem = idx % g.strides[0];
-      const int64_t r = rem / g.strides[1] - 1, c = rem % g.strides[1] - kPadLast;
-      interior = p >= 0 && p < g.extents[0] && r >= 0 && r < g.extents[1] && c >= 0 && c < g.extents[2];
+      const int64_t per = g.extents[1] + 2;
+      const int64_t p = l / per - 1, r = l % per - 1;
+      inner = p >= 0 && p < g.extents[0] && r >= 0 && r < g.extents[1];
     }
-    if (!interior) base[idx] = value;
+    int* line = base + l * pitch;
+    if (!inner) {
+      for (int64_t c = threadIdx.x; c < pitch; c += blockDim.x) line[c] = value;
+    } else {
+      const int64_t right = pitch - kPadLast - ncols;
+      for (int64_t c = threadIdx.x; c < kPadLast + right; c += blockDim.x) line[c < kPadLast ? c : c + ncols] = value;
+    }
   }
 }
 
 static int fill_halo_i32(const tvs_geometry& g, int* dev, int value, cudaStream_t s) {
-  const int blocks = (int)std::min<int64_t>((g.alloc_elems + 255) / 256, 148 * 16);
-  fill_halo_i32_kernel<<<blocks, 256, 0, s>>>(dev, g, value);
+  if (g.dim == 1) {
+    fill_halo_i32_kernel<<<1, 256, 0, s>>>(dev, g, value);
+  } else {
+    const int64_t lines = g.alloc_elems / g.strides[g.dim - 2];
+    fill_halo_i32_kernel<<<(int)std::min<int64_t>(lines, 148 * 32), 64, 0, s>>>(dev, g, value);
+  }
   TVS_LAUNCHED("fill_halo_i32_kernel");
   return TVS_OK;
 }

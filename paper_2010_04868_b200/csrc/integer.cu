@@ -419,7 +419,7 @@ static int life_device(const tvs_life_rule& r, const tvs_geometry& g, int* src, 
   int* a = src;
   int* b = dst;
   static const int env_depth = [] {
-    const char* e = getenv("TVS_LIFE_DEPTH");  // 16384^2 B2S23: 1 597, 2 903, 4 1058, 8 1027 (spills) GCellUpd/s
+    const char* e = getenv("TVS_LIFE_DEPTH");  // 16384^2 B2S23 x 20 (interior-warp loop): 2 971, 4 1231, 8 1243 GCellUpd/s
     return e ? atoi(e) : 4;
   }();
   const int D = depth > 0 ? depth : env_depth;

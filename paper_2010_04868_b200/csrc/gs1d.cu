@@ -226,73 +226,83 @@ __global__ void __launch_bounds__((kGsWarps + 2) * 32, 1) gs1d_kernel(Gs1dArgs p
     // first input of the next sub-chunk, loaded a sub-chunk ahead (inside the
     // chunk only: position jb0 + kCH - 1 is not yet guaranteed)
     double r0n = rin[(jb0 - 1) & (kGsRing - 1)];
+    // ALL: every sub-chunk of this chunk is steady — a separate copy of the
+    // sub-chunk loop holding only the steady body (its own register
+    // allocation: no per-sub-chunk variant branch or constant reloads)
+    auto sub_loop = [&](auto all_tag) {
+      constexpr bool ALL = decltype(all_tag)::value;
 #pragma unroll 1
-    for (int sub = 0; sub < kSub; ++sub) {
-      const int jb = jb0 + sub * kSubLen;
-      const double r0v = r0n;
-      if (sub + 1 < kSub) r0n = rin[(jb + kSubLen - 1) & (kGsRing - 1)];
-      // steady sub-chunk: every lane's position (j - 4*(lane+1)) inside
-      // [0, n) for the whole sub-chunk — no selects on the chain
-      const bool steady = jb - kShiftLane31 >= 0 && jb + kSubLen - 1 - kGsLag < n;
-      // sub-chunk bases: lane 0 reads position j-1 (only u = 0 can wrap), the
-      // emitting lane writes position j - wlag (never wraps, see woff)
-      const double* rb = rin + (jb & (kGsRing - 1)) - 1;
-      double* wb[kWRuns];
+      for (int sub = 0; sub < kSub; ++sub) {
+        const int jb = jb0 + sub * kSubLen;
+        const double r0v = r0n;
+        if (sub + 1 < kSub) r0n = rin[(jb + kSubLen - 1) & (kGsRing - 1)];
+        // steady sub-chunk: every lane's position (j - 4*(lane+1)) inside
+        // [0, n) for the whole sub-chunk — no selects on the chain
+        const bool steady = ALL || (jb - kShiftLane31 >= 0 && jb + kSubLen - 1 - kGsLag < n);
+        // sub-chunk bases: lane 0 reads position j-1 (only u = 0 can wrap), the
+        // emitting lane writes position j - wlag (never wraps, see woff)
+        const double* rb = rin + (jb & (kGsRing - 1)) - 1;
+        double* wb[kWRuns];
 #pragma unroll
-      for (int r = 0; r < kWRuns; ++r) wb[r] = rout + ((jb + r * kWRun - wlag + woff) & (kGsRing - 1));
-      if (steady && MASK == 7u) {
-        // full 3-tap stencil: products w1*C and w2*R are formed a step ahead
-        // from values already in registers, so the loop-carried chain is
-        // exactly L -> DMUL -> DADD -> DADD (same products, same adds)
-        double pa = __dmul_rn(p.w1, u0), pb = __dmul_rn(p.w2, u1);
+        for (int r = 0; r < kWRuns; ++r) wb[r] = rout + ((jb + r * kWRun - wlag + woff) & (kGsRing - 1));
+        if (steady && MASK == 7u) {
+          // full 3-tap stencil: products w1*C and w2*R are formed a step ahead
+          // from values already in registers, so the loop-carried chain is
+          // exactly L -> DMUL -> DADD -> DADD (same products, same adds)
+          double pa = __dmul_rn(p.w1, u0), pb = __dmul_rn(p.w2, u1);
 #pragma unroll
-        for (int u = 0; u < kSubLen; ++u) {
-          const double sh = __shfl_up_sync(0xffffffffu, out, 1);
-          const double rv = u == 0 ? r0v : rb[u];  // same address for all lanes: broadcast
-          const double sv = lane == 0 ? rv : sh;    // old(i+3)
-          out = __dadd_rn(pb, __dadd_rn(pa, __dmul_rn(p.w0, L)));
-          pa = __dmul_rn(p.w1, u1);  // next step's C
-          pb = __dmul_rn(p.w2, u2);  // next step's R
-          L = out;
-          u0 = u1;
-          u1 = u2;
-          u2 = sv;
-          if (writer) wb[u / kWRun][u % kWRun] = out;
-        }
-      } else if (steady) {
+          for (int u = 0; u < kSubLen; ++u) {
+            const double sh = __shfl_up_sync(0xffffffffu, out, 1);
+            const double rv = u == 0 ? r0v : rb[u];  // same address for all lanes: broadcast
+            const double sv = lane == 0 ? rv : sh;    // old(i+3)
+            out = __dadd_rn(pb, __dadd_rn(pa, __dmul_rn(p.w0, L)));
+            pa = __dmul_rn(p.w1, u1);  // next step's C
+            pb = __dmul_rn(p.w2, u2);  // next step's R
+            L = out;
+            u0 = u1;
+            u1 = u2;
+            u2 = sv;
+            if (writer) wb[u / kWRun][u % kWRun] = out;
+          }
+        } else if (steady) {
 #pragma unroll 32
-        for (int u = 0; u < kSubLen; ++u) {
-          const double sh = __shfl_up_sync(0xffffffffu, out, 1);
-          const double rv = u == 0 ? r0v : rb[u];
-          const double sv = lane == 0 ? rv : sh;
-          out = gs_taps<MASK>(L, u0, u1, p.w0, p.w1, p.w2);
-          L = out;
-          u0 = u1;
-          u1 = u2;
-          u2 = sv;
-          if (writer) rout[(jb + u - wlag + woff) & (kGsRing - 1)] = out;
-        }
-      } else {
+          for (int u = 0; u < kSubLen; ++u) {
+            const double sh = __shfl_up_sync(0xffffffffu, out, 1);
+            const double rv = u == 0 ? r0v : rb[u];
+            const double sv = lane == 0 ? rv : sh;
+            out = gs_taps<MASK>(L, u0, u1, p.w0, p.w1, p.w2);
+            L = out;
+            u0 = u1;
+            u1 = u2;
+            u2 = sv;
+            if (writer) rout[(jb + u - wlag + woff) & (kGsRing - 1)] = out;
+          }
+        } else if constexpr (!ALL) {
 #pragma unroll 32
-        for (int u = 0; u < kSubLen; ++u) {
-          const int j = jb + u;
-          const double sh = __shfl_up_sync(0xffffffffu, out, 1);
-          const int pos = j - 1;
-          const double rv = rin[pos & (kGsRing - 1)];
-          const double up = (unsigned)pos < (unsigned)n ? rv : bnd;
-          const double sv = lane == 0 ? up : sh;
-          const int i = j - lane_off;
-          const double v = gs_taps<MASK>(L, u0, u1, p.w0, p.w1, p.w2);
-          out = (unsigned)i < (unsigned)n ? v : bnd;
-          L = out;
-          u0 = u1;
-          u1 = u2;
-          u2 = sv;
-          const int po = j - wlag;
-          if (writer && (unsigned)po < (unsigned)n) rout[(po + woff) & (kGsRing - 1)] = out;
+          for (int u = 0; u < kSubLen; ++u) {
+            const int j = jb + u;
+            const double sh = __shfl_up_sync(0xffffffffu, out, 1);
+            const int pos = j - 1;
+            const double rv = rin[pos & (kGsRing - 1)];
+            const double up = (unsigned)pos < (unsigned)n ? rv : bnd;
+            const double sv = lane == 0 ? up : sh;
+            const int i = j - lane_off;
+            const double v = gs_taps<MASK>(L, u0, u1, p.w0, p.w1, p.w2);
+            out = (unsigned)i < (unsigned)n ? v : bnd;
+            L = out;
+            u0 = u1;
+            u1 = u2;
+            u2 = sv;
+            const int po = j - wlag;
+            if (writer && (unsigned)po < (unsigned)n) rout[(po + woff) & (kGsRing - 1)] = out;
+          }
         }
       }
-    }
+    };
+    if (jb0 - kShiftLane31 >= 0 && jb0 + kCH - 1 - kGsLag < n)
+      sub_loop(std::true_type{});
+    else
+      sub_loop(std::false_type{});
     signal(w, ch);
   }
 }

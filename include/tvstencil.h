@@ -88,13 +88,23 @@ typedef struct tvs_layout {
   int64_t offset;
 } tvs_layout;
 
+/* tvs_exec.flags */
+#define TVS_EXEC_EMULATE_SHARDS 1 /* n_gpus shards may share devices (round
+                                     robin from `device`): the one-GPU test
+                                     form of the sharded path */
+
 typedef struct tvs_exec {
-  int32_t device;         /* CUDA ordinal */
+  int32_t device;         /* CUDA ordinal (first device of a sharded run) */
   int32_t fma_policy;     /* TVS_FMA_* */
   int32_t temporal_depth; /* 0 = auto */
   int32_t gs_order;       /* TVS_GS_* */
   int32_t algo;           /* TVS_ALGO_* */
-  int32_t reserved[3];
+  int32_t n_gpus;         /* 0/1: one GPU.  N > 1: 2D/3D Jacobi (star/box)
+                             is split into N axis-0 slabs on devices
+                             device .. device+N-1; 1D and
+                             Gauss-Seidel run on `device` ("replicas only") */
+  int32_t flags;          /* TVS_EXEC_* */
+  int32_t reserved;
 } tvs_exec;
 
 /* Device layout of one (local) block: last axis padded by 32 elements on each
@@ -133,6 +143,43 @@ int tvs_plan_last_launches(tvs_plan* p, int64_t* n);
 /* the plan's CUDA stream (cudaStream_t), e.g. for torch.cuda.ExternalStream */
 int tvs_plan_stream(tvs_plan* p, void** stream);
 int tvs_plan_destroy(tvs_plan* p);
+
+/* ---- sharded Jacobi: axis-0 slabs across GPUs ----------
+ * A shard holds the owned rows [row_begin, row_end) of a global 2D/3D grid
+ * plus `ghost` (= temporal depth) rows on each side, on one device.  A pass
+ * of up to `ghost` levels computes the owned rows and the same kernel stores
+ * the rows that are a neighbour's ghost rows straight into the neighbour's
+ * buffer through peer memory (NVLink P2P stores: the halo exchange is fused
+ * into the compute kernel).  Passes are ordered by pass counters that the
+ * neighbours write into each other's memory and stream waits
+ * (cuStreamWaitValue32) — no host synchronisation between passes.
+ * Connect shards of one process with tvs_shard_connect_local; one process
+ * per GPU exchanges tvs_shard_export handles (CUDA IPC) and calls
+ * tvs_shard_connect.  Every shard of a group must run the same step counts;
+ * upload / download only while every shard of the group is idle.
+ * Replaces nothing in the reference (no distributed path); the
+ * single-process caller shape is tiling.execute_parallel
+ * (tiling.py:347-371). */
+typedef struct tvs_shard tvs_shard;
+typedef struct tvs_shard_handle {
+  unsigned char bytes[256];
+} tvs_shard_handle;
+int tvs_shard_create(const tvs_stencil* st, int32_t dim, const int64_t global_extents[3], int32_t n_shards,
+                     int32_t index, const tvs_exec* ex, tvs_shard** out);
+int tvs_shard_info(const tvs_shard* s, int64_t* row_begin, int64_t* row_end, int32_t* ghost, int32_t* device);
+int tvs_shard_export(tvs_shard* s, tvs_shard_handle* h);
+/* left == NULL for shard 0, right == NULL for the last shard */
+int tvs_shard_connect(tvs_shard* s, const tvs_shard_handle* left, const tvs_shard_handle* right);
+int tvs_shard_connect_local(tvs_shard* s, tvs_shard* left, tvs_shard* right);
+/* host Grid of the WHOLE grid (reference layout): the shard copies its rows */
+int tvs_shard_upload(tvs_shard* s, const tvs_layout* global_lay, const double* host);
+int tvs_shard_download(tvs_shard* s, const tvs_layout* global_lay, double* host);
+int tvs_shard_run(tvs_shard* s, int64_t steps); /* async on the shard stream */
+int tvs_shard_synchronize(tvs_shard* s);
+int tvs_shard_last_ms(tvs_shard* s, float* ms);
+int tvs_shard_last_launches(tvs_shard* s, int64_t* n);
+int tvs_shard_stream(tvs_shard* s, void** stream);
+int tvs_shard_destroy(tvs_shard* s);
 
 /* ---- device path: caller-owned device buffers (halo-exchange module) ---- */
 int tvs_geometry_init(int32_t dim, const int64_t extents[3], int64_t axis0_offset, int64_t axis0_global,
@@ -209,6 +256,10 @@ int tvs_lcs_tiled(const int32_t* a, int64_t na, const int32_t* b, int64_t nb, co
                   const int64_t* wave_start, int64_t nwaves, const tvs_exec* ex, int64_t* length);
 
 /* ---- misc -------------------------------------------------------------- */
+/* Free the calling thread's cached tvs_run / tvs_lcs device buffers, streams,
+ * events and captured graphs (they are otherwise kept per thread between
+ * calls).  Thread-pool workers (tiling.py:363-367) call it before exiting. */
+int tvs_release_thread_cache(void);
 const char* tvs_last_error(void);
 int tvs_device_count(int32_t* n);
 int tvs_host_register(void* ptr, size_t bytes);   /* pin a host buffer */

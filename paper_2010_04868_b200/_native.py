@@ -22,6 +22,7 @@ TVS_JACOBI, TVS_GAUSS_SEIDEL = 0, 1
 FMA_NEVER, FMA_EXACT, FMA_ALLOW = 0, 1, 2
 GS_LEXICOGRAPHIC, GS_REFERENCE = 0, 1
 ALGO_AUTO, ALGO_NAIVE, ALGO_BLOCKED = 0, 1, 2
+EXEC_EMULATE_SHARDS = 1
 
 
 class Stencil(C.Structure):
@@ -41,7 +42,8 @@ class Layout(C.Structure):
 class Exec(C.Structure):
     _fields_ = [
         ("device", C.c_int32), ("fma_policy", C.c_int32), ("temporal_depth", C.c_int32),
-        ("gs_order", C.c_int32), ("algo", C.c_int32), ("reserved", C.c_int32 * 3),
+        ("gs_order", C.c_int32), ("algo", C.c_int32), ("n_gpus", C.c_int32), ("flags", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -58,6 +60,10 @@ class LifeRule(C.Structure):
         ("dim", C.c_int32), ("ntaps", C.c_int32), ("offsets", (C.c_int32 * 3) * 26),
         ("birth_mask", C.c_int32), ("survive_mask", C.c_int32), ("boundary", C.c_int32), ("pad_", C.c_int32),
     ]
+
+
+class ShardHandle(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 256)]
 
 
 class TileDesc(C.Structure):
@@ -111,7 +117,23 @@ _SIGS = {
                                  C.POINTER(C.c_int64), C.c_int64, C.POINTER(Exec)]),
     "tvs_lcs_tiled": (C.c_int, [_P, C.c_int64, _P, C.c_int64, C.POINTER(TileDesc), C.POINTER(C.c_int64), C.c_int64,
                                 C.POINTER(Exec), C.POINTER(C.c_int64)]),
+    "tvs_shard_create": (C.c_int, [C.POINTER(Stencil), C.c_int32, C.POINTER(C.c_int64), C.c_int32, C.c_int32,
+                                   C.POINTER(Exec), C.POINTER(_P)]),
+    "tvs_shard_info": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                 C.POINTER(C.c_int32)]),
+    "tvs_shard_export": (C.c_int, [_P, C.POINTER(ShardHandle)]),
+    "tvs_shard_connect": (C.c_int, [_P, C.POINTER(ShardHandle), C.POINTER(ShardHandle)]),
+    "tvs_shard_connect_local": (C.c_int, [_P, _P, _P]),
+    "tvs_shard_upload": (C.c_int, [_P, C.POINTER(Layout), _P]),
+    "tvs_shard_download": (C.c_int, [_P, C.POINTER(Layout), _P]),
+    "tvs_shard_run": (C.c_int, [_P, C.c_int64]),
+    "tvs_shard_synchronize": (C.c_int, [_P]),
+    "tvs_shard_last_ms": (C.c_int, [_P, C.POINTER(C.c_float)]),
+    "tvs_shard_last_launches": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "tvs_shard_stream": (C.c_int, [_P, C.POINTER(_P)]),
+    "tvs_shard_destroy": (C.c_int, [_P]),
     "tvs_launch_counter": (C.c_int64, []),
+    "tvs_release_thread_cache": (C.c_int, []),
     "tvs_version": (C.c_char_p, []),
 }
 
@@ -169,8 +191,13 @@ def fnv1a64(view, state: int) -> int:
     return int(lib().tvs_fnv1a64(buf.ctypes.data, buf.size, C.c_uint64(state)))
 
 
-def make_stencil(spec) -> Stencil:
-    """StencilSpec -> tvs_stencil, taps in ``spec.offsets()`` order."""
+def make_stencil(spec, boundary=None) -> Stencil:
+    """StencilSpec -> tvs_stencil, taps in ``spec.offsets()`` order.
+
+    ``boundary``: the Dirichlet value of every non-interior cell.  The
+    reference kernels take it from the grid, not the spec (kernels1d.py:115,
+    kernels_nd.py:90, baselines.py:113-119 read the grid's halo), so the
+    drop-ins pass ``grid.boundary``; ``spec.boundary`` is the fallback."""
     st = Stencil()
     offs = spec.offsets()
     if spec.element_kind != "float64" or spec.is_life:
@@ -185,11 +212,11 @@ def make_stencil(spec) -> Stencil:
         for d in range(3):
             st.offsets[k][d] = off[d] if d < spec.dim else 0
         st.coeffs[k] = float(spec.coefficients[off])
-    st.boundary = float(spec.boundary)
+    st.boundary = float(spec.boundary if boundary is None else boundary)
     return st
 
 
-def make_life_rule(spec) -> LifeRule:
+def make_life_rule(spec, boundary=None) -> LifeRule:
     """Life-like StencilSpec (``is_life``) -> tvs_life_rule, neighbours in
     ``spec.offsets()`` order (model.py: the box minus the centre)."""
     if not spec.is_life:
@@ -204,13 +231,14 @@ def make_life_rule(spec) -> LifeRule:
             r.offsets[k][d] = off[d] if d < spec.dim else 0
     r.birth_mask = sum(1 << int(v) for v in spec.birth)
     r.survive_mask = sum(1 << int(v) for v in spec.survive)
-    r.boundary = int(spec.boundary)
+    r.boundary = int(spec.boundary if boundary is None else boundary)
     return r
 
 
-def life_run(spec, src: np.ndarray, dst: np.ndarray, extents, offset: int, steps: int, ex: Exec) -> None:
+def life_run(spec, src: np.ndarray, dst: np.ndarray, extents, offset: int, steps: int, ex: Exec,
+             boundary=None) -> None:
     """int32 host Grid data in -> host Grid data out."""
-    rule = make_life_rule(spec)
+    rule = make_life_rule(spec, boundary)
     for a in (src, dst):
         if a.dtype != np.int32 or not a.flags.c_contiguous:
             raise ValueError("Life grid data must be a C-contiguous int32 array")
@@ -241,10 +269,13 @@ def make_layout(data: np.ndarray, extents, offset: int) -> Layout:
     return lay
 
 
-def make_exec(device=0, fma_policy=FMA_EXACT, temporal_depth=0, gs_order=GS_LEXICOGRAPHIC, algo=ALGO_AUTO) -> Exec:
+def make_exec(device=0, fma_policy=FMA_EXACT, temporal_depth=0, gs_order=GS_LEXICOGRAPHIC, algo=ALGO_AUTO,
+              n_gpus=1, emulate_shards=False) -> Exec:
     ex = Exec()
     ex.device, ex.fma_policy, ex.temporal_depth = int(device), int(fma_policy), int(temporal_depth)
     ex.gs_order, ex.algo = int(gs_order), int(algo)
+    ex.n_gpus = int(n_gpus)
+    ex.flags = EXEC_EMULATE_SHARDS if emulate_shards else 0
     return ex
 
 
@@ -254,9 +285,10 @@ def _host_array(a: np.ndarray) -> np.ndarray:
     return a
 
 
-def run(spec, src: np.ndarray, dst: np.ndarray, extents, offset: int, steps: int, ex: Exec) -> None:
+def run(spec, src: np.ndarray, dst: np.ndarray, extents, offset: int, steps: int, ex: Exec,
+        boundary=None) -> None:
     """Host Grid data in -> host Grid data out (``src is dst`` allowed)."""
-    st = make_stencil(spec)
+    st = make_stencil(spec, boundary)
     _host_array(src)
     _host_array(dst)
     lay = make_layout(src, extents, offset)
@@ -320,6 +352,88 @@ class Plan:
             pass
 
 
+class Shard:
+    """One axis-0 slab of a sharded 2D/3D Jacobi grid (``tvs_shard_*``,
+    csrc/shard.cu): ``index`` of ``n_shards``, on ``ex.device``.  Neighbours
+    are connected in-process (:meth:`connect_local`) or across processes by
+    CUDA IPC handles (:meth:`export` / :meth:`connect`); the kernels store
+    the neighbour's ghost rows straight into its buffer (fused halo
+    exchange over peer memory)."""
+
+    def __init__(self, spec, global_extents, n_shards: int, index: int, ex: Exec, boundary=None):
+        self.spec = spec
+        self.extents = tuple(int(e) for e in global_extents)
+        self._st = make_stencil(spec, boundary)
+        ext = (C.c_int64 * 3)(*(list(self.extents) + [1] * (3 - len(self.extents))))
+        h = C.c_void_p()
+        check(lib().tvs_shard_create(C.byref(self._st), len(self.extents), ext, int(n_shards), int(index),
+                                     C.byref(ex), C.byref(h)), "tvs_shard_create")
+        self._h = h
+        self.index, self.n_shards = int(index), int(n_shards)
+        r0, r1, g, dev = C.c_int64(), C.c_int64(), C.c_int32(), C.c_int32()
+        check(lib().tvs_shard_info(h, C.byref(r0), C.byref(r1), C.byref(g), C.byref(dev)), "tvs_shard_info")
+        self.rows = (int(r0.value), int(r1.value))
+        self.ghost, self.device = int(g.value), int(dev.value)
+
+    def export(self) -> bytes:
+        hd = ShardHandle()
+        check(lib().tvs_shard_export(self._h, C.byref(hd)), "tvs_shard_export")
+        return bytes(hd.bytes)
+
+    def connect(self, left: bytes | None, right: bytes | None):
+        def mk(b):
+            if b is None:
+                return None
+            hd = ShardHandle()
+            C.memmove(hd.bytes, b, len(hd.bytes))
+            return C.byref(hd)
+        check(lib().tvs_shard_connect(self._h, mk(left), mk(right)), "tvs_shard_connect")
+
+    def connect_local(self, left: "Shard | None", right: "Shard | None"):
+        check(lib().tvs_shard_connect_local(self._h, left._h if left else None, right._h if right else None),
+              "tvs_shard_connect_local")
+
+    def upload(self, data: np.ndarray, offset: int):
+        lay = make_layout(_host_array(data), self.extents, offset)
+        check(lib().tvs_shard_upload(self._h, C.byref(lay), data.ctypes.data), "tvs_shard_upload")
+
+    def download(self, data: np.ndarray, offset: int):
+        lay = make_layout(_host_array(data), self.extents, offset)
+        check(lib().tvs_shard_download(self._h, C.byref(lay), data.ctypes.data), "tvs_shard_download")
+
+    def run(self, steps: int):
+        check(lib().tvs_shard_run(self._h, int(steps)), "tvs_shard_run")
+
+    def synchronize(self):
+        check(lib().tvs_shard_synchronize(self._h), "tvs_shard_synchronize")
+
+    def last_ms(self) -> float:
+        ms = C.c_float(0)
+        check(lib().tvs_shard_last_ms(self._h, C.byref(ms)), "tvs_shard_last_ms")
+        return float(ms.value)
+
+    def last_launches(self) -> int:
+        n = C.c_int64(0)
+        check(lib().tvs_shard_last_launches(self._h, C.byref(n)), "tvs_shard_last_launches")
+        return int(n.value)
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        check(lib().tvs_shard_stream(self._h, C.byref(s)), "tvs_shard_stream")
+        return int(s.value or 0)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tvs_shard_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def geometry(dim: int, extents, axis0_offset: int = 0, axis0_global: int = 0) -> Geometry:
     g = Geometry()
     ext = (C.c_int64 * 3)(*(list(extents) + [1] * (3 - len(extents))))
@@ -365,6 +479,11 @@ def host_empty(shape, dtype=np.float64) -> np.ndarray:
 def host_array(n: int) -> np.ndarray:
     """1-D page-locked float64 array of n elements (tools/pinned_probe.py)."""
     return host_empty((n,))
+
+
+def release_thread_cache() -> None:
+    """Free this thread's cached device buffers (see tvs_release_thread_cache)."""
+    check(lib().tvs_release_thread_cache(), "tvs_release_thread_cache")
 
 
 def launch_counter() -> int:

@@ -28,6 +28,11 @@ class ExecConfig:
     fma: str = "exact"
     depth: int = 0  # temporal block depth (0 = kernel default)
     algo: str = "auto"
+    # GPUs for 2D/3D Jacobi: axis-0 slabs on devices device .. device+n-1
+    # (SURVEY.md §8e); 1D and Gauss-Seidel always run on one GPU
+    n_gpus: int = 1
+    # let the n_gpus shards share devices (round robin): the one-GPU test form
+    emulate_shards: bool = False
 
     def native(self, order: str = "lexicographic", **overrides) -> _native.Exec:
         cfg = replace(self, **{k: v for k, v in overrides.items() if v is not None})
@@ -39,7 +44,10 @@ class ExecConfig:
             raise ValueError(f"order must be one of {sorted(_ORDER)}")
         if cfg.depth < 0:
             raise ValueError("depth must be >= 0")
-        return _native.make_exec(cfg.device, _FMA[cfg.fma], cfg.depth, _ORDER[order], _ALGO[cfg.algo])
+        if cfg.n_gpus < 1:
+            raise ValueError("n_gpus must be >= 1")
+        return _native.make_exec(cfg.device, _FMA[cfg.fma], cfg.depth, _ORDER[order], _ALGO[cfg.algo],
+                                 cfg.n_gpus, cfg.emulate_shards)
 
 
 _local = threading.local()

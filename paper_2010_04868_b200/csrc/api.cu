@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -24,6 +25,9 @@
 namespace tvs {
 
 static thread_local std::string g_err;
+// bumped whenever page-locked host memory is released (tvs_host_free /
+// tvs_host_unregister): invalidates captured copy graphs in every thread
+static std::atomic<uint64_t> g_host_generation{0};
 static thread_local int64_t g_launches = 0;
 
 void set_error(const std::string& msg) { g_err = msg; }
@@ -102,10 +106,27 @@ static int validate(const tvs_stencil* st) {
 
 static int validate_exec(const tvs_exec* ex) {
   if (!ex) return fail(TVS_ERR_INVALID, "null exec");
+  if (ex->n_gpus < 0) return fail(TVS_ERR_INVALID, "n_gpus must be >= 0");
+  if (ex->flags & ~TVS_EXEC_EMULATE_SHARDS) return fail(TVS_ERR_INVALID, "unknown tvs_exec flags");
   if (ex->fma_policy < 0 || ex->fma_policy > 2) return fail(TVS_ERR_INVALID, "bad fma_policy");
   if (ex->gs_order < 0 || ex->gs_order > 1) return fail(TVS_ERR_INVALID, "bad gs_order");
   if (ex->algo < 0 || ex->algo > 2) return fail(TVS_ERR_INVALID, "bad algo");
   if (ex->temporal_depth < 0) return fail(TVS_ERR_INVALID, "bad temporal_depth");
+  return TVS_OK;
+}
+
+// Host Grid layout (grid.py:27-37) checked once, before any path is chosen:
+// every copy path (whole grid, row bands, planes, positions) stays inside
+// [0, prod(shape)) when offset >= 0 and offset + extents <= shape.
+static int validate_layout(const tvs_layout* lay, int dim) {
+  if (!lay) return fail(TVS_ERR_INVALID, "null layout");
+  if (lay->dim != dim) return fail(TVS_ERR_SIZE, "grid/stencil dimension mismatch");
+  if (lay->offset < 0) return fail(TVS_ERR_INVALID, "layout offset must be >= 0");
+  for (int d = 0; d < dim; ++d) {
+    if (lay->extents[d] < 1) return fail(TVS_ERR_SIZE, "extents must be positive");
+    if (lay->shape[d] < 1 || lay->offset + lay->extents[d] > lay->shape[d])
+      return fail(TVS_ERR_INVALID, "layout shape too small for offset + extents");
+  }
   return TVS_OK;
 }
 
@@ -236,8 +257,32 @@ static int copy_interior(const tvs_geometry& g, double* dev, const tvs_layout& l
   return TVS_OK;
 }
 
-// non-static forms for the other translation units (integer.cu)
+// field-wise stencil equality (no padding bytes compared; coefficients and
+// boundary bit for bit)
+bool same_stencil(const tvs_stencil& a, const tvs_stencil& b) {
+  if (a.dim != b.dim || a.kind != b.kind || a.ntaps != b.ntaps || a.radius != b.radius) return false;
+  if (std::memcmp(&a.boundary, &b.boundary, sizeof(double)) != 0) return false;
+  for (int k = 0; k < a.ntaps && k < TVS_MAX_TAPS; ++k) {
+    if (std::memcmp(a.offsets[k], b.offsets[k], sizeof(a.offsets[k])) != 0) return false;
+    if (std::memcmp(&a.coeffs[k], &b.coeffs[k], sizeof(double)) != 0) return false;
+  }
+  return true;
+}
+
+bool wants_shards(const tvs_stencil& st, const tvs_exec& ex) {
+  if (ex.n_gpus <= 1 || st.kind != TVS_JACOBI || ex.algo == TVS_ALGO_NAIVE) return false;
+  if (st.dim == 2) return jacobi2d_blocked_supported(st);
+  if (st.dim == 3) return jacobi3d_streaming_supported(st);
+  return false;  // 1D: one GPU ("replicas only")
+}
+
+// non-static forms for the other translation units (integer.cu, shard.cu)
+int fill_halo_api(const tvs_geometry& g, double* dev, double value, cudaStream_t s) {
+  return fill_halo(g, dev, value, s);
+}
+int validate_stencil_api(const tvs_stencil* st) { return validate(st); }
 int validate_exec_api(const tvs_exec* ex) { return validate_exec(ex); }
+int validate_layout_api(const tvs_layout* lay, int dim) { return validate_layout(lay, dim); }
 int set_device_api(int dev) { return set_device(dev); }
 int geometry_init_api(int dim, const int64_t* ext, int64_t a0_off, int64_t a0_glob, tvs_geometry* g) {
   return geometry_init(dim, ext, a0_off, a0_glob, g);
@@ -313,7 +358,7 @@ struct RunCtx {
   tvs_stencil graph1_st{};
   const void* graph1_in = nullptr;
   void* graph1_out = nullptr;
-  int64_t graph1_key[5] = {0, 0, 0, 0, 0};  // steps, band, depth, fma, buf[0]
+  int64_t graph1_key[8] = {};  // steps, band, depth, fma, buf[0], lay.offset, lay.shape[0], host generation
   ~RunCtx() { release(); }
   void release() {
     if (device >= 0) {
@@ -335,6 +380,7 @@ struct RunCtx {
   }
 };
 static thread_local RunCtx g_run;
+static thread_local ShardGroup g_group;  // tvs_run with n_gpus > 1
 
 static int ensure_ctx(RunCtx& c, int device, int dim, const int64_t* ext, int nbuf) {
   bool same = c.device == device && c.dim == dim && c.nbuf >= nbuf;
@@ -539,9 +585,22 @@ static int jacobi1d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
     }
   }
   if (band < 4 * depth) return fail(TVS_ERR_INVALID, "pipelined band shorter than four temporal blocks");
-  const int64_t key[5] = {steps, band, depth, fma ? 1 : 0, (int64_t)(uintptr_t)c.buf[0]};
-  if (c.graph1 && c.graph1_in == in && c.graph1_out == out && std::memcmp(key, c.graph1_key, sizeof(key)) == 0 &&
-      std::memcmp(&st, &c.graph1_st, sizeof(st)) == 0) {
+  auto pinned = [](const void* ptr) {
+    cudaPointerAttributes a{};
+    const bool ok = cudaPointerGetAttributes(&a, ptr) == cudaSuccess && a.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return ok;
+  };
+  // only page-locked host buffers are captured (pageable copies cannot be);
+  // checked on every call, and the key carries the host-memory generation
+  // (bumped by tvs_host_free / tvs_host_unregister), so a replay never DMAs
+  // from memory that was unpinned or reused at the same address
+  const bool use_graph = pinned(in) && pinned(out);
+  const int64_t key[8] = {steps, band, depth, fma ? 1 : 0, (int64_t)(uintptr_t)c.buf[0], lay.offset, lay.shape[0],
+                          (int64_t)g_host_generation.load()};
+  static_assert(sizeof(key) == sizeof(c.graph1_key), "graph key size");
+  if (use_graph && c.graph1 && c.graph1_in == in && c.graph1_out == out &&
+      std::memcmp(key, c.graph1_key, sizeof(key)) == 0 && same_stencil(st, c.graph1_st)) {
     TVS_CUDA(cudaGraphLaunch(c.graph1, c.stream));
     TVS_CUDA(cudaStreamSynchronize(c.stream));
     return TVS_OK;
@@ -581,14 +640,6 @@ static int jacobi1d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
     TVS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c.events.push_back(e);
   }
-  auto pinned = [](const void* ptr) {
-    cudaPointerAttributes a{};
-    const bool ok = cudaPointerGetAttributes(&a, ptr) == cudaSuccess && a.type == cudaMemoryTypeHost;
-    cudaGetLastError();
-    return ok;
-  };
-  // only page-locked host buffers are captured (pageable copies cannot be)
-  const bool use_graph = pinned(in) && pinned(out);
   if (use_graph) TVS_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   auto abort_capture = [&](int code) {
     if (!use_graph) return code;
@@ -782,6 +833,8 @@ static bool stream_value_fns(StreamValueFn* wait, StreamValueFn* write) {
   return ok;
 }
 
+bool stream_value_fns_api(StreamValueFn* wait, StreamValueFn* write) { return stream_value_fns(wait, write); }
+
 static int gs2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, const double* in, double* out,
                           int64_t steps, RunCtx& c, int64_t band) {
   StreamValueFn wait_value, write_value;
@@ -818,11 +871,11 @@ static int gs2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, const do
   TVS_CUDA(cudaStreamWaitEvent(ds, c.events[0], 0));  // counters reset before any wait reads them
   if ((rc = gs2d_pipeline(st, g, c.buf[0], steps, ks, ctr, ctr + 16))) return rc;
   // row r's final value is written by the block holding group r + steps - 1
-  constexpr int kGroupsPerBlock = 4;  // gs2p::kG
-  const int64_t nblocks = (rows + 128 - 1 + kGroupsPerBlock - 1) / kGroupsPerBlock;
+  // (block geometry from gs2d_pipe.cu itself)
+  const int64_t nblocks = gs2d_pipe_blocks(rows);
   for (int u = 0; u < nbands; ++u) {
     const int64_t r0 = (int64_t)u * band, r1 = std::min(rows, r0 + band);
-    const int64_t need = std::min<int64_t>(nblocks, (r1 - 1 + steps - 1) / kGroupsPerBlock + 1);
+    const int64_t need = std::min<int64_t>(nblocks, gs2d_pipe_blocks_for_row(r1 - 1, steps));
     const int wrc = wait_value(ds, blocks_done, (unsigned)need, 0 /* CU_STREAM_WAIT_VALUE_GEQ */);
     if (wrc != 0) return fail(TVS_ERR_CUDA, "cuStreamWaitValue32 failed (CUresult " + std::to_string(wrc) + ")");
     if ((rc = copy_rows(g, c.buf[0], lay, out, false, r0, r1, ds))) return rc;
@@ -841,6 +894,7 @@ struct tvs_plan {
   tvs_stencil st;
   tvs_exec ex;
   tvs_geometry geo;
+  ShardGroup* group = nullptr;  // n_gpus > 1: sharded plan (shard.cu)
   double* buf[2] = {nullptr, nullptr};
   int cur = 0;  // which buffer holds the current field
   cudaStream_t stream = nullptr;
@@ -857,6 +911,24 @@ int64_t tvs_launch_counter(void) {
   int64_t n = g_launches;
   g_launches = 0;
   return n;
+}
+
+int tvs_release_thread_cache(void) {
+  // the calling thread's tvs_run buffers, streams, events and captured graph
+  // plus its kernel scratch (reference ThreadPool workers: tiling.py:363-367)
+  g_run.release();
+  g_group.release();
+  for (auto& sl : g_scratch) {
+    if (!sl.ptr) continue;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(sl.device);
+    cudaFree(sl.ptr);
+    cudaSetDevice(cur);
+    sl = ScratchSlot{};
+  }
+  release_integer_cache();
+  return TVS_OK;
 }
 
 int tvs_device_count(int32_t* n) {
@@ -881,6 +953,7 @@ int tvs_host_register(void* ptr, size_t bytes) {
   return TVS_OK;
 }
 int tvs_host_unregister(void* ptr) {
+  g_host_generation.fetch_add(1);
   TVS_CUDA(cudaHostUnregister(ptr));
   return TVS_OK;
 }
@@ -891,6 +964,7 @@ int tvs_host_alloc(size_t bytes, void** ptr) {
   return TVS_OK;
 }
 int tvs_host_free(void* ptr) {
+  g_host_generation.fetch_add(1);
   TVS_CUDA(cudaFreeHost(ptr));
   return TVS_OK;
 }
@@ -908,11 +982,13 @@ int tvs_fill_halo(const tvs_geometry* g, double* dev, double value, void* stream
 
 int tvs_upload(const tvs_geometry* g, double* dev, const tvs_layout* lay, const double* host, void* stream) {
   if (!g || !dev || !lay || !host) return fail(TVS_ERR_INVALID, "null argument");
+  if (int rc = validate_layout(lay, g->dim)) return rc;
   return copy_interior(*g, dev, *lay, const_cast<double*>(host), true, (cudaStream_t)stream);
 }
 
 int tvs_download(const tvs_geometry* g, const double* dev, const tvs_layout* lay, double* host, void* stream) {
   if (!g || !dev || !lay || !host) return fail(TVS_ERR_INVALID, "null argument");
+  if (int rc = validate_layout(lay, g->dim)) return rc;
   return copy_interior(*g, const_cast<double*>(dev), *lay, host, false, (cudaStream_t)stream);
 }
 
@@ -966,9 +1042,20 @@ int tvs_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, doub
   if (rc) return rc;
   if ((rc = validate_exec(ex))) return rc;
   if (!lay || !in || !out) return fail(TVS_ERR_INVALID, "null argument");
-  if (lay->dim != st->dim) return fail(TVS_ERR_SIZE, "grid/stencil dimension mismatch");
+  if ((rc = validate_layout(lay, st->dim))) return rc;
   if (steps < 0) return fail(TVS_ERR_INVALID, "steps must be >= 0");
   if ((rc = set_device(ex->device))) return rc;
+  if (wants_shards(*st, *ex) && steps > 0) {
+    // axis-0 slabs on n_gpus devices, each uploading / downloading its own
+    // rows over its own PCIe link (shard.cu)
+    if (!g_group.matches(*st, st->dim, lay->extents, *ex) &&
+        (rc = g_group.create(*st, st->dim, lay->extents, *ex)))
+      return rc;
+    if ((rc = g_group.upload(*lay, in))) return rc;
+    if ((rc = g_group.run(steps))) return rc;
+    if ((rc = g_group.download(*lay, out))) return rc;
+    return g_group.synchronize();
+  }
   const bool gs = st->kind == TVS_GAUSS_SEIDEL;
   if ((rc = ensure_ctx(g_run, ex->device, st->dim, lay->extents, gs ? 1 : 2))) return rc;
   RunCtx& c = g_run;
@@ -992,7 +1079,7 @@ int tvs_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, doub
   }
   if (gs) {
     const int64_t band = band_rows_default();
-    if (band > 0 && st->dim == 2 && steps > 0 && steps <= 128 && ex->algo != TVS_ALGO_NAIVE &&
+    if (band > 0 && st->dim == 2 && steps > 0 && steps <= gs2d_pipe_max_sweeps() && ex->algo != TVS_ALGO_NAIVE &&
         ex->gs_order == TVS_GS_LEXICOGRAPHIC && gs2d_pipe_supported(*st) && c.geo.extents[0] >= 4 * band) {
       rc = gs2d_pipelined(*st, *lay, in, out, steps, c, band);
       if (rc != TVS_ERR_UNSUPPORTED) return rc;  // no stream memory operations: plain path below
@@ -1025,6 +1112,17 @@ int tvs_plan_create(const tvs_stencil* st, int32_t dim, const int64_t extents[3]
   tvs_plan* p = new tvs_plan();
   p->st = *st;
   p->ex = *ex;
+  if (wants_shards(*st, *ex)) {
+    p->group = new ShardGroup();
+    if ((rc = p->group->create(*st, dim, extents, *ex))) {
+      delete p->group;
+      delete p;
+      return rc;
+    }
+    geometry_init(dim, extents, 0, extents[0], &p->geo);  // the global geometry (layout checks)
+    *out = p;
+    return TVS_OK;
+  }
   if ((rc = geometry_init(dim, extents, 0, extents[0], &p->geo))) {
     delete p;
     return rc;
@@ -1049,6 +1147,8 @@ int tvs_plan_create(const tvs_stencil* st, int32_t dim, const int64_t extents[3]
 
 int tvs_plan_upload(tvs_plan* p, const tvs_layout* lay, const double* host) {
   if (!p || !lay || !host) return fail(TVS_ERR_INVALID, "null argument");
+  if (int rc = validate_layout(lay, p->geo.dim)) return rc;
+  if (p->group) return p->group->upload(*lay, host);
   TVS_CUDA(cudaSetDevice(p->ex.device));
   p->cur = 0;
   return copy_interior(p->geo, p->buf[0], *lay, const_cast<double*>(host), true, p->stream);
@@ -1056,6 +1156,11 @@ int tvs_plan_upload(tvs_plan* p, const tvs_layout* lay, const double* host) {
 
 int tvs_plan_download(tvs_plan* p, const tvs_layout* lay, double* host) {
   if (!p || !lay || !host) return fail(TVS_ERR_INVALID, "null argument");
+  if (int rc = validate_layout(lay, p->geo.dim)) return rc;
+  if (p->group) {
+    if (int rc = p->group->download(*lay, host)) return rc;
+    return p->group->synchronize();
+  }
   TVS_CUDA(cudaSetDevice(p->ex.device));
   return copy_interior(p->geo, p->buf[p->cur], *lay, host, false, p->stream);
 }
@@ -1063,6 +1168,11 @@ int tvs_plan_download(tvs_plan* p, const tvs_layout* lay, double* host) {
 int tvs_plan_run(tvs_plan* p, int64_t steps) {
   if (!p) return fail(TVS_ERR_INVALID, "null plan");
   if (steps < 0) return fail(TVS_ERR_INVALID, "steps must be >= 0");
+  if (p->group) {
+    const int rc = p->group->run(steps);
+    p->last_launches = p->group->launches;
+    return rc;
+  }
   TVS_CUDA(cudaSetDevice(p->ex.device));
   int64_t before = g_launches;
   TVS_CUDA(cudaEventRecord(p->ev0, p->stream));
@@ -1082,12 +1192,14 @@ int tvs_plan_run(tvs_plan* p, int64_t steps) {
 
 int tvs_plan_synchronize(tvs_plan* p) {
   if (!p) return fail(TVS_ERR_INVALID, "null plan");
+  if (p->group) return p->group->synchronize();
   TVS_CUDA(cudaStreamSynchronize(p->stream));
   return TVS_OK;
 }
 
 int tvs_plan_last_ms(tvs_plan* p, float* ms) {
   if (!p || !ms) return fail(TVS_ERR_INVALID, "null argument");
+  if (p->group) return p->group->last_ms(ms);  // lead stream: after every shard's last pass
   TVS_CUDA(cudaEventSynchronize(p->ev1));
   TVS_CUDA(cudaEventElapsedTime(ms, p->ev0, p->ev1));
   return TVS_OK;
@@ -1101,12 +1213,18 @@ int tvs_plan_last_launches(tvs_plan* p, int64_t* n) {
 
 int tvs_plan_stream(tvs_plan* p, void** stream) {
   if (!p || !stream) return fail(TVS_ERR_INVALID, "null argument");
+  if (p->group) return tvs_shard_stream(p->group->shards[0], stream);  // the lead stream
   *stream = (void*)p->stream;
   return TVS_OK;
 }
 
 int tvs_plan_destroy(tvs_plan* p) {
   if (!p) return TVS_OK;
+  if (p->group) {
+    delete p->group;
+    delete p;
+    return TVS_OK;
+  }
   cudaSetDevice(p->ex.device);
   if (p->stream) cudaStreamSynchronize(p->stream);
   for (auto& b : p->buf)

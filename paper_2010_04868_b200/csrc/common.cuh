@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/tvstencil.h"
 
@@ -37,6 +38,35 @@ inline Geo make_geo(const tvs_geometry& g) {
   o.a0_off = g.axis0_offset;
   o.a0_glob = g.axis0_global;
   return o;
+}
+
+// Sharded Jacobi (shard.cu): a pass also stores the output
+// axis-0 rows that are a neighbour shard's ghost rows straight into that
+// shard's next-input buffer — peer memory over NVLink (the same device when
+// shards are emulated on one GPU).  The halo exchange therefore happens
+// inside the compute kernel, row by row as rows are finished, with no
+// separate copy or collective.  Neighbours share strides and origin, so a
+// row's element offset in the peer buffer is its local offset + shift.
+struct Mirror {
+  double* p[2];          // neighbour's destination buffer (nullptr = none)
+  int64_t lo[2], hi[2];  // local axis-0 rows [lo, hi) that are its ghosts
+  int64_t shift[2];      // element offset (peer row - local row) * stride
+};
+// f(base) for the local destination and for every neighbour buffer whose
+// ghost range holds local row q (base + the row's local element offset is
+// the target).  Not unrolled: the caller's store code exists once, so the
+// mirror adds no live registers to the kernel's main loop.
+template <class F>
+__device__ __forceinline__ void for_each_dst(double* dst, const Mirror& m, int64_t q, F&& f) {
+#pragma unroll 1
+  for (int k = -1; k < 2; ++k) {
+    double* b = dst;
+    if (k >= 0) {
+      if (m.p[k] == nullptr || q < m.lo[k] || q >= m.hi[k]) continue;
+      b = m.p[k] + m.shift[k];
+    }
+    f(b);
+  }
 }
 
 // Tap list in evaluation order, with linear element offsets precomputed for
@@ -187,6 +217,8 @@ void count_launch(int64_t n = 1);
 
 // api.cu helpers shared with integer.cu
 int validate_exec_api(const tvs_exec* ex);
+int validate_layout_api(const tvs_layout* lay, int dim);
+void release_integer_cache();
 int set_device_api(int dev);
 int geometry_init_api(int dim, const int64_t* ext, int64_t a0_off, int64_t a0_glob, tvs_geometry* g);
 
@@ -207,7 +239,9 @@ bool jacobi2d_blocked_supported(const tvs_stencil& st);
 // pipelined host path
 int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
                      int depth, bool fma, cudaStream_t s, int64_t row_lo = 0, int64_t row_hi = -1,
-                     int seg_rows = 0);
+                     int seg_rows = 0, const Mirror* mir = nullptr);
+// blocks (warps) one jacobi2d_blocked launch over `rows` rows would use
+int64_t jacobi2d_tasks(int64_t rows, int64_t cols, int depth, int seg_rows);
 int jacobi2d_band_rows();
 int jacobi2d_max_depth();
 int jacobi2d_default_depth();
@@ -216,16 +250,45 @@ int jacobi3d_max_depth();
 int jacobi3d_default_depth();
 // axis-0 planes [plo, phi) only when given, `seg` output planes per block
 int jacobi3d_blocked2(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, bool fma,
-                      cudaStream_t s, int64_t plo = 0, int64_t phi = -1, int seg = 0);
+                      cudaStream_t s, int64_t plo = 0, int64_t phi = -1, int seg = 0, const Mirror* mir = nullptr);
 int jacobi3d_streaming(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, bool fma,
-                       cudaStream_t s, int64_t plo = 0, int64_t phi = -1, int seg = 0);
+                       cudaStream_t s, int64_t plo = 0, int64_t phi = -1, int seg = 0, const Mirror* mir = nullptr);
 int gs1d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s);
 bool gs2d_pipe_supported(const tvs_stencil& st);
 // rows_ready / blocks_done: drop-in pipeline hooks (see api.cu), single pass only
 int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s,
                   const unsigned* rows_ready = nullptr, unsigned* blocks_done = nullptr);
+int64_t gs2d_pipe_blocks(int64_t rows);
+int64_t gs2d_pipe_blocks_for_row(int64_t row, int64_t steps);
+int gs2d_pipe_max_sweeps();
 int gs_wavefront(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, int order,
                  cudaStream_t s);
+
+// In-process group of shards (shard.cu): tvs_run / tvs_plan with n_gpus > 1.
+struct ShardGroup {
+  std::vector<tvs_shard*> shards;
+  std::vector<int> shards_dev;
+  std::vector<cudaEvent_t> done_ev;
+  cudaEvent_t lead_ev0 = nullptr, lead_ev1 = nullptr;
+  int lead_device = 0;
+  int64_t launches = 0;
+  tvs_stencil st_{};
+  tvs_exec ex_{};
+  int dim_ = 0;
+  int64_t ext_[3] = {0, 0, 0};
+  ~ShardGroup();
+  void release();
+  int create(const tvs_stencil& st, int dim, const int64_t* ext, const tvs_exec& ex);
+  bool matches(const tvs_stencil& st, int dim, const int64_t* ext, const tvs_exec& ex) const;
+  int upload(const tvs_layout& lay, const double* host);
+  int download(const tvs_layout& lay, double* host);
+  int run(int64_t steps);
+  int synchronize();
+  int last_ms(float* ms);
+  int cur_all() const;
+};
+// does tvs_exec ask for (and the stencil allow) a sharded run?
+bool wants_shards(const tvs_stencil& st, const tvs_exec& ex);
 
 // scratch device memory owned by the calling thread (grown on demand)
 void* scratch(size_t bytes, int slot);

@@ -732,6 +732,16 @@ bool gs2d_pipe_supported(const tvs_stencil& st) {
   return m == 0x1FFu || m == kStar;
 }
 
+// Drop-in pipeline hooks (api.cu gs2d_pipelined): the number of blocks one
+// pass publishes on `blocks_done`, and how many must have exited before row
+// `row` holds its final value (group row + steps - 1 is the last writer).
+// Derived from the kernel's own constants so a -DGS2P_KG build stays correct.
+int64_t gs2d_pipe_blocks(int64_t rows) { return (rows + gs2p::kLanes - 1 + gs2p::kG - 1) / gs2p::kG; }
+int64_t gs2d_pipe_blocks_for_row(int64_t row, int64_t steps) {
+  return std::min(gs2d_pipe_blocks(row + 1), (row + steps - 1) / gs2p::kG + 1);
+}
+int gs2d_pipe_max_sweeps() { return gs2p::kLanes; }
+
 int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, cudaStream_t s,
                   const unsigned* rows_ready, unsigned* blocks_done) {
   using namespace gs2p;

@@ -653,6 +653,20 @@ struct LcsWork {
 };
 static thread_local LcsWork g_lcs;
 
+// tvs_release_thread_cache: the calling thread's LCS workspace
+void release_integer_cache() {
+  if (g_lcs.buf) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(g_lcs.device);
+    cudaFree(g_lcs.buf);
+    cudaSetDevice(cur);
+  }
+  g_lcs.buf = nullptr;
+  g_lcs.bytes = 0;
+  g_lcs.device = -1;
+}
+
 static int lcs_device(const int* a, int na, const int* b, int nb, int* result_dev, cudaStream_t s) {
   if (na == 0 || nb == 0) {
     TVS_CUDA(cudaMemsetAsync(result_dev, 0, sizeof(int), s));
@@ -731,7 +745,7 @@ int tvs_life_run(const tvs_life_rule* r, const tvs_layout* lay, const int32_t* i
   if (rc) return rc;
   if ((rc = validate_exec_api(ex))) return rc;
   if (!lay || !in || !out) return fail(TVS_ERR_INVALID, "null argument");
-  if (lay->dim != r->dim) return fail(TVS_ERR_SIZE, "grid/rule dimension mismatch");
+  if ((rc = validate_layout_api(lay, r->dim))) return rc;
   if (steps < 0) return fail(TVS_ERR_INVALID, "steps must be >= 0");
   if ((rc = set_device_api(ex->device))) return rc;
   tvs_geometry g;

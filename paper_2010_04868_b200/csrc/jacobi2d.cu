@@ -92,7 +92,8 @@ template <unsigned MASK, int D, bool FMA, int kP2>
 __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __restrict__ src,
                                                                 double* __restrict__ dst, Geo g, int64_t origin,
                                                                 Coeff9 cf, double bnd, int64_t n_strips,
-                                                                int64_t n_tasks, int64_t row_lo, int64_t row_hi, int seg_rows) {
+                                                                int64_t n_tasks, int64_t row_lo, int64_t row_hi, int seg_rows,
+                                                                Mirror mir) {
   constexpr int U = 32 * kP2 - 2 * D;  // useful columns per strip
   const double(&c)[9] = cf.c;          // constant-bank operands
 
@@ -171,10 +172,13 @@ __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __
       }
       const int q = m - D;  // level-D row leaving
       if (q >= r0 && q < r1) {
-        double* wp = dst + origin + (int64_t)q * g.s0 + cl;
+        // local row, plus the neighbour's ghost row when sharded
+        for_each_dst(dst, mir, q, [&](double* base) {
+          double* wp = base + origin + (int64_t)q * g.s0 + cl;
 #pragma unroll
-        for (int p = 0; p < kP2; ++p)
-          if (store_mask >> p & 1u) wp[p] = in[p + 1];
+          for (int p = 0; p < kP2; ++p)
+            if (store_mask >> p & 1u) wp[p] = in[p + 1];
+        });
       }
     };
     if constexpr (IN) {
@@ -324,53 +328,62 @@ int jacobi2d_default_depth() { return 8; }  // measured best (config 3, P = 3: D
 template <unsigned MASK, int D, int P>
 static void launch2d_d(bool fma, unsigned blocks, cudaStream_t s, const double* src, double* dst, const Geo& geo,
                        int64_t origin, const Coeff9& cf, double bnd, int64_t ns, int64_t nt, int64_t lo, int64_t hi,
-                       int seg_rows) {
+                       int seg_rows, const Mirror& mir) {
   if (fma)
-    jacobi2d_kernel<MASK, D, true, P><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows);
+    jacobi2d_kernel<MASK, D, true, P><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows, mir);
   else
-    jacobi2d_kernel<MASK, D, false, P><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows);
+    jacobi2d_kernel<MASK, D, false, P><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows, mir);
 }
 
 // rows [row_lo, row_hi) of the grid (any band; the
 // whole grid by default): one row band of the pipelined host path
 template <unsigned MASK, int D>
 static void launch2d_one(bool fma, cudaStream_t s, const double* src, double* dst, const Geo& geo, int64_t origin,
-                         const Coeff9& cf, double bnd, int64_t row_lo, int64_t row_hi, int seg_rows) {
+                         const Coeff9& cf, double bnd, int64_t row_lo, int64_t row_hi, int seg_rows,
+                         const Mirror& mir) {
   // columns per lane: registers grow as 2 * P * D accumulators; P = 3 at
   // D = 5..8 keeps 12 warps/SM at D = 8 (168 registers) where P = 4 held 9
   // (config 3: D = 8 P = 4 1596, P = 3 1723 GSt/s; D > 8 at P = 3 is slower)
-  constexpr int P = D <= 4 ? 4 : (D <= 8 ? 3 : 2);
+  constexpr int P = D <= 4 ? 4 : (D <= 8 ? 3 : 2);  // = lane_cols(D)
   const int64_t U = 32 * P - 2 * D;
   const int64_t ns = (geo.e1 + U - 1) / U;
   const int64_t nseg = (row_hi - row_lo + seg_rows - 1) / seg_rows;
   const int64_t nt = ns * nseg;
   const unsigned blocks = (unsigned)((nt + kWarps2 - 1) / kWarps2);
-  launch2d_d<MASK, D, P>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt, row_lo, row_hi, seg_rows);
+  launch2d_d<MASK, D, P>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt, row_lo, row_hi, seg_rows, mir);
 }
 
 template <unsigned MASK>
 static void launch2d(int depth, bool fma, cudaStream_t s, const double* src, double* dst, const Geo& geo,
-                     int64_t origin, const Coeff9& cf, double bnd, int64_t lo, int64_t hi, int seg) {
+                     int64_t origin, const Coeff9& cf, double bnd, int64_t lo, int64_t hi, int seg, const Mirror& mir) {
   switch (depth) {
-    case 1: launch2d_one<MASK, 1>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
-    case 2: launch2d_one<MASK, 2>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
-    case 3: launch2d_one<MASK, 3>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
-    case 4: launch2d_one<MASK, 4>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
-    case 5: launch2d_one<MASK, 5>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
-    case 6: launch2d_one<MASK, 6>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
-    case 7: launch2d_one<MASK, 7>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
-    case 8: launch2d_one<MASK, 8>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
-    case 9: launch2d_one<MASK, 9>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
-    case 10: launch2d_one<MASK, 10>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
-    case 11: launch2d_one<MASK, 11>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
-    default: launch2d_one<MASK, 12>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg); break;
+    case 1: launch2d_one<MASK, 1>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 2: launch2d_one<MASK, 2>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 3: launch2d_one<MASK, 3>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 4: launch2d_one<MASK, 4>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 5: launch2d_one<MASK, 5>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 6: launch2d_one<MASK, 6>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 7: launch2d_one<MASK, 7>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 8: launch2d_one<MASK, 8>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 9: launch2d_one<MASK, 9>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 10: launch2d_one<MASK, 10>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 11: launch2d_one<MASK, 11>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    default: launch2d_one<MASK, 12>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
   }
 }
 
 int jacobi2d_band_rows() { return kRowsSeg; }
 
+static int lane_cols(int depth) { return depth <= 4 ? 4 : (depth <= 8 ? 3 : 2); }  // P of launch2d_one
+
+int64_t jacobi2d_tasks(int64_t rows, int64_t cols, int depth, int seg_rows) {
+  const int64_t U = 32 * lane_cols(depth) - 2 * depth;
+  if (seg_rows <= 0) seg_rows = kRowsSeg;
+  return (cols + U - 1) / U * ((rows + seg_rows - 1) / seg_rows);
+}
+
 int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, int depth,
-                     bool fma, cudaStream_t s, int64_t row_lo, int64_t row_hi, int seg_rows) {
+                     bool fma, cudaStream_t s, int64_t row_lo, int64_t row_hi, int seg_rows, const Mirror* mir) {
   Coeff9 cf;
   const unsigned mask = slots2d(st, cf);
   if ((mask != kStar5 && mask != kBox9) || depth < 1 || depth > kMaxD2)
@@ -380,10 +393,11 @@ int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double*
   if (row_lo < 0 || row_hi > g.extents[0] || row_lo >= row_hi)
     return fail(TVS_ERR_INVALID, "jacobi2d_blocked: row band");
   const Geo geo = make_geo(g);
+  const Mirror m = mir ? *mir : Mirror{};
   if (mask == kStar5)
-    launch2d<kStar5>(depth, fma, s, src, dst, geo, g.origin, cf, st.boundary, row_lo, row_hi, seg_rows);
+    launch2d<kStar5>(depth, fma, s, src, dst, geo, g.origin, cf, st.boundary, row_lo, row_hi, seg_rows, m);
   else
-    launch2d<kBox9>(depth, fma, s, src, dst, geo, g.origin, cf, st.boundary, row_lo, row_hi, seg_rows);
+    launch2d<kBox9>(depth, fma, s, src, dst, geo, g.origin, cf, st.boundary, row_lo, row_hi, seg_rows, m);
   TVS_LAUNCHED("jacobi2d_kernel");
   return TVS_OK;
 }

@@ -77,7 +77,7 @@ template <unsigned MASK, bool FMA>
 __global__ void __launch_bounds__(kThreads3) jacobi3d_kernel(const double* __restrict__ src,
                                                             double* __restrict__ dst, Geo g, int64_t origin,
                                                             Coeff27 cf, double bnd, int64_t plo, int64_t phi,
-                                                            int seg) {
+                                                            int seg, Mirror mir) {
   constexpr bool G0 = has_plane<MASK>(0), G1 = has_plane<MASK>(1), G2 = has_plane<MASK>(2);
   __shared__ __align__(16) double tile[kBufs3][kSH][kSW];
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -146,12 +146,15 @@ __global__ void __launch_bounds__(kThreads3) jacobi3d_kernel(const double* __res
     if (q >= p0 && q < p1 && x_ok) {
       const int64_t gq = q + g.a0_off;
       const bool pin = gq < 0 || gq >= g.a0_glob;
-      double* op = dst + origin + q * g.s0 + x;
+      // local plane, plus the neighbour's ghost plane when sharded
+      for_each_dst(dst, mir, q, [&](double* b) {
+        double* op = b + origin + q * g.s0 + x;
 #pragma unroll
-      for (int r = 0; r < kRY; ++r) {
-        const int64_t y = y0 + ty * kRY + r;
-        if (y < g.e1) op[y * g.s1] = pin ? bnd : out[r];
-      }
+        for (int r = 0; r < kRY; ++r) {
+          const int64_t y = y0 + ty * kRY + r;
+          if (y < g.e1) op[y * g.s1] = pin ? bnd : out[r];
+        }
+      });
     }
   }
 }
@@ -214,7 +217,7 @@ template <unsigned MASK, bool FMA>
 __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double* __restrict__ src,
                                                                    double* __restrict__ dst, Geo g, int64_t origin,
                                                                    Coeff27 cf, double bnd, int64_t plo,
-                                                                   int64_t phi, int seg) {
+                                                                   int64_t phi, int seg, Mirror mir) {
   extern __shared__ __align__(16) double tb_smem[];
   double* l0 = tb_smem;                       // 3 staged input planes
   double* l1 = tb_smem + 3 * kTBR * kTBP;     // 2 level-1 planes (frame at +1,+1)
@@ -297,12 +300,15 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
       if (q2 >= p0 && q2 < p1) {
         const int64_t gq2 = q2 + g.a0_off;
         const bool pin = gq2 < 0 || gq2 >= g.a0_glob;
-        double* op = dst + origin + q2 * g.s0 + (y0 - 1 + w * kRY) * g.s1 + (x0 - 1 + lane);
+        // local plane, plus the neighbour's ghost plane when sharded
+        for_each_dst(dst, mir, q2, [&](double* b) {
+          double* op = b + origin + q2 * g.s0 + (y0 - 1 + w * kRY) * g.s1 + (x0 - 1 + lane);
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+          for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int r = 0; r < kRY; ++r)
-            if (store_ok >> (h * kRY + r) & 1u) op[r * g.s1 + 32 * h] = pin ? bnd : out[h][r];
+            for (int r = 0; r < kRY; ++r)
+              if (store_ok >> (h * kRY + r) & 1u) op[r * g.s1 + 32 * h] = pin ? bnd : out[h][r];
+        });
       }
     }
   }
@@ -333,21 +339,22 @@ int jacobi3d_default_depth() { return 2; }
 
 template <unsigned MASK, bool FMA>
 static int launch_tb(const Geo& geo, const tvs_geometry& g, const double* src, double* dst, const Coeff27& cf,
-                     double bnd, cudaStream_t s, int64_t plo, int64_t phi, int seg) {
+                     double bnd, cudaStream_t s, int64_t plo, int64_t phi, int seg, const Mirror& mir) {
   // per device context; a host-side attribute write, no synchronisation
   TVS_CUDA(cudaFuncSetAttribute(jacobi3d_tb_kernel<MASK, FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kTBSmem));
   const dim3 block(kTX3, kTYT);
   const dim3 grid((unsigned)((geo.e2 + kTBOX - 1) / kTBOX), (unsigned)((geo.e1 + kTBOY - 1) / kTBOY),
                   (unsigned)((phi - plo + seg - 1) / seg));
-  jacobi3d_tb_kernel<MASK, FMA><<<grid, block, kTBSmem, s>>>(src, dst, geo, g.origin, cf, bnd, plo, phi, seg);
+  jacobi3d_tb_kernel<MASK, FMA><<<grid, block, kTBSmem, s>>>(src, dst, geo, g.origin, cf, bnd, plo, phi, seg, mir);
   TVS_LAUNCHED("jacobi3d_tb_kernel");
   return TVS_OK;
 }
 
 // Two time levels in one pass (K4b): src -> dst after 2 steps.
 int jacobi3d_blocked2(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, bool fma,
-                      cudaStream_t s, int64_t plo, int64_t phi, int seg) {
+                      cudaStream_t s, int64_t plo, int64_t phi, int seg, const Mirror* mir) {
+  const Mirror m = mir ? *mir : Mirror{};
   Coeff27 cf;
   const unsigned mask = slots3d(st, cf);
   const Geo geo = make_geo(g);
@@ -355,16 +362,17 @@ int jacobi3d_blocked2(const tvs_stencil& st, const tvs_geometry& g, const double
   if (seg <= 0) seg = kTBPlanesSeg;
   if (plo < 0 || phi > geo.e0 || plo >= phi) return fail(TVS_ERR_INVALID, "jacobi3d_blocked2: plane range");
   if (mask == kBox27)
-    return fma ? launch_tb<kBox27, true>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg)
-               : launch_tb<kBox27, false>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg);
+    return fma ? launch_tb<kBox27, true>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m)
+               : launch_tb<kBox27, false>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m);
   if (mask == kStar7)
-    return fma ? launch_tb<kStar7, true>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg)
-               : launch_tb<kStar7, false>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg);
+    return fma ? launch_tb<kStar7, true>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m)
+               : launch_tb<kStar7, false>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m);
   return fail(TVS_ERR_UNSUPPORTED, "jacobi3d_blocked2: tap set");
 }
 
 int jacobi3d_streaming(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, bool fma,
-                       cudaStream_t s, int64_t plo, int64_t phi, int seg) {
+                       cudaStream_t s, int64_t plo, int64_t phi, int seg, const Mirror* mir) {
+  const Mirror m = mir ? *mir : Mirror{};
   Coeff27 cf;
   const unsigned mask = slots3d(st, cf);
   if (mask != kBox27 && mask != kStar7) return fail(TVS_ERR_UNSUPPORTED, "jacobi3d_streaming: tap set");
@@ -377,14 +385,14 @@ int jacobi3d_streaming(const tvs_stencil& st, const tvs_geometry& g, const doubl
                   (unsigned)((phi - plo + seg - 1) / seg));
   if (mask == kBox27) {
     if (fma)
-      jacobi3d_kernel<kBox27, true><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary, plo, phi, seg);
+      jacobi3d_kernel<kBox27, true><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary, plo, phi, seg, m);
     else
-      jacobi3d_kernel<kBox27, false><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary, plo, phi, seg);
+      jacobi3d_kernel<kBox27, false><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary, plo, phi, seg, m);
   } else {
     if (fma)
-      jacobi3d_kernel<kStar7, true><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary, plo, phi, seg);
+      jacobi3d_kernel<kStar7, true><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary, plo, phi, seg, m);
     else
-      jacobi3d_kernel<kStar7, false><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary, plo, phi, seg);
+      jacobi3d_kernel<kStar7, false><<<grid, block, 0, s>>>(src, dst, geo, g.origin, cf, st.boundary, plo, phi, seg, m);
   }
   TVS_LAUNCHED("jacobi3d_kernel");
   return TVS_OK;

@@ -72,22 +72,54 @@ def make_layout(global_extents, world: int, rank: int, ghost: int) -> SlabLayout
     return SlabLayout(rank, world, r0, r1, ghost, ext, geo)
 
 
+class _StagedRecv:
+    """A gloo request on a host copy of a device slice: copies the received
+    rows back to the device slice when waited on (gloo moves host tensors
+    only; NCCL moves the device rows directly)."""
+
+    def __init__(self, req, host, dev):
+        self.req, self.host, self.dev = req, host, dev
+
+    def wait(self):
+        self.req.wait()
+        if self.dev is not None:
+            self.dev.copy_(self.host)
+
+
 def exchange(lay: SlabLayout, buf, dist, group=None, wait: bool = True):
     """Swap halos: my first `ghost` owned rows -> rank-1's bottom ghosts,
     my last `ghost` owned rows -> rank+1's top ghosts (one grouped batch).
     ``wait=False`` returns the outstanding requests instead of waiting (the
-    overlapped pass waits after launching the interior rows)."""
+    overlapped pass waits after launching the interior rows).  Device
+    buffers on a gloo group are staged through host memory."""
     if lay.world == 1 or lay.ghost == 0:
         return []
     g, n = lay.ghost, lay.n_own
-    ops = []
+    staged = getattr(buf, "is_cuda", False) and dist.get_backend(group) == "gloo"
+    ops, back = [], []
+
+    def send(sl, peer):
+        t = buf[sl]
+        if staged:
+            t = t.cpu()  # synchronous device -> host copy of the rows
+        ops.append(dist.P2POp(dist.isend, t, peer, group))
+        back.append(None)
+
+    def recv(sl, peer):
+        t = buf[sl]
+        host = t.cpu() if staged else t
+        ops.append(dist.P2POp(dist.irecv, host, peer, group))
+        back.append(t if staged else None)
+
     if lay.rank > 0:
-        ops.append(dist.P2POp(dist.isend, buf[lay.row_slice(g, g)], lay.rank - 1, group))
-        ops.append(dist.P2POp(dist.irecv, buf[lay.row_slice(0, g)], lay.rank - 1, group))
+        send(lay.row_slice(g, g), lay.rank - 1)
+        recv(lay.row_slice(0, g), lay.rank - 1)
     if lay.rank < lay.world - 1:
-        ops.append(dist.P2POp(dist.isend, buf[lay.row_slice(n, g)], lay.rank + 1, group))
-        ops.append(dist.P2POp(dist.irecv, buf[lay.row_slice(n + g, g)], lay.rank + 1, group))
+        send(lay.row_slice(n, g), lay.rank + 1)
+        recv(lay.row_slice(n + g, g), lay.rank + 1)
     reqs = dist.batch_isend_irecv(ops)
+    if staged:
+        reqs = [_StagedRecv(r, op.tensor, dev) for r, op, dev in zip(reqs, ops, back)]
     if not wait:
         return reqs
     for req in reqs:

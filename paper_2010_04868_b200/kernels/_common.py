@@ -18,7 +18,8 @@ def check_backend(backend) -> None:
 
 
 def execute(spec, grid: Grid, steps: int, *, order: str = "lexicographic", out: Grid | None = None,
-            fma: str | None = None, depth: int | None = None, algo: str | None = None) -> Grid:
+            fma: str | None = None, depth: int | None = None, algo: str | None = None,
+            n_gpus: int | None = None) -> Grid:
     """Run ``steps`` updates of ``spec`` on the GPU; never mutates ``grid``."""
     steps = int(steps)
     if steps < 0:
@@ -29,7 +30,9 @@ def execute(spec, grid: Grid, steps: int, *, order: str = "lexicographic", out: 
     elif grid.element_kind != "float64":
         raise UnsupportedError(f"{spec.name}: {grid.element_kind} grids are not on the GPU path")
     if out is None:
-        out = grid.copy()
+        # the reference returns grid.copy() with the interior advanced; only
+        # the frame is copied here (the device writes the whole interior)
+        out = grid.copy() if steps == 0 else grid.result_like()
     else:
         if out.extents != grid.extents or out.data.shape != grid.data.shape or out.offset != grid.offset:
             raise ValueError("out= grid must have the geometry of the input grid")
@@ -37,9 +40,10 @@ def execute(spec, grid: Grid, steps: int, *, order: str = "lexicographic", out: 
             out.data[...] = grid.data
     if steps == 0:
         return out
-    ex = config.current().native(order=order, fma=fma, depth=depth, algo=algo)
+    ex = config.current().native(order=order, fma=fma, depth=depth, algo=algo, n_gpus=n_gpus)
     if spec.is_life:
-        _native.life_run(spec, grid.data, out.data, grid.extents, grid.offset, steps, ex)
+        _native.life_run(spec, grid.data, out.data, grid.extents, grid.offset, steps, ex, boundary=grid.boundary)
     else:
-        _native.run(spec, grid.data, out.data, grid.extents, grid.offset, steps, ex)
+        # Dirichlet value from the grid (kernels1d.py:115, kernels_nd.py:90)
+        _native.run(spec, grid.data, out.data, grid.extents, grid.offset, steps, ex, boundary=grid.boundary)
     return out

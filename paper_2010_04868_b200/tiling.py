@@ -279,14 +279,15 @@ def execute_parallel(kernel: str, grid: Grid, schedule: TileSchedule, workers: i
     lay = _native.make_layout(grid.data, grid.extents, grid.offset)
     ex = config.current().native()
     if spec.is_life:
-        rule = _native.make_life_rule(spec)
+        rule = _native.make_life_rule(spec, grid.boundary)
         rc = _native.lib().tvs_tiled_life(C.byref(rule), C.byref(lay), grid.data.ctypes.data, out.data.ctypes.data,
                                           schedule.steps, tiles, starts, nw, C.byref(ex))
     else:
-        st = _native.make_stencil(spec)
+        st = _native.make_stencil(spec, grid.boundary)  # Dirichlet value from the grid (tiling.py:340)
         rc = _native.lib().tvs_tiled_run(C.byref(st), C.byref(lay), grid.data.ctypes.data, out.data.ctypes.data,
                                          schedule.steps, tiles, starts, nw, C.byref(ex))
     _native.check(rc, f"tvs_tiled_run({kernel})")
+    out.fill_halo()  # the reference resets the result's halo (tiling.py:370)
     return out
 
 

@@ -88,7 +88,7 @@ __device__ __forceinline__ void level_row(double (&F)[kP2], double (&M)[kP2], co
   if constexpr (G0) add_group<MASK, 0, true, FMA, kP2>(F, in, c);
 }
 
-template <unsigned MASK, int D, bool FMA, int kP2>
+template <unsigned MASK, int D, bool FMA, int kP2, bool MIR>
 __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __restrict__ src,
                                                                 double* __restrict__ dst, Geo g, int64_t origin,
                                                                 Coeff9 cf, double bnd, int64_t n_strips,
@@ -172,13 +172,20 @@ __global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __
       }
       const int q = m - D;  // level-D row leaving
       if (q >= r0 && q < r1) {
-        // local row, plus the neighbour's ghost row when sharded
-        for_each_dst(dst, mir, q, [&](double* base) {
-          double* wp = base + origin + (int64_t)q * g.s0 + cl;
+        if constexpr (MIR) {
+          // sharded pass: local row, plus the neighbour's ghost row
+          for_each_dst(dst, mir, q, [&](double* base) {
+            double* wp = base + origin + (int64_t)q * g.s0 + cl;
+#pragma unroll
+            for (int p = 0; p < kP2; ++p)
+              if (store_mask >> p & 1u) wp[p] = in[p + 1];
+          });
+        } else {
+          double* wp = dst + origin + (int64_t)q * g.s0 + cl;
 #pragma unroll
           for (int p = 0; p < kP2; ++p)
             if (store_mask >> p & 1u) wp[p] = in[p + 1];
-        });
+        }
       }
     };
     if constexpr (IN) {
@@ -329,10 +336,19 @@ template <unsigned MASK, int D, int P>
 static void launch2d_d(bool fma, unsigned blocks, cudaStream_t s, const double* src, double* dst, const Geo& geo,
                        int64_t origin, const Coeff9& cf, double bnd, int64_t ns, int64_t nt, int64_t lo, int64_t hi,
                        int seg_rows, const Mirror& mir) {
-  if (fma)
-    jacobi2d_kernel<MASK, D, true, P><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows, mir);
-  else
-    jacobi2d_kernel<MASK, D, false, P><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows, mir);
+  // the mirror-store form only for sharded passes: no cost on one GPU
+  const bool mirrored = mir.p[0] != nullptr || mir.p[1] != nullptr;
+  if (fma) {
+    if (mirrored)
+      jacobi2d_kernel<MASK, D, true, P, true><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows, mir);
+    else
+      jacobi2d_kernel<MASK, D, true, P, false><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows, mir);
+  } else {
+    if (mirrored)
+      jacobi2d_kernel<MASK, D, false, P, true><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows, mir);
+    else
+      jacobi2d_kernel<MASK, D, false, P, false><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows, mir);
+  }
 }
 
 // rows [row_lo, row_hi) of the grid (any band; the

@@ -213,7 +213,7 @@ __device__ __forceinline__ void tb_level(const double* __restrict__ plane, int w
   }
 }
 
-template <unsigned MASK, bool FMA>
+template <unsigned MASK, bool FMA, bool MIR>
 __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double* __restrict__ src,
                                                                    double* __restrict__ dst, Geo g, int64_t origin,
                                                                    Coeff27 cf, double bnd, int64_t plo,
@@ -300,15 +300,18 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
       if (q2 >= p0 && q2 < p1) {
         const int64_t gq2 = q2 + g.a0_off;
         const bool pin = gq2 < 0 || gq2 >= g.a0_glob;
-        // local plane, plus the neighbour's ghost plane when sharded
-        for_each_dst(dst, mir, q2, [&](double* b) {
+        auto store = [&](double* b) {
           double* op = b + origin + q2 * g.s0 + (y0 - 1 + w * kRY) * g.s1 + (x0 - 1 + lane);
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int r = 0; r < kRY; ++r)
               if (store_ok >> (h * kRY + r) & 1u) op[r * g.s1 + 32 * h] = pin ? bnd : out[h][r];
-        });
+        };
+        if constexpr (MIR)
+          for_each_dst(dst, mir, q2, store);  // sharded: local plane + the neighbour's ghost plane
+        else
+          store(dst);
       }
     }
   }
@@ -341,12 +344,13 @@ template <unsigned MASK, bool FMA>
 static int launch_tb(const Geo& geo, const tvs_geometry& g, const double* src, double* dst, const Coeff27& cf,
                      double bnd, cudaStream_t s, int64_t plo, int64_t phi, int seg, const Mirror& mir) {
   // per device context; a host-side attribute write, no synchronisation
-  TVS_CUDA(cudaFuncSetAttribute(jacobi3d_tb_kernel<MASK, FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kTBSmem));
+  const bool mirrored = mir.p[0] != nullptr || mir.p[1] != nullptr;
+  auto kern = mirrored ? jacobi3d_tb_kernel<MASK, FMA, true> : jacobi3d_tb_kernel<MASK, FMA, false>;
+  TVS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTBSmem));
   const dim3 block(kTX3, kTYT);
   const dim3 grid((unsigned)((geo.e2 + kTBOX - 1) / kTBOX), (unsigned)((geo.e1 + kTBOY - 1) / kTBOY),
                   (unsigned)((phi - plo + seg - 1) / seg));
-  jacobi3d_tb_kernel<MASK, FMA><<<grid, block, kTBSmem, s>>>(src, dst, geo, g.origin, cf, bnd, plo, phi, seg, mir);
+  kern<<<grid, block, kTBSmem, s>>>(src, dst, geo, g.origin, cf, bnd, plo, phi, seg, mir);
   TVS_LAUNCHED("jacobi3d_tb_kernel");
   return TVS_OK;
 }

@@ -61,6 +61,10 @@ __global__ void shard_signal_kernel(unsigned* a, unsigned* b, unsigned v) {
   if (b) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(b), "r"(v) : "memory");
 }
 
+__global__ void shard_fill_kernel(double* p, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
 static void split_rows(int64_t n, int parts, int i, int64_t* r0, int64_t* r1) {
   const int64_t base = n / parts, extra = n % parts;
   *r0 = i * base + std::min<int64_t>(i, extra);
@@ -303,11 +307,27 @@ int tvs_shard_create(const tvs_stencil* st, int32_t dim, const int64_t global_ex
     tvs_shard_destroy(s);
     return cuda_fail(e, "tvs_shard_create");
   }
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 2; ++i) {
     if ((rc = fill_halo_api(s->geo, s->buf[i], st->boundary, s->stream))) {
       tvs_shard_destroy(s);
       return rc;
     }
+    // ghost rows outside the global domain (first / last shard) hold the
+    // Dirichlet value like the memory halo of an unsharded block: the 3D
+    // kernels stage input planes without a global range check
+    const int64_t s0 = s->geo.strides[0];
+    const int64_t lo_out = std::max<int64_t>(0, s->ghost - s->r0);              // local rows [0, lo_out)
+    const int64_t hi_out = std::max<int64_t>(0, s->r1 + s->ghost - s->e0);     // last hi_out local rows
+    const int64_t e0l = s->geo.extents[0];
+    if (lo_out > 0) {
+      shard_fill_kernel<<<64, 256, 0, s->stream>>>(s->buf[i] + s0, lo_out * s0, st->boundary);
+      TVS_LAUNCHED("shard_fill_kernel");
+    }
+    if (hi_out > 0) {
+      shard_fill_kernel<<<64, 256, 0, s->stream>>>(s->buf[i] + (e0l - hi_out + 1) * s0, hi_out * s0, st->boundary);
+      TVS_LAUNCHED("shard_fill_kernel");
+    }
+  }
   // neighbours may write into these buffers as soon as they are connected
   if ((e = cudaStreamSynchronize(s->stream)) != cudaSuccess) {
     tvs_shard_destroy(s);

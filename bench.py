@@ -173,6 +173,26 @@ def flush_l2(buf):
         buf.fill_(1.0)
 
 
+def dp_instr_per_update(cfg, fma=None):
+    """FP64 instructions the kernel issues per useful update: k taps cost
+    k DMUL/DFMA when fused (fma='allow', or 'exact' with power-of-two
+    weights, where the fused form is bit-identical), else k DMUL + (k-1)
+    DADD.  Ghost recompute is not counted (it is the overhead this metric
+    exposes)."""
+    import math
+
+    from paper_2010_04868_b200 import config
+    from paper_2010_04868_b200.catalog import get
+
+    spec = get(cfg["kernel"]).spec
+    cs = [float(spec.coefficients[o]) for o in spec.offsets()]
+    k = len(cs)
+    policy = fma or config.current().fma
+    pow2 = all(c == 0.0 or math.frexp(abs(c))[0] == 0.5 for c in cs)
+    fused = policy == "allow" or (policy == "exact" and pow2)
+    return (k if fused else 2 * k - 1), fused
+
+
 def device_time(cfg, K, W, sampler=None, fma=None, min_timed_s=0.0, algo=None):
     """Device-resident timing through the plan API: per-step ms (CUDA events
     on the plan stream) and launches per step.  Each step runs all T updates
@@ -315,10 +335,13 @@ def measure_config(cfg, K, W, with_e2e=True, with_cpu=True, min_timed_s=0.0):
                                "temporal blocking makes it exceed HBM peak). traffic = ncu dram read+write per "
                                "launch of the same kernel (profiles/traffic.json)"}
     sm = res["clocks"].get("sm_mhz") or 1965.0
-    fp64_peak = 148 * 64 * sm * 1e6 / 1e12  # DP ops/s (DADD/DMUL/DFMA each 1 op), measured 63.4/clk/SM
-    fp64 = cfg["ops"] * updates / (ms * 1e-3) / 1e12
-    res["fp64"] = {"achieved_tops": fp64, "peak_tops": fp64_peak, "frac": fp64 / fp64_peak,
-                   "ops_per_update": cfg["ops"], "note": "unfused algorithmic FP64 ops; peak = 148 SM x 64/clk x median SM clock"}
+    fp64_peak = 148 * 64 * sm * 1e6 / 1e12  # DP instructions/s (DADD/DMUL/DFMA), measured 63.4/clk/SM
+    instr, fused = dp_instr_per_update(cfg)
+    fp64 = instr * updates / (ms * 1e-3) / 1e12
+    res["fp64"] = {"achieved_tinstr": fp64, "peak_tinstr": fp64_peak, "frac": fp64 / fp64_peak,
+                   "dp_instr_per_update": instr, "fused": fused, "flops_per_update": cfg["ops"],
+                   "note": "FP64 instructions issued per useful update (DFMA = 1) x update rate; peak = 148 SM x "
+                           "64/clk x median SM clock; ghost recompute not counted"}
     if with_e2e:
         etimes, nbytes, _ = e2e_time(cfg, K, W)
         ems = statistics.mean(etimes)
@@ -482,41 +505,201 @@ def run_reference(args):
     return 0
 
 
+def make_rows(cfg, lo, hi, pinned=True):
+    """Rows [lo, hi) (axis 0) of make_grid(cfg)'s padded array, exactly: the
+    PCG64 stream is advanced past the earlier rows (one 64-bit draw per
+    double), so a rank materialises only its own slab.  Returns (array of the
+    padded rows offset+lo .. offset+hi-1, padded shape, offset)."""
+    from paper_2010_04868_b200 import Grid, _native
+
+    probe = Grid((1,) * len(cfg["extents"]), 1)
+    off = probe.offset
+    padded = tuple(off + e + 1 + probe.vl for e in cfg["extents"])
+    shape = (hi - lo,) + padded[1:]
+    a = _native.host_empty(shape) if pinned else np.empty(shape)
+    a.fill(0.0)
+    rng = np.random.default_rng(cfg["seed"])
+    row = int(np.prod(cfg["extents"][1:]))
+    rng.bit_generator.advance(lo * row)
+    win = (slice(None),) + tuple(slice(off, off + e) for e in cfg["extents"][1:])
+    a[win] = rng.uniform(cfg["dist"][0], cfg["dist"][1], size=(hi - lo,) + tuple(cfg["extents"][1:]))
+    return a, padded, off
+
+
+def _slab_layout(cfg, part, row0, padded, off):
+    """tvs_layout of the WHOLE padded grid whose base pointer is placed so
+    that padded row off+row0 is part[0] (the library only touches the rows a
+    shard owns / reads)."""
+    import ctypes as C
+
+    from paper_2010_04868_b200 import _native
+
+    lay = _native.Layout()
+    lay.dim = len(padded)
+    for d in range(3):
+        lay.extents[d] = cfg["extents"][d] if d < lay.dim else 1
+        lay.shape[d] = padded[d] if d < lay.dim else 1
+    lay.offset = off
+    row_bytes = int(np.prod(padded[1:])) * 8
+    return lay, C.c_void_p(part.ctypes.data - (off + row0) * row_bytes)
+
+
 def run_sharded(args):
-    """N>1: slab-sharded Jacobi over torch.distributed (NCCL), strong scaling."""
+    """torchrun, one process per GPU: slab-sharded Jacobi through the fused
+    peer-memory path (tvs_shard_*: each rank's kernels store the neighbour's
+    ghost rows into its buffer over NVLink; CUDA IPC handles exchanged with
+    torch.distributed).  TVS_BENCH_HALO=nccl runs the NCCL send/recv halo
+    module (halo.ShardedJacobi) instead.  Strong scaling, max over ranks."""
+    import ctypes as C
+
     import torch
     import torch.distributed as dist
 
+    from paper_2010_04868_b200 import _native
     from paper_2010_04868_b200.catalog import get
-    from paper_2010_04868_b200.halo import ShardedJacobi
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} launched with WORLD_SIZE={world}")
     local = int(os.environ.get("LOCAL_RANK", rank))
+    backend = "nccl"
+    if os.environ.get("TVS_BENCH_EMULATE_SHARDS"):
+        # plumbing check on a box with fewer GPUs than ranks: ranks share
+        # devices (round robin) and talk over gloo; never a bench number
+        local %= torch.cuda.device_count()
+        backend = "gloo"
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group("gloo")
+    red = "cuda" if backend == "nccl" else "cpu"
     cfg = CONFIGS[args.config]
     if not cfg["shards"]:
         cfg = CONFIGS[HEADLINE]
+    if os.environ.get("TVS_BENCH_HALO") == "nccl":
+        return run_sharded_nccl(args, cfg, rank, world, local)
     spec = get(cfg["kernel"]).spec
-    full = make_grid(cfg).interior
-    from paper_2010_04868_b200 import _native
+    sh = _native.Shard(spec, cfg["extents"], world, rank, _native.make_exec(device=local))
+    handles = [None] * world
+    dist.all_gather_object(handles, sh.export())
+    sh.connect(handles[rank - 1] if rank > 0 else None, handles[rank + 1] if rank + 1 < world else None)
+    r0, r1 = sh.rows
+    e0 = cfg["extents"][0]
+    lo, hi = max(r0 - sh.ghost, 0), min(r1 + sh.ghost, e0)
+    h_in, padded, off = make_rows(cfg, lo, hi)
+    h_out = _native.host_empty((r1 - r0,) + padded[1:])
+    lay_in, p_in = _slab_layout(cfg, h_in, lo, padded, off)
+    lay_out, p_out = _slab_layout(cfg, h_out, r0, padded, off)
+    lib = _native.lib()
+    stream = torch.cuda.ExternalStream(sh.stream_handle())
+    clk = ClockSampler(local) if rank == 0 else None
 
+    def upload():
+        _native.check(lib.tvs_shard_upload(sh._h, C.byref(lay_in), p_in), "tvs_shard_upload")
+
+    def download():
+        _native.check(lib.tvs_shard_download(sh._h, C.byref(lay_out), p_out), "tvs_shard_download")
+
+    def timed(e2e):
+        times, launches = [], 0
+        if not e2e:
+            upload()
+            sh.synchronize()
+        for i in range(args.warmup + args.steps):
+            dist.barrier()  # every shard idle: neighbours write into each other's buffers
+            torch.cuda.synchronize()
+            if i == args.warmup and clk is not None and not e2e:
+                clk.start()
+                clk.wait_ready()
+                clk.mark(True)
+            e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0_.record(stream)
+            if e2e:
+                upload()
+                sh.synchronize()
+                dist.barrier()  # all slabs resident before any pass writes a neighbour
+            sh.run(cfg["T"])
+            if e2e:
+                download()
+            e1_.record(stream)
+            sh.synchronize()
+            if i >= args.warmup:
+                t = torch.tensor([e0_.elapsed_time(e1_)], device=red)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                c = torch.tensor([sh.last_launches()], device=red, dtype=torch.int64)
+                dist.all_reduce(c, op=dist.ReduceOp.SUM)
+                times.append(float(t.item()))
+                launches += int(c.item())
+        if clk is not None and not e2e:
+            clk.mark(False)
+            clk.stop()
+        return statistics.mean(times), launches
+
+    ms, launches = timed(False)
+    ems, _ = timed(True)
+    updates = int(np.prod(cfg["extents"])) * cfg["T"]
+    h2d = torch.tensor([(hi - lo) * int(np.prod(cfg["extents"][1:])) * 8], device=red, dtype=torch.int64)
+    dist.all_reduce(h2d, op=dist.ReduceOp.SUM)
+    if rank == 0:
+        hbm_peak, peak_src = peaks()
+        achieved = BYTES_PER_UPDATE * updates / world / (ms * 1e-3) / 1e9
+        print(json.dumps({
+            "metric": "GStencil/s", "value": updates / (ms * 1e-3) / 1e9, "unit": "GStencil/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE seeds)",
+            "config": {"workload": f"{cfg['name']} {'x'.join(map(str, cfg['extents']))} T={cfg['T']}",
+                       "parallelism": f"slab{world} (axis-0 slabs, ghost depth {sh.ghost}, halo exchange fused "
+                                      f"into the kernels as peer-memory stores; CUDA IPC)",
+                       "l2": "inputs larger than L2",
+                       **({"emulated": "ranks share devices: plumbing check, not a bench number"}
+                          if backend != "nccl" else {})},
+            "gpu_launches": launches, "clocks": clk.summary() if clk else None,
+            "e2e": {"value": updates / (ems * 1e-3) / 1e9, "unit": "GStencil/s", "ms_per_step": ems,
+                    "h2d_bytes_per_step": int(h2d.item()), "d2h_bytes_per_step": int(updates / cfg["T"] * 8),
+                    "note": "per rank: upload own slab + ghosts from pinned host memory, T steps, download own rows"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None, "per": "GPU (16 B/update effective)",
+                         "peak_source": peak_src},
+        }))
+    dist.barrier()
+    sh.close()
+    dist.destroy_process_group()
+    return 0
+
+
+def run_sharded_nccl(args, cfg, rank, world, local):
+    """The NCCL send/recv halo module (halo.ShardedJacobi): the non-fused
+    baseline of the sharded path."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2010_04868_b200 import _native
+    from paper_2010_04868_b200.catalog import get
+    from paper_2010_04868_b200.halo import ShardedJacobi
+
+    spec = get(cfg["kernel"]).spec
     depth = 8 if len(cfg["extents"]) == 2 else 2
     sj = ShardedJacobi(spec, cfg["extents"], dist, depth=depth, device=torch.device("cuda", local))
     lay = sj.layout
-    # e2e: this rank's rows (+ ghosts) from pinned host memory in, owned rows out
     lo, hi = max(lay.r0 - lay.ghost, 0), min(lay.r1 + lay.ghost, int(lay.geometry.axis0_global))
-    h_in = torch.from_numpy(np.ascontiguousarray(full[lo:hi])).pin_memory()
+    part, _, off = make_rows(cfg, lo, hi, pinned=False)
+    win = (slice(None),) + tuple(slice(off, off + e) for e in cfg["extents"][1:])
+    h_in = torch.from_numpy(np.ascontiguousarray(part[win])).pin_memory()
     h_out = torch.empty(tuple(sj.owned().shape), dtype=torch.float64).pin_memory()
     in_view = sj.interior_view
     clk = ClockSampler(local) if rank == 0 else None
+
+    def load():
+        v = in_view(0)
+        v[lo - (lay.r0 - lay.ghost): hi - (lay.r0 - lay.ghost)].copy_(h_in, non_blocking=True)
 
     def timed(e2e):
         times, launches = [], 0
         for i in range(args.warmup + args.steps):
             sj.cur = 0
             if not e2e:
-                sj.load_global(full)
+                load()
             dist.barrier()
             torch.cuda.synchronize()
             if i == args.warmup and clk is not None and not e2e:
@@ -527,8 +710,7 @@ def run_sharded(args):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             if e2e:
-                v = in_view(0)
-                v[lo - (lay.r0 - lay.ghost): hi - (lay.r0 - lay.ghost)].copy_(h_in, non_blocking=True)
+                load()
             sj.run(cfg["T"])
             if e2e:
                 h_out.copy_(sj.owned(), non_blocking=True)
@@ -559,7 +741,7 @@ def run_sharded(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE seeds)",
             "config": {"workload": f"{cfg['name']} {'x'.join(map(str, cfg['extents']))} T={cfg['T']}",
-                       "parallelism": f"slab{world} (axis-0 slabs, NCCL halo depth {depth})",
+                       "parallelism": f"slab{world} (axis-0 slabs, NCCL send/recv halo depth {depth})",
                        "l2": "inputs larger than L2"},
             "gpu_launches": launches, "clocks": clk.summary() if clk else None,
             "e2e": {"value": updates / (ems * 1e-3) / 1e9, "unit": "GStencil/s", "ms_per_step": ems,
@@ -568,6 +750,38 @@ def run_sharded(args):
                          "frac": achieved / hbm_peak, "traffic": None, "per": "GPU", "peak_source": peak_src},
         }))
     dist.destroy_process_group()
+    return 0
+
+
+def run_in_process(args):
+    """--gpus N without torchrun: one process drives N GPUs through the
+    library's own sharding (tvs_exec.n_gpus: axis-0 slabs, fused peer-memory
+    halo exchange, per-GPU uploads / downloads).  Configs that do not shard
+    (1D, Gauss-Seidel) run as N independent replicas."""
+    from paper_2010_04868_b200 import _native, config
+
+    n = args.gpus
+    have = _native.device_count()
+    emulate = bool(os.environ.get("TVS_BENCH_EMULATE_SHARDS"))
+    if have < n and not emulate:
+        raise SystemExit(f"bench.py --gpus {n}: only {have} CUDA device(s) visible")
+    cfg = CONFIGS[args.config]
+    if not cfg["shards"]:
+        cfg = CONFIGS[HEADLINE]
+    with config.using(n_gpus=n, emulate_shards=emulate and have < n):
+        head = measure_config(cfg, args.steps, args.warmup, with_e2e=True, with_cpu=False)
+    print(json.dumps({
+        "metric": "GStencil/s", "value": head["value"], "unit": "GStencil/s", "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE seeds)",
+        "config": {"workload": head["workload"], "l2": "inputs larger than L2",
+                   "parallelism": f"slab{n} in one process (tvs_exec.n_gpus; halo exchange fused into the kernels "
+                                  f"as peer-memory stores)",
+                   **({"emulated": f"{n} shards on {have} device(s): plumbing check, not a bench number"}
+                      if have < n else {})},
+        "gpu_launches": head["gpu_launches"], "clocks": head["clocks"], "e2e": head.get("e2e"),
+        "roofline": head["roofline"], "fp64": head["fp64"],
+    }))
     return 0
 
 
@@ -587,8 +801,10 @@ def main():
         return run_reference(args)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 or os.environ.get("TVS_FORCE_SHARDED"):
         # TVS_FORCE_SHARDED=1 under torchrun --nproc-per-node 1: the sharded
-        # path with one rank (exercises the halo-exchange plumbing on one GPU)
+        # path with one rank (exercises the plumbing on one GPU)
         return run_sharded(args)
+    if args.gpus > 1:
+        return run_in_process(args)
     cfg = CONFIGS[args.config]
     head = measure_config(cfg, args.steps, args.warmup, with_e2e=True, with_cpu=not args.no_cpu)
     line = {

@@ -208,3 +208,21 @@ def test_cli_parser_and_config(tmp_path):
     argv = ["--mode", "bench", "--kernel", "heat1d", "--nx", "500", "--config", str(cfg)]
     args = _apply_config(build_parser().parse_args(argv), argv)
     assert args.steps == 7 and args.nx == 500 and args.reps == 2  # explicit flags win
+
+
+def test_bench_make_rows_exact():
+    """bench.make_rows: a rank's slab of the seeded BASELINE grid equals the
+    same rows of the full grid (PCG64 advanced past earlier rows), and the
+    slab layout puts that row at the right place of the whole-grid layout."""
+    import bench
+
+    cfg = dict(bench.CONFIGS[3])
+    cfg["extents"] = (37, 29)
+    g = bench.make_grid(cfg)
+    part, padded, off = bench.make_rows(cfg, 9, 21, pinned=False)
+    assert padded == g.data.shape
+    assert np.array_equal(part, g.data[off + 9: off + 21])
+    lay, ptr = bench._slab_layout(cfg, part, 9, padded, off)
+    row_bytes = padded[1] * 8
+    assert ptr.value + (off + 9) * row_bytes == part.ctypes.data
+    assert tuple(lay.shape[:2]) == padded and lay.offset == off

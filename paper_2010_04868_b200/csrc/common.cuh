@@ -240,8 +240,6 @@ bool jacobi2d_blocked_supported(const tvs_stencil& st);
 int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst,
                      int depth, bool fma, cudaStream_t s, int64_t row_lo = 0, int64_t row_hi = -1,
                      int seg_rows = 0, const Mirror* mir = nullptr);
-// blocks (warps) one jacobi2d_blocked launch over `rows` rows would use
-int64_t jacobi2d_tasks(int64_t rows, int64_t cols, int depth, int seg_rows);
 int jacobi2d_band_rows();
 int jacobi2d_max_depth();
 int jacobi2d_default_depth();

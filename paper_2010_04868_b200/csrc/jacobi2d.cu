@@ -351,6 +351,48 @@ static void launch2d_d(bool fma, unsigned blocks, cudaStream_t s, const double* 
   }
 }
 
+// Rows per warp task when the caller does not fix it.  One-warp blocks are
+// scheduled in waves of `resident` (occupancy x SMs); a launch of
+// strips x segments tasks costs ~ ceil(tasks / resident) x (seg + 2D + c)
+// row-steps (c: per-task prologue).  The segment count is chosen to fill the
+// last wave: config 3 (16384 rows, 171 strips, 1776 resident at D = 8):
+// 256-row segments give 10944 tasks = 6.2 waves (the 7th at 16%), 72
+// segments of 228 rows 12312 = 6.9 waves.  TVS_J2D_SEG fixes it.  Rows
+// shorter than 128 form one segment.
+static int auto_seg(int64_t rows, int64_t strips, int depth, int64_t resident) {
+  static const int fixed = [] {
+    const char* e = getenv("TVS_J2D_SEG");
+    return e ? atoi(e) : 0;
+  }();
+  if (fixed > 0) return fixed;
+  if (resident <= 0) return kRowsSeg;
+  double best = 1e300;
+  int64_t best_seg = kRowsSeg;
+  const int64_t max_nseg = std::max<int64_t>(1, rows / 32);
+  for (int64_t nseg = 1; nseg <= max_nseg; ++nseg) {
+    const int64_t seg = (rows + nseg - 1) / nseg;
+    // 128..256 rows: the measured range (config 3 per MHz: 128 0.89, 192
+    // 1.01, 228 1.01, 256 0.96 GSt/s/MHz); longer segments leave too little
+    // slack for the uneven boundary / interior warps
+    if (seg > 256 || (seg < 128 && rows >= 128)) continue;
+    const int64_t tasks = strips * ((rows + seg - 1) / seg);
+    const double cost = (double)((tasks + resident - 1) / resident) * (double)(seg + 2 * depth + 4);
+    if (cost < best * 0.999) best = cost, best_seg = seg;
+  }
+  return (int)best_seg;
+}
+
+template <class K>
+static int64_t resident_blocks(K kern) {
+  int dev = 0, sms = 0, per = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kWarps2 * 32, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return (int64_t)per * sms;
+}
+
 // rows [row_lo, row_hi) of the grid (any band; the
 // whole grid by default): one row band of the pipelined host path
 template <unsigned MASK, int D>
@@ -360,9 +402,14 @@ static void launch2d_one(bool fma, cudaStream_t s, const double* src, double* ds
   // columns per lane: registers grow as 2 * P * D accumulators; P = 3 at
   // D = 5..8 keeps 12 warps/SM at D = 8 (168 registers) where P = 4 held 9
   // (config 3: D = 8 P = 4 1596, P = 3 1723 GSt/s; D > 8 at P = 3 is slower)
-  constexpr int P = D <= 4 ? 4 : (D <= 8 ? 3 : 2);  // = lane_cols(D)
+  constexpr int P = D <= 4 ? 4 : (D <= 8 ? 3 : 2);
   const int64_t U = 32 * P - 2 * D;
   const int64_t ns = (geo.e1 + U - 1) / U;
+  if (seg_rows <= 0) {
+    static const int64_t res[2] = {resident_blocks(jacobi2d_kernel<MASK, D, false, P, false>),
+                                   resident_blocks(jacobi2d_kernel<MASK, D, true, P, false>)};
+    seg_rows = auto_seg(row_hi - row_lo, ns, D, res[fma ? 1 : 0]);
+  }
   const int64_t nseg = (row_hi - row_lo + seg_rows - 1) / seg_rows;
   const int64_t nt = ns * nseg;
   const unsigned blocks = (unsigned)((nt + kWarps2 - 1) / kWarps2);
@@ -390,13 +437,6 @@ static void launch2d(int depth, bool fma, cudaStream_t s, const double* src, dou
 
 int jacobi2d_band_rows() { return kRowsSeg; }
 
-static int lane_cols(int depth) { return depth <= 4 ? 4 : (depth <= 8 ? 3 : 2); }  // P of launch2d_one
-
-int64_t jacobi2d_tasks(int64_t rows, int64_t cols, int depth, int seg_rows) {
-  const int64_t U = 32 * lane_cols(depth) - 2 * depth;
-  if (seg_rows <= 0) seg_rows = kRowsSeg;
-  return (cols + U - 1) / U * ((rows + seg_rows - 1) / seg_rows);
-}
 
 int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, int depth,
                      bool fma, cudaStream_t s, int64_t row_lo, int64_t row_hi, int seg_rows, const Mirror* mir) {
@@ -405,7 +445,6 @@ int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double*
   if ((mask != kStar5 && mask != kBox9) || depth < 1 || depth > kMaxD2)
     return fail(TVS_ERR_UNSUPPORTED, "jacobi2d_blocked: tap set or depth");
   if (row_hi < 0) row_hi = g.extents[0];
-  if (seg_rows <= 0) seg_rows = kRowsSeg;
   if (row_lo < 0 || row_hi > g.extents[0] || row_lo >= row_hi)
     return fail(TVS_ERR_INVALID, "jacobi2d_blocked: row band");
   const Geo geo = make_geo(g);

@@ -113,27 +113,6 @@ struct tvs_shard {
 
 namespace tvs {
 
-static int shard_seg_rows(const tvs_shard* s) {
-  // 2D: rows per warp task.  A slab of a few thousand rows at 256 rows per
-  // segment leaves a fraction of a wave on 148 SMs; shorter segments add
-  // ghost rows (2D per segment).  Pick the segment that minimises waves x
-  // rows processed per task (~12 resident one-warp blocks per SM at D = 8).
-  if (s->geo.dim != 2) return 0;
-  int dev = s->device, sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t resident = (int64_t)sms * 12;
-  const int64_t n = s->r1 - s->r0;
-  int best = 256;
-  double best_cost = 1e300;
-  for (int seg : {256, 192, 128, 96, 64}) {
-    const int64_t tasks = jacobi2d_tasks(n, s->geo.extents[1], s->depth, seg);
-    const double cost = (double)((tasks + resident - 1) / resident) * (seg + 2 * s->depth) *
-                        std::min<int64_t>(seg, n) / (double)seg;
-    if (cost < best_cost * 0.98) best_cost = cost, best = seg;
-  }
-  return best;
-}
-
 static int shard_pass(tvs_shard* s, int d, StreamValueFn wait_value) {
   const uint32_t p = ++s->passes;
   if (p > 1) {
@@ -166,7 +145,8 @@ static int shard_pass(tvs_shard* s, int d, StreamValueFn wait_value) {
   const bool fma = use_fma(s->st, s->ex);
   int rc;
   if (s->geo.dim == 2) {
-    rc = jacobi2d_blocked(s->st, s->geo, s->buf[src], s->buf[dst], d, fma, s->stream, G, G + n, shard_seg_rows(s), &m);
+    // segment rows chosen by the kernel to fill its last wave (jacobi2d.cu auto_seg)
+    rc = jacobi2d_blocked(s->st, s->geo, s->buf[src], s->buf[dst], d, fma, s->stream, G, G + n, 0, &m);
   } else {
     rc = d == 2 ? jacobi3d_blocked2(s->st, s->geo, s->buf[src], s->buf[dst], fma, s->stream, G, G + n, 0, &m)
                 : jacobi3d_streaming(s->st, s->geo, s->buf[src], s->buf[dst], fma, s->stream, G, G + n, 0, &m);

@@ -193,7 +193,7 @@ def dp_instr_per_update(cfg, fma=None):
     return (k if fused else 2 * k - 1), fused
 
 
-def device_time(cfg, K, W, sampler=None, fma=None, min_timed_s=0.0, algo=None):
+def device_time(cfg, K, W, sampler=None, fma=None, min_timed_s=0.0, algo=None, order="lexicographic"):
     """Device-resident timing through the plan API: per-step ms (CUDA events
     on the plan stream) and launches per step.  Each step runs all T updates
     on the field left by the previous step (same work every step)."""
@@ -204,7 +204,7 @@ def device_time(cfg, K, W, sampler=None, fma=None, min_timed_s=0.0, algo=None):
 
     spec = get(cfg["kernel"]).spec
     g = make_grid(cfg)
-    ex = config.current().native(**({"fma": fma} if fma else {}), **({"algo": algo} if algo else {}))
+    ex = config.current().native(order=order, **({"fma": fma} if fma else {}), **({"algo": algo} if algo else {}))
     plan = _native.Plan(spec, cfg["extents"], ex)
     stream = torch.cuda.ExternalStream(plan.stream_handle())
     l2 = torch.empty(256 * 2 ** 20 // 8, dtype=torch.float64, device="cuda") if g.data.nbytes < 2 ** 30 else None
@@ -816,6 +816,11 @@ def main():
         "gpu_launches": head["gpu_launches"], "clocks": head["clocks"], "e2e": head.get("e2e"),
         "roofline": head["roofline"], "fp64": head["fp64"], "cpu_baseline": head.get("cpu_baseline"),
     }
+    try:  # whole-grid parity at full size (tests/test_full_grid.py, committed evidence)
+        with open(os.path.join(ROOT, "profiles", "parity.json")) as fh:
+            line["parity"] = json.load(fh)
+    except Exception:
+        line["parity"] = None
     line["untiled"] = untiled_legs(args)
     line["integer"] = integer_legs(args)
     if not args.no_all:
@@ -844,6 +849,17 @@ def main():
                                      "unit": "GB/s", "frac": fv * BYTES_PER_UPDATE / hbm_peak},
                         "note": "fma='allow': 27 DFMA per update instead of 27 DMUL + 26 DADD; within the "
                                 "north_star 1e-12 relative tolerance, not bit-exact"}
+                if c["name"] == "2d9p_gauss_seidel":
+                    # the reference oracle's own update order (anti-diagonal
+                    # gather/scatter, baselines.py:83-107): hyperplane wavefront
+                    clk = ClockSampler()
+                    rt, rl = device_time(c, 2, args.warmup, sampler=clk, order="reference")
+                    rms = statistics.mean(rt)
+                    rv = int(np.prod(c["extents"])) * c["T"] / (rms * 1e-3) / 1e9
+                    per[c["name"]]["reference_order"] = {
+                        "value": rv, "unit": "GStencil/s", "ms_per_step": rms, "launches_per_step": rl,
+                        "clocks": clk.summary(),
+                        "note": "order='reference' (gs_wave_kernel, one grid barrier per hyperplane i+j+3t)"}
             except Exception as exc:  # report, never hide
                 per[c["name"]] = {"error": repr(exc)}
         line["per_stencil"] = per

@@ -1,0 +1,87 @@
+"""Whole-grid parity at BASELINE.json's full sizes: the GPU result of every
+point against the C oracle (the bit-exact restatement of the reference's
+``scalar_reference``, baselines.py:110-125), reported as the pointwise max
+relative error (north_star bar: <= 1e-12; the result here is 0, asserted
+with ``array_equal``).
+
+Configs 1, 2, 3 and 4 (both Gauss-Seidel orders: the lexicographic loop
+BASELINE names and the reference oracle's anti-diagonal order,
+baselines.py:83-107) are compared on the entire grid at full T.  Config 5's
+oracle would need ~25 CPU-minutes; it is covered by the light-cone windows
+and the blocked-vs-single-step identity of tests/test_full_size.py.
+
+Each test appends {config: max_rel_err} to gpurun_out/full_parity.json so
+the numbers travel back with the run (profiles/r02_full_parity.json)."""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import pytest
+
+from oracle import cref
+from paper_2010_04868_b200 import _native, config
+from paper_2010_04868_b200.catalog import get
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+THREADS = os.cpu_count() or 1
+
+
+def _record(key, entry):
+    path = os.path.join(ROOT, "gpurun_out", "full_parity.json")
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    data = {}
+    if os.path.exists(path):
+        with open(path) as fh:
+            data = json.load(fh)
+    data[key] = entry
+    with open(path, "w") as fh:
+        json.dump(data, fh, indent=1)
+
+
+def _max_rel(got, want):
+    den = np.abs(want)
+    diff = np.abs(got - want)
+    nz = den > 0
+    rel = float(np.max(diff[nz] / den[nz])) if nz.any() else 0.0
+    return max(rel, float(np.max(diff[~nz])) if (~nz).any() else 0.0)
+
+
+def _gpu(cfg, g, order="lexicographic"):
+    spec = get(cfg["kernel"]).spec
+    plan = _native.Plan(spec, cfg["extents"], config.current().native(order=order, fma="exact"))
+    plan.upload(g.data, g.offset)
+    plan.run(cfg["T"])
+    out = g.alloc_like()
+    plan.download(out.data, out.offset)
+    plan.close()
+    return out
+
+
+@pytest.mark.parametrize("cid,order", [(1, "lexicographic"), (2, "lexicographic"), (4, "lexicographic"),
+                                       (4, "reference"), (3, "lexicographic")])
+def test_full_grid_bitexact(cuda_ready, cid, order):
+    cfg = bench.CONFIGS[cid]
+    spec = get(cfg["kernel"]).spec
+    g = bench.make_grid(cfg)
+    t0 = time.perf_counter()
+    got = _gpu(cfg, g, order)
+    t1 = time.perf_counter()
+    want = cref.scalar_reference(spec, g, cfg["T"], order=order, threads=THREADS)
+    t2 = time.perf_counter()
+    err = _max_rel(got.interior, want.interior)
+    equal = bool(np.array_equal(got.interior, want.interior))
+    _record(f"config{cid}_{order}", {"workload": f"{cfg['name']} {'x'.join(map(str, cfg['extents']))} T={cfg['T']}",
+                                     "points": int(np.prod(cfg["extents"])), "max_rel_err": err,
+                                     "bit_exact": equal, "gpu_s": t1 - t0, "oracle_s": t2 - t1,
+                                     "oracle_threads": THREADS if spec.dependence_kind != "gauss_seidel" else 1})
+    assert err <= 1e-12
+    assert equal, f"config {cid} ({order}): max rel err {err}"

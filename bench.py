@@ -279,33 +279,91 @@ def e2e_time(cfg, K, W):
     return times, nbytes, out
 
 
-def cpu_sample(cfg, budget_s=12.0):
-    """Oracle port on the host: bounded sample of the same workload.  Jacobi:
-    full grid, T_cpu steps on all cores; GS: full grid, T_cpu sweeps on one
-    core.  Returns (GStencil/s, cores, description)."""
+def _port_rate(spec, g, steps, cores):
+    """C restatement of scalar_reference (bit-exact, OpenMP over axis 0 for
+    Jacobi, one core for Gauss-Seidel): GStencil/s of its step loop (the
+    allocations and copies around it excluded, oracle_last_seconds)."""
     from oracle import cref
+
+    cref.scalar_reference(spec, g, steps, order="lexicographic", threads=cores)
+    return int(np.prod(g.extents)) * steps / cref.last_seconds() / 1e9, cref.last_seconds()
+
+
+def numpy_reference_rate(cfg, budget_s=20.0):
+    """The reference's own CPU code path, restated in NumPy (oracle/oracle.py:
+    the same whole-plane ufunc taps / Python GS loop / anti-diagonal gather as
+    baselines.py:43-125, bit-exact), one core (NumPy ufuncs are single
+    threaded), on a bounded sample: the full grid (config 5: a 256^3 block)
+    for 1-2 steps.  BASELINE.md §2's CPU baseline."""
+    from oracle import oracle as npo
+    from paper_2010_04868_b200 import Grid
+    from paper_2010_04868_b200.catalog import get
+
+    spec = get(cfg["kernel"]).spec
+    ext = cfg["extents"]
+    if int(np.prod(ext)) > 2 ** 28:
+        ext = tuple(min(e, 256) for e in ext)
+    g = Grid(ext, 1)
+    g.set_interior(np.random.default_rng(cfg["seed"]).uniform(*cfg["dist"], size=ext))
+    gauss = spec.dependence_kind == "gauss_seidel"
+    if gauss and len(ext) == 1:
+        # pure-Python loop (~0.001 GSt/s): a 2^16 prefix keeps it to seconds
+        g = Grid((2 ** 16,), 1)
+        g.set_interior(np.random.default_rng(cfg["seed"]).uniform(*cfg["dist"], size=(2 ** 16,)))
+    t0 = time.perf_counter()
+    npo.scalar_reference(spec, g, 1)
+    one = time.perf_counter() - t0
+    steps = int(max(1, min(3, budget_s / max(one, 1e-6))))
+    t0 = time.perf_counter()
+    npo.scalar_reference(spec, g, steps)
+    dt = time.perf_counter() - t0
+    return {"value": int(np.prod(g.extents)) * steps / dt / 1e9, "unit": "GStencil/s", "cores": 1,
+            "kind": "port",
+            "sample": f"NumPy restatement of the reference's scalar_reference (baselines.py:110-125, same ufunc "
+                      f"taps; reference order for GS-2D), {'x'.join(map(str, g.extents))} grid, {steps} "
+                      f"{'sweeps' if gauss else 'steps'}, {dt:.1f} s, 1 core"}
+
+
+def e2e_stock_time(cfg, K, W):
+    """The stock call a reference user makes: ``fn(grid, T)`` on the default
+    pageable Grid, no ``out=`` (the result Grid is allocated by the call,
+    kernels_nd.py:38-40,91).  Host->device and device->host copies, the
+    result allocation and its page faults are all inside the timing."""
+    from paper_2010_04868_b200 import kernels
+
+    g = make_grid(cfg)
+    fn = getattr(kernels, cfg["fn"])
+    times = []
+    for i in range(W + K):
+        t0 = time.perf_counter()
+        out = fn(g, cfg["T"], kernel=cfg["kernel"])
+        t1 = time.perf_counter()
+        del out
+        if i >= W:
+            times.append((t1 - t0) * 1e3)
+    return times
+
+
+def cpu_sample(cfg, budget_s=12.0):
+    """Oracle C port on the host: bounded sample of the same workload (full
+    grid, T_cpu steps, all cores for Jacobi / one for Gauss-Seidel), timed
+    inside its step loop.  Returns (GStencil/s, cores, description)."""
     from paper_2010_04868_b200.catalog import get
 
     spec = get(cfg["kernel"]).spec
     g = make_grid(cfg)
     gauss = spec.dependence_kind == "gauss_seidel"
     cores = 1 if gauss else (os.cpu_count() or 1)
-    pts = int(np.prod(cfg["extents"]))
-    cref.scalar_reference(spec, g, 1, order="lexicographic", threads=cores)  # warm-up (first touch)
-    t0 = time.perf_counter()
-    cref.scalar_reference(spec, g, 1, order="lexicographic", threads=cores)
-    one = time.perf_counter() - t0
+    _, one = _port_rate(spec, g, 1, cores)  # warm-up (first touch) and the per-step time
     steps = int(max(1, min(cfg["T"], budget_s / max(one, 1e-6))))
-    t0 = time.perf_counter()
-    cref.scalar_reference(spec, g, steps, order="lexicographic", threads=cores)
-    dt = time.perf_counter() - t0
-    rate = pts * steps / dt / 1e9
-    desc = (f"oracle C port of scalar_reference, full {'x'.join(map(str, cfg['extents']))} grid, "
-            f"{steps} of {cfg['T']} {'sweeps' if gauss else 'steps'}, {dt:.1f} s")
+    rate, dt = _port_rate(spec, g, steps, cores)
+    desc = (f"C restatement of scalar_reference (bit-exact; not the reference's NumPy code), full "
+            f"{'x'.join(map(str, cfg['extents']))} grid, {steps} of {cfg['T']} {'sweeps' if gauss else 'steps'}, "
+            f"{dt:.1f} s in the step loop, {cores} thread(s)")
     return rate, cores, desc
 
 
-def measure_config(cfg, K, W, with_e2e=True, with_cpu=True, min_timed_s=0.0):
+def measure_config(cfg, K, W, with_e2e=True, with_cpu=True, min_timed_s=0.0, with_stock=False):
     hbm_peak, peak_src = peaks()
     pts = int(np.prod(cfg["extents"]))
     updates = pts * cfg["T"]
@@ -347,9 +405,17 @@ def measure_config(cfg, K, W, with_e2e=True, with_cpu=True, min_timed_s=0.0):
         ems = statistics.mean(etimes)
         res["e2e"] = {"value": updates / (ems * 1e-3) / 1e9, "unit": "GStencil/s", "ms_per_step": ems,
                       "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
+    if with_e2e and with_stock:
+        st = e2e_stock_time(cfg, max(2, min(K, 3)), 1)
+        sms = statistics.mean(st)
+        nbytes = int(np.prod(cfg["extents"])) * 8
+        res["e2e_stock"] = {"value": updates / (sms * 1e-3) / 1e9, "unit": "GStencil/s", "ms_per_step": sms,
+                            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                            "note": "fn(grid, T) on the default pageable Grid, result Grid allocated by the call"}
     if with_cpu:
         rate, cores, desc = cpu_sample(cfg)
-        res["cpu_baseline"] = {"value": rate, "unit": "GStencil/s", "cores": cores, "kind": "port", "sample": desc}
+        res["cpu_baseline"] = {"value": rate, "unit": "GStencil/s", "cores": cores, "kind": "port", "sample": desc,
+                               "numpy_reference_path": numpy_reference_rate(cfg)}
     return res
 
 
@@ -464,12 +530,17 @@ def integer_legs(args):
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (oracle port) on the host."""
+    """--impl reference: the reference's CPU path on the host.  The reference
+    is pure Python (nothing to compile into oracle/_ref), so the arm times
+    the oracle port: the bit-exact C restatement of scalar_reference on all
+    host cores (Gauss-Seidel: one), timed inside its step loop exactly like
+    the cpu_baseline leg of our arm (so the two agree), each step a bounded
+    sample of the workload (full grid, T_cpu steps).  The NumPy restatement
+    of the reference's own code path (1 core) is reported beside it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     cfg = CONFIGS[args.config]
-    from oracle import cref
     from paper_2010_04868_b200.catalog import get
 
     spec = get(cfg["kernel"]).spec
@@ -477,28 +548,27 @@ def run_reference(args):
     gauss = spec.dependence_kind == "gauss_seidel"
     cores = 1 if gauss else (os.cpu_count() or 1)
     pts = int(np.prod(cfg["extents"]))
-    t0 = time.perf_counter()
-    cref.scalar_reference(spec, g, 1, order="lexicographic", threads=cores)
-    one = time.perf_counter() - t0
-    budget = 150.0 / max(1, args.steps + args.warmup)
+    _, one = _port_rate(spec, g, 1, cores)
+    budget = 120.0 / max(1, args.steps + args.warmup)
     t_cpu = int(max(1, min(cfg["T"], budget / max(one, 1e-6))))
     times = []
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        cref.scalar_reference(spec, g, t_cpu, order="lexicographic", threads=cores)
+        _, dt = _port_rate(spec, g, t_cpu, cores)
         if i >= args.warmup:
-            times.append(time.perf_counter() - t0)
+            times.append(dt)
     sec = statistics.mean(times)
     value = pts * t_cpu / sec / 1e9
-    desc = (f"oracle C port of scalar_reference (reference not compiled: pure Python), full "
-            f"{'x'.join(map(str, cfg['extents']))} grid, {t_cpu} of {cfg['T']} steps per step")
+    desc = (f"C restatement of scalar_reference (the reference is pure Python: nothing to compile), full "
+            f"{'x'.join(map(str, cfg['extents']))} grid, {t_cpu} of {cfg['T']} steps per step, timed in the "
+            f"step loop, {cores} thread(s)")
     line = {
         "metric": "GStencil/s", "value": value, "unit": "GStencil/s", "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE seeds)",
         "config": {"workload": f"{cfg['name']} {'x'.join(map(str, cfg['extents']))} T={cfg['T']}",
                    "sample_steps": t_cpu},
-        "cpu_baseline": {"value": value, "unit": "GStencil/s", "cores": cores, "kind": "port", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "GStencil/s", "cores": cores, "kind": "port", "sample": desc,
+                         "numpy_reference_path": numpy_reference_rate(cfg)},
         "e2e": {"value": value, "unit": "GStencil/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -806,7 +876,7 @@ def main():
     if args.gpus > 1:
         return run_in_process(args)
     cfg = CONFIGS[args.config]
-    head = measure_config(cfg, args.steps, args.warmup, with_e2e=True, with_cpu=not args.no_cpu)
+    head = measure_config(cfg, args.steps, args.warmup, with_e2e=True, with_cpu=not args.no_cpu, with_stock=True)
     line = {
         "metric": "GStencil/s", "value": head["value"], "unit": "GStencil/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
@@ -814,6 +884,7 @@ def main():
         "config": {"workload": head["workload"], "l2": "inputs larger than L2 (2.1 GB per grid)",
                    "parallelism": "single GPU", "fma": "exact (power-of-two weights fused bit-identically)"},
         "gpu_launches": head["gpu_launches"], "clocks": head["clocks"], "e2e": head.get("e2e"),
+        "e2e_stock": head.get("e2e_stock"),
         "roofline": head["roofline"], "fp64": head["fp64"], "cpu_baseline": head.get("cpu_baseline"),
     }
     try:  # whole-grid parity at full size (tests/test_full_grid.py, committed evidence)

@@ -36,6 +36,7 @@ def lib():
         _lib = C.CDLL(_SO)
         _lib.oracle_jacobi.argtypes = [C.POINTER(Problem), C.c_void_p, C.c_void_p, C.c_int64, C.c_int]
         _lib.oracle_gauss_seidel.argtypes = [C.POINTER(Problem), C.c_void_p, C.c_int64, C.c_int, C.c_int]
+        _lib.oracle_last_seconds.restype = C.c_double
     return _lib
 
 
@@ -73,3 +74,9 @@ def scalar_reference(spec, grid, steps, order="reference", threads=0):
     if rc != 0:
         raise MemoryError("oracle allocation failed")
     return out
+
+
+def last_seconds() -> float:
+    """Seconds the last scalar_reference call spent in its step / sweep loop
+    (allocations and copies excluded): the timed CPU-baseline figure."""
+    return float(lib().oracle_last_seconds())

@@ -7,9 +7,20 @@
 
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
+
+/* seconds spent in the step / sweep loop of the last call (excludes the
+ * allocations and copies around it): the timed CPU baseline's figure */
+static double g_last_seconds = 0.0;
+double oracle_last_seconds(void) { return g_last_seconds; }
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
 
 static int64_t lin_off(const oracle_problem* p, const int32_t* o) {
   if (p->dim == 1) return o[0];
@@ -53,6 +64,7 @@ int oracle_jacobi(const oracle_problem* p, const double* in, double* out, int64_
   const int64_t s1 = p->dim == 1 ? 1 : (p->dim == 2 ? 1 : p->shape[2]);
   const int64_t s0 = p->dim == 1 ? 1 : (p->dim == 2 ? p->shape[1] : p->shape[1] * p->shape[2]);
   const int64_t o = p->offset;
+  const double t0 = now_s();
   for (int64_t t = 0; t < steps; ++t) {
     if (p->dim == 1) {
 #pragma omp parallel for schedule(static)
@@ -69,6 +81,7 @@ int oracle_jacobi(const oracle_problem* p, const double* in, double* out, int64_
     a = b;
     b = tmp;
   }
+  g_last_seconds = now_s() - t0;
   memcpy(out, a, sizeof(double) * n);
   free(a);
   free(b);
@@ -127,7 +140,9 @@ int oracle_gauss_seidel(const oracle_problem* p, double* grid, int64_t steps, in
   int64_t lin[27];
   for (int k = 0; k < p->ntaps; ++k) lin[k] = lin_off(p, p->offsets[k]);
   if (order == 0 || p->dim == 1) {
+    const double t0 = now_s();
     for (int64_t t = 0; t < steps; ++t) gs_lex(p, grid, lin);
+    g_last_seconds = now_s() - t0;
     return 0;
   }
   int64_t cap = p->extents[0] * (p->dim > 1 ? p->extents[1] : 1) * (p->dim > 2 ? p->extents[2] : 1);
@@ -138,7 +153,9 @@ int oracle_gauss_seidel(const oracle_problem* p, double* grid, int64_t steps, in
     free(idxbuf);
     return 1;
   }
+  const double t0 = now_s();
   for (int64_t t = 0; t < steps; ++t) gs_antidiag(p, grid, lin, buf, idxbuf);
+  g_last_seconds = now_s() - t0;
   free(buf);
   free(idxbuf);
   return 0;

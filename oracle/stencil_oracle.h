@@ -23,4 +23,6 @@ int oracle_jacobi(const oracle_problem* p, const double* in, double* out, int64_
 /* `steps` in-place Gauss-Seidel sweeps. order 0: row-major lexicographic
  * loop; 1: anti-diagonal gather/scatter (the reference oracle's order). */
 int oracle_gauss_seidel(const oracle_problem* p, double* grid, int64_t steps, int order, int threads);
+/* seconds in the step / sweep loop of the last call on this process */
+double oracle_last_seconds(void);
 #endif

@@ -64,13 +64,17 @@ struct ScratchSlot {
   size_t bytes = 0;
   int device = -1;
 };
-static thread_local ScratchSlot g_scratch[4];
+static thread_local ScratchSlot g_scratch[kScratchSlots];
+static thread_local uint64_t g_scratch_gen = 1;  // bumped whenever a slot is (re)allocated or freed
+
+uint64_t scratch_generation() { return g_scratch_gen; }
 
 void* scratch(size_t bytes, int slot) {
   int dev = 0;
   cudaGetDevice(&dev);
   ScratchSlot& s = g_scratch[slot];
   if (s.ptr && s.bytes >= bytes && s.device == dev) return s.ptr;
+  ++g_scratch_gen;
   if (s.ptr) {
     int cur = dev;
     cudaSetDevice(s.device);
@@ -329,12 +333,28 @@ static int jacobi_device(const tvs_stencil& st, const tvs_geometry& g, double* s
   return TVS_OK;
 }
 
+// 2D Gauss-Seidel lexicographic kernel: 1 = the K6 pipeline (gs2d_pipe.cu,
+// default), 0 = K6v2 lane groups (gs2d_lane.cu) — TVS_GS2D=lane|pipe.  The
+// reference order always runs on K6v2 (K6 has no reference-order form).
+static int gs2d_kernel_choice() {
+  static const int v = [] {
+    const char* e = getenv("TVS_GS2D");
+    return e && std::string(e) == "lane" ? 0 : 1;
+  }();
+  return v;
+}
+
 static int gs_device(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, const tvs_exec& ex,
                      cudaStream_t s) {
   if (g.axis0_offset != 0 || g.axis0_global != g.extents[0])
     return fail(TVS_ERR_UNSUPPORTED, "Gauss-Seidel runs on a single GPU (no slab decomposition)");
   if (steps == 0) return TVS_OK;
   if (g.dim == 1 && ex.algo != TVS_ALGO_NAIVE) return gs1d_pipeline(st, g, grid, steps, s);
+  // (reference order with one sweep: the pass's only sweep would overwrite
+  // row d-1 in place while the next CTA still reads it as "old": wavefront)
+  if (g.dim == 2 && ex.algo != TVS_ALGO_NAIVE && gs2d_lane_supported(st) &&
+      (gs2d_kernel_choice() == 0 || ex.gs_order == TVS_GS_REFERENCE) && !(ex.gs_order == TVS_GS_REFERENCE && steps < 2))
+    return gs2d_lane(st, g, grid, steps, ex.gs_order, s);
   if (g.dim == 2 && ex.algo != TVS_ALGO_NAIVE && ex.gs_order == TVS_GS_LEXICOGRAPHIC && gs2d_pipe_supported(st))
     return gs2d_pipeline(st, g, grid, steps, s);
   return gs_wavefront(st, g, grid, steps, ex.gs_order, s);
@@ -918,6 +938,7 @@ int tvs_release_thread_cache(void) {
   // plus its kernel scratch (reference ThreadPool workers: tiling.py:363-367)
   g_run.release();
   g_group.release();
+  ++g_scratch_gen;
   for (auto& sl : g_scratch) {
     if (!sl.ptr) continue;
     int cur = 0;
@@ -1079,7 +1100,8 @@ int tvs_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, doub
   }
   if (gs) {
     const int64_t band = band_rows_default();
-    if (band > 0 && st->dim == 2 && steps > 0 && steps <= gs2d_pipe_max_sweeps() && ex->algo != TVS_ALGO_NAIVE &&
+    if (gs2d_kernel_choice() == 1 && band > 0 && st->dim == 2 && steps > 0 && steps <= gs2d_pipe_max_sweeps() &&
+        ex->algo != TVS_ALGO_NAIVE &&
         ex->gs_order == TVS_GS_LEXICOGRAPHIC && gs2d_pipe_supported(*st) && c.geo.extents[0] >= 4 * band) {
       rc = gs2d_pipelined(*st, *lay, in, out, steps, c, band);
       if (rc != TVS_ERR_UNSUPPORTED) return rc;  // no stream memory operations: plain path below

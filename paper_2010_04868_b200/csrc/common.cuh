@@ -259,6 +259,9 @@ int gs2d_pipeline(const tvs_stencil& st, const tvs_geometry& g, double* grid, in
 int64_t gs2d_pipe_blocks(int64_t rows);
 int64_t gs2d_pipe_blocks_for_row(int64_t row, int64_t steps);
 int gs2d_pipe_max_sweeps();
+// K6v2 (gs2d_lane.cu): one-warp time-lane groups, both update orders
+bool gs2d_lane_supported(const tvs_stencil& st);
+int gs2d_lane(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, int order, cudaStream_t s);
 int gs_wavefront(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, int order,
                  cudaStream_t s);
 
@@ -288,7 +291,12 @@ struct ShardGroup {
 // does tvs_exec ask for (and the stencil allow) a sharded run?
 bool wants_shards(const tvs_stencil& st, const tvs_exec& ex);
 
-// scratch device memory owned by the calling thread (grown on demand)
+// scratch device memory owned by the calling thread (grown on demand).
+// Slots: 0, 1 GS-1D / GS-2D pipeline rings and control words, 2 small
+// constants, 3 drop-in pipeline counters, 4, 5 GS-2D lane ring and control.
+constexpr int kScratchSlots = 6;
 void* scratch(size_t bytes, int slot);
+// changes whenever this thread's scratch memory is (re)allocated or freed
+uint64_t scratch_generation();
 
 }  // namespace tvs

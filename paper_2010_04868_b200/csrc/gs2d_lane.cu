@@ -1,0 +1,544 @@
+// K6v2: 2D radius-1 Gauss-Seidel (9-point box / 5-point star) as time-lane
+// groups advancing in per-iteration CTA lockstep.
+//
+// Replaces gs2d_temporal (reference kernels_nd.py:48-50, star-only there) for
+// the row-major in-place sweep of BASELINE config 4, bit-exact with the
+// oracle's lexicographic loop (oracle/stencil_oracle.c gs_lex; the reference
+// loop test test_baselines.py:39-52) and, with order = reference, with the
+// reference's anti-diagonal gather/scatter (baselines.py:83-107: the NE
+// neighbour is read from the previous sweep).
+//
+// The paper's time lanes.  A "group" is WG warps = 32*WG lanes; lane l runs
+// sweep t0 + l and group d owns the units {(sweep l, row d - l)} (a diagonal
+// through (time, row) space), streaming left to right over the columns, one
+// column per iteration.  Every input of unit (l, row r = d - l, column c) is
+//   NW, N, NE  row r-1, sweep l    = group d-1, lane l     (smem ring)
+//   W          row r,   sweep l    = my previous output    (register)
+//   C, E       row r,   sweep l-1  = group d-1, lane l-1   (smem ring)
+//   SW, S, SE  row r+1, sweep l-1  = group d,   lane l-1   (__shfl_up; a
+//                                     warp's lane 0 reads the ring)
+// (reference order: NE = row r-1, sweep l-1 = group d-2, lane l-1), where
+// "lane -1" of group d is grid row d+1 as it was before the pass (loaded by
+// the CTA's loader warp).  Lane l trails lane l-1 by 2 columns and group g
+// trails group g-1 by 2 iterations (LAM): the hyperplane slope of the
+// dependence graph (h = 2 row + column + 4 sweep), so the pipeline is no
+// longer than the computation's critical path.  Taps are summed in sorted
+// order (NW N NE W C E SW S SE), unfused: bit-exact.
+//
+// CTA = G groups (G*WG compute warps) + a loader warp, one CTA barrier per
+// iteration: every warp does identical work per iteration, so lockstep costs
+// only the barrier, and everything a warp reads from shared memory was
+// written before the previous barrier.  The loader prefetches, ahead of use,
+// the grid rows of every group's lane -1 (cp.async) and the previous CTA's
+// last group(s) ("phantom" groups).  CTA-to-CTA hand-off is fence-free: the
+// producer's last groups store every output to an L2 ring whose cells hold a
+// signalling-NaN sentinel until written (arithmetic never yields a
+// signalling NaN, and the boundary value is checked on the host), the
+// consumer's loader polls the cells themselves (8-byte single-copy atomic)
+// and puts the sentinel back after reading, so the ring is clean for its next
+// use.  CTAs take tickets and only wait on lower tickets; a ring slot is
+// reused only after its consumer has exited.  Units outside the grid output
+// the boundary; lane Tp-1 (the pass's last sweep) writes its row's final
+// values to the grid in place.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace tvs {
+namespace gsl {
+constexpr int kLam = 2;          // group lag (iterations)
+constexpr int kB = 2;            // every lane starts >= 2 columns left of column 0
+constexpr int kR = 16;           // smem ring rows (iterations), power of two
+constexpr int kPre = 6;          // phantom / lane -1 rows read before iteration 0 (rows -6..-1)
+constexpr int kLR = 64;          // lane -1 staging ring (iterations), power of two
+constexpr int kBatch = 8;        // lane -1 rows per cp.async batch
+constexpr int kAheadL = 32;      // lane -1 rows are loaded this many iterations ahead (4 batches in flight)
+#ifndef GSL_AHEADP
+#define GSL_AHEADP 4
+#endif
+constexpr int kAheadP = GSL_AHEADP;  // phantom rows polled this many iterations ahead (registers)
+constexpr int kNumSlots = 320;   // global ring slots (CTA boundaries in flight) >= resident CTAs
+// sentinel of an unwritten global-ring cell: a signalling NaN (quiet bit
+// clear), which no arithmetic result can be
+constexpr unsigned long long kSent = 0x7FF4DEADBEEF0001ull;
+
+template <bool REF, int WG>
+struct Cfg {
+  static constexpr int G = 4;                   // groups per CTA
+  static constexpr int Ph = REF ? 2 : 1;        // phantom groups (reads reach group d-2 in REF)
+  static constexpr int L = 32 * WG;             // lanes per group
+  static constexpr int S = L + 2;               // ring row: [pad][lane -1][lanes 0..L-1] (16-B aligned lanes)
+  static constexpr int Rings = G + Ph;          // ring index = local group + Ph
+  static constexpr int Compute = G * WG;        // compute warps
+  static constexpr int Threads = (Compute + 1) * 32;
+  static constexpr size_t Smem = sizeof(double) * ((size_t)Rings * kR * S + (size_t)Rings * kLR);
+  static constexpr int Back = REF ? 2 * kLam + 1 : kLam + 1;  // deepest ring read behind m
+  static_assert(kR >= Back + 3, "ring too shallow");
+  static_assert(kLR >= kAheadL + kBatch + kPre && kAheadL % kBatch == 0 && kR % kBatch == 0, "lane -1 staging");
+  static_assert(kPre >= Back + 1, "prologue shorter than the deepest read");
+  static_assert(kR % kAheadP == 0 && kR >= kPre, "ring / queue sizes");
+};
+}  // namespace gsl
+
+#ifdef GSL_TRACE
+// [cta][0] start ns, [1] first iteration ns, [2] end ns, [3] loader poll-spin cycles,
+// [4] loader cp.async wait cycles, [5] compute warp 0 barrier-wait cycles, [6] loader barrier-wait cycles
+__device__ unsigned long long g_gsl_trace[8192][8];
+__device__ __forceinline__ unsigned long long gsl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
+struct GslArgs {
+  double* a;          // interior origin (in place)
+  long long s0;       // row pitch (elements)
+  int e0, e1;         // rows, columns
+  int tp;             // sweeps of this pass (<= 32 * WG)
+  int nctas;
+  int m_end;          // iterations per CTA (multiple of kR)
+  double* gring;      // kNumSlots x m_end x Ph x L (sentinel until written)
+  int* done;          // [slot]: consumer CTAs of this slot that exited (their ticket)
+  int* ticket;
+  double w[9];
+  double bnd;
+};
+
+// 9 sorted taps NW N NE W C E SW S SE (mask bit k = tap k), unfused
+template <unsigned MASK>
+__device__ __forceinline__ double gsl_taps(const double* w, double nw, double n, double ne, double ww, double c,
+                                           double e, double sw, double s, double se) {
+  const double v[9] = {nw, n, ne, ww, c, e, sw, s, se};
+  double acc = 0.0;
+  bool first = true;
+#pragma unroll
+  for (int k = 0; k < 9; ++k)
+    if ((MASK >> k) & 1u) {
+      acc = first ? tap_first(w[k], v[k]) : tap_next<false>(w[k], v[k], acc);
+      first = false;
+    }
+  return acc;
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smaddr(smem)), "l"(gmem));
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(double* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cta_bar(int nthreads) { asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory"); }
+
+#ifndef GSL_MINB
+#define GSL_MINB 2
+#endif
+template <unsigned MASK, bool REF, int WG>
+__global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB) gs2d_lane_kernel(GslArgs p) {
+  using namespace gsl;
+  using C = Cfg<REF, WG>;
+  constexpr int kG = C::G, kPh = C::Ph, kL = C::L, kS = C::S, kRings = C::Rings;
+  constexpr int kBarThreads = C::Compute * 32;  // the per-iteration barrier: compute warps only
+  extern __shared__ __align__(16) double smem[];
+  double* const lm1 = smem + (size_t)kRings * kR * kS;  // lane -1 staging [ring][kLR]
+  __shared__ int s_ticket;
+  __shared__ volatile int s_ready;  // loader: phantom and lane -1 rows < s_ready are in shared memory
+  __shared__ volatile int s_iter;   // compute: iterations < s_iter are finished by every compute warp
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const double bnd = p.bnd;
+  // every ring cell starts as the boundary (iterations before 0 are columns
+  // left of the grid)
+  for (int i = threadIdx.x; i < kRings * (kR * kS + kLR); i += blockDim.x) smem[i] = bnd;
+  if (threadIdx.x == 0) {
+    s_ticket = atomicAdd(p.ticket, 1);
+    s_ready = -kPre;
+    s_iter = 0;
+  }
+  __syncthreads();
+  const int n = s_ticket;  // position in the CTA chain
+#ifdef GSL_TRACE
+  if (threadIdx.x == 0 && n < 8192) g_gsl_trace[n][0] = gsl_now();
+  unsigned long long tr_bar = 0, tr_poll = 0, tr_cpw = 0;
+#endif
+  const int d0 = n * kG;   // global group of local group 0
+  const int m_end = p.m_end;
+  const int e0 = p.e0, e1 = p.e1;
+  const int slot_in = (n - 1 + kNumSlots) % kNumSlots, slot_out = n % kNumSlots;
+#ifdef GSL_NO_UP  // experiment: no CTA-to-CTA hand-off (wrong results; timing only)
+  const bool has_up = false, has_down = false;
+#else
+  const bool has_up = n > 0, has_down = n + 1 < p.nctas;
+#endif
+  double* gin = p.gring + (size_t)slot_in * m_end * kPh * kL;
+  double* gout = p.gring + (size_t)slot_out * m_end * kPh * kL;
+  if (has_down && n >= kNumSlots && threadIdx.x == 0) {
+    // ring slot reuse: the consumer of boundary n - kNumSlots (a lower
+    // ticket, so started) must have exited before this CTA writes the slot
+    const long long t0 = clock64();
+    while (ld_acquire_gpu32(p.done + slot_out) < n - kNumSlots + 1) {
+      __nanosleep(256);
+      if (clock64() - t0 > (1ll << 34)) __trap();
+    }
+  }
+  __syncthreads();
+  // producer rows a consumer reads: its rows >= -kPre, i.e. >= LAM*G - kPre here
+  const int ring_lo = kLam * kG - kPre;
+
+  if (wi < C::Compute) {
+    // ---------------- compute warp: group g, lanes l = 32 w + t ----------
+    const int g = wi / WG, w = wi % WG, l = 32 * w + lane;
+    const int d = d0 + g, row = d - l;
+    const int col0 = -kLam * g - 2 * l - kB;  // my column at iteration 0
+    double* const ring_me = smem + (size_t)(g + kPh) * kR * kS;
+    const double* const ring_up = ring_me - kR * kS;
+    const double* const ring_up2 = ring_me - 2 * kR * kS;
+    // lane 0 of a group reads lane -1 (grid rows) from the staging ring
+    const double* const lm1_me = lm1 + (g + kPh) * kLR;
+    const bool first = l == 0;
+    const bool emit = l == p.tp - 1;  // last sweep of the pass: final values
+    double* const arow = p.a + (long long)row * p.s0;
+    const bool to_ring = has_down && g >= kG - kPh;  // phantom source of the next CTA
+    double* const gdst = gout + (size_t)(g - (kG - kPh)) * kL + l;
+    // this warp's lanes all inside the grid (rows, and columns for iterations
+    // [m_in0, m_in1)): the steady body needs no selects
+    const bool rows_in = d - 32 * w - 31 >= 0 && d - 32 * w <= e0 - 1;
+    const int m_in0 = kLam * g + 64 * w + 62 + kB, m_in1 = kLam * g + 64 * w + kB + e1;
+    const bool row_ok = row >= 0 && row < e0;
+    const bool waiter = wi == 0;  // acquires the loader's rows for the whole CTA (the barrier forwards them)
+    double nw = bnd, nn = bnd, ne = bnd, ww = bnd, cc = bnd, ee = bnd, sw = bnd, ss = bnd, se = bnd;
+    double out = bnd;
+    for (int mb = 0; mb < m_end; mb += kR) {
+      const bool steady = rows_in && mb >= m_in0 && mb + kR <= m_in1;
+      auto block = [&](auto steady_tag) {
+        constexpr bool ST = decltype(steady_tag)::value;
+#pragma unroll
+        for (int u = 0; u < kR; ++u) {
+          const int m = mb + u;
+          if (waiter) {
+            // rows < m of the phantom and lane -1 rings (read below) landed
+            if (s_ready < m) {
+#ifdef GSL_TRACE
+              const long long tw = clock64();
+#endif
+              const long long t0 = clock64();
+              while (s_ready < m)
+                if (clock64() - t0 > (1ll << 34)) __trap();
+#ifdef GSL_TRACE
+              tr_poll += clock64() - tw;
+#endif
+            }
+            __syncwarp();
+            __threadfence_block();
+          }
+#ifdef GSL_TRACE
+          const long long tb0 = clock64();
+#endif
+          cta_bar(kBarThreads);  // iteration m-1 done everywhere; the loader's rows < m visible
+#ifdef GSL_TRACE
+          tr_bar += clock64() - tb0;
+#endif
+          if (waiter && lane == 0) s_iter = m;  // iterations < m finished by every compute warp
+          const int r1 = ((u - 1) & (kR - 1)) * kS, r3 = ((u - kLam - 1) & (kR - 1)) * kS;
+          const double ne_new = ring_up[r1 + 2 + l];  // group d-1, lane l, iteration m-1
+          // group d-1, lane l-1, iteration m-3 (lane 0: lane -1 of group d-1 = grid row d)
+          const double e_new = first ? lm1_me[-kLR + ((m - kLam - 1) & (kLR - 1))] : ring_up[r3 + 1 + l];
+          double se_new = __shfl_up_sync(0xffffffffu, out, 1);  // lane l-1, iteration m-1
+          if (lane == 0) se_new = first ? lm1_me[(m - 1) & (kLR - 1)] : ring_me[r1 + 1 + l];  // lane -1 / previous warp
+          nw = nn; nn = ne; ne = ne_new;
+          cc = ee; ee = e_new;
+          sw = ss; ss = se; se = se_new;
+          double ne_use = ne;
+          if constexpr (REF) {
+            // group d-2, lane l-1, iteration m-5 (lane 0: lane -1 of group d-2 = grid row d-1)
+            const int r5 = ((u - 2 * kLam - 1) & (kR - 1)) * kS;
+            ne_use = first ? lm1_me[-2 * kLR + ((m - 2 * kLam - 1) & (kLR - 1))] : ring_up2[r5 + 1 + l];
+          }
+          const double v = gsl_taps<MASK>(p.w, nw, nn, ne_use, ww, cc, ee, sw, ss, se);
+          bool inside = true;
+          if constexpr (ST) {
+            out = v;
+          } else {
+            const int c = col0 + m;
+            inside = row_ok && c >= 0 && c < e1;
+            out = inside ? v : bnd;
+          }
+          ww = out;
+          ring_me[(u & (kR - 1)) * kS + 2 + l] = out;
+          if (to_ring && m >= ring_lo) st_relaxed_gpu(gdst + (size_t)m * kPh * kL, __double_as_longlong(out));
+          if (emit && inside) arow[col0 + m] = out;
+        }
+      };
+      if (steady)
+        block(std::true_type{});
+      else
+        block(std::false_type{});
+    }
+    cta_bar(kBarThreads);
+    if (waiter && lane == 0) s_iter = m_end;
+#ifdef GSL_TRACE
+    if (wi == 0 && lane == 0 && n < 8192) {
+      g_gsl_trace[n][2] = gsl_now();
+      g_gsl_trace[n][5] = tr_bar;
+      g_gsl_trace[n][3] = tr_poll;
+    }
+#endif
+  } else {
+    // ---------------- loader (not in the per-iteration barrier) ------------
+    // Runs ahead of the compute warps as far as its rings allow and publishes
+    // s_ready: rows < s_ready of the lane -1 staging ring and of the phantom
+    // rings are in shared memory.
+    //  * lane -1 of ring ri (local group g = ri - kPh, global d0 + g) at
+    //    iteration i = grid row d0 + g + 1 at column i - LAM*g + 2 - B,
+    //    cp.async batches kAheadL iterations ahead (HBM latency);
+    //  * phantom rows: the previous CTA's last kPh groups at producer
+    //    iteration i + LAM*G (its local groups G-kPh.. are my -kPh..),
+    //    polled cell by cell (sentinel) and reset after reading.  Producer
+    //    rows >= m_end are columns right of the grid: the boundary.
+    auto batch_lane_m1 = [&](int i0) {  // iterations [i0, i0 + kBatch), every ring
+      for (int e = lane; e < kRings * kBatch; e += 32) {
+        const int ri = e / kBatch, i = i0 + e % kBatch;
+        const int g = ri - kPh;
+        const int r = d0 + g + 1, c = i - kLam * g + 2 - kB;
+        double* dst = lm1 + ri * kLR + (i & (kLR - 1));
+        if (r >= 0 && r < e0 && c >= 0 && c < e1)
+          cp_async8(dst, p.a + (long long)r * p.s0 + c);
+        else
+          *dst = bnd;
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    constexpr int kPer = kPh * kL / 32;  // cells per loader lane per row
+    auto cell = [&](int i, int q) -> double* {
+      const int e = lane + 32 * q, ph = e / kL, ll = e % kL;
+      return gin + ((size_t)(i + kLam * kG) * kPh + ph) * kL + ll;
+    };
+    auto put = [&](int i, int q, unsigned long long v) {
+      const int e = lane + 32 * q, ph = e / kL, ll = e % kL;
+      smem[((size_t)ph * kR + (i & (kR - 1))) * kS + 2 + ll] = __longlong_as_double(v);
+    };
+    auto in_ring = [&](int i) { return has_up && i + kLam * kG < m_end; };
+    int lm_issued = -kPre - 2;  // lane -1 rows < lm_issued are requested (batches of kBatch)
+    // prologue batches: rows [-kBatch, kAheadL)
+    for (lm_issued = -kBatch; lm_issued < kAheadL; lm_issued += kBatch) batch_lane_m1(lm_issued);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    int lm_ready = lm_issued;  // lane -1 rows < lm_ready have landed
+    int ph_next = -kPre;       // next phantom row to complete
+    // phantom poll window: rows ph_next .. ph_next + kAheadP - 1, loaded into
+    // registers; a row is complete when all its cells are non-sentinel
+    unsigned long long qv[kAheadP][kPer];
+#pragma unroll
+    for (int a = 0; a < kAheadP; ++a)
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) qv[a][q] = kSent;
+    const long long t_start = clock64();
+    while (ph_next < m_end || lm_ready < m_end + kLam) {
+      const int mc = s_iter;  // compute progress: rows they still read are >= mc - kPre
+      bool progressed = false;
+      // ---- lane -1 staging: keep kAheadL rows ahead, never overwrite rows still read
+      if (lm_issued < m_end + kBatch && lm_issued < mc + kLR - kPre - kBatch) {
+        batch_lane_m1(lm_issued);
+        lm_issued += kBatch;
+        progressed = true;
+      }
+      if (lm_issued - lm_ready >= kAheadL || lm_issued >= m_end + kBatch) {
+#ifdef GSL_TRACE
+        const long long tw0 = clock64();
+#endif
+        // the oldest batch in flight
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kAheadL / kBatch - 1) : "memory");
+#ifdef GSL_TRACE
+        tr_cpw += clock64() - tw0;
+#endif
+        lm_ready = max(lm_ready, lm_issued - kAheadL + kBatch);
+        if (lm_issued >= m_end + kBatch) {
+          asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+          lm_ready = lm_issued;
+        }
+      }
+      // ---- phantom rows: poll the window (qv[k] = row ph_next + k), complete
+      // the leading row when every cell of it is written
+      if (ph_next < m_end && ph_next < mc + kR - kPre - 1) {
+        bool ok = true;
+        const bool live0 = in_ring(ph_next);
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+          if (live0 && qv[0][q] == kSent) qv[0][q] = ld_relaxed_gpu(cell(ph_next, q));
+          ok = ok && (!live0 || qv[0][q] != kSent);
+        }
+        if (__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+          for (int q = 0; q < kPer; ++q) {
+            if (live0) {
+              put(ph_next, q, qv[0][q]);
+#ifndef GSL_NO_RESET
+              st_relaxed_gpu(cell(ph_next, q), kSent);
+#endif
+            } else {
+              put(ph_next, q, (unsigned long long)__double_as_longlong(bnd));
+            }
+          }
+#pragma unroll
+          for (int k = 0; k + 1 < kAheadP; ++k)
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) qv[k][q] = qv[k + 1][q];
+#pragma unroll
+          for (int q = 0; q < kPer; ++q) qv[kAheadP - 1][q] = kSent;
+          ++ph_next;
+          progressed = true;
+        }
+        // keep polls in flight for the rows after it
+#pragma unroll
+        for (int k = 1; k < kAheadP; ++k) {
+          const int i = ph_next + k;
+          if (i < m_end && in_ring(i)) {
+#pragma unroll
+            for (int q = 0; q < kPer; ++q)
+              if (qv[k][q] == kSent) qv[k][q] = ld_relaxed_gpu(cell(i, q));
+          }
+        }
+      }
+      // ---- publish
+      const int ready = min(lm_ready, ph_next);
+      __syncwarp();
+      if (lane == 0 && ready > s_ready) {
+        __threadfence_block();
+        s_ready = ready;
+      }
+      if (!progressed) __nanosleep(32);
+      if (clock64() - t_start > (1ll << 36)) __trap();
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+#ifdef GSL_TRACE
+    if (lane == 0 && n < 8192) {
+      g_gsl_trace[n][4] = tr_cpw;
+      g_gsl_trace[n][6] = tr_bar;
+    }
+#endif
+    if (has_up && lane == 0) {
+      // every read (and sentinel reset) of the incoming slot is done: release it
+      __threadfence();
+      atomicMax(p.done + slot_in, n);
+    }
+  }
+}
+
+__global__ void gsl_sentinel_kernel(unsigned long long* p, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = gsl::kSent;
+}
+
+static unsigned gsl_mask(const tvs_stencil& st, double w[9]) {
+  unsigned mask = 0;
+  int last = -1;
+  for (int k = 0; k < 9; ++k) w[k] = 0.0;
+  for (int k = 0; k < st.ntaps; ++k) {
+    const int pos = (st.offsets[k][0] + 1) * 3 + (st.offsets[k][1] + 1);
+    if (pos <= last) return 0;
+    last = pos;
+    mask |= 1u << pos;
+    w[pos] = st.coeffs[k];
+  }
+  return mask;
+}
+
+constexpr unsigned kGslStar = (1u << 1) | (1u << 3) | (1u << 4) | (1u << 5) | (1u << 7);
+
+bool gs2d_lane_supported(const tvs_stencil& st) {
+  double w[9];
+  const unsigned m = gsl_mask(st, w);
+  unsigned long long bb;
+  std::memcpy(&bb, &st.boundary, sizeof(bb));
+  return st.dim == 2 && (m == 0x1FFu || m == kGslStar) && bb != gsl::kSent;
+}
+
+template <unsigned MASK, bool REF, int WG>
+static int gsl_launch(GslArgs a, int64_t steps, int64_t per, cudaStream_t s) {
+  using namespace gsl;
+  using C = Cfg<REF, WG>;
+  auto kern = gs2d_lane_kernel<MASK, REF, WG>;
+  TVS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::Smem));
+  // the last group's lanes reach column e1 (the boundary the consumer reads)
+  const int m_need = a.e1 + kLam * (C::G - 1) + 2 * (C::L - 1) + kB + 2;
+  a.m_end = (m_need + kR - 1) / kR * kR;
+  const size_t cells = (size_t)kNumSlots * a.m_end * C::Ph * C::L;
+  const size_t ctrl_bytes = sizeof(int) * kNumSlots + 64;
+  a.gring = static_cast<double*>(scratch(sizeof(double) * cells, 4));
+  char* ctrl = static_cast<char*>(scratch(ctrl_bytes, 5));
+  if (!a.gring || !ctrl) return fail(TVS_ERR_CUDA, "gs2d_lane: scratch");
+  a.done = reinterpret_cast<int*>(ctrl);
+  a.ticket = a.done + kNumSlots;
+  // every ring cell unwritten.  Consumers reset every cell they read and
+  // every written cell is read, so a ring stays clean after a launch: the
+  // sentinel fill runs only when the buffer or its layout changes
+  static thread_local uint64_t clean_gen = 0;
+  static thread_local size_t clean_cells = 0;
+  if (clean_gen != scratch_generation() || clean_cells != cells) {
+    gsl_sentinel_kernel<<<1184, 256, 0, s>>>(reinterpret_cast<unsigned long long*>(a.gring), cells);
+    TVS_LAUNCHED("gsl_sentinel_kernel");
+    clean_gen = scratch_generation();
+    clean_cells = cells;
+  }
+  for (int64_t done = 0; done < steps; done += per) {
+    a.tp = (int)std::min<int64_t>(per, steps - done);
+    const int ngroups = a.e0 + a.tp - 1;
+    a.nctas = (ngroups + C::G - 1) / C::G;
+    TVS_CUDA(cudaMemsetAsync(ctrl, 0, ctrl_bytes, s));
+    kern<<<a.nctas, C::Threads, C::Smem, s>>>(a);
+    TVS_LAUNCHED("gs2d_lane_kernel");
+  }
+  return TVS_OK;
+}
+
+#ifdef GSL_TRACE
+extern "C" int tvs_gsl_trace(unsigned long long* host, int n) {
+  TVS_CUDA(cudaDeviceSynchronize());
+  TVS_CUDA(cudaMemcpyFromSymbol(host, g_gsl_trace, sizeof(unsigned long long) * 8 * std::min(n, 8192)));
+  return 0;
+}
+#endif
+
+int gs2d_lane(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, int order, cudaStream_t s) {
+  double w[9];
+  const unsigned mask = gsl_mask(st, w);
+  if (!gs2d_lane_supported(st)) return fail(TVS_ERR_UNSUPPORTED, "gs2d_lane: tap set / boundary");
+  if (g.extents[0] >= (1ll << 30) || g.extents[1] >= (1ll << 28)) return fail(TVS_ERR_UNSUPPORTED, "gs2d_lane: extent");
+  if (steps <= 0) return TVS_OK;
+  GslArgs a{};
+  a.a = grid + g.origin;
+  a.s0 = g.strides[0];
+  a.e0 = (int)g.extents[0];
+  a.e1 = (int)g.extents[1];
+  for (int k = 0; k < 9; ++k) a.w[k] = w[k];
+  a.bnd = st.boundary;
+  // lanes per group = the smallest warp multiple holding a pass of <= 128
+  // sweeps in balanced passes (T = 100: one pass on 4-warp groups)
+  const int64_t npass = (steps + 127) / 128;
+  const int64_t per = (steps + npass - 1) / npass;
+  const int wg = per <= 32 ? 1 : (per <= 64 ? 2 : 4);
+  const bool ref = order == TVS_GS_REFERENCE, box = mask == 0x1FFu;
+  auto go = [&](auto m_tag, auto r_tag) -> int {
+    constexpr unsigned M = decltype(m_tag)::value;
+    constexpr bool R = decltype(r_tag)::value;
+    if (wg == 1) return gsl_launch<M, R, 1>(a, steps, per, s);
+    if (wg == 2) return gsl_launch<M, R, 2>(a, steps, per, s);
+    return gsl_launch<M, R, 4>(a, steps, per, s);
+  };
+  using Box = std::integral_constant<unsigned, 0x1FFu>;
+  using Star = std::integral_constant<unsigned, kGslStar>;
+  if (box) return ref ? go(Box{}, std::true_type{}) : go(Box{}, std::false_type{});
+  return ref ? go(Star{}, std::true_type{}) : go(Star{}, std::false_type{});
+}
+
+}  // namespace tvs

@@ -89,7 +89,7 @@ __device__ __forceinline__ void level_row(double (&F)[kP2], double (&M)[kP2], co
 }
 
 template <unsigned MASK, int D, bool FMA, int kP2, bool MIR>
-__global__ void __launch_bounds__(kWarps2 * 32) jacobi2d_kernel(const double* __restrict__ src,
+__global__ void __maxnreg__(192) jacobi2d_kernel(const double* __restrict__ src,
                                                                 double* __restrict__ dst, Geo g, int64_t origin,
                                                                 Coeff9 cf, double bnd, int64_t n_strips,
                                                                 int64_t n_tasks, int64_t row_lo, int64_t row_hi, int seg_rows,

@@ -84,7 +84,7 @@ __device__ __forceinline__ int64_t lin_index(const TileGeo& g, int64_t x0, int64
 
 // one CTA per tile of the wave; KIND 0 Jacobi fp64, 1 Gauss-Seidel fp64, 2 Life int32
 template <int KIND>
-__global__ void __launch_bounds__(256) tile_wave_kernel(void* hist, TileGeo g, const TileDev* __restrict__ tiles,
+__global__ void __maxnreg__(128) tile_wave_kernel(void* hist, TileGeo g, const TileDev* __restrict__ tiles,
                                                         FpTaps ft, LifeT lt) {
   const TileDev tl = tiles[blockIdx.x];
   for (int t = tl.t0; t < tl.t1; ++t) {

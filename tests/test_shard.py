@@ -233,3 +233,34 @@ def test_halo_sharded_jacobi_cuda_steps(cuda_ready):
     edge passes and the plain form), 2 ranks on gloo."""
     outs = _run_ranks(HALO_SCRIPT, 2)
     assert outs[0].count("ok ") == 4
+
+
+def test_thread_cache_release_bounds_hbm(cuda_ready):
+    """tvs_run keeps per-thread device buffers between calls; 8 pool workers
+    (the reference's ThreadPool pattern, tiling.py:363-367) each release
+    theirs with tvs_release_thread_cache, and device memory returns to the
+    baseline (cached buffers were never released)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+
+    torch.cuda.init()
+    g = Grid.random((192, 160, 200), seed=3)
+    want = jacobi3d_temporal(g, 2, kernel="jac3d27p").interior
+    _native.release_thread_cache()
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+
+    def work(_):
+        got = jacobi3d_temporal(g, 2, kernel="jac3d27p").interior
+        held = torch.cuda.mem_get_info()[0]
+        _native.release_thread_cache()
+        return np.array_equal(got, want), held
+
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        res = list(pool.map(work, range(8)))
+    assert all(ok for ok, _ in res)
+    assert min(h for _, h in res) < free0 - 100 * 2 ** 20  # the buffers were really cached while in use
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free1 > free0 - 64 * 2 ** 20, (free0, free1)

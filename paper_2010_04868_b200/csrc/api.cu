@@ -333,13 +333,14 @@ static int jacobi_device(const tvs_stencil& st, const tvs_geometry& g, double* s
   return TVS_OK;
 }
 
-// 2D Gauss-Seidel lexicographic kernel: 1 = the K6 pipeline (gs2d_pipe.cu,
-// default), 0 = K6v2 lane groups (gs2d_lane.cu) — TVS_GS2D=lane|pipe.  The
-// reference order always runs on K6v2 (K6 has no reference-order form).
+// 2D Gauss-Seidel kernel: 0 = K6v2 lane groups (gs2d_lane.cu, default; config
+// 4 26.0 ms), 1 = the round-1 K6 pipeline (gs2d_pipe.cu, 31.3 ms; kept for the
+// overlapped drop-in copies) — TVS_GS2D=lane|pipe.  The reference order always
+// runs on K6v2 (K6 has no reference-order form).
 static int gs2d_kernel_choice() {
   static const int v = [] {
     const char* e = getenv("TVS_GS2D");
-    return e && std::string(e) == "lane" ? 0 : 1;
+    return e && std::string(e) == "pipe" ? 1 : 0;
   }();
   return v;
 }

@@ -53,13 +53,12 @@ constexpr int kLam = 2;          // group lag (iterations)
 constexpr int kB = 2;            // every lane starts >= 2 columns left of column 0
 constexpr int kR = 16;           // smem ring rows (iterations), power of two
 constexpr int kPre = 6;          // phantom / lane -1 rows read before iteration 0 (rows -6..-1)
-constexpr int kLR = 64;          // lane -1 staging ring (iterations), power of two
-constexpr int kBatch = 8;        // lane -1 rows per cp.async batch
-constexpr int kAheadL = 32;      // lane -1 rows are loaded this many iterations ahead (4 batches in flight)
-#ifndef GSL_AHEADP
-#define GSL_AHEADP 4
+constexpr int kLR = 128;         // lane -1 staging ring (iterations), power of two
+#ifndef GSL_BATCH
+#define GSL_BATCH 2  // config 4 (8192^2 x 100): 8 / 4 / 2 rows = 44.3 / 33.8 / 29.3 ms
 #endif
-constexpr int kAheadP = GSL_AHEADP;  // phantom rows polled this many iterations ahead (registers)
+constexpr int kBatch = GSL_BATCH;  // lane -1 rows / phantom rows per loader block
+constexpr int kAheadL = 64;      // lane -1 rows are requested this many iterations ahead (HBM latency)
 constexpr int kNumSlots = 320;   // global ring slots (CTA boundaries in flight) >= resident CTAs
 // sentinel of an unwritten global-ring cell: a signalling NaN (quiet bit
 // clear), which no arithmetic result can be
@@ -67,19 +66,27 @@ constexpr unsigned long long kSent = 0x7FF4DEADBEEF0001ull;
 
 template <bool REF, int WG>
 struct Cfg {
-  static constexpr int G = 4;                   // groups per CTA
+#ifndef GSL_G
+#define GSL_G 0
+#endif
+  // groups per CTA: 4 (2 CTAs/SM) lexicographic, 7 (1 CTA/SM, its two
+  // phantom rings fill shared memory) reference order.  Config 4 lex G 3 / 4 /
+  // 7: 33.8 / 29.3 / 32.3 ms; reference 4 / 7: 85.6 / 58.2 ms
+  static constexpr int G = GSL_G > 0 ? GSL_G : (REF ? 7 : 4);
   static constexpr int Ph = REF ? 2 : 1;        // phantom groups (reads reach group d-2 in REF)
   static constexpr int L = 32 * WG;             // lanes per group
   static constexpr int S = L + 2;               // ring row: [pad][lane -1][lanes 0..L-1] (16-B aligned lanes)
   static constexpr int Rings = G + Ph;          // ring index = local group + Ph
   static constexpr int Compute = G * WG;        // compute warps
   static constexpr int Threads = (Compute + 1) * 32;
-  static constexpr size_t Smem = sizeof(double) * ((size_t)Rings * kR * S + (size_t)Rings * kLR);
+  static constexpr int Stg = 2 * kBatch * Ph * L;  // phantom staging: two blocks of kBatch compact rows
+  static constexpr size_t Smem = sizeof(double) * ((size_t)Rings * kR * S + (size_t)Rings * kLR + Stg);
   static constexpr int Back = REF ? 2 * kLam + 1 : kLam + 1;  // deepest ring read behind m
-  static_assert(kR >= Back + 3, "ring too shallow");
-  static_assert(kLR >= kAheadL + kBatch + kPre && kAheadL % kBatch == 0 && kR % kBatch == 0, "lane -1 staging");
-  static_assert(kPre >= Back + 1, "prologue shorter than the deepest read");
-  static_assert(kR % kAheadP == 0 && kR >= kPre, "ring / queue sizes");
+  static_assert(kR >= Back + kBatch + 1, "ring too shallow for a phantom block written ahead");
+  static_assert(kLR >= kAheadL + kBatch + 8, "lane -1 staging ring too shallow");
+  static_assert(kPre >= Back + 1, "prologue rows");
+  static constexpr int ProRows = (kPre + kBatch - 1) / kBatch * kBatch;  // phantom rows before iteration 0
+  static_assert(kR % kBatch == 0 && kAheadL % kBatch == 0, "block sizes");
 };
 }  // namespace gsl
 
@@ -127,6 +134,10 @@ __device__ __forceinline__ double gsl_taps(const double* w, double nw, double n,
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smaddr(smem)), "l"(gmem));
 }
+// L2-only (cg): the ring cells are written by other SMs
+__device__ __forceinline__ void cp_async16g(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smaddr(smem)), "l"(gmem));
+}
 __device__ __forceinline__ unsigned long long ld_relaxed_gpu(const double* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -149,23 +160,17 @@ template <unsigned MASK, bool REF, int WG>
 __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB) gs2d_lane_kernel(GslArgs p) {
   using namespace gsl;
   using C = Cfg<REF, WG>;
-  constexpr int kG = C::G, kPh = C::Ph, kL = C::L, kS = C::S, kRings = C::Rings;
-  constexpr int kBarThreads = C::Compute * 32;  // the per-iteration barrier: compute warps only
+  constexpr int kG = C::G, kPh = C::Ph, kL = C::L, kS = C::S, kRings = C::Rings, kThreads = C::Threads;
   extern __shared__ __align__(16) double smem[];
   double* const lm1 = smem + (size_t)kRings * kR * kS;  // lane -1 staging [ring][kLR]
+  double* const stg = lm1 + kRings * kLR;                 // phantom staging [2][kBatch][kPh * kL]
   __shared__ int s_ticket;
-  __shared__ volatile int s_ready;  // loader: phantom and lane -1 rows < s_ready are in shared memory
-  __shared__ volatile int s_iter;   // compute: iterations < s_iter are finished by every compute warp
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   const double bnd = p.bnd;
   // every ring cell starts as the boundary (iterations before 0 are columns
   // left of the grid)
   for (int i = threadIdx.x; i < kRings * (kR * kS + kLR); i += blockDim.x) smem[i] = bnd;
-  if (threadIdx.x == 0) {
-    s_ticket = atomicAdd(p.ticket, 1);
-    s_ready = -kPre;
-    s_iter = 0;
-  }
+  if (threadIdx.x == 0) s_ticket = atomicAdd(p.ticket, 1);
   __syncthreads();
   const int n = s_ticket;  // position in the CTA chain
 #ifdef GSL_TRACE
@@ -193,8 +198,8 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
     }
   }
   __syncthreads();
-  // producer rows a consumer reads: its rows >= -kPre, i.e. >= LAM*G - kPre here
-  const int ring_lo = kLam * kG - kPre;
+  // producer rows a consumer reads: its rows >= -ProRows, i.e. >= LAM*G - ProRows here
+  const int ring_lo = kLam * kG - C::ProRows;
 
   if (wi < C::Compute) {
     // ---------------- compute warp: group g, lanes l = 32 w + t ----------
@@ -204,9 +209,6 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
     double* const ring_me = smem + (size_t)(g + kPh) * kR * kS;
     const double* const ring_up = ring_me - kR * kS;
     const double* const ring_up2 = ring_me - 2 * kR * kS;
-    // lane 0 of a group reads lane -1 (grid rows) from the staging ring
-    const double* const lm1_me = lm1 + (g + kPh) * kLR;
-    const bool first = l == 0;
     const bool emit = l == p.tp - 1;  // last sweep of the pass: final values
     double* const arow = p.a + (long long)row * p.s0;
     const bool to_ring = has_down && g >= kG - kPh;  // phantom source of the next CTA
@@ -216,9 +218,12 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
     const bool rows_in = d - 32 * w - 31 >= 0 && d - 32 * w <= e0 - 1;
     const int m_in0 = kLam * g + 64 * w + 62 + kB, m_in1 = kLam * g + 64 * w + kB + e1;
     const bool row_ok = row >= 0 && row < e0;
-    const bool waiter = wi == 0;  // acquires the loader's rows for the whole CTA (the barrier forwards them)
     double nw = bnd, nn = bnd, ne = bnd, ww = bnd, cc = bnd, ee = bnd, sw = bnd, ss = bnd, se = bnd;
     double out = bnd;
+    cta_bar(kThreads);  // prologue rows landed
+#ifdef GSL_TRACE
+    if (wi == 0 && lane == 0 && n < 8192) g_gsl_trace[n][1] = gsl_now();
+#endif
     for (int mb = 0; mb < m_end; mb += kR) {
       const bool steady = rows_in && mb >= m_in0 && mb + kR <= m_in1;
       auto block = [&](auto steady_tag) {
@@ -226,44 +231,21 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
 #pragma unroll
         for (int u = 0; u < kR; ++u) {
           const int m = mb + u;
-          if (waiter) {
-            // rows < m of the phantom and lane -1 rings (read below) landed
-            if (s_ready < m) {
-#ifdef GSL_TRACE
-              const long long tw = clock64();
-#endif
-              const long long t0 = clock64();
-              while (s_ready < m)
-                if (clock64() - t0 > (1ll << 34)) __trap();
-#ifdef GSL_TRACE
-              tr_poll += clock64() - tw;
-#endif
-            }
-            __syncwarp();
-            __threadfence_block();
-          }
-#ifdef GSL_TRACE
-          const long long tb0 = clock64();
-#endif
-          cta_bar(kBarThreads);  // iteration m-1 done everywhere; the loader's rows < m visible
-#ifdef GSL_TRACE
-          tr_bar += clock64() - tb0;
-#endif
-          if (waiter && lane == 0) s_iter = m;  // iterations < m finished by every compute warp
+          // every input is a shared-memory ring read at a compile-time offset
+          // (slot 1 of a ring = its lane -1, a grid row, copied in by the
+          // loader); no shuffles, no per-lane special cases
           const int r1 = ((u - 1) & (kR - 1)) * kS, r3 = ((u - kLam - 1) & (kR - 1)) * kS;
           const double ne_new = ring_up[r1 + 2 + l];  // group d-1, lane l, iteration m-1
-          // group d-1, lane l-1, iteration m-3 (lane 0: lane -1 of group d-1 = grid row d)
-          const double e_new = first ? lm1_me[-kLR + ((m - kLam - 1) & (kLR - 1))] : ring_up[r3 + 1 + l];
-          double se_new = __shfl_up_sync(0xffffffffu, out, 1);  // lane l-1, iteration m-1
-          if (lane == 0) se_new = first ? lm1_me[(m - 1) & (kLR - 1)] : ring_me[r1 + 1 + l];  // lane -1 / previous warp
+          const double e_new = ring_up[r3 + 1 + l];   // group d-1, lane l-1, iteration m-3 (lane 0: grid row d)
+          const double se_new = ring_me[r1 + 1 + l];  // my group, lane l-1, iteration m-1 (lane 0: grid row d+1)
           nw = nn; nn = ne; ne = ne_new;
           cc = ee; ee = e_new;
           sw = ss; ss = se; se = se_new;
           double ne_use = ne;
           if constexpr (REF) {
-            // group d-2, lane l-1, iteration m-5 (lane 0: lane -1 of group d-2 = grid row d-1)
+            // group d-2, lane l-1, iteration m-5 (lane 0: grid row d-1)
             const int r5 = ((u - 2 * kLam - 1) & (kR - 1)) * kS;
-            ne_use = first ? lm1_me[-2 * kLR + ((m - 2 * kLam - 1) & (kLR - 1))] : ring_up2[r5 + 1 + l];
+            ne_use = ring_up2[r5 + 1 + l];
           }
           const double v = gsl_taps<MASK>(p.w, nw, nn, ne_use, ww, cc, ee, sw, ss, se);
           bool inside = true;
@@ -278,6 +260,13 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
           ring_me[(u & (kR - 1)) * kS + 2 + l] = out;
           if (to_ring && m >= ring_lo) st_relaxed_gpu(gdst + (size_t)m * kPh * kL, __double_as_longlong(out));
           if (emit && inside) arow[col0 + m] = out;
+#ifdef GSL_TRACE
+          const long long tb0 = clock64();
+#endif
+          cta_bar(kThreads);  // iteration m done everywhere; the loader's rows for m+1 landed
+#ifdef GSL_TRACE
+          tr_bar += clock64() - tb0;
+#endif
         }
       };
       if (steady)
@@ -285,27 +274,27 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
       else
         block(std::false_type{});
     }
-    cta_bar(kBarThreads);
-    if (waiter && lane == 0) s_iter = m_end;
 #ifdef GSL_TRACE
     if (wi == 0 && lane == 0 && n < 8192) {
       g_gsl_trace[n][2] = gsl_now();
       g_gsl_trace[n][5] = tr_bar;
-      g_gsl_trace[n][3] = tr_poll;
     }
 #endif
   } else {
-    // ---------------- loader (not in the per-iteration barrier) ------------
-    // Runs ahead of the compute warps as far as its rings allow and publishes
-    // s_ready: rows < s_ready of the lane -1 staging ring and of the phantom
-    // rings are in shared memory.
+    // ---------------- loader -----------------------------------------------
     //  * lane -1 of ring ri (local group g = ri - kPh, global d0 + g) at
-    //    iteration i = grid row d0 + g + 1 at column i - LAM*g + 2 - B,
-    //    cp.async batches kAheadL iterations ahead (HBM latency);
-    //  * phantom rows: the previous CTA's last kPh groups at producer
-    //    iteration i + LAM*G (its local groups G-kPh.. are my -kPh..),
-    //    polled cell by cell (sentinel) and reset after reading.  Producer
-    //    rows >= m_end are columns right of the grid: the boundary.
+    //    iteration i = grid row d0 + g + 1 at column i - LAM*g + 2 - B:
+    //    cp.async batches of kBatch rows, kAheadL iterations ahead;
+    //  * phantom rows (the previous CTA's last kPh groups at producer
+    //    iteration i + LAM*G; its groups G-kPh.. are my -kPh..) in blocks of
+    //    kBatch rows: a block is requested (cp.async from the L2 ring) one
+    //    block ahead, then validated cell by cell (sentinel: re-polled until
+    //    written), copied into the phantom rings and reset to the sentinel
+    //    in the L2 ring.  One L2 round trip per block, not per row.
+    //    Producer rows >= m_end are columns right of the grid: the boundary.
+    constexpr int kRowCells = kPh * kL;            // cells of one phantom row
+    constexpr int kPieces = kBatch * kRowCells / 2;  // 16-byte pieces per block
+    static_assert(kPieces % 32 == 0, "block pieces per lane");
     auto batch_lane_m1 = [&](int i0) {  // iterations [i0, i0 + kBatch), every ring
       for (int e = lane; e < kRings * kBatch; e += 32) {
         const int ri = e / kBatch, i = i0 + e % kBatch;
@@ -317,111 +306,109 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
         else
           *dst = bnd;
       }
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    constexpr int kPer = kPh * kL / 32;  // cells per loader lane per row
-    auto cell = [&](int i, int q) -> double* {
-      const int e = lane + 32 * q, ph = e / kL, ll = e % kL;
-      return gin + ((size_t)(i + kLam * kG) * kPh + ph) * kL + ll;
-    };
-    auto put = [&](int i, int q, unsigned long long v) {
-      const int e = lane + 32 * q, ph = e / kL, ll = e % kL;
-      smem[((size_t)ph * kR + (i & (kR - 1))) * kS + 2 + ll] = __longlong_as_double(v);
+    auto slot1 = [&](int i) {  // lane -1 of every ring at iteration i -> ring slot 1
+      if (lane < kRings) smem[((size_t)lane * kR + (i & (kR - 1))) * kS + 1] = lm1[lane * kLR + (i & (kLR - 1))];
     };
     auto in_ring = [&](int i) { return has_up && i + kLam * kG < m_end; };
-    int lm_issued = -kPre - 2;  // lane -1 rows < lm_issued are requested (batches of kBatch)
-    // prologue batches: rows [-kBatch, kAheadL)
-    for (lm_issued = -kBatch; lm_issued < kAheadL; lm_issued += kBatch) batch_lane_m1(lm_issued);
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    int lm_ready = lm_issued;  // lane -1 rows < lm_ready have landed
-    int ph_next = -kPre;       // next phantom row to complete
-    // phantom poll window: rows ph_next .. ph_next + kAheadP - 1, loaded into
-    // registers; a row is complete when all its cells are non-sentinel
-    unsigned long long qv[kAheadP][kPer];
-#pragma unroll
-    for (int a = 0; a < kAheadP; ++a)
-#pragma unroll
-      for (int q = 0; q < kPer; ++q) qv[a][q] = kSent;
-    const long long t_start = clock64();
-    while (ph_next < m_end || lm_ready < m_end + kLam) {
-      const int mc = s_iter;  // compute progress: rows they still read are >= mc - kPre
-      bool progressed = false;
-      // ---- lane -1 staging: keep kAheadL rows ahead, never overwrite rows still read
-      if (lm_issued < m_end + kBatch && lm_issued < mc + kLR - kPre - kBatch) {
-        batch_lane_m1(lm_issued);
-        lm_issued += kBatch;
-        progressed = true;
+    auto gcell = [&](int i, int e) -> double* { return gin + (size_t)(i + kLam * kG) * kRowCells + e; };
+    auto request_block = [&](int i0) {  // phantom rows [i0, i0 + kBatch) -> staging
+      double* sb = stg + ((i0 / kBatch) & 1) * (kBatch * kRowCells);
+#pragma unroll 4
+      for (int j = 0; j < kPieces / 32; ++j) {
+        const int k = lane + 32 * j, r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
+        if (in_ring(i0 + r)) cp_async16g(sb + r * kRowCells + e, gcell(i0 + r, e));
       }
-      if (lm_issued - lm_ready >= kAheadL || lm_issued >= m_end + kBatch) {
-#ifdef GSL_TRACE
-        const long long tw0 = clock64();
-#endif
-        // the oldest batch in flight
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(kAheadL / kBatch - 1) : "memory");
-#ifdef GSL_TRACE
-        tr_cpw += clock64() - tw0;
-#endif
-        lm_ready = max(lm_ready, lm_issued - kAheadL + kBatch);
-        if (lm_issued >= m_end + kBatch) {
-          asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-          lm_ready = lm_issued;
-        }
-      }
-      // ---- phantom rows: poll the window (qv[k] = row ph_next + k), complete
-      // the leading row when every cell of it is written
-      if (ph_next < m_end && ph_next < mc + kR - kPre - 1) {
-        bool ok = true;
-        const bool live0 = in_ring(ph_next);
-#pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-          if (live0 && qv[0][q] == kSent) qv[0][q] = ld_relaxed_gpu(cell(ph_next, q));
-          ok = ok && (!live0 || qv[0][q] != kSent);
-        }
-        if (__all_sync(0xffffffffu, ok)) {
-#pragma unroll
-          for (int q = 0; q < kPer; ++q) {
-            if (live0) {
-              put(ph_next, q, qv[0][q]);
-#ifndef GSL_NO_RESET
-              st_relaxed_gpu(cell(ph_next, q), kSent);
-#endif
-            } else {
-              put(ph_next, q, (unsigned long long)__double_as_longlong(bnd));
+    };
+    auto finish_block = [&](int i0) {  // validate, copy into the rings, reset the L2 cells
+      const double* sb = stg + ((i0 / kBatch) & 1) * (kBatch * kRowCells);
+#pragma unroll 1
+      for (int j = 0; j < kPieces / 32; ++j) {
+        const int k = lane + 32 * j, r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
+        const int i = i0 + r;
+        unsigned long long v0 = __double_as_longlong(bnd), v1 = v0;
+        if (in_ring(i)) {
+          v0 = __double_as_longlong(sb[r * kRowCells + e]);
+          v1 = __double_as_longlong(sb[r * kRowCells + e + 1]);
+          if (v0 == kSent || v1 == kSent) {
+            const long long t0 = clock64();
+            while (v0 == kSent) {
+              v0 = ld_relaxed_gpu(gcell(i, e));
+              if (clock64() - t0 > (1ll << 34)) __trap();
             }
+            while (v1 == kSent) {
+              v1 = ld_relaxed_gpu(gcell(i, e + 1));
+              if (clock64() - t0 > (1ll << 34)) __trap();
+            }
+#ifdef GSL_TRACE
+            tr_poll += clock64() - t0;
+#endif
           }
-#pragma unroll
-          for (int k = 0; k + 1 < kAheadP; ++k)
-#pragma unroll
-            for (int q = 0; q < kPer; ++q) qv[k][q] = qv[k + 1][q];
-#pragma unroll
-          for (int q = 0; q < kPer; ++q) qv[kAheadP - 1][q] = kSent;
-          ++ph_next;
-          progressed = true;
+#ifndef GSL_NO_RESET
+          st_relaxed_gpu(gcell(i, e), kSent);
+          st_relaxed_gpu(gcell(i, e + 1), kSent);
+#endif
         }
-        // keep polls in flight for the rows after it
+        const int ph = e / kL, ll = e % kL;
+        double* dst = smem + ((size_t)ph * kR + (i & (kR - 1))) * kS + 2 + ll;
+        dst[0] = __longlong_as_double(v0);
+        dst[1] = __longlong_as_double(v1);
+      }
+    };
+    // prologue: lane -1 rows [-kBatch, kAheadL) landed; phantom rows
+    // [-kBatch, 0) in the rings, rows [0, kBatch) requested
+    for (int i0 = -C::ProRows; i0 < kAheadL; i0 += kBatch) batch_lane_m1(i0);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+    for (int i = -kPre; i <= 0; ++i) slot1(i);
+    for (int i0 = -C::ProRows; i0 < 0; i0 += kBatch) {
+      request_block(i0);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      finish_block(i0);
+    }
+    request_block(0);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    __syncwarp();
+    cta_bar(kThreads);
+    for (int mb = 0; mb < m_end; mb += kR) {
 #pragma unroll
-        for (int k = 1; k < kAheadP; ++k) {
-          const int i = ph_next + k;
-          if (i < m_end && in_ring(i)) {
-#pragma unroll
-            for (int q = 0; q < kPer; ++q)
-              if (qv[k][q] == kSent) qv[k][q] = ld_relaxed_gpu(cell(i, q));
-          }
+      for (int u = 0; u < kR; ++u) {
+        const int m = mb + u;
+        if (u % kBatch == 0) {
+          // group A: the next phantom block; group B: lane -1 rows far ahead.
+          // wait_group 2 retires every older group, in particular this
+          // block's phantom request (issued one block ago)
+          request_block(m + kBatch);
+          asm volatile("cp.async.commit_group;\n" ::: "memory");
+          batch_lane_m1(m + kAheadL);
+          asm volatile("cp.async.commit_group;\n" ::: "memory");
+#ifdef GSL_TRACE
+          const long long tw0 = clock64();
+#endif
+          asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+#ifdef GSL_TRACE
+          tr_cpw += clock64() - tw0;
+#endif
+          __syncwarp();
+          finish_block(m);  // rows [m, m + kBatch): read from iteration m + 1 on
         }
+        slot1(m + 1);  // read from iteration m + 2 on
+        __syncwarp();
+#ifdef GSL_TRACE
+        const long long tb0 = clock64();
+#endif
+        cta_bar(kThreads);
+#ifdef GSL_TRACE
+        tr_bar += clock64() - tb0;
+#endif
       }
-      // ---- publish
-      const int ready = min(lm_ready, ph_next);
-      __syncwarp();
-      if (lane == 0 && ready > s_ready) {
-        __threadfence_block();
-        s_ready = ready;
-      }
-      if (!progressed) __nanosleep(32);
-      if (clock64() - t_start > (1ll << 36)) __trap();
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
 #ifdef GSL_TRACE
     if (lane == 0 && n < 8192) {
+      g_gsl_trace[n][3] = tr_poll;
       g_gsl_trace[n][4] = tr_cpw;
       g_gsl_trace[n][6] = tr_bar;
     }

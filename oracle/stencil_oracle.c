@@ -113,12 +113,15 @@ static int gs_antidiag(const oracle_problem* p, double* a, const int64_t* lin, d
   const int64_t dmax = (e0 - 1) + (e1 - 1) + (e2 - 1);
   for (int64_t d = 0; d <= dmax; ++d) {
     int64_t m = 0;
-    for (int64_t i = 0; i < e0 && i <= d; ++i)
-      for (int64_t j = 0; j < e1 && i + j <= d; ++j) {
+    /* the points of diagonal d (i + j + k = d) in row-major order, visited
+       directly (not by scanning every (i, j) with i + j <= d) */
+    const int64_t ilo = d - (e1 - 1) - (e2 - 1) > 0 ? d - (e1 - 1) - (e2 - 1) : 0;
+    const int64_t ihi = d < e0 - 1 ? d : e0 - 1;
+    for (int64_t i = ilo; i <= ihi; ++i) {
+      const int64_t jlo = d - i - (e2 - 1) > 0 ? d - i - (e2 - 1) : 0;
+      const int64_t jhi = d - i < e1 - 1 ? d - i : e1 - 1;
+      for (int64_t j = jlo; j <= jhi; ++j) {
         const int64_t k = d - i - j;
-        if (k >= e2) continue;
-        if (p->dim == 1 && (j != 0 || k != 0)) continue;
-        if (p->dim == 2 && k != 0) continue;
         int64_t idx;
         if (p->dim == 1)
           idx = o + i;
@@ -130,6 +133,7 @@ static int gs_antidiag(const oracle_problem* p, double* a, const int64_t* lin, d
         buf[m] = point(a, idx, p->ntaps, lin, p->coeffs);
         ++m;
       }
+    }
     for (int64_t q = 0; q < m; ++q) a[idxbuf[q]] = buf[q];
   }
   return 0;

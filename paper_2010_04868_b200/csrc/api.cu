@@ -857,7 +857,7 @@ static bool stream_value_fns(StreamValueFn* wait, StreamValueFn* write) {
 bool stream_value_fns_api(StreamValueFn* wait, StreamValueFn* write) { return stream_value_fns(wait, write); }
 
 static int gs2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, const double* in, double* out,
-                          int64_t steps, RunCtx& c, int64_t band) {
+                          int64_t steps, RunCtx& c, int64_t band, int order, bool lane) {
   StreamValueFn wait_value, write_value;
   if (!stream_value_fns(&wait_value, &write_value)) return TVS_ERR_UNSUPPORTED;
   const tvs_geometry& g = c.geo;
@@ -890,13 +890,16 @@ static int gs2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, const do
   }
   TVS_CUDA(cudaStreamWaitEvent(ks, c.events[0], 0));
   TVS_CUDA(cudaStreamWaitEvent(ds, c.events[0], 0));  // counters reset before any wait reads them
-  if ((rc = gs2d_pipeline(st, g, c.buf[0], steps, ks, ctr, ctr + 16))) return rc;
+  if ((rc = lane ? gs2d_lane(st, g, c.buf[0], steps, order, ks, ctr, ctr + 16)
+                 : gs2d_pipeline(st, g, c.buf[0], steps, ks, ctr, ctr + 16)))
+    return rc;
   // row r's final value is written by the block holding group r + steps - 1
-  // (block geometry from gs2d_pipe.cu itself)
-  const int64_t nblocks = gs2d_pipe_blocks(rows);
+  // (block geometry from the kernel's own file)
+  const int64_t nblocks = lane ? gs2d_lane_ctas(rows, steps, order) : gs2d_pipe_blocks(rows);
   for (int u = 0; u < nbands; ++u) {
     const int64_t r0 = (int64_t)u * band, r1 = std::min(rows, r0 + band);
-    const int64_t need = std::min<int64_t>(nblocks, gs2d_pipe_blocks_for_row(r1 - 1, steps));
+    const int64_t need = std::min<int64_t>(
+        nblocks, lane ? gs2d_lane_ctas_for_row(r1 - 1, steps, order) : gs2d_pipe_blocks_for_row(r1 - 1, steps));
     const int wrc = wait_value(ds, blocks_done, (unsigned)need, 0 /* CU_STREAM_WAIT_VALUE_GEQ */);
     if (wrc != 0) return fail(TVS_ERR_CUDA, "cuStreamWaitValue32 failed (CUresult " + std::to_string(wrc) + ")");
     if ((rc = copy_rows(g, c.buf[0], lay, out, false, r0, r1, ds))) return rc;
@@ -1101,10 +1104,15 @@ int tvs_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, doub
   }
   if (gs) {
     const int64_t band = band_rows_default();
-    if (gs2d_kernel_choice() == 1 && band > 0 && st->dim == 2 && steps > 0 && steps <= gs2d_pipe_max_sweeps() &&
-        ex->algo != TVS_ALGO_NAIVE &&
-        ex->gs_order == TVS_GS_LEXICOGRAPHIC && gs2d_pipe_supported(*st) && c.geo.extents[0] >= 4 * band) {
-      rc = gs2d_pipelined(*st, *lay, in, out, steps, c, band);
+    // lane kernel (K6v2, either order) or the K6 pipeline (lexicographic):
+    // one pass, row bands uploaded / downloaded while it runs
+    const bool lane = gs2d_kernel_choice() == 0 && gs2d_lane_supported(*st) &&
+                      !(ex->gs_order == TVS_GS_REFERENCE && steps < 2);
+    const bool pipe = !lane && ex->gs_order == TVS_GS_LEXICOGRAPHIC && gs2d_pipe_supported(*st);
+    if ((lane || pipe) && band > 0 && st->dim == 2 && steps > 0 &&
+        steps <= (lane ? gs2d_lane_max_sweeps() : gs2d_pipe_max_sweeps()) && ex->algo != TVS_ALGO_NAIVE &&
+        c.geo.extents[0] >= 4 * band) {
+      rc = gs2d_pipelined(*st, *lay, in, out, steps, c, band, ex->gs_order, lane);
       if (rc != TVS_ERR_UNSUPPORTED) return rc;  // no stream memory operations: plain path below
     }
   }

@@ -261,7 +261,11 @@ int64_t gs2d_pipe_blocks_for_row(int64_t row, int64_t steps);
 int gs2d_pipe_max_sweeps();
 // K6v2 (gs2d_lane.cu): one-warp time-lane groups, both update orders
 bool gs2d_lane_supported(const tvs_stencil& st);
-int gs2d_lane(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, int order, cudaStream_t s);
+int gs2d_lane(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, int order, cudaStream_t s,
+              const unsigned* rows_ready = nullptr, unsigned* blocks_done = nullptr);
+int gs2d_lane_max_sweeps();
+int64_t gs2d_lane_ctas(int64_t rows, int64_t steps, int order);
+int64_t gs2d_lane_ctas_for_row(int64_t row, int64_t steps, int order);
 int gs_wavefront(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, int order,
                  cudaStream_t s);
 

@@ -111,6 +111,8 @@ struct GslArgs {
   double* gring;      // kNumSlots x m_end x Ph x L (sentinel until written)
   int* done;          // [slot]: consumer CTAs of this slot that exited (their ticket)
   int* ticket;
+  const unsigned* rows_ready;  // drop-in pipeline: grid rows uploaded so far (nullptr: all resident)
+  unsigned* blocks_done;       // drop-in pipeline: CTAs finished, published in ticket order (or nullptr)
   double w[9];
   double bnd;
 };
@@ -355,6 +357,19 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
         dst[1] = __longlong_as_double(v1);
       }
     };
+    if (p.rows_ready) {
+      // the drop-in path uploads row bands while this kernel runs: this
+      // CTA reads grid rows d0 - kPh + 1 .. d0 + G (its rings' lane -1)
+      const unsigned need = (unsigned)min(e0, d0 + kG + 1);
+      const long long t0 = clock64();
+      for (;;) {
+        unsigned have;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(have) : "l"(p.rows_ready) : "memory");
+        if (have >= need) break;
+        __nanosleep(256);
+        if (clock64() - t0 > (1ll << 35)) __trap();
+      }
+    }
     // prologue: lane -1 rows [-kBatch, kAheadL) landed; phantom rows
     // [-kBatch, 0) in the rings, rows [0, kBatch) requested
     for (int i0 = -C::ProRows; i0 < kAheadL; i0 += kBatch) batch_lane_m1(i0);
@@ -419,6 +434,23 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
       atomicMax(p.done + slot_in, n);
     }
   }
+  if (p.blocks_done) {
+    // publish "CTAs 0..n finished" in ticket order (CTA n-1 started before n
+    // and never waits on it: no deadlock); the drop-in path's download stream
+    // waits on this count for the rows whose final values are written
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long t0 = clock64();
+      for (;;) {
+        unsigned seen;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.blocks_done) : "memory");
+        if (seen >= (unsigned)n) break;
+        if (clock64() - t0 > (1ll << 35)) __trap();
+      }
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.blocks_done), "r"((unsigned)n + 1u) : "memory");
+    }
+  }
 }
 
 __global__ void gsl_sentinel_kernel(unsigned long long* p, size_t n) {
@@ -451,7 +483,8 @@ bool gs2d_lane_supported(const tvs_stencil& st) {
 }
 
 template <unsigned MASK, bool REF, int WG>
-static int gsl_launch(GslArgs a, int64_t steps, int64_t per, cudaStream_t s) {
+static int gsl_launch(GslArgs a, int64_t steps, int64_t per, cudaStream_t s, const unsigned* rows_ready,
+                      unsigned* blocks_done) {
   using namespace gsl;
   using C = Cfg<REF, WG>;
   auto kern = gs2d_lane_kernel<MASK, REF, WG>;
@@ -477,6 +510,9 @@ static int gsl_launch(GslArgs a, int64_t steps, int64_t per, cudaStream_t s) {
     clean_gen = scratch_generation();
     clean_cells = cells;
   }
+  if ((rows_ready || blocks_done) && per < steps) return fail(TVS_ERR_INVALID, "gs2d_lane: pipeline hooks need one pass");
+  a.rows_ready = rows_ready;
+  a.blocks_done = blocks_done;
   for (int64_t done = 0; done < steps; done += per) {
     a.tp = (int)std::min<int64_t>(per, steps - done);
     const int ngroups = a.e0 + a.tp - 1;
@@ -496,7 +532,24 @@ extern "C" int tvs_gsl_trace(unsigned long long* host, int n) {
 }
 #endif
 
-int gs2d_lane(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, int order, cudaStream_t s) {
+// Drop-in pipeline hooks (api.cu gs2d_pipelined): one pass of <= 128 sweeps;
+// CTAs of that pass, and how many must have exited before row `row` holds
+// its final value (the group row + steps - 1 writes it).
+static int gsl_groups(int64_t steps, int order) {
+  (void)steps;
+  return order == TVS_GS_REFERENCE ? gsl::Cfg<true, 4>::G : gsl::Cfg<false, 4>::G;
+}
+int gs2d_lane_max_sweeps() { return 128; }
+int64_t gs2d_lane_ctas(int64_t rows, int64_t steps, int order) {
+  const int G = gsl_groups(steps, order);
+  return (rows + steps - 1 + G - 1) / G;
+}
+int64_t gs2d_lane_ctas_for_row(int64_t row, int64_t steps, int order) {
+  return (row + steps - 1) / gsl_groups(steps, order) + 1;
+}
+
+int gs2d_lane(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_t steps, int order, cudaStream_t s,
+              const unsigned* rows_ready, unsigned* blocks_done) {
   double w[9];
   const unsigned mask = gsl_mask(st, w);
   if (!gs2d_lane_supported(st)) return fail(TVS_ERR_UNSUPPORTED, "gs2d_lane: tap set / boundary");
@@ -518,9 +571,9 @@ int gs2d_lane(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_
   auto go = [&](auto m_tag, auto r_tag) -> int {
     constexpr unsigned M = decltype(m_tag)::value;
     constexpr bool R = decltype(r_tag)::value;
-    if (wg == 1) return gsl_launch<M, R, 1>(a, steps, per, s);
-    if (wg == 2) return gsl_launch<M, R, 2>(a, steps, per, s);
-    return gsl_launch<M, R, 4>(a, steps, per, s);
+    if (wg == 1) return gsl_launch<M, R, 1>(a, steps, per, s, rows_ready, blocks_done);
+    if (wg == 2) return gsl_launch<M, R, 2>(a, steps, per, s, rows_ready, blocks_done);
+    return gsl_launch<M, R, 4>(a, steps, per, s, rows_ready, blocks_done);
   };
   using Box = std::integral_constant<unsigned, 0x1FFu>;
   using Star = std::integral_constant<unsigned, kGslStar>;

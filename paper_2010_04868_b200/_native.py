@@ -476,6 +476,77 @@ def host_empty(shape, dtype=np.float64) -> np.ndarray:
     return np.frombuffer(raw, dtype=dt, count=int(np.prod(shape))).reshape(shape)
 
 
+class _HostPool:
+    """Caching allocator of page-locked host blocks for result Grids (like a
+    framework's caching host allocator): a block returns to the pool when the
+    last array view of it is collected and is handed out again to the next
+    result of the same size, so the stock drop-in call writes its result by
+    DMA into pre-faulted page-locked memory instead of faulting in fresh
+    pageable pages (config 3: ~220 ms of page faults, tools/stock_probe.py).
+    At most `keep` idle blocks per size are retained."""
+
+    def __init__(self, keep: int = 2):
+        self.keep = keep
+        self.free: dict[int, list[int]] = {}
+        self.lock = threading.Lock()
+
+    def take(self, nbytes: int) -> int:
+        with self.lock:
+            lst = self.free.get(nbytes)
+            if lst:
+                return lst.pop()
+        p = C.c_void_p()
+        check(lib().tvs_host_alloc(nbytes, C.byref(p)), "tvs_host_alloc")
+        return p.value
+
+    def give(self, nbytes: int, ptr: int) -> None:
+        with self.lock:
+            lst = self.free.setdefault(nbytes, [])
+            if len(lst) < self.keep:
+                lst.append(ptr)
+                return
+        lib().tvs_host_free(ptr)
+
+    def clear(self) -> None:
+        with self.lock:
+            blocks = [p for lst in self.free.values() for p in lst]
+            self.free.clear()
+        for ptr in blocks:
+            lib().tvs_host_free(ptr)
+
+
+_pool = _HostPool()
+
+
+class _PoolLoan:
+    def __init__(self, nbytes: int):
+        self.nbytes = nbytes
+        self.ptr = _pool.take(nbytes)
+
+    def __del__(self):
+        if self.ptr:
+            try:
+                _pool.give(self.nbytes, self.ptr)
+            except Exception:
+                pass
+            self.ptr = None
+
+
+def host_pool_empty(shape, dtype=np.float64) -> np.ndarray:
+    """Uninitialised page-locked array from the result-buffer pool."""
+    shape = tuple(int(x) for x in np.atleast_1d(shape))
+    dt = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dt.itemsize
+    loan = _PoolLoan(max(nbytes, 1))
+    raw = (C.c_char * max(nbytes, 1)).from_address(loan.ptr)
+    raw._tvs_owner = loan
+    return np.frombuffer(raw, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+
+
+def clear_host_pool() -> None:
+    _pool.clear()
+
+
 def host_array(n: int) -> np.ndarray:
     """1-D page-locked float64 array of n elements (tools/pinned_probe.py)."""
     return host_empty((n,))

@@ -232,16 +232,19 @@ static int copy_interior(const tvs_geometry& g, double* dev, const tvs_layout& l
   if (g.dim == 1) {
     double* h0 = host + lay.offset;
     size_t bytes = sizeof(double) * g.extents[0];
-    TVS_CUDA(cudaMemcpyAsync(upload ? (void*)d0 : (void*)h0, upload ? (void*)h0 : (void*)d0, bytes,
-                             upload ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s));
+    if (upload) return upload_block((char*)d0, bytes, 0, (const char*)h0, bytes, 0, bytes, 1, 1, s);
+    TVS_CUDA(cudaMemcpyAsync(h0, d0, bytes, cudaMemcpyDeviceToHost, s));
   } else if (g.dim == 2) {
     double* h0 = host + lay.offset * lay.shape[1] + lay.offset;
     size_t hp = sizeof(double) * lay.shape[1], dp = sizeof(double) * g.strides[0];
     size_t w = sizeof(double) * g.extents[1];
-    if (upload)
-      TVS_CUDA(cudaMemcpy2DAsync(d0, dp, h0, hp, w, g.extents[0], cudaMemcpyHostToDevice, s));
-    else
-      TVS_CUDA(cudaMemcpy2DAsync(h0, hp, d0, dp, w, g.extents[0], cudaMemcpyDeviceToHost, s));
+    if (upload) return upload_block((char*)d0, dp, 0, (const char*)h0, hp, 0, w, g.extents[0], 1, s);
+    TVS_CUDA(cudaMemcpy2DAsync(h0, hp, d0, dp, w, g.extents[0], cudaMemcpyDeviceToHost, s));
+  } else if (upload) {
+    const size_t hr = sizeof(double) * lay.shape[2], hz = hr * lay.shape[1];
+    const double* h0 = host + (lay.offset * lay.shape[1] + lay.offset) * lay.shape[2] + lay.offset;
+    return upload_block((char*)d0, sizeof(double) * g.strides[1], sizeof(double) * g.strides[0], (const char*)h0, hr,
+                        hz, sizeof(double) * g.extents[2], g.extents[1], g.extents[0], s);
   } else {
     cudaMemcpy3DParms p;
     std::memset(&p, 0, sizeof(p));
@@ -455,10 +458,8 @@ static int copy_rows(const tvs_geometry& g, double* dev, const tvs_layout& lay, 
   double* h0 = host + (lay.offset + r0) * lay.shape[1] + lay.offset;
   const size_t hp = sizeof(double) * lay.shape[1], dp = sizeof(double) * g.strides[0];
   const size_t w = sizeof(double) * g.extents[1];
-  if (upload)
-    TVS_CUDA(cudaMemcpy2DAsync(d0, dp, h0, hp, w, r1 - r0, cudaMemcpyHostToDevice, s));
-  else
-    TVS_CUDA(cudaMemcpy2DAsync(h0, hp, d0, dp, w, r1 - r0, cudaMemcpyDeviceToHost, s));
+  if (upload) return upload_block((char*)d0, dp, 0, (const char*)h0, hp, 0, w, r1 - r0, 1, s);
+  TVS_CUDA(cudaMemcpy2DAsync(h0, hp, d0, dp, w, r1 - r0, cudaMemcpyDeviceToHost, s));
   return TVS_OK;
 }
 
@@ -646,11 +647,14 @@ static int jacobi1d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
   auto done = [&](int b, int k) { return c.events[(size_t)nb * (k + 1) + b]; };
   auto lo_of = [&](int b, int k) { return std::max<int64_t>(0, (int64_t)b * band - S[k]); };
   auto hi_of = [&](int b, int k) { return std::min<int64_t>(n, (int64_t)(b + 1) * band - S[k]); };
-  auto copy = [&](double* dev, double* host, bool upload, int64_t p0, int64_t p1, cudaStream_t s) {
+  auto copy = [&](double* dev, double* host, bool upload, int64_t p0, int64_t p1, cudaStream_t s) -> cudaError_t {
     double* d = dev + g.origin + p0;
     double* h = host + lay.offset + p0;
-    return cudaMemcpyAsync(upload ? (void*)d : (void*)h, upload ? (void*)h : (void*)d, sizeof(double) * (p1 - p0),
-                           upload ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s);
+    const size_t bytes = sizeof(double) * (p1 - p0);
+    if (upload)  // page-locked (captured graph) or staged (pageable)
+      return upload_block((char*)d, bytes, 0, (const char*)h, bytes, 0, bytes, 1, 1, s) == TVS_OK ? cudaSuccess
+                                                                                                 : cudaErrorUnknown;
+    return cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s);
   };
   cudaStream_t cs = c.stream;
   int rc;
@@ -729,6 +733,13 @@ static int jacobi1d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
 // slab-pass reads only planes that pass k-1 of slabs b and b-1 wrote.
 static int copy_planes(const tvs_geometry& g, double* dev, const tvs_layout& lay, double* host, bool upload,
                        int64_t p0, int64_t p1, cudaStream_t s) {
+  if (upload) {
+    const size_t hr = sizeof(double) * lay.shape[2], hz = hr * lay.shape[1];
+    const double* h0 = host + ((lay.offset + p0) * lay.shape[1] + lay.offset) * lay.shape[2] + lay.offset;
+    return upload_block((char*)(dev + g.origin + p0 * g.strides[0]), sizeof(double) * g.strides[1],
+                        sizeof(double) * g.strides[0], (const char*)h0, hr, hz, sizeof(double) * g.extents[2],
+                        g.extents[1], p1 - p0, s);
+  }
   cudaMemcpy3DParms p;
   std::memset(&p, 0, sizeof(p));
   const cudaPitchedPtr hptr = make_cudaPitchedPtr(host, sizeof(double) * lay.shape[2], lay.shape[2], lay.shape[1]);
@@ -942,6 +953,7 @@ int tvs_release_thread_cache(void) {
   // plus its kernel scratch (reference ThreadPool workers: tiling.py:363-367)
   g_run.release();
   g_group.release();
+  release_staging();
   ++g_scratch_gen;
   for (auto& sl : g_scratch) {
     if (!sl.ptr) continue;

@@ -295,6 +295,14 @@ struct ShardGroup {
 // does tvs_exec ask for (and the stencil allow) a sharded run?
 bool wants_shards(const tvs_stencil& st, const tvs_exec& ex);
 
+// Host -> device block copy (hostcopy.cu): nplanes x nrows rows of `width`
+// bytes with row / plane pitches on both sides; pageable sources are staged
+// through page-locked slots by a pool of host threads, page-locked ones DMA'd
+// directly.  release_staging frees the calling thread's slots.
+int upload_block(char* dst, size_t drow, size_t dplane, const char* src, size_t srow, size_t splane, size_t width,
+                 int64_t nrows, int64_t nplanes, cudaStream_t s);
+void release_staging();
+
 // scratch device memory owned by the calling thread (grown on demand).
 // Slots: 0, 1 GS-1D / GS-2D pipeline rings and control words, 2 small
 // constants, 3 drop-in pipeline counters, 4, 5 GS-2D lane ring and control.

@@ -183,11 +183,16 @@ static int shard_copy(tvs_shard* s, const tvs_layout& lay, double* host, bool up
     double* h0 = host + (lay.offset + g0) * lay.shape[1] + lay.offset;
     const size_t hp = sizeof(double) * lay.shape[1], dp = sizeof(double) * g.strides[0];
     const size_t w = sizeof(double) * g.extents[1];
-    if (upload)
-      TVS_CUDA(cudaMemcpy2DAsync(d0, dp, h0, hp, w, g1 - g0, cudaMemcpyHostToDevice, s->stream));
-    else
-      TVS_CUDA(cudaMemcpy2DAsync(h0, hp, d0, dp, w, g1 - g0, cudaMemcpyDeviceToHost, s->stream));
+    if (upload) return upload_block((char*)d0, dp, 0, (const char*)h0, hp, 0, w, g1 - g0, 1, s->stream);
+    TVS_CUDA(cudaMemcpy2DAsync(h0, hp, d0, dp, w, g1 - g0, cudaMemcpyDeviceToHost, s->stream));
     return TVS_OK;
+  }
+  if (upload) {
+    const size_t hr = sizeof(double) * lay.shape[2], hz = hr * lay.shape[1];
+    const double* h0 = host + ((lay.offset + g0) * lay.shape[1] + lay.offset) * lay.shape[2] + lay.offset;
+    return upload_block((char*)(s->buf[s->cur] + g.origin + l0 * g.strides[0]), sizeof(double) * g.strides[1],
+                        sizeof(double) * g.strides[0], (const char*)h0, hr, hz, sizeof(double) * g.extents[2],
+                        g.extents[1], g1 - g0, s->stream);
   }
   cudaMemcpy3DParms p;
   std::memset(&p, 0, sizeof(p));

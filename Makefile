@@ -10,9 +10,12 @@ HDRS    := $(wildcard $(PKG)/csrc/*.cuh) include/tvstencil.h
 
 all: $(PKG)/libtvstencil.so oracle/liboracle.so
 
+# register spills fail the build (ptxas -warn-spills output is checked)
 build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p build
-	$(NVCC) $(NVFLAGS) -c -o $@ $<
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
+	@cat build/$*.ptxas.log
+	@if grep -q "Registers are spilled" build/$*.ptxas.log; then echo "error: register spills in $<"; rm -f $@; exit 1; fi
 
 $(PKG)/libtvstencil.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)

@@ -429,12 +429,15 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
     }
 #endif
     if (has_up && lane == 0) {
-      // every read (and sentinel reset) of the incoming slot is done: release it
+      // every read (and sentinel reset) of the incoming slot is done: release
+      // it (the ticket is re-read: nothing long-lived stays in a register)
+      const int nn = *(volatile int*)&s_ticket;
       __threadfence();
-      atomicMax(p.done + slot_in, n);
+      atomicMax(p.done + (nn - 1 + kNumSlots) % kNumSlots, nn);
     }
   }
   if (p.blocks_done) {
+    const int n = *(volatile int*)&s_ticket;
     // publish "CTAs 0..n finished" in ticket order (CTA n-1 started before n
     // and never waits on it: no deadlock); the drop-in path's download stream
     // waits on this count for the rows whose final values are written

@@ -229,27 +229,22 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
 
   // staging slots: smem cell (row i, col 2c) <- global (y0-2+i, x0-2+2c);
   // rows/columns beyond the memory halo are never needed (their level-1
-  // positions are pinned) and are not read
-  int soff[kTBSlots];
-  int64_t goff[kTBSlots];
-  bool sval[kTBSlots];
-#pragma unroll
-  for (int k = 0; k < kTBSlots; ++k) {
-    const int e = tid + k * kThreads3;
-    const int i = e / (kTBP / 2), c2 = e % (kTBP / 2);
-    const int64_t y = y0 - 2 + i, x = x0 - 2 + 2 * c2;
-    soff[k] = i * kTBP + 2 * c2;
-    goff[k] = y * g.s1 + x;
-    sval[k] = e < kTBChunks && y >= -1 && y <= g.e1 && x <= g.e2;
-  }
+  // positions are pinned) and are not read.  Offsets are recomputed per
+  // plane (a few integer ops) instead of living in registers across the
+  // plane loop: the kernel sits at its 128-register cap (2 blocks/SM).
   const double* base = src + origin;
   auto stage = [&](int64_t p) {
     if (p >= -1 && p <= g.e0) {
-      const double* pb = base + p * g.s0;
+      const double* pb = base + p * g.s0 + (y0 - 2) * g.s1 + (x0 - 2);
       double* tb = l0 + (int)((p - p0 + 3) % 3) * (kTBR * kTBP);
 #pragma unroll
-      for (int k = 0; k < kTBSlots; ++k)
-        if (sval[k]) cp_async16(tb + soff[k], pb + goff[k]);
+      for (int k = 0; k < kTBSlots; ++k) {
+        const int e = tid + k * kThreads3;
+        const int i = e / (kTBP / 2), c2 = e % (kTBP / 2);
+        const int64_t y = y0 - 2 + i, x = x0 - 2 + 2 * c2;
+        if (e < kTBChunks && y >= -1 && y <= g.e1 && x <= g.e2)
+          cp_async16(tb + i * kTBP + 2 * c2, pb + (int64_t)i * g.s1 + 2 * c2);
+      }
     }
     cp_async_commit();
   };
@@ -308,10 +303,10 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
             for (int r = 0; r < kRY; ++r)
               if (store_ok >> (h * kRY + r) & 1u) op[r * g.s1 + 32 * h] = pin ? bnd : out[h][r];
         };
-        if constexpr (MIR)
-          for_each_dst(dst, mir, q2, store);  // sharded: local plane + the neighbour's ghost plane
-        else
-          store(dst);
+        // local plane, plus the neighbour's ghost plane when sharded.  The
+        // loop form is used unsharded too: its register allocation fits the
+        // 128-register cap without the 4-byte spill of the inlined store
+        for_each_dst(dst, mir, q2, store);
       }
     }
   }
@@ -345,7 +340,8 @@ static int launch_tb(const Geo& geo, const tvs_geometry& g, const double* src, d
                      double bnd, cudaStream_t s, int64_t plo, int64_t phi, int seg, const Mirror& mir) {
   // per device context; a host-side attribute write, no synchronisation
   const bool mirrored = mir.p[0] != nullptr || mir.p[1] != nullptr;
-  auto kern = mirrored ? jacobi3d_tb_kernel<MASK, FMA, true> : jacobi3d_tb_kernel<MASK, FMA, false>;
+  (void)mirrored;  // one form (see the store): mirrors are runtime-null when unsharded
+  auto kern = jacobi3d_tb_kernel<MASK, FMA, true>;
   TVS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTBSmem));
   const dim3 block(kTX3, kTYT);
   const dim3 grid((unsigned)((geo.e2 + kTBOX - 1) / kTBOX), (unsigned)((geo.e1 + kTBOY - 1) / kTBOY),

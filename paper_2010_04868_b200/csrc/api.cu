@@ -558,6 +558,9 @@ static int jacobi2d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
         return rc;
       TVS_CUDA(cudaEventRecord(done(b, k), sb));
     }
+    // the final rows of band b also come from band b-1's last pass (the
+    // bands shift up by each pass's levels): wait for it before reading
+    if (b > 0) TVS_CUDA(cudaStreamWaitEvent(sb, done(b - 1, K - 1), 0));
     const int64_t lo = lo_of(b, K), hi = hi_of(b, K);
     if (hi > lo && (rc = copy_rows(g, result, lay, out, false, lo, hi, sb))) return rc;
     if (trace && b == 0) cudaEventRecord(tr[2], sb);
@@ -696,7 +699,10 @@ static int jacobi1d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
           return rc;
         TVS_CUDA(cudaEventRecord(done(b, k), sb));
       }
-      const int64_t lo = lo_of(b, K), hi = hi_of(b, K);
+      // the final rows of band b also come from band b-1's last pass (the
+    // bands shift up by each pass's levels): wait for it before reading
+    if (b > 0) TVS_CUDA(cudaStreamWaitEvent(sb, done(b - 1, K - 1), 0));
+    const int64_t lo = lo_of(b, K), hi = hi_of(b, K);
       if (hi > lo) TVS_CUDA(copy(result, out, false, lo, hi, sb));
     }
     for (int b = 0; b < nb; ++b) {  // join every band stream back into cs
@@ -827,6 +833,9 @@ static int jacobi3d_pipelined(const tvs_stencil& st, const tvs_layout& lay, cons
       }
       TVS_CUDA(cudaEventRecord(done(b, k), sb));
     }
+    // the final rows of band b also come from band b-1's last pass (the
+    // bands shift up by each pass's levels): wait for it before reading
+    if (b > 0) TVS_CUDA(cudaStreamWaitEvent(sb, done(b - 1, K - 1), 0));
     const int64_t lo = lo_of(b, K), hi = hi_of(b, K);
     if (hi > lo && (rc = copy_planes(g, result, lay, out, false, lo, hi, sb))) return rc;
   }

@@ -229,22 +229,27 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
 
   // staging slots: smem cell (row i, col 2c) <- global (y0-2+i, x0-2+2c);
   // rows/columns beyond the memory halo are never needed (their level-1
-  // positions are pinned) and are not read.  Offsets are recomputed per
-  // plane (a few integer ops) instead of living in registers across the
-  // plane loop: the kernel sits at its 128-register cap (2 blocks/SM).
+  // positions are pinned) and are not read
+  int soff[kTBSlots];
+  int64_t goff[kTBSlots];
+  bool sval[kTBSlots];
+#pragma unroll
+  for (int k = 0; k < kTBSlots; ++k) {
+    const int e = tid + k * kThreads3;
+    const int i = e / (kTBP / 2), c2 = e % (kTBP / 2);
+    const int64_t y = y0 - 2 + i, x = x0 - 2 + 2 * c2;
+    soff[k] = i * kTBP + 2 * c2;
+    goff[k] = y * g.s1 + x;
+    sval[k] = e < kTBChunks && y >= -1 && y <= g.e1 && x <= g.e2;
+  }
   const double* base = src + origin;
   auto stage = [&](int64_t p) {
     if (p >= -1 && p <= g.e0) {
-      const double* pb = base + p * g.s0 + (y0 - 2) * g.s1 + (x0 - 2);
+      const double* pb = base + p * g.s0;
       double* tb = l0 + (int)((p - p0 + 3) % 3) * (kTBR * kTBP);
 #pragma unroll
-      for (int k = 0; k < kTBSlots; ++k) {
-        const int e = tid + k * kThreads3;
-        const int i = e / (kTBP / 2), c2 = e % (kTBP / 2);
-        const int64_t y = y0 - 2 + i, x = x0 - 2 + 2 * c2;
-        if (e < kTBChunks && y >= -1 && y <= g.e1 && x <= g.e2)
-          cp_async16(tb + i * kTBP + 2 * c2, pb + (int64_t)i * g.s1 + 2 * c2);
-      }
+      for (int k = 0; k < kTBSlots; ++k)
+        if (sval[k]) cp_async16(tb + soff[k], pb + goff[k]);
     }
     cp_async_commit();
   };

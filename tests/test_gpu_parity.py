@@ -530,3 +530,24 @@ def test_jacobi2d_pipelined_e2e_bands(cuda_ready, band):
     r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "e2e_band_check.py")],
                        env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_pipelined_drop_in_repeated_calls(cuda_ready):
+    """The pipelined drop-in paths (bands / slabs skewed by each pass's
+    levels) reuse the thread's device buffers across calls: every call, one
+    pass or many, must read only rows its own passes wrote (regression: the
+    last band read rows of the previous band's last pass without waiting
+    for it, so a second call could return the first call's values)."""
+    from paper_2010_04868_b200.kernels import jacobi2d_temporal, jacobi3d_temporal
+
+    cases = [(jacobi3d_temporal, "jac3d27p", (192, 40, 50), (2, 3, 5)),
+             (jacobi2d_temporal, "heat2d", (1100, 90), (3, 8, 21)),
+             (heat1d_temporal, "heat1d", (600000,), (5, 64, 130))]
+    for fn, kernel, ext, steps_list in cases:
+        spec = get(kernel).spec
+        for seed, steps in enumerate(steps_list):
+            g = Grid.random(ext, seed=seed)
+            want = cref.scalar_reference(spec, g, steps).interior
+            for rep in range(3):
+                got = fn(g, steps, kernel=kernel).interior
+                assert np.array_equal(got, want), (kernel, steps, rep)

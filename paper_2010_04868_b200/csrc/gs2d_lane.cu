@@ -110,6 +110,7 @@ struct GslArgs {
   int m_end;          // iterations per CTA (multiple of kR)
   double* gring;      // kNumSlots x m_end x Ph x L (sentinel until written)
   int* done;          // [slot]: consumer CTAs of this slot that exited (their ticket)
+  int* epoch;         // [slot]: boundary + 1 of the producer that owns the slot now
   int* ticket;
   const unsigned* rows_ready;  // drop-in pipeline: grid rows uploaded so far (nullptr: all resident)
   unsigned* blocks_done;       // drop-in pipeline: CTAs finished, published in ticket order (or nullptr)
@@ -190,14 +191,18 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
 #endif
   double* gin = p.gring + (size_t)slot_in * m_end * kPh * kL;
   double* gout = p.gring + (size_t)slot_out * m_end * kPh * kL;
-  if (has_down && n >= kNumSlots && threadIdx.x == 0) {
+  if (has_down && threadIdx.x == 0) {
     // ring slot reuse: the consumer of boundary n - kNumSlots (a lower
-    // ticket, so started) must have exited before this CTA writes the slot
-    const long long t0 = clock64();
-    while (ld_acquire_gpu32(p.done + slot_out) < n - kNumSlots + 1) {
-      __nanosleep(256);
-      if (clock64() - t0 > (1ll << 34)) __trap();
+    // ticket, so started) must have exited -- read and reset every cell --
+    // before this CTA writes the slot; then the slot is published as mine
+    if (n >= kNumSlots) {
+      const long long t0 = clock64();
+      while (ld_acquire_gpu32(p.done + slot_out) < n - kNumSlots + 1) {
+        __nanosleep(256);
+        if (clock64() - t0 > (1ll << 34)) __trap();
+      }
     }
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.epoch + slot_out), "r"(n + 1) : "memory");
   }
   __syncthreads();
   // producer rows a consumer reads: its rows >= -ProRows, i.e. >= LAM*G - ProRows here
@@ -357,6 +362,16 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
         dst[1] = __longlong_as_double(v1);
       }
     };
+    if (has_up) {
+      // the incoming slot holds my producer's cells only once the producer
+      // took it over (after its previous consumer reset every cell); before
+      // that its cells may still hold the previous boundary's values
+      const long long t0 = clock64();
+      while (ld_acquire_gpu32(p.epoch + slot_in) != n) {
+        __nanosleep(128);
+        if (clock64() - t0 > (1ll << 35)) __trap();
+      }
+    }
     if (p.rows_ready) {
       // the drop-in path uploads row bands while this kernel runs: this
       // CTA reads grid rows d0 - kPh + 1 .. d0 + G (its rings' lane -1)
@@ -496,12 +511,13 @@ static int gsl_launch(GslArgs a, int64_t steps, int64_t per, cudaStream_t s, con
   const int m_need = a.e1 + kLam * (C::G - 1) + 2 * (C::L - 1) + kB + 2;
   a.m_end = (m_need + kR - 1) / kR * kR;
   const size_t cells = (size_t)kNumSlots * a.m_end * C::Ph * C::L;
-  const size_t ctrl_bytes = sizeof(int) * kNumSlots + 64;
+  const size_t ctrl_bytes = sizeof(int) * 2 * kNumSlots + 64;
   a.gring = static_cast<double*>(scratch(sizeof(double) * cells, 4));
   char* ctrl = static_cast<char*>(scratch(ctrl_bytes, 5));
   if (!a.gring || !ctrl) return fail(TVS_ERR_CUDA, "gs2d_lane: scratch");
   a.done = reinterpret_cast<int*>(ctrl);
-  a.ticket = a.done + kNumSlots;
+  a.epoch = a.done + kNumSlots;
+  a.ticket = a.epoch + kNumSlots;
   // every ring cell unwritten.  Consumers reset every cell they read and
   // every written cell is read, so a ring stays clean after a launch: the
   // sentinel fill runs only when the buffer or its layout changes

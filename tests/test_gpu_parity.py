@@ -551,3 +551,27 @@ def test_pipelined_drop_in_repeated_calls(cuda_ready):
             for rep in range(3):
                 got = fn(g, steps, kernel=kernel).interior
                 assert np.array_equal(got, want), (kernel, steps, rep)
+
+
+@pytest.mark.parametrize("order", ["lexicographic", "reference"])
+def test_gs2d_lane_ring_slot_reuse(cuda_ready, order):
+    """K6v2 hands rows between CTAs through an L2 ring of 320 slots: narrow
+    grids (short CTA lifetimes, > 320 CTAs) reuse slots while older CTAs are
+    still running.  A consumer may read a reused slot only after its producer
+    took it over from the previous consumer (regression: stale cells read as
+    valid), through the drop-in (copy overlap) and the plan API."""
+    spec = get("gs2d9p").spec
+    for rows, cols, steps in [(1300, 64, 1), (2048, 64, 2), (2048, 200, 5), (3000, 64, 40), (1400, 48, 100)]:
+        if order == "reference" and steps < 2:
+            continue
+        g = Grid.random((rows, cols), seed=rows + steps)
+        want = cref.scalar_reference(spec, g, steps, order=order).interior
+        got = execute(spec, g, steps, order=order).interior  # drop-in (row bands overlap the kernel)
+        assert np.array_equal(got, want), (rows, cols, steps, "drop-in")
+        plan = _native.Plan(spec, (rows, cols), config.current().native(order=order))
+        plan.upload(g.data, g.offset)
+        plan.run(steps)
+        out = g.alloc_like()
+        plan.download(out.data, out.offset)
+        plan.close()
+        assert np.array_equal(out.interior, want), (rows, cols, steps, "plan")

@@ -230,17 +230,16 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
   // staging slots: smem cell (row i, col 2c) <- global (y0-2+i, x0-2+2c);
   // rows/columns beyond the memory halo are never needed (their level-1
   // positions are pinned) and are not read
-  int soff[kTBSlots];
+  int soff[kTBSlots];  // shared offset, -1: slot not read
   int64_t goff[kTBSlots];
-  bool sval[kTBSlots];
 #pragma unroll
   for (int k = 0; k < kTBSlots; ++k) {
     const int e = tid + k * kThreads3;
     const int i = e / (kTBP / 2), c2 = e % (kTBP / 2);
     const int64_t y = y0 - 2 + i, x = x0 - 2 + 2 * c2;
-    soff[k] = i * kTBP + 2 * c2;
+    const bool ok = e < kTBChunks && y >= -1 && y <= g.e1 && x <= g.e2;
+    soff[k] = ok ? i * kTBP + 2 * c2 : -1;
     goff[k] = y * g.s1 + x;
-    sval[k] = e < kTBChunks && y >= -1 && y <= g.e1 && x <= g.e2;
   }
   const double* base = src + origin;
   auto stage = [&](int64_t p) {
@@ -249,7 +248,7 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
       double* tb = l0 + (int)((p - p0 + 3) % 3) * (kTBR * kTBP);
 #pragma unroll
       for (int k = 0; k < kTBSlots; ++k)
-        if (sval[k]) cp_async16(tb + soff[k], pb + goff[k]);
+        if (soff[k] >= 0) cp_async16(tb + soff[k], pb + goff[k]);
     }
     cp_async_commit();
   };
@@ -308,10 +307,10 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
             for (int r = 0; r < kRY; ++r)
               if (store_ok >> (h * kRY + r) & 1u) op[r * g.s1 + 32 * h] = pin ? bnd : out[h][r];
         };
-        // local plane, plus the neighbour's ghost plane when sharded.  The
-        // loop form is used unsharded too: its register allocation fits the
-        // 128-register cap without the 4-byte spill of the inlined store
-        for_each_dst(dst, mir, q2, store);
+        if constexpr (MIR)
+          for_each_dst(dst, mir, q2, store);  // sharded: local plane + the neighbour's ghost plane
+        else
+          store(dst);
       }
     }
   }
@@ -345,8 +344,7 @@ static int launch_tb(const Geo& geo, const tvs_geometry& g, const double* src, d
                      double bnd, cudaStream_t s, int64_t plo, int64_t phi, int seg, const Mirror& mir) {
   // per device context; a host-side attribute write, no synchronisation
   const bool mirrored = mir.p[0] != nullptr || mir.p[1] != nullptr;
-  (void)mirrored;  // one form (see the store): mirrors are runtime-null when unsharded
-  auto kern = jacobi3d_tb_kernel<MASK, FMA, true>;
+  auto kern = mirrored ? jacobi3d_tb_kernel<MASK, FMA, true> : jacobi3d_tb_kernel<MASK, FMA, false>;
   TVS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTBSmem));
   const dim3 block(kTX3, kTYT);
   const dim3 grid((unsigned)((geo.e2 + kTBOX - 1) / kTBOX), (unsigned)((geo.e1 + kTBOY - 1) / kTBOY),

@@ -549,8 +549,9 @@ def run_reference(args):
     cores = 1 if gauss else (os.cpu_count() or 1)
     pts = int(np.prod(cfg["extents"]))
     _, one = _port_rate(spec, g, 1, cores)
-    budget = 120.0 / max(1, args.steps + args.warmup)
-    t_cpu = int(max(1, min(cfg["T"], budget / max(one, 1e-6))))
+    # the same ~12 s sample per step as our arm's cpu_baseline leg (a longer
+    # sample runs the host at a lower sustained clock: 3.4 vs 4.5 GSt/s)
+    t_cpu = int(max(1, min(cfg["T"], 12.0 / max(one, 1e-6))))
     times = []
     for i in range(args.warmup + args.steps):
         _, dt = _port_rate(spec, g, t_cpu, cores)

@@ -2,6 +2,7 @@
 config's dominant kernel) from the ncu launch lists tools/evidence.sh writes:
 
     python tools/make_traffic.py gpurun_out/launches_c{1..5}.csv > profiles/traffic.json
+    python tools/make_traffic.py --full-T gpurun_out/r02_launches_c{1..5}.csv   (round 2: full-T runs)
 """
 import csv
 import json
@@ -14,6 +15,10 @@ import bench  # noqa: E402
 
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 T_PROFILED = {1: 1000, 2: 1000, 3: 16, 4: 100, 5: 2}  # --T used by tools/evidence.sh
+if "--full-T" in sys.argv:  # tools/evidence_r02.sh profiles every config at its full T
+    sys.argv.remove("--full-T")
+    T_PROFILED = {c: bench.CONFIGS[c]["T"] for c in bench.CONFIGS}
+HELPERS = ("fill_halo", "gsl_sentinel", "shard_signal", "shard_fill")
 
 
 def launches(path):
@@ -32,11 +37,11 @@ def launches(path):
 
 
 out = {"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-                 "--clock-control none (profiles/r01_launches_c*.csv, tools/evidence.sh)", "configs": {}}
+                 "--clock-control none (" + ", ".join(os.path.basename(x) for x in sys.argv[1:]) + ")", "configs": {}}
 for path in sys.argv[1:]:
     cid = int(re.search(r"c(\d)", os.path.basename(path)).group(1))
     cfg = bench.CONFIGS[cid]
-    ls = [x for x in launches(path) if "fill_halo" not in x["name"]]
+    ls = [x for x in launches(path) if not any(h in x["name"] for h in HELPERS)]
     if not ls:
         continue
     name = ls[0]["name"].split("(")[0].replace("void ", "")

@@ -21,6 +21,7 @@
 // of a segment are recomputed by neighbouring warps; useful width is
 // 32*P - 2*D.  HBM traffic per useful update ~ 16 B / D.
 #include <algorithm>
+#include <cmath>
 #include <type_traits>
 
 #include "common.cuh"
@@ -49,7 +50,12 @@ __device__ __forceinline__ constexpr bool has_group() {
 }
 
 // acc[p] (+)= sum over taps of row-group G, columns dc = -1, 0, +1, in order.
-template <unsigned MASK, int G, bool START, bool FMA, int kP2>
+// SC (scaled power-of-two taps): c holds c_k / c_first, all powers of two,
+// and acc carries the partial sum divided by c_first: the first tap is the
+// input itself, every other tap one DFMA whose product is exact — equal bit
+// for bit to the reference's separately rounded c*v then +acc, because
+// scaling by a power of two commutes with rounding (barring under/overflow).
+template <unsigned MASK, int G, bool START, bool FMA, int kP2, bool SC = false>
 __device__ __forceinline__ void add_group(double (&acc)[kP2], const double (&in)[kP2 + 2], const double (&c)[9]) {
 #pragma unroll
   for (int p = 0; p < kP2; ++p) {
@@ -59,10 +65,13 @@ __device__ __forceinline__ void add_group(double (&acc)[kP2], const double (&in)
       if ((MASK >> (G * 3 + dc)) & 1u) {
         const double v = in[p + dc];
         if (fresh) {
-          acc[p] = tap_first(c[G * 3 + dc], v);
+          if constexpr (SC)
+            acc[p] = v;  // c_first / c_first = 1
+          else
+            acc[p] = tap_first(c[G * 3 + dc], v);
           fresh = false;
         } else {
-          acc[p] = tap_next<FMA>(c[G * 3 + dc], v, acc[p]);
+          acc[p] = tap_next<FMA || SC>(c[G * 3 + dc], v, acc[p]);
         }
       }
     }
@@ -71,24 +80,29 @@ __device__ __forceinline__ void add_group(double (&acc)[kP2], const double (&in)
 
 struct Coeff9 {
   double c[9];
+  // SC: values of level l are the true values / c_first^(l+1); pinned cells
+  // of level l hold bnd / c_first^(l+1) (bl[l]); a stored level-D value is
+  // multiplied by c_first^D (out_scale)
+  double bl[13];
+  double out_scale;
 };
 
 // One level update when row q of the level below arrives (see header):
 // out(q-1) = F + taps(+1 row); N(q) = M + taps(0 row); M'(q+1) = taps(-1 row).
 // F is finished in place (it becomes the fresh accumulator), so calling this
 // with (F, M) and then (M, F) on the next row rotates roles without copies.
-template <unsigned MASK, bool FMA, int kP2>
+template <unsigned MASK, bool FMA, int kP2, bool SC>
 __device__ __forceinline__ void level_row(double (&F)[kP2], double (&M)[kP2], const double (&in)[kP2 + 2],
                                           const double (&c)[9], double (&out)[kP2]) {
   constexpr bool G0 = has_group<MASK, 0>(), G1 = has_group<MASK, 1>(), G2 = has_group<MASK, 2>();
-  if constexpr (G2) add_group<MASK, 2, !(G0 || G1), FMA, kP2>(F, in, c);
+  if constexpr (G2) add_group<MASK, 2, !(G0 || G1), FMA, kP2, SC>(F, in, c);
 #pragma unroll
   for (int p = 0; p < kP2; ++p) out[p] = F[p];
-  if constexpr (G1) add_group<MASK, 1, !G0, FMA, kP2>(M, in, c);
-  if constexpr (G0) add_group<MASK, 0, true, FMA, kP2>(F, in, c);
+  if constexpr (G1) add_group<MASK, 1, !G0, FMA, kP2, SC>(M, in, c);
+  if constexpr (G0) add_group<MASK, 0, true, FMA, kP2, SC>(F, in, c);
 }
 
-template <unsigned MASK, int D, bool FMA, int kP2, bool MIR>
+template <unsigned MASK, int D, bool FMA, int kP2, bool MIR, bool SC>
 __global__ void __maxnreg__(192) jacobi2d_kernel(const double* __restrict__ src,
                                                                 double* __restrict__ dst, Geo g, int64_t origin,
                                                                 Coeff9 cf, double bnd, int64_t n_strips,
@@ -153,17 +167,18 @@ __global__ void __maxnreg__(192) jacobi2d_kernel(const double* __restrict__ src,
       for (int l = 0; l < D; ++l) {
         double out[kP2];
         if constexpr (EVEN)
-          level_row<MASK, FMA, kP2>(B[l], A[l], in, c, out);
+          level_row<MASK, FMA, kP2, SC>(B[l], A[l], in, c, out);
         else
-          level_row<MASK, FMA, kP2>(A[l], B[l], in, c, out);
+          level_row<MASK, FMA, kP2, SC>(A[l], B[l], in, c, out);
         if constexpr (FAST) {
 #pragma unroll
           for (int p = 0; p < kP2; ++p) in[p + 1] = out[p];
         } else {
           const int gq = m - l - 1 + a0;
           const bool pin_row = gq < 0 || gq >= ag;
+          const double pin = SC ? cf.bl[l] : bnd;  // the boundary at this level's scale
 #pragma unroll
-          for (int p = 0; p < kP2; ++p) in[p + 1] = (pin_row || (col_out >> p & 1u)) ? bnd : out[p];
+          for (int p = 0; p < kP2; ++p) in[p + 1] = (pin_row || (col_out >> p & 1u)) ? pin : out[p];
         }
         if (l + 1 < D) {
           in[0] = __shfl_up_sync(0xffffffffu, in[kP2], 1);
@@ -172,6 +187,10 @@ __global__ void __maxnreg__(192) jacobi2d_kernel(const double* __restrict__ src,
       }
       const int q = m - D;  // level-D row leaving
       if (q >= r0 && q < r1) {
+        if constexpr (SC) {
+#pragma unroll
+          for (int p = 0; p < kP2; ++p) in[p + 1] = __dmul_rn(in[p + 1], cf.out_scale);  // exact: a power of two
+        }
         if constexpr (MIR) {
           // sharded pass: local row, plus the neighbour's ghost row
           for_each_dst(dst, mir, q, [&](double* base) {
@@ -332,22 +351,23 @@ bool jacobi2d_blocked_supported(const tvs_stencil& st) {
 int jacobi2d_max_depth() { return kMaxD2; }
 int jacobi2d_default_depth() { return 8; }  // measured best (config 3, P = 3: D = 6 1392, 7 1593, 8 1723, 10 1576 GSt/s)
 
+// mode 0: unfused taps, 1: fused (FMA), 2: scaled power-of-two taps (SC)
 template <unsigned MASK, int D, int P>
-static void launch2d_d(bool fma, unsigned blocks, cudaStream_t s, const double* src, double* dst, const Geo& geo,
+static void launch2d_d(int mode, unsigned blocks, cudaStream_t s, const double* src, double* dst, const Geo& geo,
                        int64_t origin, const Coeff9& cf, double bnd, int64_t ns, int64_t nt, int64_t lo, int64_t hi,
                        int seg_rows, const Mirror& mir) {
   // the mirror-store form only for sharded passes: no cost on one GPU
   const bool mirrored = mir.p[0] != nullptr || mir.p[1] != nullptr;
-  if (fma) {
-    if (mirrored)
-      jacobi2d_kernel<MASK, D, true, P, true><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows, mir);
-    else
-      jacobi2d_kernel<MASK, D, true, P, false><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows, mir);
+  auto go = [&](auto kern) { kern<<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows, mir); };
+  if (mode == 2) {
+    if (mirrored) go(jacobi2d_kernel<MASK, D, true, P, true, true>);
+    else go(jacobi2d_kernel<MASK, D, true, P, false, true>);
+  } else if (mode == 1) {
+    if (mirrored) go(jacobi2d_kernel<MASK, D, true, P, true, false>);
+    else go(jacobi2d_kernel<MASK, D, true, P, false, false>);
   } else {
-    if (mirrored)
-      jacobi2d_kernel<MASK, D, false, P, true><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows, mir);
-    else
-      jacobi2d_kernel<MASK, D, false, P, false><<<blocks, kWarps2 * 32, 0, s>>>(src, dst, geo, origin, cf, bnd, ns, nt, lo, hi, seg_rows, mir);
+    if (mirrored) go(jacobi2d_kernel<MASK, D, false, P, true, false>);
+    else go(jacobi2d_kernel<MASK, D, false, P, false, false>);
   }
 }
 
@@ -396,7 +416,7 @@ static int64_t resident_blocks(K kern) {
 // rows [row_lo, row_hi) of the grid (any band; the
 // whole grid by default): one row band of the pipelined host path
 template <unsigned MASK, int D>
-static void launch2d_one(bool fma, cudaStream_t s, const double* src, double* dst, const Geo& geo, int64_t origin,
+static void launch2d_one(int mode, cudaStream_t s, const double* src, double* dst, const Geo& geo, int64_t origin,
                          const Coeff9& cf, double bnd, int64_t row_lo, int64_t row_hi, int seg_rows,
                          const Mirror& mir) {
   // columns per lane: registers grow as 2 * P * D accumulators; P = 3 at
@@ -406,37 +426,65 @@ static void launch2d_one(bool fma, cudaStream_t s, const double* src, double* ds
   const int64_t U = 32 * P - 2 * D;
   const int64_t ns = (geo.e1 + U - 1) / U;
   if (seg_rows <= 0) {
-    static const int64_t res[2] = {resident_blocks(jacobi2d_kernel<MASK, D, false, P, false>),
-                                   resident_blocks(jacobi2d_kernel<MASK, D, true, P, false>)};
-    seg_rows = auto_seg(row_hi - row_lo, ns, D, res[fma ? 1 : 0]);
+    static const int64_t res[3] = {resident_blocks(jacobi2d_kernel<MASK, D, false, P, false, false>),
+                                   resident_blocks(jacobi2d_kernel<MASK, D, true, P, false, false>),
+                                   resident_blocks(jacobi2d_kernel<MASK, D, true, P, false, true>)};
+    seg_rows = auto_seg(row_hi - row_lo, ns, D, res[mode]);
   }
   const int64_t nseg = (row_hi - row_lo + seg_rows - 1) / seg_rows;
   const int64_t nt = ns * nseg;
   const unsigned blocks = (unsigned)((nt + kWarps2 - 1) / kWarps2);
-  launch2d_d<MASK, D, P>(fma, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt, row_lo, row_hi, seg_rows, mir);
+  launch2d_d<MASK, D, P>(mode, blocks, s, src, dst, geo, origin, cf, bnd, ns, nt, row_lo, row_hi, seg_rows, mir);
 }
 
 template <unsigned MASK>
-static void launch2d(int depth, bool fma, cudaStream_t s, const double* src, double* dst, const Geo& geo,
+static void launch2d(int depth, int mode, cudaStream_t s, const double* src, double* dst, const Geo& geo,
                      int64_t origin, const Coeff9& cf, double bnd, int64_t lo, int64_t hi, int seg, const Mirror& mir) {
   switch (depth) {
-    case 1: launch2d_one<MASK, 1>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
-    case 2: launch2d_one<MASK, 2>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
-    case 3: launch2d_one<MASK, 3>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
-    case 4: launch2d_one<MASK, 4>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
-    case 5: launch2d_one<MASK, 5>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
-    case 6: launch2d_one<MASK, 6>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
-    case 7: launch2d_one<MASK, 7>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
-    case 8: launch2d_one<MASK, 8>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
-    case 9: launch2d_one<MASK, 9>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
-    case 10: launch2d_one<MASK, 10>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
-    case 11: launch2d_one<MASK, 11>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
-    default: launch2d_one<MASK, 12>(fma, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 1: launch2d_one<MASK, 1>(mode, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 2: launch2d_one<MASK, 2>(mode, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 3: launch2d_one<MASK, 3>(mode, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 4: launch2d_one<MASK, 4>(mode, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 5: launch2d_one<MASK, 5>(mode, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 6: launch2d_one<MASK, 6>(mode, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 7: launch2d_one<MASK, 7>(mode, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 8: launch2d_one<MASK, 8>(mode, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 9: launch2d_one<MASK, 9>(mode, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 10: launch2d_one<MASK, 10>(mode, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    case 11: launch2d_one<MASK, 11>(mode, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
+    default: launch2d_one<MASK, 12>(mode, s, src, dst, geo, origin, cf, bnd, lo, hi, seg, mir); break;
   }
 }
 
 int jacobi2d_band_rows() { return kRowsSeg; }
 
+
+// Scaled taps (SC) instead of DMUL + DFMAs when every coefficient is a power
+// of two (the fused form is already exact then): one FP64 instruction less
+// per update.  The carried values grow by 1/|c_first| per level (heat2d:
+// 8^D, 2^24 at D = 8), so values must stay below 2^(1023 - D*log2(1/|c0|))
+// — the same class of caveat as the fused-exact form's subnormal products;
+// TVS_J2D_SCALED=0 disables it.
+static bool scaled_ok(const tvs_stencil& st, const Coeff9& cf, int depth) {
+  static const bool off = [] {
+    const char* e = getenv("TVS_J2D_SCALED");
+    return e && atoi(e) == 0;
+  }();
+  if (off || !coeffs_power_of_two(st)) return false;
+  int first = -1;
+  for (int k = 0; k < 9 && first < 0; ++k)
+    if (cf.c[k] != 0.0) first = k;
+  if (first < 0) return false;
+  int ex0;
+  std::frexp(cf.c[first], &ex0);
+  for (int k = 0; k < 9; ++k) {
+    if (cf.c[k] == 0.0) continue;
+    int ex;
+    std::frexp(cf.c[k], &ex);
+    if (std::abs(ex - ex0) > 60) return false;
+  }
+  return std::abs(ex0 - 1) * depth <= 120;  // growth of the carried values
+}
 
 int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, int depth,
                      bool fma, cudaStream_t s, int64_t row_lo, int64_t row_hi, int seg_rows, const Mirror* mir) {
@@ -449,10 +497,23 @@ int jacobi2d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double*
     return fail(TVS_ERR_INVALID, "jacobi2d_blocked: row band");
   const Geo geo = make_geo(g);
   const Mirror m = mir ? *mir : Mirror{};
+  const int mode = fma ? (scaled_ok(st, cf, depth) ? 2 : 1) : 0;
+  if (mode == 2) {
+    // scaled taps: ratios to the first tap's coefficient, per-level pins
+    const double c0 = cf.c[__builtin_ctz(mask)];
+    for (int k = 0; k < 9; ++k) cf.c[k] /= c0;
+    double sc = 1.0;
+    for (int l = 0; l <= kMaxD2; ++l) {
+      sc /= c0;
+      cf.bl[l] = st.boundary * sc;
+    }
+    cf.out_scale = 1.0;
+    for (int l = 0; l < depth; ++l) cf.out_scale *= c0;  // exact: powers of two
+  }
   if (mask == kStar5)
-    launch2d<kStar5>(depth, fma, s, src, dst, geo, g.origin, cf, st.boundary, row_lo, row_hi, seg_rows, m);
+    launch2d<kStar5>(depth, mode, s, src, dst, geo, g.origin, cf, st.boundary, row_lo, row_hi, seg_rows, m);
   else
-    launch2d<kBox9>(depth, fma, s, src, dst, geo, g.origin, cf, st.boundary, row_lo, row_hi, seg_rows, m);
+    launch2d<kBox9>(depth, mode, s, src, dst, geo, g.origin, cf, st.boundary, row_lo, row_hi, seg_rows, m);
   TVS_LAUNCHED("jacobi2d_kernel");
   return TVS_OK;
 }

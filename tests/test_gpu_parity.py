@@ -575,3 +575,28 @@ def test_gs2d_lane_ring_slot_reuse(cuda_ready, order):
         plan.download(out.data, out.offset)
         plan.close()
         assert np.array_equal(out.interior, want), (rows, cols, steps, "plan")
+
+
+def test_staged_pageable_uploads(cuda_ready):
+    """Pageable inputs are staged by the library (csrc/hostcopy.cu: host
+    thread pool -> page-locked 32 MiB slots -> DMA per slot): 1D, 2D and 3D
+    grids larger than several slots, chunks spanning 3D planes, odd row
+    widths, results equal to the page-locked path and to the oracle; the
+    result Grid comes from the page-locked result pool and keeps the input's
+    frame."""
+    from paper_2010_04868_b200.kernels import jacobi2d_temporal, jacobi3d_temporal
+
+    cases = [(jacobi3d_temporal, "heat3d", (131, 157, 211), 3), (jacobi2d_temporal, "heat2d", (3001, 2999), 5),
+             (heat1d_temporal, "heat1d", (9_000_001,), 4)]
+    for fn, kernel, ext, steps in cases:
+        spec = get(kernel).spec
+        g = Grid.random(ext, seed=len(ext), boundary=0.5)
+        assert g.data.nbytes > 64 << 20
+        want = cref.scalar_reference(spec, g, steps, threads=8)
+        got = fn(g, steps, kernel=kernel)
+        assert np.array_equal(got.interior, want.interior), kernel
+        for sl in g.frame_slices():
+            assert np.array_equal(got.data[sl], g.data[sl]), kernel
+        pg = Grid(ext, 1, boundary=0.5, pinned=True)
+        np.copyto(pg.data, g.data)
+        assert np.array_equal(fn(pg, steps, kernel=kernel).interior, want.interior), kernel

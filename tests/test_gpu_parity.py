@@ -586,12 +586,12 @@ def test_staged_pageable_uploads(cuda_ready):
     frame."""
     from paper_2010_04868_b200.kernels import jacobi2d_temporal, jacobi3d_temporal
 
-    cases = [(jacobi3d_temporal, "heat3d", (131, 157, 211), 3), (jacobi2d_temporal, "heat2d", (3001, 2999), 5),
+    cases = [(jacobi3d_temporal, "heat3d", (163, 171, 301), 3), (jacobi2d_temporal, "heat2d", (3001, 2999), 5),
              (heat1d_temporal, "heat1d", (9_000_001,), 4)]
     for fn, kernel, ext, steps in cases:
         spec = get(kernel).spec
         g = Grid.random(ext, seed=len(ext), boundary=0.5)
-        assert g.data.nbytes > 64 << 20
+        assert g.data.nbytes > 2 * (32 << 20)  # several staging slots
         want = cref.scalar_reference(spec, g, steps, threads=8)
         got = fn(g, steps, kernel=kernel)
         assert np.array_equal(got.interior, want.interior), kernel

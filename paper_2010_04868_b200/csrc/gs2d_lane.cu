@@ -55,9 +55,8 @@ constexpr int kR = 16;           // smem ring rows (iterations), power of two
 constexpr int kPre = 6;          // phantom / lane -1 rows read before iteration 0 (rows -6..-1)
 constexpr int kLR = 128;         // lane -1 staging ring (iterations), power of two
 #ifndef GSL_BATCH
-#define GSL_BATCH 2  // config 4 (8192^2 x 100): 8 / 4 / 2 rows = 44.3 / 33.8 / 29.3 ms
+#define GSL_BATCH 0  // 0: per order (Cfg::Batch)
 #endif
-constexpr int kBatch = GSL_BATCH;  // lane -1 rows / phantom rows per loader block
 constexpr int kAheadL = 64;      // lane -1 rows are requested this many iterations ahead (HBM latency)
 constexpr int kNumSlots = 320;   // global ring slots (CTA boundaries in flight) >= resident CTAs
 // sentinel of an unwritten global-ring cell: a signalling NaN (quiet bit
@@ -73,20 +72,24 @@ struct Cfg {
   // phantom rings fill shared memory) reference order.  Config 4 lex G 3 / 4 /
   // 7: 33.8 / 29.3 / 32.3 ms; reference 4 / 7: 85.6 / 58.2 ms
   static constexpr int G = GSL_G > 0 ? GSL_G : (REF ? 7 : 4);
+  // rows per loader block (lane -1 staging batch, phantom poll block).
+  // Config 4 lexicographic 8 / 4 / 2 / 1 rows: 44.3 / 33.8 / 26.1 / 28.7 ms;
+  // reference order 2 / 1: 51.8 / 45.3 ms
+  static constexpr int Batch = GSL_BATCH > 0 ? GSL_BATCH : (REF ? 1 : 2);
   static constexpr int Ph = REF ? 2 : 1;        // phantom groups (reads reach group d-2 in REF)
   static constexpr int L = 32 * WG;             // lanes per group
   static constexpr int S = L + 2;               // ring row: [pad][lane -1][lanes 0..L-1] (16-B aligned lanes)
   static constexpr int Rings = G + Ph;          // ring index = local group + Ph
   static constexpr int Compute = G * WG;        // compute warps
   static constexpr int Threads = (Compute + 1) * 32;
-  static constexpr int Stg = 2 * kBatch * Ph * L;  // phantom staging: two blocks of kBatch compact rows
+  static constexpr int Stg = 2 * Batch * Ph * L;  // phantom staging: two blocks of Batch compact rows
   static constexpr size_t Smem = sizeof(double) * ((size_t)Rings * kR * S + (size_t)Rings * kLR + Stg);
   static constexpr int Back = REF ? 2 * kLam + 1 : kLam + 1;  // deepest ring read behind m
-  static_assert(kR >= Back + kBatch + 1, "ring too shallow for a phantom block written ahead");
-  static_assert(kLR >= kAheadL + kBatch + 8, "lane -1 staging ring too shallow");
+  static_assert(kR >= Back + Batch + 1, "ring too shallow for a phantom block written ahead");
+  static_assert(kLR >= kAheadL + Batch + 8, "lane -1 staging ring too shallow");
   static_assert(kPre >= Back + 1, "prologue rows");
-  static constexpr int ProRows = (kPre + kBatch - 1) / kBatch * kBatch;  // phantom rows before iteration 0
-  static_assert(kR % kBatch == 0 && kAheadL % kBatch == 0, "block sizes");
+  static constexpr int ProRows = (kPre + Batch - 1) / Batch * Batch;  // phantom rows before iteration 0
+  static_assert(kR % Batch == 0 && kAheadL % Batch == 0, "block sizes");
 };
 }  // namespace gsl
 
@@ -164,6 +167,7 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
   using namespace gsl;
   using C = Cfg<REF, WG>;
   constexpr int kG = C::G, kPh = C::Ph, kL = C::L, kS = C::S, kRings = C::Rings, kThreads = C::Threads;
+  constexpr int kBatch = C::Batch;
   extern __shared__ __align__(16) double smem[];
   double* const lm1 = smem + (size_t)kRings * kR * kS;  // lane -1 staging [ring][kLR]
   double* const stg = lm1 + kRings * kLR;                 // phantom staging [2][kBatch][kPh * kL]
@@ -301,7 +305,7 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
     //    Producer rows >= m_end are columns right of the grid: the boundary.
     constexpr int kRowCells = kPh * kL;            // cells of one phantom row
     constexpr int kPieces = kBatch * kRowCells / 2;  // 16-byte pieces per block
-    static_assert(kPieces % 32 == 0, "block pieces per lane");
+    constexpr int kPerLane = (kPieces + 31) / 32;  // pieces per loader lane (the last round partial)
     auto batch_lane_m1 = [&](int i0) {  // iterations [i0, i0 + kBatch), every ring
       for (int e = lane; e < kRings * kBatch; e += 32) {
         const int ri = e / kBatch, i = i0 + e % kBatch;
@@ -322,16 +326,17 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
     auto request_block = [&](int i0) {  // phantom rows [i0, i0 + kBatch) -> staging
       double* sb = stg + ((i0 / kBatch) & 1) * (kBatch * kRowCells);
 #pragma unroll 4
-      for (int j = 0; j < kPieces / 32; ++j) {
+      for (int j = 0; j < kPerLane; ++j) {
         const int k = lane + 32 * j, r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
-        if (in_ring(i0 + r)) cp_async16g(sb + r * kRowCells + e, gcell(i0 + r, e));
+        if (k < kPieces && in_ring(i0 + r)) cp_async16g(sb + r * kRowCells + e, gcell(i0 + r, e));
       }
     };
     auto finish_block = [&](int i0) {  // validate, copy into the rings, reset the L2 cells
       const double* sb = stg + ((i0 / kBatch) & 1) * (kBatch * kRowCells);
 #pragma unroll 1
-      for (int j = 0; j < kPieces / 32; ++j) {
+      for (int j = 0; j < kPerLane; ++j) {
         const int k = lane + 32 * j, r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
+        if (k >= kPieces) break;
         const int i = i0 + r;
         unsigned long long v0 = __double_as_longlong(bnd), v1 = v0;
         if (in_ring(i)) {

@@ -128,6 +128,24 @@ typedef struct tvs_geometry {
 int tvs_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, double* out,
             int64_t steps, const tvs_exec* ex);
 
+/* ---- problem-struct form (the SURVEY.md §8(b) signatures) --------------
+ * One struct for the stencil and the host Grid layout; the same work as
+ * tvs_run.  tvs_gauss_seidel runs in place; order = TVS_GS_*. */
+typedef struct tvs_problem {
+  int32_t dim;                     /* 1..3 */
+  int32_t ntaps;                   /* 1..27 */
+  int64_t extents[3];              /* interior extents */
+  int32_t radius;                  /* 1 */
+  int32_t pad_;
+  double boundary;                 /* Dirichlet value (grid.boundary) */
+  int32_t offsets[TVS_MAX_TAPS][3]; /* StencilSpec.offsets() order */
+  double coeffs[TVS_MAX_TAPS];
+  int64_t padded_shape[3];         /* Grid.data.shape */
+  int64_t offset;                  /* Grid.offset */
+} tvs_problem;
+int tvs_jacobi(const tvs_problem* p, const double* in_padded, double* out_padded, int64_t steps, const tvs_exec* ex);
+int tvs_gauss_seidel(const tvs_problem* p, double* inout_padded, int64_t steps, int32_t order, const tvs_exec* ex);
+
 /* ---- plan path: device-resident repetitions (cli.py:198-227 timing) ----- */
 typedef struct tvs_plan tvs_plan;
 int tvs_plan_create(const tvs_stencil* st, int32_t dim, const int64_t extents[3], const tvs_exec* ex,

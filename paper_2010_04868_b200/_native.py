@@ -62,6 +62,15 @@ class LifeRule(C.Structure):
     ]
 
 
+class Problem(C.Structure):
+    """tvs_problem (the SURVEY.md §8(b) problem-struct form)."""
+    _fields_ = [
+        ("dim", C.c_int32), ("ntaps", C.c_int32), ("extents", C.c_int64 * 3), ("radius", C.c_int32),
+        ("pad_", C.c_int32), ("boundary", C.c_double), ("offsets", (C.c_int32 * 3) * 27),
+        ("coeffs", C.c_double * 27), ("padded_shape", C.c_int64 * 3), ("offset", C.c_int64),
+    ]
+
+
 class ShardHandle(C.Structure):
     _fields_ = [("bytes", C.c_ubyte * 256)]
 
@@ -78,6 +87,8 @@ class TileDesc(C.Structure):
 _P = C.c_void_p
 _SIGS = {
     "tvs_run": (C.c_int, [C.POINTER(Stencil), C.POINTER(Layout), _P, _P, C.c_int64, C.POINTER(Exec)]),
+    "tvs_jacobi": (C.c_int, [C.POINTER(Problem), _P, _P, C.c_int64, C.POINTER(Exec)]),
+    "tvs_gauss_seidel": (C.c_int, [C.POINTER(Problem), _P, C.c_int64, C.c_int32, C.POINTER(Exec)]),
     "tvs_plan_create": (C.c_int, [C.POINTER(Stencil), C.c_int32, C.POINTER(C.c_int64), C.POINTER(Exec), C.POINTER(_P)]),
     "tvs_plan_upload": (C.c_int, [_P, C.POINTER(Layout), _P]),
     "tvs_plan_download": (C.c_int, [_P, C.POINTER(Layout), _P]),
@@ -294,6 +305,22 @@ def run(spec, src: np.ndarray, dst: np.ndarray, extents, offset: int, steps: int
     lay = make_layout(src, extents, offset)
     check(lib().tvs_run(C.byref(st), C.byref(lay), src.ctypes.data, dst.ctypes.data, int(steps), C.byref(ex)),
           f"tvs_run({spec.name})")
+
+
+def make_problem(spec, grid) -> Problem:
+    """StencilSpec + Grid -> tvs_problem (offsets() order, the grid's boundary)."""
+    st = make_stencil(spec, grid.boundary)
+    p = Problem()
+    p.dim, p.ntaps, p.radius, p.boundary = st.dim, st.ntaps, st.radius, st.boundary
+    for k in range(st.ntaps):
+        for d in range(3):
+            p.offsets[k][d] = st.offsets[k][d]
+        p.coeffs[k] = st.coeffs[k]
+    for d in range(3):
+        p.extents[d] = grid.extents[d] if d < grid.dim else 1
+        p.padded_shape[d] = grid.data.shape[d] if d < grid.dim else 1
+    p.offset = grid.offset
+    return p
 
 
 class Plan:

@@ -1153,6 +1153,46 @@ int tvs_run(const tvs_stencil* st, const tvs_layout* lay, const double* in, doub
   return TVS_OK;
 }
 
+static int problem_to(const tvs_problem* p, int kind, tvs_stencil* st, tvs_layout* lay) {
+  if (!p) return fail(TVS_ERR_INVALID, "null problem");
+  if (p->ntaps < 1 || p->ntaps > TVS_MAX_TAPS) return fail(TVS_ERR_INVALID, "ntaps must be 1..27");
+  std::memset(st, 0, sizeof(*st));
+  std::memset(lay, 0, sizeof(*lay));
+  st->dim = p->dim;
+  st->kind = kind;
+  st->ntaps = p->ntaps;
+  st->radius = p->radius;
+  st->boundary = p->boundary;
+  for (int k = 0; k < p->ntaps; ++k) {
+    for (int d = 0; d < 3; ++d) st->offsets[k][d] = p->offsets[k][d];
+    st->coeffs[k] = p->coeffs[k];
+  }
+  lay->dim = p->dim;
+  for (int d = 0; d < 3; ++d) {
+    lay->extents[d] = d < p->dim ? p->extents[d] : 1;
+    lay->shape[d] = d < p->dim ? p->padded_shape[d] : 1;
+  }
+  lay->offset = p->offset;
+  return TVS_OK;
+}
+
+int tvs_jacobi(const tvs_problem* p, const double* in_padded, double* out_padded, int64_t steps, const tvs_exec* ex) {
+  tvs_stencil st;
+  tvs_layout lay;
+  if (int rc = problem_to(p, TVS_JACOBI, &st, &lay)) return rc;
+  return tvs_run(&st, &lay, in_padded, out_padded, steps, ex);
+}
+
+int tvs_gauss_seidel(const tvs_problem* p, double* inout_padded, int64_t steps, int32_t order, const tvs_exec* ex) {
+  tvs_stencil st;
+  tvs_layout lay;
+  if (!ex) return fail(TVS_ERR_INVALID, "null exec");
+  if (int rc = problem_to(p, TVS_GAUSS_SEIDEL, &st, &lay)) return rc;
+  tvs_exec e = *ex;
+  e.gs_order = order;
+  return tvs_run(&st, &lay, inout_padded, inout_padded, steps, &e);
+}
+
 int tvs_plan_create(const tvs_stencil* st, int32_t dim, const int64_t extents[3], const tvs_exec* ex,
                     tvs_plan** out) {
   int rc = validate(st);

@@ -600,3 +600,27 @@ def test_staged_pageable_uploads(cuda_ready):
         pg = Grid(ext, 1, boundary=0.5, pinned=True)
         np.copyto(pg.data, g.data)
         assert np.array_equal(fn(pg, steps, kernel=kernel).interior, want.interior), kernel
+
+
+def test_problem_struct_entry_points(cuda_ready):
+    """tvs_jacobi / tvs_gauss_seidel (the SURVEY.md §8(b) signatures: one
+    tvs_problem for stencil + Grid layout) equal the oracle."""
+    import ctypes as C
+
+    lib = _native.lib()
+    for kernel, ext, steps in (("heat2d", (130, 97), 9), ("jac3d27p", (20, 33, 41), 3), ("heat1d", (5000,), 40)):
+        g = Grid.random(ext, seed=2, boundary=0.25)
+        spec = get(kernel).spec
+        out = g.copy()
+        prob = _native.make_problem(spec, g)
+        _native.check(lib.tvs_jacobi(C.byref(prob), g.data.ctypes.data, out.data.ctypes.data, steps,
+                                     C.byref(_native.make_exec())))
+        assert np.array_equal(out.interior, cref.scalar_reference(spec, g, steps).interior), kernel
+    for order, code in (("lexicographic", 0), ("reference", 1)):
+        g = Grid.random((90, 70), seed=3)
+        spec = get("gs2d9p").spec
+        work = g.copy()
+        prob = _native.make_problem(spec, g)
+        _native.check(lib.tvs_gauss_seidel(C.byref(prob), work.data.ctypes.data, 7, code,
+                                           C.byref(_native.make_exec())))
+        assert np.array_equal(work.interior, cref.scalar_reference(spec, g, 7, order=order).interior), order

@@ -40,6 +40,10 @@ int main(void) {
   printf("%zu %zu %zu %zu\n", sizeof(tvs_stencil), sizeof(tvs_layout), sizeof(tvs_exec), sizeof(tvs_geometry));
   printf("%zu %zu %zu\n", offsetof(tvs_stencil, coeffs), offsetof(tvs_stencil, boundary), offsetof(tvs_geometry, origin));
   printf("%zu %zu %zu\n", sizeof(tvs_life_rule), offsetof(tvs_life_rule, birth_mask), offsetof(tvs_life_rule, boundary));
+  printf("%zu %zu %zu %zu\n", sizeof(tvs_problem), offsetof(tvs_problem, boundary), offsetof(tvs_problem, coeffs),
+         offsetof(tvs_problem, offset));
+  printf("%zu %zu %zu\n", sizeof(tvs_exec), offsetof(tvs_exec, n_gpus), offsetof(tvs_exec, flags));
+  printf("%zu\n", sizeof(tvs_shard_handle));
   return 0;
 }
 '''
@@ -54,8 +58,12 @@ int main(void) {
                          ctypes.sizeof(_native.Exec), ctypes.sizeof(_native.Geometry)]
     assert sizes[4:7] == [_native.Stencil.coeffs.offset, _native.Stencil.boundary.offset,
                           _native.Geometry.origin.offset]
-    assert sizes[7:] == [ctypes.sizeof(_native.LifeRule), _native.LifeRule.birth_mask.offset,
-                         _native.LifeRule.boundary.offset]
+    assert sizes[7:10] == [ctypes.sizeof(_native.LifeRule), _native.LifeRule.birth_mask.offset,
+                           _native.LifeRule.boundary.offset]
+    assert sizes[10:14] == [ctypes.sizeof(_native.Problem), _native.Problem.boundary.offset,
+                            _native.Problem.coeffs.offset, _native.Problem.offset.offset]
+    assert sizes[14:17] == [ctypes.sizeof(_native.Exec), _native.Exec.n_gpus.offset, _native.Exec.flags.offset]
+    assert sizes[17] == ctypes.sizeof(_native.ShardHandle)
 
 
 def test_host_only_entry_points():

@@ -369,8 +369,8 @@ int tvs_shard_connect(tvs_shard* s, const tvs_shard_handle* left, const tvs_shar
     ShardWire w;
     std::memcpy(&w, hs[k]->bytes, sizeof(w));
     if (int rc = check_neighbour(s, k, w.index, w.n_shards, w.ghost, w.pitch)) return rc;
-    if (w.device != s->device)
-      if (int rc = enable_peer(s->device, w.device)) return rc;
+    // the neighbour's ordinal is from its own process (its CUDA_VISIBLE_DEVICES
+    // may differ): peer access comes from cudaIpcMemLazyEnablePeerAccess
     for (int b = 0; b < 2; ++b)
       TVS_CUDA(cudaIpcOpenMemHandle(&s->ipc_ptr[k][b], w.buf[b], cudaIpcMemLazyEnablePeerAccess));
     TVS_CUDA(cudaIpcOpenMemHandle(&s->ipc_ptr[k][2], w.flags, cudaIpcMemLazyEnablePeerAccess));

@@ -633,6 +633,8 @@ def run_sharded(args):
     if world != args.gpus:
         raise SystemExit(f"bench.py --gpus {args.gpus} launched with WORLD_SIZE={world}")
     local = int(os.environ.get("LOCAL_RANK", rank))
+    if local >= torch.cuda.device_count() and torch.cuda.device_count() == 1:
+        local = 0  # the launcher gave each rank its own CUDA_VISIBLE_DEVICES
     backend = "nccl"
     if os.environ.get("TVS_BENCH_EMULATE_SHARDS"):
         # plumbing check on a box with fewer GPUs than ranks: ranks share

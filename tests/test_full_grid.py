@@ -4,11 +4,10 @@ point against the C oracle (the bit-exact restatement of the reference's
 relative error (north_star bar: <= 1e-12; the result here is 0, asserted
 with ``array_equal``).
 
-Configs 1, 2, 3 and 4 (both Gauss-Seidel orders: the lexicographic loop
+Configs 1, 2, 3, 4 (both Gauss-Seidel orders: the lexicographic loop
 BASELINE names and the reference oracle's anti-diagonal order,
-baselines.py:83-107) are compared on the entire grid at full T.  Config 5's
-oracle would need ~25 CPU-minutes; it is covered by the light-cone windows
-and the blocked-vs-single-step identity of tests/test_full_size.py.
+baselines.py:83-107) and 5 (when the host has ~45 GB free) are compared on
+the entire grid at full T.
 
 Each test appends {config: max_rel_err} to gpurun_out/full_parity.json so
 the numbers travel back with the run (profiles/r02_full_parity.json)."""
@@ -67,9 +66,16 @@ def _gpu(cfg, g, order="lexicographic"):
 
 
 @pytest.mark.parametrize("cid,order", [(1, "lexicographic"), (2, "lexicographic"), (4, "lexicographic"),
-                                       (4, "reference"), (3, "lexicographic")])
+                                       (4, "reference"), (3, "lexicographic"), (5, "lexicographic")])
 def test_full_grid_bitexact(cuda_ready, cid, order):
     cfg = bench.CONFIGS[cid]
+    if cid == 5:
+        # 1033^3 doubles = 8.8 GB per array; input, GPU result and the
+        # oracle's two planes plus its output: ~45 GB of host memory
+        import psutil
+
+        if psutil.virtual_memory().available < 64 << 30:
+            pytest.skip("config 5 whole-grid parity needs ~45 GB of free host memory")
     spec = get(cfg["kernel"]).spec
     g = bench.make_grid(cfg)
     t0 = time.perf_counter()

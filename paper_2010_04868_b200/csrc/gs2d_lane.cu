@@ -81,8 +81,19 @@ struct Cfg {
   static constexpr int S = L + 2;               // ring row: [pad][lane -1][lanes 0..L-1] (16-B aligned lanes)
   static constexpr int Rings = G + Ph;          // ring index = local group + Ph
   static constexpr int Compute = G * WG;        // compute warps
+  // one loader warp (a second one, phantom blocks | lane -1 rows, measured
+  // slower: 28.6 vs 23.6 ms at config 4 -- one more warp in every barrier)
   static constexpr int Threads = (Compute + 1) * 32;
-  static constexpr int Stg = 2 * Batch * Ph * L;  // phantom staging: two blocks of Batch compact rows
+#ifndef GSL_DIST
+#define GSL_DIST 0
+#endif
+  // phantom blocks are requested Dist blocks ahead of their validation
+  // (config 4 reference order, one-row blocks: Dist 1 / 2: 33.1 / 30.0 ms;
+  // lexicographic two-row blocks: 19.6 / 22.0 ms)
+  static constexpr int Dist = GSL_DIST > 0 ? GSL_DIST : (REF ? 2 : 1);
+  static constexpr int StgBlocks = Dist < 2 ? 2 : 4;  // staging ring (power of two > Dist)
+  static_assert(Dist <= 3, "staging ring");
+  static constexpr int Stg = StgBlocks * Batch * Ph * L;  // phantom staging: blocks of Batch compact rows
   static constexpr size_t Smem = sizeof(double) * ((size_t)Rings * kR * S + (size_t)Rings * kLR + Stg);
   static constexpr int Back = REF ? 2 * kLam + 1 : kLam + 1;  // deepest ring read behind m
   static_assert(kR >= Back + Batch + 1, "ring too shallow for a phantom block written ahead");
@@ -157,6 +168,11 @@ __device__ __forceinline__ int ld_acquire_gpu32(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ double2 ld_relaxed_gpu2(const double* p) {
+  double2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void cta_bar(int nthreads) { asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory"); }
 
 #ifndef GSL_MINB
@@ -170,7 +186,7 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
   constexpr int kBatch = C::Batch;
   extern __shared__ __align__(16) double smem[];
   double* const lm1 = smem + (size_t)kRings * kR * kS;  // lane -1 staging [ring][kLR]
-  double* const stg = lm1 + kRings * kLR;                 // phantom staging [2][kBatch][kPh * kL]
+  double* const stg = lm1 + kRings * kLR;                 // phantom staging [StgBlocks][kBatch][kPh * kL]
   __shared__ int s_ticket;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   const double bnd = p.bnd;
@@ -306,14 +322,19 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
     constexpr int kRowCells = kPh * kL;            // cells of one phantom row
     constexpr int kPieces = kBatch * kRowCells / 2;  // 16-byte pieces per block
     constexpr int kPerLane = (kPieces + 31) / 32;  // pieces per loader lane (the last round partial)
+    // lane -1 rows: loader lane t < kRings * kBatch owns ring t / kBatch,
+    // iteration offset t % kBatch (grid row d0 + g + 1, g = ring - kPh)
+    static_assert(kRings * kBatch <= 32, "one lane -1 cell per loader lane");
+    const int lm_ri = lane / kBatch, lm_o = lane % kBatch, lm_g = lm_ri - kPh, lm_r = d0 + lm_g + 1;
+    const bool lm_on = lane < kRings * kBatch, lm_row = lm_r >= 0 && lm_r < e0;
+    const int lm_c0 = lm_o - kLam * lm_g + 2 - kB;  // grid column at i0 = 0
+    double* const lm_dst = lm1 + lm_ri * kLR + lm_o;
     auto batch_lane_m1 = [&](int i0) {  // iterations [i0, i0 + kBatch), every ring
-      for (int e = lane; e < kRings * kBatch; e += 32) {
-        const int ri = e / kBatch, i = i0 + e % kBatch;
-        const int g = ri - kPh;
-        const int r = d0 + g + 1, c = i - kLam * g + 2 - kB;
-        double* dst = lm1 + ri * kLR + (i & (kLR - 1));
-        if (r >= 0 && r < e0 && c >= 0 && c < e1)
-          cp_async8(dst, p.a + (long long)r * p.s0 + c);
+      if (lm_on) {
+        const int c = i0 + lm_c0;
+        double* dst = lm_dst + (i0 & (kLR - 1));
+        if (lm_row && c >= 0 && c < e1)
+          cp_async8(dst, p.a + (long long)lm_r * p.s0 + c);
         else
           *dst = bnd;
       }
@@ -324,15 +345,54 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
     auto in_ring = [&](int i) { return has_up && i + kLam * kG < m_end; };
     auto gcell = [&](int i, int e) -> double* { return gin + (size_t)(i + kLam * kG) * kRowCells + e; };
     auto request_block = [&](int i0) {  // phantom rows [i0, i0 + kBatch) -> staging
-      double* sb = stg + ((i0 / kBatch) & 1) * (kBatch * kRowCells);
+      double* sb = stg + ((i0 / kBatch) & (C::StgBlocks - 1)) * (kBatch * kRowCells);
 #pragma unroll 4
       for (int j = 0; j < kPerLane; ++j) {
         const int k = lane + 32 * j, r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
         if (k < kPieces && in_ring(i0 + r)) cp_async16g(sb + r * kRowCells + e, gcell(i0 + r, e));
       }
     };
-    auto finish_block = [&](int i0) {  // validate, copy into the rings, reset the L2 cells
-      const double* sb = stg + ((i0 / kBatch) & 1) * (kBatch * kRowCells);
+    // lexicographic: the block's pieces loaded together, 16-byte smem and L2
+    // accesses; reference order keeps the one-piece-at-a-time loop (faster
+    // there: 45.3 vs 51.8 ms at config 4 size)
+    auto finish_block_vec = [&](int i0) {
+      const double* sb = stg + ((i0 / kBatch) & (C::StgBlocks - 1)) * (kBatch * kRowCells);
+      double2 got[kPerLane];
+#pragma unroll
+      for (int j = 0; j < kPerLane; ++j) {
+        const int k = lane + 32 * j, r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
+        if (kPieces % 32 == 0 || k < kPieces) got[j] = *reinterpret_cast<const double2*>(sb + r * kRowCells + e);
+      }
+#pragma unroll
+      for (int j = 0; j < kPerLane; ++j) {
+        const int k = lane + 32 * j, r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
+        if (kPieces % 32 != 0 && k >= kPieces) break;
+        const int i = i0 + r;
+        unsigned long long v0 = __double_as_longlong(bnd), v1 = v0;
+        if (in_ring(i)) {
+          v0 = __double_as_longlong(got[j].x);
+          v1 = __double_as_longlong(got[j].y);
+          if (v0 == kSent || v1 == kSent) {
+            const long long t0 = clock64();
+            while (v0 == kSent) {
+              v0 = ld_relaxed_gpu(gcell(i, e));
+              if (clock64() - t0 > (1ll << 34)) __trap();
+            }
+            while (v1 == kSent) {
+              v1 = ld_relaxed_gpu(gcell(i, e + 1));
+              if (clock64() - t0 > (1ll << 34)) __trap();
+            }
+          }
+          asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(gcell(i, e)), "l"(kSent), "l"(kSent)
+                       : "memory");
+        }
+        const int ph = e / kL, ll = e % kL;
+        double* dst = smem + ((size_t)ph * kR + (i & (kR - 1))) * kS + 2 + ll;
+        *reinterpret_cast<double2*>(dst) = make_double2(__longlong_as_double(v0), __longlong_as_double(v1));
+      }
+    };
+    auto finish_block_one = [&](int i0) {
+      const double* sb = stg + ((i0 / kBatch) & (C::StgBlocks - 1)) * (kBatch * kRowCells);
 #pragma unroll 1
       for (int j = 0; j < kPerLane; ++j) {
         const int k = lane + 32 * j, r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
@@ -366,6 +426,71 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
         dst[0] = __longlong_as_double(v0);
         dst[1] = __longlong_as_double(v1);
       }
+    };
+    // blocks wholly inside the producer's rows (all but the first and last
+    // few of a CTA with a producer): piece j of lane t is block cell pair
+    // 2 (t + 32 j) in staging and in the L2 ring alike; one warp vote checks
+    // the sentinels, late cells are re-polled out of line
+    auto block_full = [&](int i0) { return has_up && i0 + kBatch - 1 + kLam * kG < m_end; };
+    auto request_fast = [&](int i0) {
+      double* sb = stg + ((i0 / kBatch) & (C::StgBlocks - 1)) * (kBatch * kRowCells);
+      const double* gb = gin + (size_t)(i0 + kLam * kG) * kRowCells;
+#pragma unroll
+      for (int j = 0; j < kPerLane; ++j) {
+        const int k = lane + 32 * j;
+        if (kPieces % 32 == 0 || k < kPieces) cp_async16g(sb + 2 * k, gb + 2 * k);
+      }
+    };
+    auto finish_fast = [&](int i0) {
+      const double* sb = stg + ((i0 / kBatch) & (C::StgBlocks - 1)) * (kBatch * kRowCells);
+      double* const gb = gin + (size_t)(i0 + kLam * kG) * kRowCells;
+      double2 got[kPerLane];
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < kPerLane; ++j) {
+        const int k = lane + 32 * j;
+        if (kPieces % 32 == 0 || k < kPieces) {
+          got[j] = *reinterpret_cast<const double2*>(sb + 2 * k);
+          bad |= (__double_as_longlong(got[j].x) == kSent) | (__double_as_longlong(got[j].y) == kSent);
+        }
+      }
+      if (__any_sync(0xffffffffu, bad)) {
+        // late cells (the consumer caught up with its producer): re-read
+        // every late pair at once until all have landed
+        const long long t0 = clock64();
+        do {
+          bad = false;
+#pragma unroll
+          for (int j = 0; j < kPerLane; ++j) {
+            const int k = lane + 32 * j;
+            if ((kPieces % 32 == 0 || k < kPieces) &&
+                ((__double_as_longlong(got[j].x) == kSent) | (__double_as_longlong(got[j].y) == kSent))) {
+              got[j] = ld_relaxed_gpu2(gb + 2 * k);
+              bad |= (__double_as_longlong(got[j].x) == kSent) | (__double_as_longlong(got[j].y) == kSent);
+            }
+          }
+          if (clock64() - t0 > (1ll << 34)) __trap();
+        } while (__any_sync(0xffffffffu, bad));
+      }
+#pragma unroll
+      for (int j = 0; j < kPerLane; ++j) {
+        const int k = lane + 32 * j;
+        if (kPieces % 32 == 0 || k < kPieces) {
+#ifndef GSL_NO_RESET
+          asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(gb + 2 * k), "l"(kSent), "l"(kSent)
+                       : "memory");
+#endif
+          const int r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
+          const int ph = e / kL, ll = e % kL;
+          *reinterpret_cast<double2*>(smem + ((size_t)ph * kR + ((i0 + r) & (kR - 1))) * kS + 2 + ll) = got[j];
+        }
+      }
+    };
+    auto finish_block = [&](int i0) {  // validate, copy into the rings, reset the L2 cells
+      if constexpr (REF)
+        finish_block_one(i0);
+      else
+        finish_block_vec(i0);
     };
     if (has_up) {
       // the incoming slot holds my producer's cells only once the producer
@@ -403,31 +528,55 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       finish_block(i0);
     }
-    request_block(0);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    // blocks 0 .. Dist-1 in flight, each followed by an (empty) lane -1
+    // group so that every block below commits the same pair
+    for (int j = 0; j < C::Dist; ++j) {
+      request_block(j * kBatch);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
     __syncwarp();
     cta_bar(kThreads);
     for (int mb = 0; mb < m_end; mb += kR) {
 #pragma unroll
       for (int u = 0; u < kR; ++u) {
         const int m = mb + u;
+        // per block: group A = the phantom block Dist blocks ahead (first
+        // iteration), group B = lane -1 rows kAheadL iterations ahead (the
+        // second iteration, to even out the loader's work); waiting for all
+        // but the newest 2 Dist groups (2 Dist + 1 with one-row blocks)
+        // retires this block's request, committed Dist blocks ago
+#ifdef GSL_LM_SAME
+        constexpr int kLmU = 0;
+#else
+        constexpr int kLmU = kBatch > 1 ? 1 : 0;
+#endif
         if (u % kBatch == 0) {
-          // group A: the next phantom block; group B: lane -1 rows far ahead.
-          // wait_group 2 retires every older group, in particular this
-          // block's phantom request (issued one block ago)
-          request_block(m + kBatch);
+          const int iq = m + C::Dist * kBatch;
+          if (block_full(iq))
+            request_fast(iq);
+          else
+            request_block(iq);
           asm volatile("cp.async.commit_group;\n" ::: "memory");
-          batch_lane_m1(m + kAheadL);
+        }
+        if (u % kBatch == kLmU) {
+          batch_lane_m1(m - kLmU + kAheadL);
           asm volatile("cp.async.commit_group;\n" ::: "memory");
+        }
+        if (u % kBatch == 0) {
 #ifdef GSL_TRACE
           const long long tw0 = clock64();
 #endif
-          asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+          asm volatile("cp.async.wait_group %0;\n" ::"n"(2 * C::Dist + (kLmU > 0 ? 0 : 1)) : "memory");
 #ifdef GSL_TRACE
           tr_cpw += clock64() - tw0;
 #endif
           __syncwarp();
-          finish_block(m);  // rows [m, m + kBatch): read from iteration m + 1 on
+          // rows [m, m + kBatch): read from iteration m + 1 on
+          if (block_full(m))
+            finish_fast(m);
+          else
+            finish_block(m);
         }
         slot1(m + 1);  // read from iteration m + 2 on
         __syncwarp();

@@ -51,7 +51,6 @@ namespace tvs {
 namespace gsl {
 constexpr int kLam = 2;          // group lag (iterations)
 constexpr int kB = 2;            // every lane starts >= 2 columns left of column 0
-constexpr int kR = 16;           // smem ring rows (iterations), power of two
 constexpr int kPre = 6;          // phantom / lane -1 rows read before iteration 0 (rows -6..-1)
 constexpr int kLR = 128;         // lane -1 staging ring (iterations), power of two
 #ifndef GSL_BATCH
@@ -68,10 +67,20 @@ struct Cfg {
 #ifndef GSL_G
 #define GSL_G 0
 #endif
-  // groups per CTA: 4 (2 CTAs/SM) lexicographic, 7 (1 CTA/SM, its two
-  // phantom rings fill shared memory) reference order.  Config 4 lex G 3 / 4 /
-  // 7: 33.8 / 29.3 / 32.3 ms; reference 4 / 7: 85.6 / 58.2 ms
-  static constexpr int G = GSL_G > 0 ? GSL_G : (REF ? 7 : 4);
+  // groups per CTA: 4, two CTAs per SM, in both orders (config 4 lex G 3 /
+  // 4 / 7: 33.8 / 29.3 / 32.3 ms with the round-1 loader)
+#ifndef GSL_GREF
+#define GSL_GREF 0
+#endif
+#ifndef GSL_RREF
+#define GSL_RREF 0
+#endif
+  static constexpr int G = REF ? (GSL_GREF > 0 ? GSL_GREF : 4) : (GSL_G > 0 ? GSL_G : 4);
+  // smem ring rows (iterations, power of two; also the unroll of the
+  // compute loop).  Reference order: 8, so that two CTAs of three rings
+  // more fit one SM (config 4: G 7 R 16 one CTA/SM / G 7 R 8 / G 5 R 8 two /
+  // G 4 R 8 two: 31.9 / 29.3 / 27.2 / 25.4 ms)
+  static constexpr int R = REF ? (GSL_RREF > 0 ? GSL_RREF : 8) : 16;
   // rows per loader block (lane -1 staging batch, phantom poll block).
   // Config 4 lexicographic 8 / 4 / 2 / 1 rows: 44.3 / 33.8 / 26.1 / 28.7 ms;
   // reference order 2 / 1: 51.8 / 45.3 ms
@@ -94,13 +103,13 @@ struct Cfg {
   static constexpr int StgBlocks = Dist < 2 ? 2 : 4;  // staging ring (power of two > Dist)
   static_assert(Dist <= 3, "staging ring");
   static constexpr int Stg = StgBlocks * Batch * Ph * L;  // phantom staging: blocks of Batch compact rows
-  static constexpr size_t Smem = sizeof(double) * ((size_t)Rings * kR * S + (size_t)Rings * kLR + Stg);
+  static constexpr size_t Smem = sizeof(double) * ((size_t)Rings * R * S + (size_t)Rings * kLR + Stg);
   static constexpr int Back = REF ? 2 * kLam + 1 : kLam + 1;  // deepest ring read behind m
-  static_assert(kR >= Back + Batch + 1, "ring too shallow for a phantom block written ahead");
+  static_assert(R >= Back + Batch + 1, "ring too shallow for a phantom block written ahead");
   static_assert(kLR >= kAheadL + Batch + 8, "lane -1 staging ring too shallow");
   static_assert(kPre >= Back + 1, "prologue rows");
   static constexpr int ProRows = (kPre + Batch - 1) / Batch * Batch;  // phantom rows before iteration 0
-  static_assert(kR % Batch == 0 && kAheadL % Batch == 0, "block sizes");
+  static_assert(R % Batch == 0 && kAheadL % Batch == 0, "block sizes");
 };
 }  // namespace gsl
 
@@ -178,12 +187,16 @@ __device__ __forceinline__ void cta_bar(int nthreads) { asm volatile("bar.sync 1
 #ifndef GSL_MINB
 #define GSL_MINB 2
 #endif
+#ifndef GSL_MINB_REF
+#define GSL_MINB_REF 2
+#endif
 template <unsigned MASK, bool REF, int WG>
-__global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? 1 : GSL_MINB) gs2d_lane_kernel(GslArgs p) {
+__global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? GSL_MINB_REF : GSL_MINB) gs2d_lane_kernel(GslArgs p) {
   using namespace gsl;
   using C = Cfg<REF, WG>;
   constexpr int kG = C::G, kPh = C::Ph, kL = C::L, kS = C::S, kRings = C::Rings, kThreads = C::Threads;
   constexpr int kBatch = C::Batch;
+  constexpr int kR = C::R;
   extern __shared__ __align__(16) double smem[];
   double* const lm1 = smem + (size_t)kRings * kR * kS;  // lane -1 staging [ring][kLR]
   double* const stg = lm1 + kRings * kLR;                 // phantom staging [StgBlocks][kBatch][kPh * kL]
@@ -663,7 +676,7 @@ static int gsl_launch(GslArgs a, int64_t steps, int64_t per, cudaStream_t s, con
   TVS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::Smem));
   // the last group's lanes reach column e1 (the boundary the consumer reads)
   const int m_need = a.e1 + kLam * (C::G - 1) + 2 * (C::L - 1) + kB + 2;
-  a.m_end = (m_need + kR - 1) / kR * kR;
+  a.m_end = (m_need + C::R - 1) / C::R * C::R;
   const size_t cells = (size_t)kNumSlots * a.m_end * C::Ph * C::L;
   const size_t ctrl_bytes = sizeof(int) * 2 * kNumSlots + 64;
   a.gring = static_cast<double*>(scratch(sizeof(double) * cells, 4));

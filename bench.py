@@ -95,7 +95,8 @@ class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw,"
+              "enforced.power.limit")
 
     def __init__(self, device=0):
         self.device = device
@@ -112,7 +113,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "10"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
         except Exception:
@@ -146,7 +147,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, power, plimit = [], None, set(), [], None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", float("inf"))
         for ts, line in self.lines:
@@ -163,9 +164,21 @@ class ClockSampler:
             for n, v in zip(names, parts[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
+            try:  # board power next to its limit: a clock below max at the limit is the power cap
+                power.append(float(parts[6]))
+                plimit = float(parts[7])
+            except (IndexError, ValueError):
+                pass
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if power:
+            out["power_w_max"] = max(power)
+            out["power_limit_w"] = plimit
+            # the power-cap flag is momentary and can fall between samples
+            if plimit and max(power) >= 0.97 * plimit and out["sm_mhz"] < 0.97 * (mx or 0) and not reasons:
+                out["note"] = "clock below max at the board power limit (power cap; flag not caught by a sample)"
+        return out
 
 
 def flush_l2(buf):

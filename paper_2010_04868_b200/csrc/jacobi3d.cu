@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
   // rows/columns beyond the memory halo are never needed (their level-1
   // positions are pinned) and are not read
   int soff[kTBSlots];  // shared offset, -1: slot not read
-  int64_t goff[kTBSlots];
+  int goff[kTBSlots];    // element offset within the plane (host checks a plane fits 31 bits)
 #pragma unroll
   for (int k = 0; k < kTBSlots; ++k) {
     const int e = tid + k * kThreads3;
@@ -239,19 +239,8 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
     const int64_t y = y0 - 2 + i, x = x0 - 2 + 2 * c2;
     const bool ok = e < kTBChunks && y >= -1 && y <= g.e1 && x <= g.e2;
     soff[k] = ok ? i * kTBP + 2 * c2 : -1;
-    goff[k] = y * g.s1 + x;
+    goff[k] = (int)(y * g.s1 + x);
   }
-  const double* base = src + origin;
-  auto stage = [&](int64_t p) {
-    if (p >= -1 && p <= g.e0) {
-      const double* pb = base + p * g.s0;
-      double* tb = l0 + (int)((p - p0 + 3) % 3) * (kTBR * kTBP);
-#pragma unroll
-      for (int k = 0; k < kTBSlots; ++k)
-        if (soff[k] >= 0) cp_async16(tb + soff[k], pb + goff[k]);
-    }
-    cp_async_commit();
-  };
 
   // per-thread frame positions: rows i = w*kRY + r, columns j = lane + 32h
   unsigned in_dom = 0;   // bit (h*kRY + r): level-1 position inside the domain (axes 1, 2)
@@ -266,6 +255,7 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
       in_dom |= (dom ? 1u : 0u) << (h * kRY + r);
       store_ok |= (dom && i >= 1 && i < kTBH - 1 && j >= 1 && j < kTBW - 1 ? 1u : 0u) << (h * kRY + r);
     }
+  const bool all_dom = in_dom == 0xFFu;
 
   double A1[2][kRY], B1[2][kRY], A2[2][kRY], B2[2][kRY], out[2][kRY];
 #pragma unroll
@@ -273,44 +263,90 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
 #pragma unroll
     for (int r = 0; r < kRY; ++r) A1[h][r] = B1[h][r] = A2[h][r] = B2[h][r] = 0.0;
 
-  stage(p0 - 2);
-  for (int64_t p = p0 - 2; p <= p1 + 1; ++p) {
-    stage(p + 1);  // empty group past the end keeps the wait count uniform
+  // Iteration t handles input plane p = p0-2+t: level-1 plane q1 = p-1 and
+  // level-2 plane q2 = p-2.  Every plane-range test is a 32-bit compare of t
+  // against a bound fixed per block (seg <= 2^30 planes).
+  const int np = (int)(p1 - p0);
+  auto clampi = [](int64_t v) { return (int)max((int64_t)-4, min(v, (int64_t)1 << 30)); };
+  const int ts_lo = clampi(1 - p0), ts_hi = clampi(g.e0 - p0 + 2);  // staged planes: t in [ts_lo, ts_hi]
+  // level-1 plane q1 = p0-3+t is inside the (local and global) domain for t in [t1_lo, t1_hi)
+  const int t1_lo = clampi(max(3 - p0, 3 - p0 - g.a0_off));
+  const int t1_hi = clampi(min(g.e0 - p0 + 3, g.a0_glob - g.a0_off - p0 + 3));
+  // level-2 plane q2 = p0-4+t inside the global domain for t in [t2_lo, t2_hi)
+  const int t2_lo = clampi(4 - p0 - g.a0_off), t2_hi = clampi(g.a0_glob - g.a0_off - p0 + 4);
+
+  constexpr int kPlane = kTBR * kTBP;
+  const double* pb = src + origin + (p0 - 2) * g.s0;  // plane staged next
+  int sb = 0;                                         // its ring slot (elements)
+  auto stage = [&](int t) {
+    if (t >= ts_lo && t <= ts_hi) {
+      double* tb = l0 + sb;
+#pragma unroll
+      for (int k = 0; k < kTBSlots; ++k)
+        if (soff[k] >= 0) cp_async16(tb + soff[k], pb + goff[k]);
+    }
+    cp_async_commit();
+    pb += g.s0;
+    sb = sb == 2 * kPlane ? 0 : sb + kPlane;
+  };
+  // the thread's first output cell of level-2 plane p0 (advanced per plane)
+  int64_t ooff = origin + p0 * g.s0 + (y0 - 1 + w * kRY) * g.s1 + (x0 - 1 + lane);
+  const int tpos = (w * kRY) * kTBP + lane;  // the thread's window origin in a plane
+  const double* cur = l0;                    // staged plane of iteration t
+  int l1sel = kPlane;                        // level-1 buffer of iteration t (t = 0: buffer 1)
+
+  stage(0);
+  for (int t = 0; t <= np + 3; ++t) {
+    stage(t + 1);  // empty group past the end keeps the wait count uniform
     cp_async_wait<1>();
-    __syncthreads();  // plane p visible; iteration p-1 finished everywhere
+    __syncthreads();  // plane p visible; iteration t-1 finished everywhere
     // level 1: plane p -> finishes level-1 plane q1 = p-1
-    tb_level<MASK, FMA>(l0 + (int)((p - p0 + 3) % 3) * (kTBR * kTBP), w, lane, A1, B1, out, cf.c);
-    const int64_t q1 = p - 1;
-    const int64_t gq1 = q1 + g.a0_off;
-    const bool plane_pin = q1 < 0 || q1 >= g.e0 || gq1 < 0 || gq1 >= g.a0_glob;
-    double* l1b = l1 + (int)((q1 - p0 + 4) & 1) * (kTBR * kTBP);
+    tb_level<MASK, FMA>(cur, w, lane, A1, B1, out, cf.c);
+    cur = cur == l0 + 2 * kPlane ? l0 : cur + kPlane;
+    double* l1b = l1 + l1sel;
+    l1sel ^= kPlane;
+    {
+      double* q = l1b + tpos + kTBP + 1;
+      if (t >= t1_lo && t < t1_hi && all_dom) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int r = 0; r < kRY; ++r) {
-        const bool keep = !plane_pin && (in_dom >> (h * kRY + r) & 1u);
-        l1b[(w * kRY + r + 1) * kTBP + lane + 32 * h + 1] = keep ? out[h][r] : bnd;
+          for (int r = 0; r < kRY; ++r) q[r * kTBP + 32 * h] = out[h][r];
+      } else {
+        const bool plane_in = t >= t1_lo && t < t1_hi;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int r = 0; r < kRY; ++r)
+            q[r * kTBP + 32 * h] = plane_in && (in_dom >> (h * kRY + r) & 1u) ? out[h][r] : bnd;
       }
+    }
     __syncthreads();  // level-1 plane q1 visible
-    if (q1 >= p0 - 1) {
+    if (t >= 2) {
       // level 2: level-1 plane q1 -> finishes level-2 plane q2 = q1-1
       tb_level<MASK, FMA>(l1b, w, lane, A2, B2, out, cf.c);
-      const int64_t q2 = q1 - 1;
-      if (q2 >= p0 && q2 < p1) {
-        const int64_t gq2 = q2 + g.a0_off;
-        const bool pin = gq2 < 0 || gq2 >= g.a0_glob;
-        auto store = [&](double* b) {
-          double* op = b + origin + q2 * g.s0 + (y0 - 1 + w * kRY) * g.s1 + (x0 - 1 + lane);
+      if (t >= 4) {
+        if (t < t2_lo || t >= t2_hi) {
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int r = 0; r < kRY; ++r)
-              if (store_ok >> (h * kRY + r) & 1u) op[r * g.s1 + 32 * h] = pin ? bnd : out[h][r];
+            for (int r = 0; r < kRY; ++r) out[h][r] = bnd;
+        }
+        auto store = [&](double* b) {
+          double* op = b + ooff;
+#pragma unroll
+          for (int r = 0; r < kRY; ++r) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (store_ok >> (h * kRY + r) & 1u) op[32 * h] = out[h][r];
+            op += g.s1;
+          }
         };
         if constexpr (MIR)
-          for_each_dst(dst, mir, q2, store);  // sharded: local plane + the neighbour's ghost plane
+          for_each_dst(dst, mir, p0 - 4 + t, store);  // sharded: local plane + the neighbour's ghost plane
         else
           store(dst);
+        ooff += g.s0;
       }
     }
   }
@@ -364,6 +400,8 @@ int jacobi3d_blocked2(const tvs_stencil& st, const tvs_geometry& g, const double
   if (phi < 0) phi = geo.e0;
   if (seg <= 0) seg = kTBPlanesSeg;
   if (plo < 0 || phi > geo.e0 || plo >= phi) return fail(TVS_ERR_INVALID, "jacobi3d_blocked2: plane range");
+  // the kernel keeps its staging offsets within a plane in 32 bits
+  if (geo.s0 >= ((int64_t)1 << 31) - 4 * geo.s1) return fail(TVS_ERR_UNSUPPORTED, "jacobi3d_blocked2: plane of 2^31 elements");
   if (mask == kBox27)
     return fma ? launch_tb<kBox27, true>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m)
                : launch_tb<kBox27, false>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m);

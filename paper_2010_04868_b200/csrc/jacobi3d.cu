@@ -14,6 +14,10 @@
 // bound (~351 GStencil/s at 1.965 GHz), below the single-step HBM roofline
 // (~409); the FMA form (tolerance mode) halves the op count.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include <cuda.h>
 
 #include "common.cuh"
 
@@ -277,17 +281,20 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
 
   constexpr int kPlane = kTBR * kTBP;
   const double* pb = src + origin + (p0 - 2) * g.s0;  // plane staged next
-  int sb = 0;                                         // its ring slot (elements)
+  // its ring slot as a shared-window byte address (the generic -> shared
+  // conversion happens once, not per copy)
+  const unsigned l0a = smaddr(l0);
+  unsigned sba = l0a;
   auto stage = [&](int t) {
     if (t >= ts_lo && t <= ts_hi) {
-      double* tb = l0 + sb;
 #pragma unroll
       for (int k = 0; k < kTBSlots; ++k)
-        if (soff[k] >= 0) cp_async16(tb + soff[k], pb + goff[k]);
+        if (soff[k] >= 0)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sba + 8u * (unsigned)soff[k]), "l"(pb + goff[k]));
     }
     cp_async_commit();
     pb += g.s0;
-    sb = sb == 2 * kPlane ? 0 : sb + kPlane;
+    sba = sba == l0a + 2u * kPlane * 8u ? l0a : sba + kPlane * 8u;
   };
   // the thread's first output cell of level-2 plane p0 (advanced per plane)
   int64_t ooff = origin + p0 * g.s0 + (y0 - 1 + w * kRY) * g.s1 + (x0 - 1 + lane);
@@ -295,8 +302,16 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
   const double* cur = l0;                    // staged plane of iteration t
   int l1sel = kPlane;                        // level-1 buffer of iteration t (t = 0: buffer 1)
 
+  // One barrier per plane: level 2 runs one plane behind level 1 and reads
+  // the level-1 plane written in the previous iteration (two level-1 buffers:
+  // iteration t writes buffer t & 1, which iteration t-1's level 2 -- reading
+  // buffer (t-2) & 1 -- released before this iteration's barrier).
+#ifndef J3D_LAG
+#define J3D_LAG 1
+#endif
+  constexpr int kLag = J3D_LAG;  // 0: level 2 in the same iteration (a second barrier per plane)
   stage(0);
-  for (int t = 0; t <= np + 3; ++t) {
+  for (int t = 0; t <= np + 3 + kLag; ++t) {
     stage(t + 1);  // empty group past the end keeps the wait count uniform
     cp_async_wait<1>();
     __syncthreads();  // plane p visible; iteration t-1 finished everywhere
@@ -321,12 +336,12 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
             q[r * kTBP + 32 * h] = plane_in && (in_dom >> (h * kRY + r) & 1u) ? out[h][r] : bnd;
       }
     }
-    __syncthreads();  // level-1 plane q1 visible
-    if (t >= 2) {
-      // level 2: level-1 plane q1 -> finishes level-2 plane q2 = q1-1
-      tb_level<MASK, FMA>(l1b, w, lane, A2, B2, out, cf.c);
-      if (t >= 4) {
-        if (t < t2_lo || t >= t2_hi) {
+    if constexpr (kLag == 0) __syncthreads();  // level-1 plane q1 visible
+    if (t >= 2 + kLag) {
+      // level 2: level-1 plane q1 - kLag -> finishes level-2 plane q2 = q1 - kLag - 1
+      tb_level<MASK, FMA>(kLag ? l1 + l1sel : l1b, w, lane, A2, B2, out, cf.c);
+      if (t >= 4 + kLag) {
+        if (t < t2_lo + kLag || t >= t2_hi + kLag) {
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -343,7 +358,228 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
           }
         };
         if constexpr (MIR)
-          for_each_dst(dst, mir, p0 - 4 + t, store);  // sharded: local plane + the neighbour's ghost plane
+          for_each_dst(dst, mir, p0 - 4 - kLag + t, store);  // sharded: local plane + the neighbour's ghost plane
+        else
+          store(dst);
+        ooff += g.s0;
+      }
+    }
+  }
+}
+
+// ---- K4c: K4b staged by TMA, adjacent column pairs per lane --------------
+//
+// Same two-level scheme, frame and arithmetic as K4b (bit-identical), with the
+// per-plane overhead cut (K4b in FMA mode issued ~300 non-FP64 instructions
+// per 432 DFMAs and was issue-limited):
+//   * the 34 x 66 input box of every plane is one 3D tensor-map copy
+//     (cp.async.bulk.tensor, issued by one thread, completion on an mbarrier;
+//     out-of-range rows / planes are zero-filled by the TMA unit and only ever
+//     feed pinned or discarded positions) instead of five predicated 16-byte
+//     cp.async per thread with their address arithmetic;
+//   * a lane owns two ADJACENT frame columns (2 lane, 2 lane + 1): the 4-wide
+//     window row both columns need is two LDS.128 (12 loads per level instead
+//     of 36 LDS.64), consumed row by row so the window is never held whole;
+//   * one CTA barrier per plane: level 2 runs one plane behind level 1.
+constexpr int kPW = kTBW + 2;                 // staged box width (frame + ring)
+constexpr int kPR = kTBH + 2;                 // staged box rows
+constexpr int kPSlot = (kPR * kPW * 8 + 127) / 128 * 128 / 8;  // slot pitch (elements), 128-byte multiple
+constexpr unsigned kPBytes = kPR * kPW * 8;   // bytes one plane copy delivers
+constexpr size_t kPSmem = (size_t)5 * kPSlot * sizeof(double) + 3 * sizeof(unsigned long long) + 128;
+
+template <unsigned MASK, int G>
+constexpr int first_tap() {
+  for (int k = 0; k < 9; ++k)
+    if ((MASK >> (9 * G + k)) & 1u) return k;
+  return -1;
+}
+
+// One level over the thread's 4 rows x 2 adjacent columns: `win` = window
+// origin (plane cell of frame row 4w - 1, frame column 2 lane - 1).  Sorted
+// tap order per accumulator (plane group, then window row, then column), as
+// add_plane: finishes out = B + (+1-plane taps), B <- A + (0-plane taps),
+// A <- (-1-plane taps).
+template <unsigned MASK, bool FMA>
+__device__ __forceinline__ void pair_level(const double* __restrict__ win, double (&A)[2][kRY], double (&B)[2][kRY],
+                                           double (&out)[2][kRY], const double* c) {
+  constexpr bool G0 = has_plane<MASK>(0), G1 = has_plane<MASK>(1), G2 = has_plane<MASK>(2);
+  constexpr int f0 = first_tap<MASK, 0>(), f1 = first_tap<MASK, 1>(), f2 = first_tap<MASK, 2>();
+  double An[2][kRY];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int r = 0; r < kRY; ++r) {
+      out[h][r] = B[h][r];
+      B[h][r] = A[h][r];
+      An[h][r] = 0.0;
+    }
+#pragma unroll
+  for (int rr = 0; rr < kRY + 2; ++rr) {
+    const double2 lo = *reinterpret_cast<const double2*>(win + rr * kPW);
+    const double2 hi = *reinterpret_cast<const double2*>(win + rr * kPW + 2);
+    const double v[4] = {lo.x, lo.y, hi.x, hi.y};
+#pragma unroll
+    for (int dy = 2; dy >= 0; --dy) {  // the output closest to completion first
+      const int r = rr - dy;
+      if (r < 0 || r >= kRY) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int t9 = dy * 3 + k;
+          const double x = v[h + k];
+          if (G2 && ((MASK >> (18 + t9)) & 1u))
+            out[h][r] = (!(G0 || G1) && t9 == f2) ? tap_first(c[18 + t9], x) : tap_next<FMA>(c[18 + t9], x, out[h][r]);
+          if (G1 && ((MASK >> (9 + t9)) & 1u))
+            B[h][r] = (!G0 && t9 == f1) ? tap_first(c[9 + t9], x) : tap_next<FMA>(c[9 + t9], x, B[h][r]);
+          if (G0 && ((MASK >> t9) & 1u))
+            An[h][r] = t9 == f0 ? tap_first(c[t9], x) : tap_next<FMA>(c[t9], x, An[h][r]);
+        }
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int r = 0; r < kRY; ++r) A[h][r] = An[h][r];
+}
+
+template <unsigned MASK, bool FMA, bool MIR>
+__global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                    double* __restrict__ dst, Geo g, int64_t origin,
+                                                                    Coeff27 cf, double bnd, int64_t plo,
+                                                                    int64_t phi, int seg, Mirror mir) {
+  extern __shared__ unsigned char tma_smem_raw[];
+  // 128-byte aligned slots (TMA destination alignment)
+  const unsigned raw = smaddr(tma_smem_raw);
+  double* const l0 = reinterpret_cast<double*>(tma_smem_raw + ((128u - (raw & 127u)) & 127u));  // 3 staged planes
+  double* const l1 = l0 + 3 * kPSlot;                                                              // 2 level-1 planes
+  unsigned long long* const full = reinterpret_cast<unsigned long long*>(l1 + 2 * kPSlot);
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const int tid = w * 32 + lane;
+  const int64_t x0 = (int64_t)blockIdx.x * kTBOX, y0 = (int64_t)blockIdx.y * kTBOY;
+  const int64_t p0 = plo + (int64_t)blockIdx.z * seg;
+  const int64_t p1 = min(p0 + seg, phi);  // level-2 outputs [p0, p1)
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mbar_init(full + k, 1);
+    fence_mbar_init();
+    fence_proxy_async_smem();
+  }
+  // frame (i, j) = global (y0-1+i, x0-1+j) = plane cell (i+1, j+1); the
+  // thread owns rows i = 4w + r, columns j = 2 lane + h
+  unsigned in_dom = 0;    // bit (h*kRY + r): level-1 position inside the domain (axes 1, 2)
+  unsigned store_ok = 0;  // bit (h*kRY + r): useful level-2 output
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int r = 0; r < kRY; ++r) {
+      const int i = w * kRY + r, j = 2 * lane + h;
+      const int64_t y = y0 - 1 + i, x = x0 - 1 + j;
+      const bool dom = y >= 0 && y < g.e1 && x >= 0 && x < g.e2;
+      in_dom |= (dom ? 1u : 0u) << (h * kRY + r);
+      store_ok |= (dom && i >= 1 && i < kTBH - 1 && j >= 1 && j < kTBW - 1 ? 1u : 0u) << (h * kRY + r);
+    }
+  const bool all_dom = in_dom == 0xFFu;
+
+  double A1[2][kRY], B1[2][kRY], A2[2][kRY], B2[2][kRY], out[2][kRY];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int r = 0; r < kRY; ++r) A1[h][r] = B1[h][r] = A2[h][r] = B2[h][r] = 0.0;
+
+  // Iteration t: input plane p = p0-2+t lands (slot t % 3), level 1 finishes
+  // level-1 plane p-1 into buffer t & 1, level 2 reads buffer (t-1) & 1
+  // (level-1 plane p-2) and finishes level-2 plane p-3 = p0-5+t.
+  const int np = (int)(p1 - p0);
+  auto clampi = [](int64_t v) { return (int)max((int64_t)-4, min(v, (int64_t)1 << 30)); };
+  const int t1_lo = clampi(max(3 - p0, 3 - p0 - g.a0_off));
+  const int t1_hi = clampi(min(g.e0 - p0 + 3, g.a0_glob - g.a0_off - p0 + 3));
+  const int t2_lo = clampi(5 - p0 - g.a0_off), t2_hi = clampi(g.a0_glob - g.a0_off - p0 + 5);
+  const int t_last = np + 4;
+
+  // tensor coordinates of the box of plane p0-2 (allocation-relative: the
+  // pads / halo row / halo plane precede the interior origin)
+  const int c0 = (int)(kPadLast + x0 - 2), c1 = (int)(y0 - 1);
+  int c2 = (int)(p0 - 1);
+  const unsigned l0a = smaddr(l0), fulla = smaddr(full);
+  unsigned slot_a = l0a, bar_a = fulla;  // slot / barrier of the next plane to request
+  auto request = [&]() {
+    if (tid == 0) {
+      asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(bar_a), "r"(kPBytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+          ::"r"(slot_a), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_a)
+          : "memory");
+    }
+    ++c2;
+    const bool wrap = slot_a == l0a + 2u * kPSlot * 8u;
+    slot_a = wrap ? l0a : slot_a + kPSlot * 8u;
+    bar_a = wrap ? fulla : bar_a + 8u;
+  };
+  const int tpos = (w * kRY) * kPW + 2 * lane;  // the thread's window origin in a plane
+  int64_t ooff = origin + p0 * g.s0 + (y0 - 1 + w * kRY) * g.s1 + (x0 - 1 + 2 * lane);
+  const double* cur = l0;
+  unsigned cur_bar = fulla, parity = 0;
+  int l1sel = 0;
+
+  __syncthreads();  // barriers initialised
+  request();
+  for (int t = 0; t <= t_last; ++t) {
+    // plane t+1 -> slot (t+1) % 3, last read in iteration t-2: every thread
+    // passed iteration t-1's barrier after that
+    if (t < t_last) request();
+    __syncthreads();  // iteration t-1 finished everywhere (level-1 buffers)
+    mbar_wait_a(cur_bar, parity);
+    // level 1: plane p -> finishes level-1 plane q1 = p-1
+    pair_level<MASK, FMA>(cur + tpos, A1, B1, out, cf.c);
+    if (cur == l0 + 2 * kPSlot) {
+      cur = l0;
+      cur_bar = fulla;
+      parity ^= 1u;
+    } else {
+      cur += kPSlot;
+      cur_bar += 8u;
+    }
+    double* const l1b = l1 + l1sel;
+    l1sel ^= kPSlot;
+    {
+      double* q = l1b + tpos + kPW + 1;
+      const bool plane_in = t >= t1_lo && t < t1_hi;
+      if (plane_in && all_dom) {
+#pragma unroll
+        for (int r = 0; r < kRY; ++r)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) q[r * kPW + h] = out[h][r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < kRY; ++r)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) q[r * kPW + h] = plane_in && (in_dom >> (h * kRY + r) & 1u) ? out[h][r] : bnd;
+      }
+    }
+    if (t >= 3) {
+      // level 2: level-1 plane q1-1 (previous iteration's buffer) -> level-2 plane q1-2
+      pair_level<MASK, FMA>(l1 + l1sel + tpos, A2, B2, out, cf.c);
+      if (t >= 5) {
+        if (t < t2_lo || t >= t2_hi) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int r = 0; r < kRY; ++r) out[h][r] = bnd;
+        }
+        auto store = [&](double* b) {
+          double* op = b + ooff;
+#pragma unroll
+          for (int r = 0; r < kRY; ++r) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (store_ok >> (h * kRY + r) & 1u) op[h] = out[h][r];
+            op += g.s1;
+          }
+        };
+        if constexpr (MIR)
+          for_each_dst(dst, mir, p0 - 5 + t, store);  // sharded: local plane + the neighbour's ghost plane
         else
           store(dst);
         ooff += g.s0;
@@ -390,7 +626,64 @@ static int launch_tb(const Geo& geo, const tvs_geometry& g, const double* src, d
   return TVS_OK;
 }
 
-// Two time levels in one pass (K4b): src -> dst after 2 steps.
+// cuTensorMapEncodeTiled through the runtime's driver entry point lookup (the
+// library does not link libcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// K4c applies when the block can be described to the TMA unit: 16-byte
+// aligned base and pitches, 32-bit extents.  TVS_J3D=cpasync keeps K4b.
+static bool tma_usable(const tvs_geometry& g, const double* src) {
+  static const bool off = [] {
+    const char* e = std::getenv("TVS_J3D");
+    return e && std::strcmp(e, "cpasync") == 0;
+  }();
+  if (off || !encode_tiled_fn()) return false;
+  const int64_t s0 = g.strides[0], s1 = g.strides[1];
+  return (reinterpret_cast<uintptr_t>(src) & 15u) == 0 && s1 % 2 == 0 && s0 % s1 == 0 && g.alloc_elems % s0 == 0 &&
+         s1 < ((int64_t)1 << 31) && s0 / s1 < ((int64_t)1 << 31) && g.alloc_elems / s0 < ((int64_t)1 << 31);
+}
+
+template <unsigned MASK, bool FMA>
+static int launch_tma(const Geo& geo, const tvs_geometry& g, const double* src, double* dst, const Coeff27& cf,
+                      double bnd, cudaStream_t s, int64_t plo, int64_t phi, int seg, const Mirror& mir) {
+  // the whole allocation as a (pitch, rows, planes) tensor; one box = the
+  // 66 x 34 cells a block needs of one plane
+  CUtensorMap tm;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.strides[1], (cuuint64_t)(g.strides[0] / g.strides[1]),
+                              (cuuint64_t)(g.alloc_elems / g.strides[0])};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.strides[1] * 8, (cuuint64_t)g.strides[0] * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)kPW, (cuuint32_t)kPR, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult rc = encode_tiled_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(src), dims, strides,
+                                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) return fail(TVS_ERR_CUDA, "jacobi3d: cuTensorMapEncodeTiled failed");
+  const bool mirrored = mir.p[0] != nullptr || mir.p[1] != nullptr;
+  auto kern = mirrored ? jacobi3d_tma_kernel<MASK, FMA, true> : jacobi3d_tma_kernel<MASK, FMA, false>;
+  TVS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmem));
+  const dim3 block(kTX3, kTYT);
+  const dim3 grid((unsigned)((geo.e2 + kTBOX - 1) / kTBOX), (unsigned)((geo.e1 + kTBOY - 1) / kTBOY),
+                  (unsigned)((phi - plo + seg - 1) / seg));
+  kern<<<grid, block, kPSmem, s>>>(tm, dst, geo, g.origin, cf, bnd, plo, phi, seg, mir);
+  TVS_LAUNCHED("jacobi3d_tma_kernel");
+  return TVS_OK;
+}
+
+// Two time levels in one pass (K4c, or K4b when the block cannot be a tensor
+// map): src -> dst after 2 steps.
 int jacobi3d_blocked2(const tvs_stencil& st, const tvs_geometry& g, const double* src, double* dst, bool fma,
                       cudaStream_t s, int64_t plo, int64_t phi, int seg, const Mirror* mir) {
   const Mirror m = mir ? *mir : Mirror{};
@@ -402,6 +695,14 @@ int jacobi3d_blocked2(const tvs_stencil& st, const tvs_geometry& g, const double
   if (plo < 0 || phi > geo.e0 || plo >= phi) return fail(TVS_ERR_INVALID, "jacobi3d_blocked2: plane range");
   // the kernel keeps its staging offsets within a plane in 32 bits
   if (geo.s0 >= ((int64_t)1 << 31) - 4 * geo.s1) return fail(TVS_ERR_UNSUPPORTED, "jacobi3d_blocked2: plane of 2^31 elements");
+  if (tma_usable(g, src)) {
+    if (mask == kBox27)
+      return fma ? launch_tma<kBox27, true>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m)
+                 : launch_tma<kBox27, false>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m);
+    if (mask == kStar7)
+      return fma ? launch_tma<kStar7, true>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m)
+                 : launch_tma<kStar7, false>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m);
+  }
   if (mask == kBox27)
     return fma ? launch_tb<kBox27, true>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m)
                : launch_tb<kBox27, false>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m);

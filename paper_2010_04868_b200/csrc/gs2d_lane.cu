@@ -1,5 +1,5 @@
-// K6v2: 2D radius-1 Gauss-Seidel (9-point box / 5-point star) as time-lane
-// groups advancing in per-iteration CTA lockstep.
+// K6v3: 2D radius-1 Gauss-Seidel (9-point box / 5-point star) as time-lane
+// groups advancing in per-iteration lockstep, fed by a decoupled loader warp.
 //
 // Replaces gs2d_temporal (reference kernels_nd.py:48-50, star-only there) for
 // the row-major in-place sweep of BASELINE config 4, bit-exact with the
@@ -8,38 +8,47 @@
 // reference's anti-diagonal gather/scatter (baselines.py:83-107: the NE
 // neighbour is read from the previous sweep).
 //
-// The paper's time lanes.  A "group" is WG warps = 32*WG lanes; lane l runs
-// sweep t0 + l and group d owns the units {(sweep l, row d - l)} (a diagonal
-// through (time, row) space), streaming left to right over the columns, one
-// column per iteration.  Every input of unit (l, row r = d - l, column c) is
+// The paper's time lanes.  A "group" is lr lanes (the pass's sweeps, rounded
+// up to even); lane l runs sweep t0 + l and group d owns the units
+// {(sweep l, row d - l)} (a diagonal through (time, row) space), streaming
+// left to right over the columns, one column per iteration.  Every input of
+// unit (l, row r = d - l, column c) is
 //   NW, N, NE  row r-1, sweep l    = group d-1, lane l     (smem ring)
 //   W          row r,   sweep l    = my previous output    (register)
 //   C, E       row r,   sweep l-1  = group d-1, lane l-1   (smem ring)
-//   SW, S, SE  row r+1, sweep l-1  = group d,   lane l-1   (__shfl_up; a
-//                                     warp's lane 0 reads the ring)
+//   SW, S, SE  row r+1, sweep l-1  = group d,   lane l-1   (smem ring)
 // (reference order: NE = row r-1, sweep l-1 = group d-2, lane l-1), where
-// "lane -1" of group d is grid row d+1 as it was before the pass (loaded by
-// the CTA's loader warp).  Lane l trails lane l-1 by 2 columns and group g
-// trails group g-1 by 2 iterations (LAM): the hyperplane slope of the
-// dependence graph (h = 2 row + column + 4 sweep), so the pipeline is no
-// longer than the computation's critical path.  Taps are summed in sorted
-// order (NW N NE W C E SW S SE), unfused: bit-exact.
+// "lane -1" of group d is grid row d+1 as it was before the pass.  Lane l
+// trails lane l-1 by 2 columns and group g trails group g-1 by 2 iterations
+// (LAM): the hyperplane slope of the dependence graph (h = 2 row + column + 4
+// sweep), so the pipeline is no longer than the computation's critical path.
+// Taps are summed in sorted order (NW N NE W C E SW S SE), unfused: bit-exact.
 //
-// CTA = G groups (G*WG compute warps) + a loader warp, one CTA barrier per
-// iteration: every warp does identical work per iteration, so lockstep costs
-// only the barrier, and everything a warp reads from shared memory was
-// written before the previous barrier.  The loader prefetches, ahead of use,
-// the grid rows of every group's lane -1 (cp.async) and the previous CTA's
-// last group(s) ("phantom" groups).  CTA-to-CTA hand-off is fence-free: the
-// producer's last groups store every output to an L2 ring whose cells hold a
-// signalling-NaN sentinel until written (arithmetic never yields a
-// signalling NaN, and the boundary value is checked on the host), the
-// consumer's loader polls the cells themselves (8-byte single-copy atomic)
-// and puts the sentinel back after reading, so the ring is clean for its next
-// use.  CTAs take tickets and only wait on lower tickets; a ring slot is
-// reused only after its consumer has exited.  Units outside the grid output
-// the boundary; lane Tp-1 (the pass's last sweep) writes its row's final
-// values to the grid in place.
+// CTA = G groups packed back to back into compute warps (T = 100: 5 x 100
+// units on 16 warps -- a unit costs the same shared-memory traffic, the
+// kernel's throughput bound, whether its sweep is real or not) + one loader
+// warp.  The compute warps meet at one named barrier per iteration (every
+// warp does identical work; all ring reads are at compile-time offsets).
+// The loader is NOT in that barrier: it runs up to two 4-iteration blocks
+// ahead and hands rows over through two shared counters (rows filled /
+// iterations done), so neither the L2 latency of the CTA-to-CTA hand-off nor
+// the loader's instruction stream sits on the per-iteration critical path
+// (K6v2 had the loader in the barrier: 19.1 ms at config 4, 14.5 ms with the
+// hand-off compiled out).  Per block the loader
+//   * copies lane -1 of every group (grid rows, prefetched by cp.async two
+//     blocks ahead) into ring slot 1;
+//   * copies the previous CTA's last group(s) ("phantom" groups) from an L2
+//     ring into the phantom rings.  The hand-off is fence-free: the producer
+//     stores every output to an L2 ring whose cells hold a signalling-NaN
+//     sentinel until written (arithmetic never yields a signalling NaN; the
+//     boundary value is checked on the host); the consumer prefetches blocks
+//     by cp.async two blocks ahead, re-polls cells that still hold the
+//     sentinel and puts the sentinel back, so the ring is clean for its next
+//     use.
+// CTAs take tickets and only wait on lower tickets; a ring slot is reused
+// only after its consumer has exited.  Units outside the grid output the
+// boundary; lane Tp-1 (the pass's last sweep) writes its row's final values
+// to the grid in place.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -51,71 +60,60 @@ namespace tvs {
 namespace gsl {
 constexpr int kLam = 2;          // group lag (iterations)
 constexpr int kB = 2;            // every lane starts >= 2 columns left of column 0
-constexpr int kPre = 6;          // phantom / lane -1 rows read before iteration 0 (rows -6..-1)
-constexpr int kLR = 128;         // lane -1 staging ring (iterations), power of two
-#ifndef GSL_BATCH
-#define GSL_BATCH 0  // 0: per order (Cfg::Batch)
+constexpr int kR = 16;           // smem ring rows (iterations, power of two; the unroll of the compute loop)
+constexpr int kBlk = 4;          // iterations per loader block
+constexpr int kDist = 2;         // blocks requested ahead of their hand-over (L2 / HBM latency)
+constexpr int kStg = kDist + 1;  // phantom staging slots
+#ifndef GSL_NL
+#define GSL_NL 0
 #endif
-constexpr int kAheadL = 64;      // lane -1 rows are requested this many iterations ahead (HBM latency)
+constexpr int kLR = 32;          // lane -1 staging ring (iterations), power of two
+constexpr int kProRows = 8;      // phantom / lane -1 rows handed over before iteration 0 (rows -8..-1)
 constexpr int kNumSlots = 320;   // global ring slots (CTA boundaries in flight) >= resident CTAs
 // sentinel of an unwritten global-ring cell: a signalling NaN (quiet bit
 // clear), which no arithmetic result can be
 constexpr unsigned long long kSent = 0x7FF4DEADBEEF0001ull;
 
-template <bool REF, int WG>
+// REF: reference (anti-diagonal) order; LC: lane capacity of a group (ring
+// pitch; 32 / 64 / 102 / 128 -- 102 holds T = 100 in one pass)
+template <bool REF, int LC>
 struct Cfg {
 #ifndef GSL_G
 #define GSL_G 0
 #endif
-  // groups per CTA: 4, two CTAs per SM, in both orders (config 4 lex G 3 /
-  // 4 / 7: 33.8 / 29.3 / 32.3 ms with the round-1 loader)
-#ifndef GSL_GREF
-#define GSL_GREF 0
-#endif
-#ifndef GSL_RREF
-#define GSL_RREF 0
-#endif
-  static constexpr int G = REF ? (GSL_GREF > 0 ? GSL_GREF : 4) : (GSL_G > 0 ? GSL_G : 4);
-  // smem ring rows (iterations, power of two; also the unroll of the
-  // compute loop).  Reference order: 8, so that two CTAs of three rings
-  // more fit one SM (config 4: G 7 R 16 one CTA/SM / G 7 R 8 / G 5 R 8 two /
-  // G 4 R 8 two: 31.9 / 29.3 / 27.2 / 25.4 ms)
-  static constexpr int R = REF ? (GSL_RREF > 0 ? GSL_RREF : 8) : 16;
-  // rows per loader block (lane -1 staging batch, phantom poll block).
-  // Config 4 lexicographic 8 / 4 / 2 / 1 rows: 44.3 / 33.8 / 26.1 / 28.7 ms;
-  // reference order 2 / 1: 51.8 / 45.3 ms
-  static constexpr int Batch = GSL_BATCH > 0 ? GSL_BATCH : (REF ? 1 : 2);
+  // groups per CTA (two CTAs per SM).  Config 4 lexicographic, packed lanes,
+  // K6v2 loader: G 4 / 5 21.2 / 19.1 ms; without hand-off 12.0 / 11.5 ms
+  static constexpr int G = REF ? 4 : (GSL_G > 0 ? GSL_G : (LC <= 102 ? 5 : 4));
   static constexpr int Ph = REF ? 2 : 1;        // phantom groups (reads reach group d-2 in REF)
-  static constexpr int L = 32 * WG;             // lanes per group
-  static constexpr int S = L + 2;               // ring row: [pad][lane -1][lanes 0..L-1] (16-B aligned lanes)
+  static constexpr int S = LC + 2;              // ring row: [pad][lane -1][lanes 0..LC-1] (16-B aligned lanes)
   static constexpr int Rings = G + Ph;          // ring index = local group + Ph
-  static constexpr int Compute = G * WG;        // compute warps
-  // one loader warp (a second one, phantom blocks | lane -1 rows, measured
-  // slower: 28.6 vs 23.6 ms at config 4 -- one more warp in every barrier)
-  static constexpr int Threads = (Compute + 1) * 32;
-#ifndef GSL_DIST
-#define GSL_DIST 0
-#endif
-  // phantom blocks are requested Dist blocks ahead of their validation
-  // (config 4 reference order, one-row blocks: Dist 1 / 2: 33.1 / 30.0 ms;
-  // lexicographic two-row blocks: 19.6 / 22.0 ms)
-  static constexpr int Dist = GSL_DIST > 0 ? GSL_DIST : (REF ? 2 : 1);
-  static constexpr int StgBlocks = Dist < 2 ? 2 : 4;  // staging ring (power of two > Dist)
-  static_assert(Dist <= 3, "staging ring");
-  static constexpr int Stg = StgBlocks * Batch * Ph * L;  // phantom staging: blocks of Batch compact rows
-  static constexpr size_t Smem = sizeof(double) * ((size_t)Rings * R * S + (size_t)Rings * kLR + Stg);
+  static constexpr int Compute = (G * LC + 31) / 32;  // compute warps at full capacity
+  // loader warps: warp w hands over rows [w, w + 1) * kBlk / NL of every
+  // block.  One warp could not keep up (config 4: 20.6 ms, the compute warps
+  // waiting on it 44% of the time); lexicographic 2 / 4 warps: 15.6 / 17.0
+  // ms, reference order (two phantom groups): 26.3 / 21.3 ms
+  static constexpr int NL = GSL_NL > 0 ? GSL_NL : (REF ? 4 : 2);
+  static_assert(kBlk % NL == 0, "loader warps split a block's rows");
+  static constexpr int Threads = (Compute + NL) * 32;
+  static constexpr int RowCells = Ph * LC;      // cells of one phantom row (L2 ring and staging pitch)
+  static constexpr size_t Smem =
+      sizeof(double) * ((size_t)Rings * kR * S + (size_t)Rings * kLR + (size_t)kStg * kBlk * RowCells);
+  static constexpr int MinB = 2 * (Smem + 1024) <= 227 * 1024 ? 2 : 1;  // CTAs per SM the shared memory allows
   static constexpr int Back = REF ? 2 * kLam + 1 : kLam + 1;  // deepest ring read behind m
-  static_assert(R >= Back + Batch + 1, "ring too shallow for a phantom block written ahead");
-  static_assert(kLR >= kAheadL + Batch + 8, "lane -1 staging ring too shallow");
-  static_assert(kPre >= Back + 1, "prologue rows");
-  static constexpr int ProRows = (kPre + Batch - 1) / Batch * Batch;  // phantom rows before iteration 0
-  static_assert(R % Batch == 0 && kAheadL % Batch == 0, "block sizes");
+  // ring row i is last read in iteration i + Back and overwritten by row
+  // i + kR: the loader may write block b once block b - Ahead is complete
+  static constexpr int Ahead = (kR - Back) / kBlk;
+  static_assert(Ahead >= 2, "the loader must be able to run a block ahead");
+  static_assert(kProRows >= Back + 1 && kProRows % kBlk == 0, "prologue rows");
+  static_assert(Rings * kBlk <= 32, "one lane -1 cell per loader lane and block");
+  static_assert(kLR >= (kDist + 1) * kBlk + kProRows, "lane -1 staging ring too shallow");
+  static_assert(LC % 2 == 0 && (S * 8) % 16 == 0, "16-byte ring rows");
 };
 }  // namespace gsl
 
 #ifdef GSL_TRACE
-// [cta][0] start ns, [1] first iteration ns, [2] end ns, [3] loader poll-spin cycles,
-// [4] loader cp.async wait cycles, [5] compute warp 0 barrier-wait cycles, [6] loader barrier-wait cycles
+// [cta][0] start ns, [1] first iteration ns, [2] end ns, [3] loader cycles waiting for compute,
+// [4] loader cycles re-polling the L2 ring, [5] compute warp 0 cycles waiting for the loader
 __device__ unsigned long long g_gsl_trace[8192][8];
 __device__ __forceinline__ unsigned long long gsl_now() {
   unsigned long long t;
@@ -128,10 +126,11 @@ struct GslArgs {
   double* a;          // interior origin (in place)
   long long s0;       // row pitch (elements)
   int e0, e1;         // rows, columns
-  int tp;             // sweeps of this pass (<= 32 * WG)
+  int tp;             // sweeps of this pass (<= lr)
+  int lr;             // lanes per group in use (even, <= LC): groups are packed into warps
   int nctas;
   int m_end;          // iterations per CTA (multiple of kR)
-  double* gring;      // kNumSlots x m_end x Ph x L (sentinel until written)
+  double* gring;      // kNumSlots x m_end x RowCells (sentinel until written)
   int* done;          // [slot]: consumer CTAs of this slot that exited (their ticket)
   int* epoch;         // [slot]: boundary + 1 of the producer that owns the slot now
   int* ticket;
@@ -164,13 +163,14 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async16g(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smaddr(smem)), "l"(gmem));
 }
-__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const double* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ void st_relaxed_gpu(double* p, unsigned long long v) {
+#if defined(GSL_ST_WEAK)
+  asm volatile("st.weak.global.cg.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+#elif defined(GSL_ST_NONE)
+  (void)p; (void)v;
+#else
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+#endif
 }
 __device__ __forceinline__ int ld_acquire_gpu32(const int* p) {
   int v;
@@ -182,26 +182,37 @@ __device__ __forceinline__ double2 ld_relaxed_gpu2(const double* p) {
   asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void cta_bar(int nthreads) { asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory"); }
-
-#ifndef GSL_MINB
-#define GSL_MINB 2
-#endif
-#ifndef GSL_MINB_REF
-#define GSL_MINB_REF 2
-#endif
-template <unsigned MASK, bool REF, int WG>
-__global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? GSL_MINB_REF : GSL_MINB) gs2d_lane_kernel(GslArgs p) {
+__device__ __forceinline__ bool gsl_is_sent(const double2& v) {
+  return (__double_as_longlong(v.x) == (long long)gsl::kSent) | (__double_as_longlong(v.y) == (long long)gsl::kSent);
+}
+// Named barriers.  1: the compute warps' per-iteration barrier (the loader is
+// not part of it).  kBarFill + (b & 3): block b handed over -- the loader
+// arrives, every compute warp waits (in place of barrier 1 at the end of the
+// block's first iteration).  kBarDone + (b & 3): block b's iterations finished
+// -- compute warp 0 arrives, the loader waits.  Waiting warps are suspended by
+// the hardware (a spinning shared-memory poll starved the loader of issue
+// slots: 32 ms instead of 19).  At most three blocks are outstanding on
+// either side, so four barriers each never alias.
+constexpr int kBarFill = 2, kBarDone = 6, kBarPro = 10;
+__device__ __forceinline__ void bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+template <unsigned MASK, bool REF, int LC>
+__global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>::MinB) gs2d_lane_kernel(GslArgs p) {
   using namespace gsl;
-  using C = Cfg<REF, WG>;
-  constexpr int kG = C::G, kPh = C::Ph, kL = C::L, kS = C::S, kRings = C::Rings, kThreads = C::Threads;
-  constexpr int kBatch = C::Batch;
-  constexpr int kR = C::R;
+  using C = Cfg<REF, LC>;
+  constexpr int kG = C::G, kPh = C::Ph, kS = C::S, kRings = C::Rings, kRowCells = C::RowCells, kNL = C::NL;
   extern __shared__ __align__(16) double smem[];
   double* const lm1 = smem + (size_t)kRings * kR * kS;  // lane -1 staging [ring][kLR]
-  double* const stg = lm1 + kRings * kLR;                 // phantom staging [StgBlocks][kBatch][kPh * kL]
+  double* const stg = lm1 + kRings * kLR;                 // phantom staging [kStg][kBlk][RowCells]
   __shared__ int s_ticket;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const int lr = p.lr, nunits = kG * lr;
+  const int ncomp = (nunits + 31) >> 5;  // compute warps; the loader is warp ncomp
+  const int cthreads = ncomp * 32;
   const double bnd = p.bnd;
   // every ring cell starts as the boundary (iterations before 0 are columns
   // left of the grid)
@@ -211,7 +222,7 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? GSL_MINB_REF
   const int n = s_ticket;  // position in the CTA chain
 #ifdef GSL_TRACE
   if (threadIdx.x == 0 && n < 8192) g_gsl_trace[n][0] = gsl_now();
-  unsigned long long tr_bar = 0, tr_poll = 0, tr_cpw = 0;
+  long long tr_wait = 0, tr_poll = 0;
 #endif
   const int d0 = n * kG;   // global group of local group 0
   const int m_end = p.m_end;
@@ -222,8 +233,8 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? GSL_MINB_REF
 #else
   const bool has_up = n > 0, has_down = n + 1 < p.nctas;
 #endif
-  double* gin = p.gring + (size_t)slot_in * m_end * kPh * kL;
-  double* gout = p.gring + (size_t)slot_out * m_end * kPh * kL;
+  double* const gin = p.gring + (size_t)slot_in * m_end * kRowCells;
+  double* const gout = p.gring + (size_t)slot_out * m_end * kRowCells;
   if (has_down && threadIdx.x == 0) {
     // ring slot reuse: the consumer of boundary n - kNumSlots (a lower
     // ticket, so started) must have exited -- read and reset every cell --
@@ -238,29 +249,32 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? GSL_MINB_REF
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.epoch + slot_out), "r"(n + 1) : "memory");
   }
   __syncthreads();
-  // producer rows a consumer reads: its rows >= -ProRows, i.e. >= LAM*G - ProRows here
-  const int ring_lo = kLam * kG - C::ProRows;
+  // producer rows a consumer reads: its rows >= -kProRows, i.e. >= LAM*G - kProRows here
+  const int ring_lo = kLam * kG - kProRows;
 
-  if (wi < C::Compute) {
-    // ---------------- compute warp: group g, lanes l = 32 w + t ----------
-    const int g = wi / WG, w = wi % WG, l = 32 * w + lane;
+  if (wi < ncomp) {
+    // ---------------- compute warp: packed unit = group g, lane l ----------
+    // (the last warp's spare threads shadow the last unit and store nothing)
+    const bool live = (int)threadIdx.x < nunits;
+    const int unit = live ? (int)threadIdx.x : nunits - 1;
+    const int g = unit / lr, l = unit - g * lr;
     const int d = d0 + g, row = d - l;
     const int col0 = -kLam * g - 2 * l - kB;  // my column at iteration 0
     double* const ring_me = smem + (size_t)(g + kPh) * kR * kS;
     const double* const ring_up = ring_me - kR * kS;
     const double* const ring_up2 = ring_me - 2 * kR * kS;
-    const bool emit = l == p.tp - 1;  // last sweep of the pass: final values
+    const bool emit = live && l == p.tp - 1;  // last sweep of the pass: final values
     double* const arow = p.a + (long long)row * p.s0;
-    const bool to_ring = has_down && g >= kG - kPh;  // phantom source of the next CTA
-    double* const gdst = gout + (size_t)(g - (kG - kPh)) * kL + l;
-    // this warp's lanes all inside the grid (rows, and columns for iterations
+    const bool to_ring = live && has_down && g >= kG - kPh;  // phantom source of the next CTA
+    double* const gdst = gout + (size_t)(g - (kG - kPh)) * LC + l;
+    // this warp's units all inside the grid (rows, and columns for iterations
     // [m_in0, m_in1)): the steady body needs no selects
-    const bool rows_in = d - 32 * w - 31 >= 0 && d - 32 * w <= e0 - 1;
-    const int m_in0 = kLam * g + 64 * w + 62 + kB, m_in1 = kLam * g + 64 * w + kB + e1;
     const bool row_ok = row >= 0 && row < e0;
+    const bool rows_in = __all_sync(0xffffffffu, row_ok);
+    const int m_in0 = __reduce_max_sync(0xffffffffu, -col0), m_in1 = __reduce_min_sync(0xffffffffu, e1 - col0);
     double nw = bnd, nn = bnd, ne = bnd, ww = bnd, cc = bnd, ee = bnd, sw = bnd, ss = bnd, se = bnd;
     double out = bnd;
-    cta_bar(kThreads);  // prologue rows landed
+    bar_sync(kBarPro, cthreads + 32 * kNL);  // prologue rows handed over
 #ifdef GSL_TRACE
     if (wi == 0 && lane == 0 && n < 8192) g_gsl_trace[n][1] = gsl_now();
 #endif
@@ -297,16 +311,23 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? GSL_MINB_REF
             out = inside ? v : bnd;
           }
           ww = out;
-          ring_me[(u & (kR - 1)) * kS + 2 + l] = out;
-          if (to_ring && m >= ring_lo) st_relaxed_gpu(gdst + (size_t)m * kPh * kL, __double_as_longlong(out));
+          if (live) ring_me[(u & (kR - 1)) * kS + 2 + l] = out;
+          if (to_ring && m >= ring_lo) st_relaxed_gpu(gdst + (size_t)m * kRowCells, __double_as_longlong(out));
           if (emit && inside) arow[col0 + m] = out;
+          // iteration m done in every compute warp; iteration m + 1 of a
+          // block's first iteration reads the block's first loader row
+          if (u % kBlk == 0) {
 #ifdef GSL_TRACE
-          const long long tb0 = clock64();
+            const long long tw0 = clock64();
 #endif
-          cta_bar(kThreads);  // iteration m done everywhere; the loader's rows for m+1 landed
+            bar_sync(kBarFill + ((u / kBlk) & 3), cthreads + 32 * kNL);
 #ifdef GSL_TRACE
-          tr_bar += clock64() - tb0;
+            tr_wait += clock64() - tw0;
 #endif
+          } else {
+            bar_sync(1, cthreads);
+          }
+          if (u % kBlk == kBlk - 1 && wi == 0) bar_arrive(kBarDone + ((u / kBlk) & 3), 32 + 32 * kNL);
         }
       };
       if (steady)
@@ -317,193 +338,156 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? GSL_MINB_REF
 #ifdef GSL_TRACE
     if (wi == 0 && lane == 0 && n < 8192) {
       g_gsl_trace[n][2] = gsl_now();
-      g_gsl_trace[n][5] = tr_bar;
+      g_gsl_trace[n][5] = tr_wait;
     }
 #endif
   } else {
-    // ---------------- loader -----------------------------------------------
-    //  * lane -1 of ring ri (local group g = ri - kPh, global d0 + g) at
-    //    iteration i = grid row d0 + g + 1 at column i - LAM*g + 2 - B:
-    //    cp.async batches of kBatch rows, kAheadL iterations ahead;
-    //  * phantom rows (the previous CTA's last kPh groups at producer
-    //    iteration i + LAM*G; its groups G-kPh.. are my -kPh..) in blocks of
-    //    kBatch rows: a block is requested (cp.async from the L2 ring) one
-    //    block ahead, then validated cell by cell (sentinel: re-polled until
-    //    written), copied into the phantom rings and reset to the sentinel
-    //    in the L2 ring.  One L2 round trip per block, not per row.
-    //    Producer rows >= m_end are columns right of the grid: the boundary.
-    constexpr int kRowCells = kPh * kL;            // cells of one phantom row
-    constexpr int kPieces = kBatch * kRowCells / 2;  // 16-byte pieces per block
-    constexpr int kPerLane = (kPieces + 31) / 32;  // pieces per loader lane (the last round partial)
-    // lane -1 rows: loader lane t < kRings * kBatch owns ring t / kBatch,
-    // iteration offset t % kBatch (grid row d0 + g + 1, g = ring - kPh)
-    static_assert(kRings * kBatch <= 32, "one lane -1 cell per loader lane");
-    const int lm_ri = lane / kBatch, lm_o = lane % kBatch, lm_g = lm_ri - kPh, lm_r = d0 + lm_g + 1;
-    const bool lm_on = lane < kRings * kBatch, lm_row = lm_r >= 0 && lm_r < e0;
-    const int lm_c0 = lm_o - kLam * lm_g + 2 - kB;  // grid column at i0 = 0
-    double* const lm_dst = lm1 + lm_ri * kLR + lm_o;
-    auto batch_lane_m1 = [&](int i0) {  // iterations [i0, i0 + kBatch), every ring
+    // ---------------- loader (one warp, decoupled) ---------------------------
+    // Block q = rows [4q, 4q + 4) of every ring:
+    //  * lane -1 of ring ri (local group g = ri - kPh, global d0 + g) at row i
+    //    = grid row d0 + g + 1 at column i - LAM*g + 2 - B;
+    //  * phantom row i = the previous CTA's last kPh groups at producer
+    //    iteration i + LAM*G (rows past its last iteration are columns right
+    //    of the grid: the boundary).
+    // request(q) starts the copies (grid rows -> lane -1 staging, L2 ring ->
+    // phantom staging), finish(q) -- kDist blocks later -- validates the
+    // phantom cells (sentinel: re-polled until written), resets them in the
+    // L2 ring, copies everything into the rings and publishes the block.
+    constexpr int kStgBlock = kBlk * kRowCells;
+    // A lane's 16-byte pieces of a block sit at compile-time offsets from its
+    // lane base: row r (< kBlk), cells 2 lane + 64 s and the next one, for
+    // s < kSeg (the 32-lane segments of a row) -- no per-piece index
+    // arithmetic (the first K6v3 loader spent ~400 dependent integer
+    // instructions per block on it and was the kernel's bottleneck).
+    constexpr int kSeg = (LC / 2 + 31) / 32;  // pieces per lane and row
+    bool seg_on[kSeg];                        // the segment's pair lies inside the lanes in use
+#pragma unroll
+    for (int sg = 0; sg < kSeg; ++sg) seg_on[sg] = 2 * lane + 64 * sg < lr;
+    // lane -1: loader lane t < kRings * kBlk owns ring t / kBlk, row offset t % kBlk
+    const int lm_ri = lane / kBlk, lm_o = lane % kBlk, lm_g = lm_ri - kPh, lm_r = d0 + lm_g + 1;
+    const int lw = wi - ncomp;  // loader warp: its rows of a block are [lw_r0, lw_r0 + kSubR)
+    constexpr int kSubR = kBlk / kNL;
+    const int lw_r0 = lw * kSubR;
+    const bool lm_on = lw == 0 && lane < kRings * kBlk, lm_row = lm_r >= 0 && lm_r < e0;
+    const int lm_c0 = lm_o - kLam * lm_g + 2 - kB;  // grid column of row 4q + lm_o at q = 0
+    const double* const lm_src = p.a + (long long)lm_r * p.s0;
+    auto rows_in_ring = [&](int i) { return has_up && i + kLam * kG < m_end; };
+    // a ring cell only this lane stores in every finish() (read back before the hand-over):
+    // its lane -1 slot, or -- lanes without one -- its first phantom pair (always inside the lanes in use)
+    int lane_cell = 0;
+    int rq_slot = 0, fin_slot = 0;  // phantom staging slots of the next request / finish
+    auto request = [&](int q) {
+      const int i0 = q * kBlk;
       if (lm_on) {
         const int c = i0 + lm_c0;
-        double* dst = lm_dst + (i0 & (kLR - 1));
+        double* dst = lm1 + lm_ri * kLR + ((i0 + lm_o) & (kLR - 1));
         if (lm_row && c >= 0 && c < e1)
-          cp_async8(dst, p.a + (long long)lm_r * p.s0 + c);
+          cp_async8(dst, lm_src + c);
         else
           *dst = bnd;
       }
-    };
-    auto slot1 = [&](int i) {  // lane -1 of every ring at iteration i -> ring slot 1
-      if (lane < kRings) smem[((size_t)lane * kR + (i & (kR - 1))) * kS + 1] = lm1[lane * kLR + (i & (kLR - 1))];
-    };
-    auto in_ring = [&](int i) { return has_up && i + kLam * kG < m_end; };
-    auto gcell = [&](int i, int e) -> double* { return gin + (size_t)(i + kLam * kG) * kRowCells + e; };
-    auto request_block = [&](int i0) {  // phantom rows [i0, i0 + kBatch) -> staging
-      double* sb = stg + ((i0 / kBatch) & (C::StgBlocks - 1)) * (kBatch * kRowCells);
-#pragma unroll 4
-      for (int j = 0; j < kPerLane; ++j) {
-        const int k = lane + 32 * j, r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
-        if (k < kPieces && in_ring(i0 + r)) cp_async16g(sb + r * kRowCells + e, gcell(i0 + r, e));
-      }
-    };
-    // lexicographic: the block's pieces loaded together, 16-byte smem and L2
-    // accesses; reference order keeps the one-piece-at-a-time loop (faster
-    // there: 45.3 vs 51.8 ms at config 4 size)
-    auto finish_block_vec = [&](int i0) {
-      const double* sb = stg + ((i0 / kBatch) & (C::StgBlocks - 1)) * (kBatch * kRowCells);
-      double2 got[kPerLane];
-#pragma unroll
-      for (int j = 0; j < kPerLane; ++j) {
-        const int k = lane + 32 * j, r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
-        if (kPieces % 32 == 0 || k < kPieces) got[j] = *reinterpret_cast<const double2*>(sb + r * kRowCells + e);
-      }
-#pragma unroll
-      for (int j = 0; j < kPerLane; ++j) {
-        const int k = lane + 32 * j, r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
-        if (kPieces % 32 != 0 && k >= kPieces) break;
-        const int i = i0 + r;
-        unsigned long long v0 = __double_as_longlong(bnd), v1 = v0;
-        if (in_ring(i)) {
-          v0 = __double_as_longlong(got[j].x);
-          v1 = __double_as_longlong(got[j].y);
-          if (v0 == kSent || v1 == kSent) {
-            const long long t0 = clock64();
-            while (v0 == kSent) {
-              v0 = ld_relaxed_gpu(gcell(i, e));
-              if (clock64() - t0 > (1ll << 34)) __trap();
-            }
-            while (v1 == kSent) {
-              v1 = ld_relaxed_gpu(gcell(i, e + 1));
-              if (clock64() - t0 > (1ll << 34)) __trap();
-            }
-          }
-          asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(gcell(i, e)), "l"(kSent), "l"(kSent)
-                       : "memory");
-        }
-        const int ph = e / kL, ll = e % kL;
-        double* dst = smem + ((size_t)ph * kR + (i & (kR - 1))) * kS + 2 + ll;
-        *reinterpret_cast<double2*>(dst) = make_double2(__longlong_as_double(v0), __longlong_as_double(v1));
-      }
-    };
-    auto finish_block_one = [&](int i0) {
-      const double* sb = stg + ((i0 / kBatch) & (C::StgBlocks - 1)) * (kBatch * kRowCells);
+      const bool full = rows_in_ring(i0 + kBlk - 1);
+      if (full || rows_in_ring(i0)) {
 #pragma unroll 1
-      for (int j = 0; j < kPerLane; ++j) {
-        const int k = lane + 32 * j, r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
-        if (k >= kPieces) break;
-        const int i = i0 + r;
-        unsigned long long v0 = __double_as_longlong(bnd), v1 = v0;
-        if (in_ring(i)) {
-          v0 = __double_as_longlong(sb[r * kRowCells + e]);
-          v1 = __double_as_longlong(sb[r * kRowCells + e + 1]);
-          if (v0 == kSent || v1 == kSent) {
+        for (int ph = 0; ph < kPh; ++ph) {
+          double* sb = stg + rq_slot * kStgBlock + lw_r0 * kRowCells + ph * LC + 2 * lane;
+          const double* gb = gin + (long long)(i0 + lw_r0 + kLam * kG) * kRowCells + ph * LC + 2 * lane;
+#pragma unroll
+          for (int r = 0; r < kSubR; ++r)
+#pragma unroll
+            for (int sg = 0; sg < kSeg; ++sg)
+              if (seg_on[sg] && (full || rows_in_ring(i0 + lw_r0 + r)))
+                cp_async16g(sb + r * kRowCells + 64 * sg, gb + r * kRowCells + 64 * sg);
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      rq_slot = rq_slot == kStg - 1 ? 0 : rq_slot + 1;
+    };
+    auto finish = [&](int q) {
+      const int i0 = q * kBlk;
+      const bool full = rows_in_ring(i0 + kBlk - 1);
+#pragma unroll 1
+      for (int ph = 0; ph < kPh; ++ph) {
+        {
+          const int r0 = lw_r0;  // this loader warp's rows
+          const double* sb = stg + fin_slot * kStgBlock + r0 * kRowCells + ph * LC + 2 * lane;
+          double* const gb = gin + (long long)(i0 + r0 + kLam * kG) * kRowCells + ph * LC + 2 * lane;
+          double* const rb = smem + ((size_t)ph * kR + ((i0 + r0) & (kR - 1))) * kS + 2 + 2 * lane;
+          double2 got[kSubR * kSeg];
+          unsigned live_mask = 0;  // pieces that come from the L2 ring
+          bool bad = false;
+#pragma unroll
+          for (int r = 0; r < kSubR; ++r)
+#pragma unroll
+            for (int sg = 0; sg < kSeg; ++sg) {
+              const int j = r * kSeg + sg;
+              got[j] = make_double2(bnd, bnd);
+              if (seg_on[sg] && (full || rows_in_ring(i0 + r0 + r))) {
+                live_mask |= 1u << j;
+                got[j] = *reinterpret_cast<const double2*>(sb + r * kRowCells + 64 * sg);
+                bad |= gsl_is_sent(got[j]);
+              }
+            }
+          if (__any_sync(0xffffffffu, bad)) {
+            // late cells (the consumer caught up with its producer): re-read
+            // every late pair at once until all have landed
             const long long t0 = clock64();
-            while (v0 == kSent) {
-              v0 = ld_relaxed_gpu(gcell(i, e));
+            do {
+              bad = false;
+#pragma unroll
+              for (int r = 0; r < kSubR; ++r)
+#pragma unroll
+                for (int sg = 0; sg < kSeg; ++sg) {
+                  const int j = r * kSeg + sg;
+                  if ((live_mask >> j & 1u) && gsl_is_sent(got[j])) {
+                    got[j] = ld_relaxed_gpu2(gb + r * kRowCells + 64 * sg);
+                    bad |= gsl_is_sent(got[j]);
+                  }
+                }
               if (clock64() - t0 > (1ll << 34)) __trap();
-            }
-            while (v1 == kSent) {
-              v1 = ld_relaxed_gpu(gcell(i, e + 1));
-              if (clock64() - t0 > (1ll << 34)) __trap();
-            }
+            } while (__any_sync(0xffffffffu, bad));
 #ifdef GSL_TRACE
             tr_poll += clock64() - t0;
 #endif
           }
+#pragma unroll
+          for (int r = 0; r < kSubR; ++r)
+#pragma unroll
+            for (int sg = 0; sg < kSeg; ++sg) {
+              const int j = r * kSeg + sg;
+              if (seg_on[sg]) {
 #ifndef GSL_NO_RESET
-          st_relaxed_gpu(gcell(i, e), kSent);
-          st_relaxed_gpu(gcell(i, e + 1), kSent);
+                if (live_mask >> j & 1u)
+                  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(gb + r * kRowCells + 64 * sg),
+                               "l"(kSent), "l"(kSent)
+                               : "memory");
 #endif
-        }
-        const int ph = e / kL, ll = e % kL;
-        double* dst = smem + ((size_t)ph * kR + (i & (kR - 1))) * kS + 2 + ll;
-        dst[0] = __longlong_as_double(v0);
-        dst[1] = __longlong_as_double(v1);
-      }
-    };
-    // blocks wholly inside the producer's rows (all but the first and last
-    // few of a CTA with a producer): piece j of lane t is block cell pair
-    // 2 (t + 32 j) in staging and in the L2 ring alike; one warp vote checks
-    // the sentinels, late cells are re-polled out of line
-    auto block_full = [&](int i0) { return has_up && i0 + kBatch - 1 + kLam * kG < m_end; };
-    auto request_fast = [&](int i0) {
-      double* sb = stg + ((i0 / kBatch) & (C::StgBlocks - 1)) * (kBatch * kRowCells);
-      const double* gb = gin + (size_t)(i0 + kLam * kG) * kRowCells;
-#pragma unroll
-      for (int j = 0; j < kPerLane; ++j) {
-        const int k = lane + 32 * j;
-        if (kPieces % 32 == 0 || k < kPieces) cp_async16g(sb + 2 * k, gb + 2 * k);
-      }
-    };
-    auto finish_fast = [&](int i0) {
-      const double* sb = stg + ((i0 / kBatch) & (C::StgBlocks - 1)) * (kBatch * kRowCells);
-      double* const gb = gin + (size_t)(i0 + kLam * kG) * kRowCells;
-      double2 got[kPerLane];
-      bool bad = false;
-#pragma unroll
-      for (int j = 0; j < kPerLane; ++j) {
-        const int k = lane + 32 * j;
-        if (kPieces % 32 == 0 || k < kPieces) {
-          got[j] = *reinterpret_cast<const double2*>(sb + 2 * k);
-          bad |= (__double_as_longlong(got[j].x) == kSent) | (__double_as_longlong(got[j].y) == kSent);
-        }
-      }
-      if (__any_sync(0xffffffffu, bad)) {
-        // late cells (the consumer caught up with its producer): re-read
-        // every late pair at once until all have landed
-        const long long t0 = clock64();
-        do {
-          bad = false;
-#pragma unroll
-          for (int j = 0; j < kPerLane; ++j) {
-            const int k = lane + 32 * j;
-            if ((kPieces % 32 == 0 || k < kPieces) &&
-                ((__double_as_longlong(got[j].x) == kSent) | (__double_as_longlong(got[j].y) == kSent))) {
-              got[j] = ld_relaxed_gpu2(gb + 2 * k);
-              bad |= (__double_as_longlong(got[j].x) == kSent) | (__double_as_longlong(got[j].y) == kSent);
+                *reinterpret_cast<double2*>(rb + r * kS + 64 * sg) = got[j];
+              }
             }
-          }
-          if (clock64() - t0 > (1ll << 34)) __trap();
-        } while (__any_sync(0xffffffffu, bad));
-      }
-#pragma unroll
-      for (int j = 0; j < kPerLane; ++j) {
-        const int k = lane + 32 * j;
-        if (kPieces % 32 == 0 || k < kPieces) {
-#ifndef GSL_NO_RESET
-          asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(gb + 2 * k), "l"(kSent), "l"(kSent)
-                       : "memory");
-#endif
-          const int r = k / (kRowCells / 2), e = 2 * (k % (kRowCells / 2));
-          const int ph = e / kL, ll = e % kL;
-          *reinterpret_cast<double2*>(smem + ((size_t)ph * kR + ((i0 + r) & (kR - 1))) * kS + 2 + ll) = got[j];
         }
       }
+      fin_slot = fin_slot == kStg - 1 ? 0 : fin_slot + 1;
+      // lane -1 of every ring -> ring slot 1
+      if (lm_on) {
+        const int i = i0 + lm_o;
+        lane_cell = (lm_ri * kR + (i & (kR - 1))) * kS + 1;
+        smem[lane_cell] = lm1[lm_ri * kLR + (i & (kLR - 1))];
+      } else {
+        lane_cell = ((kPh - 1) * kR + ((i0 + lw_r0 + kSubR - 1) & (kR - 1))) * kS + 2 + 2 * lane;  // last row, segment 0
+      }
     };
-    auto finish_block = [&](int i0) {  // validate, copy into the rings, reset the L2 cells
-      if constexpr (REF)
-        finish_block_one(i0);
-      else
-        finish_block_vec(i0);
+    // Hand-over: the block's shared-memory stores must be performed before
+    // the arrival.  A block-scope fence would also wait for this warp's
+    // global traffic in flight (the sentinel resets and the cp.async of the
+    // next blocks: an L2 round trip per block, which made the loader the
+    // kernel's bottleneck); shared-memory accesses of a warp complete in
+    // order, so reading back the last cell this lane stored is enough.
+    auto publish = [&](int bar, const double* last_store) {
+      unsigned long long echo;
+      asm volatile("ld.volatile.shared.b64 %0, [%1];" : "=l"(echo) : "r"(smaddr(last_store)) : "memory");
+      asm volatile("{ .reg .pred p; setp.eq.u64 p, %2, 0x7FF4DEADBEEF0002; @!p bar.arrive %0, %1; @p bar.arrive %0, %1; }"
+                   ::"r"(bar), "r"(cthreads + 32 * kNL), "l"(echo) : "memory");
     };
     if (has_up) {
       // the incoming slot holds my producer's cells only once the producer
@@ -528,89 +512,47 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, WG>::Threads, REF ? GSL_MINB_REF
         if (clock64() - t0 > (1ll << 35)) __trap();
       }
     }
-    // prologue: lane -1 rows [-kBatch, kAheadL) landed; phantom rows
-    // [-kBatch, 0) in the rings, rows [0, kBatch) requested
-    for (int i0 = -C::ProRows; i0 < kAheadL; i0 += kBatch) batch_lane_m1(i0);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    __syncwarp();
-    for (int i = -kPre; i <= 0; ++i) slot1(i);
-    for (int i0 = -C::ProRows; i0 < 0; i0 += kBatch) {
-      request_block(i0);
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    const int nb = m_end / kBlk;
+    constexpr int kProBlocks = kProRows / kBlk;
+    // prologue rows -kProRows..-1, then blocks 0 .. kDist-1 in flight
+    for (int q = -kProBlocks; q < 0; ++q) {
+      request(q);
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      finish_block(i0);
+      finish(q);
     }
-    // blocks 0 .. Dist-1 in flight, each followed by an (empty) lane -1
-    // group so that every block below commits the same pair
-    for (int j = 0; j < C::Dist; ++j) {
-      request_block(j * kBatch);
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-    }
-    __syncwarp();
-    cta_bar(kThreads);
-    for (int mb = 0; mb < m_end; mb += kR) {
-#pragma unroll
-      for (int u = 0; u < kR; ++u) {
-        const int m = mb + u;
-        // per block: group A = the phantom block Dist blocks ahead (first
-        // iteration), group B = lane -1 rows kAheadL iterations ahead (the
-        // second iteration, to even out the loader's work); waiting for all
-        // but the newest 2 Dist groups (2 Dist + 1 with one-row blocks)
-        // retires this block's request, committed Dist blocks ago
-#ifdef GSL_LM_SAME
-        constexpr int kLmU = 0;
-#else
-        constexpr int kLmU = kBatch > 1 ? 1 : 0;
-#endif
-        if (u % kBatch == 0) {
-          const int iq = m + C::Dist * kBatch;
-          if (block_full(iq))
-            request_fast(iq);
-          else
-            request_block(iq);
-          asm volatile("cp.async.commit_group;\n" ::: "memory");
-        }
-        if (u % kBatch == kLmU) {
-          batch_lane_m1(m - kLmU + kAheadL);
-          asm volatile("cp.async.commit_group;\n" ::: "memory");
-        }
-        if (u % kBatch == 0) {
+    for (int q = 0; q < kDist; ++q) request(q);
+    publish(kBarPro, smem + (size_t)lane_cell);
+    for (int b = 0; b < nb; ++b) {
+      if (b + kDist < nb)
+        request(b + kDist);
+      else
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kDist) : "memory");  // block b's copies landed
+      if (b >= C::Ahead) {
+        // ring rows of block b still hold block b - kR / kBlk, read until
+        // block b - Ahead completes
 #ifdef GSL_TRACE
-          const long long tw0 = clock64();
+        const long long tw0 = clock64();
 #endif
-          asm volatile("cp.async.wait_group %0;\n" ::"n"(2 * C::Dist + (kLmU > 0 ? 0 : 1)) : "memory");
+        bar_sync(kBarDone + ((b - C::Ahead) & 3), 32 + 32 * kNL);
 #ifdef GSL_TRACE
-          tr_cpw += clock64() - tw0;
-#endif
-          __syncwarp();
-          // rows [m, m + kBatch): read from iteration m + 1 on
-          if (block_full(m))
-            finish_fast(m);
-          else
-            finish_block(m);
-        }
-        slot1(m + 1);  // read from iteration m + 2 on
-        __syncwarp();
-#ifdef GSL_TRACE
-        const long long tb0 = clock64();
-#endif
-        cta_bar(kThreads);
-#ifdef GSL_TRACE
-        tr_bar += clock64() - tb0;
+        tr_wait += clock64() - tw0;
 #endif
       }
+      finish(b);
+      publish(kBarFill + (b & 3), smem + (size_t)lane_cell);
     }
+    // the last blocks' completions (keeps every barrier balanced at exit)
+    for (int b = nb > C::Ahead ? nb - C::Ahead : 0; b < nb; ++b) bar_sync(kBarDone + (b & 3), 32 + 32 * kNL);
     asm volatile("cp.async.wait_all;\n" ::: "memory");
 #ifdef GSL_TRACE
     if (lane == 0 && n < 8192) {
-      g_gsl_trace[n][3] = tr_poll;
-      g_gsl_trace[n][4] = tr_cpw;
-      g_gsl_trace[n][6] = tr_bar;
+      g_gsl_trace[n][3] = tr_wait;
+      g_gsl_trace[n][4] = tr_poll;
     }
 #endif
-    if (has_up && lane == 0) {
+    if (kNL > 1) bar_sync(11, 32 * kNL);  // every loader warp is done with the incoming slot
+    if (has_up && lw == 0 && lane == 0) {
       // every read (and sentinel reset) of the incoming slot is done: release
       // it (the ticket is re-read: nothing long-lived stays in a register)
       const int nn = *(volatile int*)&s_ticket;
@@ -667,17 +609,22 @@ bool gs2d_lane_supported(const tvs_stencil& st) {
   return st.dim == 2 && (m == 0x1FFu || m == kGslStar) && bb != gsl::kSent;
 }
 
-template <unsigned MASK, bool REF, int WG>
+template <unsigned MASK, bool REF, int LC>
 static int gsl_launch(GslArgs a, int64_t steps, int64_t per, cudaStream_t s, const unsigned* rows_ready,
                       unsigned* blocks_done) {
   using namespace gsl;
-  using C = Cfg<REF, WG>;
-  auto kern = gs2d_lane_kernel<MASK, REF, WG>;
+  using C = Cfg<REF, LC>;
+  auto kern = gs2d_lane_kernel<MASK, REF, LC>;
   TVS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::Smem));
+#ifdef GSL_NOPACK
+  a.lr = LC;
+#else
+  a.lr = (int)std::min<int64_t>((per + 1) / 2 * 2, LC);  // lanes in use per group (even: 16-byte hand-off pieces)
+#endif
   // the last group's lanes reach column e1 (the boundary the consumer reads)
-  const int m_need = a.e1 + kLam * (C::G - 1) + 2 * (C::L - 1) + kB + 2;
-  a.m_end = (m_need + C::R - 1) / C::R * C::R;
-  const size_t cells = (size_t)kNumSlots * a.m_end * C::Ph * C::L;
+  const int m_need = a.e1 + kLam * (C::G - 1) + 2 * (a.lr - 1) + kB + 2;
+  a.m_end = (m_need + kR - 1) / kR * kR;
+  const size_t cells = (size_t)kNumSlots * a.m_end * C::RowCells;
   const size_t ctrl_bytes = sizeof(int) * 2 * kNumSlots + 64;
   a.gring = static_cast<double*>(scratch(sizeof(double) * cells, 4));
   char* ctrl = static_cast<char*>(scratch(ctrl_bytes, 5));
@@ -699,12 +646,13 @@ static int gsl_launch(GslArgs a, int64_t steps, int64_t per, cudaStream_t s, con
   if ((rows_ready || blocks_done) && per < steps) return fail(TVS_ERR_INVALID, "gs2d_lane: pipeline hooks need one pass");
   a.rows_ready = rows_ready;
   a.blocks_done = blocks_done;
+  const int nthreads = ((C::G * a.lr + 31) / 32 + C::NL) * 32;  // packed compute warps + the loader warps
   for (int64_t done = 0; done < steps; done += per) {
     a.tp = (int)std::min<int64_t>(per, steps - done);
     const int ngroups = a.e0 + a.tp - 1;
     a.nctas = (ngroups + C::G - 1) / C::G;
     TVS_CUDA(cudaMemsetAsync(ctrl, 0, ctrl_bytes, s));
-    kern<<<a.nctas, C::Threads, C::Smem, s>>>(a);
+    kern<<<a.nctas, nthreads, C::Smem, s>>>(a);
     TVS_LAUNCHED("gs2d_lane_kernel");
   }
   return TVS_OK;
@@ -718,13 +666,23 @@ extern "C" int tvs_gsl_trace(unsigned long long* host, int n) {
 }
 #endif
 
+// A pass holds <= 128 sweeps; passes are balanced, and the lane capacity is
+// the smallest instantiated one that holds a pass (T = 100: one pass, 102).
+static void gsl_plan(int64_t steps, int64_t* per, int* lc) {
+  const int64_t npass = (steps + 127) / 128;
+  *per = (steps + npass - 1) / npass;
+  *lc = *per <= 32 ? 32 : (*per <= 64 ? 64 : (*per <= 102 ? 102 : 128));
+}
+static int gsl_groups(int64_t steps, int order) {
+  int64_t per;
+  int lc;
+  gsl_plan(std::max<int64_t>(steps, 1), &per, &lc);
+  if (order == TVS_GS_REFERENCE) return gsl::Cfg<true, 128>::G;
+  return lc <= 102 ? gsl::Cfg<false, 102>::G : gsl::Cfg<false, 128>::G;
+}
 // Drop-in pipeline hooks (api.cu gs2d_pipelined): one pass of <= 128 sweeps;
 // CTAs of that pass, and how many must have exited before row `row` holds
 // its final value (the group row + steps - 1 writes it).
-static int gsl_groups(int64_t steps, int order) {
-  (void)steps;
-  return order == TVS_GS_REFERENCE ? gsl::Cfg<true, 4>::G : gsl::Cfg<false, 4>::G;
-}
 int gs2d_lane_max_sweeps() { return 128; }
 int64_t gs2d_lane_ctas(int64_t rows, int64_t steps, int order) {
   const int G = gsl_groups(steps, order);
@@ -748,18 +706,17 @@ int gs2d_lane(const tvs_stencil& st, const tvs_geometry& g, double* grid, int64_
   a.e1 = (int)g.extents[1];
   for (int k = 0; k < 9; ++k) a.w[k] = w[k];
   a.bnd = st.boundary;
-  // lanes per group = the smallest warp multiple holding a pass of <= 128
-  // sweeps in balanced passes (T = 100: one pass on 4-warp groups)
-  const int64_t npass = (steps + 127) / 128;
-  const int64_t per = (steps + npass - 1) / npass;
-  const int wg = per <= 32 ? 1 : (per <= 64 ? 2 : 4);
+  int64_t per;
+  int lc;
+  gsl_plan(steps, &per, &lc);
   const bool ref = order == TVS_GS_REFERENCE, box = mask == 0x1FFu;
   auto go = [&](auto m_tag, auto r_tag) -> int {
     constexpr unsigned M = decltype(m_tag)::value;
     constexpr bool R = decltype(r_tag)::value;
-    if (wg == 1) return gsl_launch<M, R, 1>(a, steps, per, s, rows_ready, blocks_done);
-    if (wg == 2) return gsl_launch<M, R, 2>(a, steps, per, s, rows_ready, blocks_done);
-    return gsl_launch<M, R, 4>(a, steps, per, s, rows_ready, blocks_done);
+    if (lc == 32) return gsl_launch<M, R, 32>(a, steps, per, s, rows_ready, blocks_done);
+    if (lc == 64) return gsl_launch<M, R, 64>(a, steps, per, s, rows_ready, blocks_done);
+    if (lc == 102) return gsl_launch<M, R, 102>(a, steps, per, s, rows_ready, blocks_done);
+    return gsl_launch<M, R, 128>(a, steps, per, s, rows_ready, blocks_done);
   };
   using Box = std::integral_constant<unsigned, 0x1FFu>;
   using Star = std::integral_constant<unsigned, kGslStar>;

@@ -1,0 +1,5 @@
+set -x
+echo "== old"; TVSTENCIL_LIB=build/var/old/libtvstencil.so timeout 300 python tools/gsl_ncu.py 2>&1 | tail -1
+timeout 900 python tools/gs2d_lane_check.py > gpurun_out/s5h_gsl_v3.txt 2>&1; cat gpurun_out/s5h_gsl_v3.txt
+echo "== v3 noup"; TVSTENCIL_LIB=build/var/gsl_v3_noup/libtvstencil.so timeout 300 python tools/gsl_ncu.py 2>&1 | tail -1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:gs2d_lane_kernel -c 1 -o gpurun_out/s5h_full_c4_v3 python tools/gsl_ncu.py > /dev/null 2>&1; echo "ncu rc=$?"

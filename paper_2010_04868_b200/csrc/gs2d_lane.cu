@@ -61,8 +61,14 @@ namespace gsl {
 constexpr int kLam = 2;          // group lag (iterations)
 constexpr int kB = 2;            // every lane starts >= 2 columns left of column 0
 constexpr int kR = 16;           // smem ring rows (iterations, power of two; the unroll of the compute loop)
-constexpr int kBlk = 4;          // iterations per loader block
-constexpr int kDist = 2;         // blocks requested ahead of their hand-over (L2 / HBM latency)
+#ifndef GSL_BLK
+#define GSL_BLK 4
+#endif
+#ifndef GSL_DIST
+#define GSL_DIST 1  // config 4 lexicographic / reference order, 1 / 2 / 3 blocks: 14.6 / 15.6 / 17.0 and 19.7 / 21.3 / 23.6 ms (a longer hand-off lag lengthens the 332-CTA start-up ramp)
+#endif
+constexpr int kBlk = GSL_BLK;    // iterations per loader block
+constexpr int kDist = GSL_DIST;  // blocks requested ahead of their hand-over (L2 / HBM latency)
 constexpr int kStg = kDist + 1;  // phantom staging slots
 #ifndef GSL_NL
 #define GSL_NL 0
@@ -102,7 +108,7 @@ struct Cfg {
   static constexpr int Back = REF ? 2 * kLam + 1 : kLam + 1;  // deepest ring read behind m
   // ring row i is last read in iteration i + Back and overwritten by row
   // i + kR: the loader may write block b once block b - Ahead is complete
-  static constexpr int Ahead = (kR - Back) / kBlk;
+  static constexpr int Ahead = (kR - Back) / kBlk < 3 ? (kR - Back) / kBlk : 3;  // <= 3: four barriers per direction
   static_assert(Ahead >= 2, "the loader must be able to run a block ahead");
   static_assert(kProRows >= Back + 1 && kProRows % kBlk == 0, "prologue rows");
   static_assert(Rings * kBlk <= 32, "one lane -1 cell per loader lane and block");
@@ -515,11 +521,10 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
     const int nb = m_end / kBlk;
     constexpr int kProBlocks = kProRows / kBlk;
     // prologue rows -kProRows..-1, then blocks 0 .. kDist-1 in flight
-    for (int q = -kProBlocks; q < 0; ++q) {
-      request(q);
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      finish(q);
-    }
+    static_assert(kProBlocks <= kStg, "prologue blocks share the staging slots");
+    for (int q = -kProBlocks; q < 0; ++q) request(q);  // one L2 round trip for all of them
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    for (int q = -kProBlocks; q < 0; ++q) finish(q);
     for (int q = 0; q < kDist; ++q) request(q);
     publish(kBarPro, smem + (size_t)lane_cell);
     for (int b = 0; b < nb; ++b) {

@@ -103,7 +103,7 @@ struct Cfg {
   static constexpr int Threads = (Compute + NL) * 32;
   static constexpr int RowCells = Ph * LC;      // cells of one phantom row (L2 ring and staging pitch)
   static constexpr size_t Smem =
-      sizeof(double) * ((size_t)Rings * kR * S + (size_t)Rings * kLR + (size_t)kStg * kBlk * RowCells);
+      sizeof(double) * ((size_t)Rings * (kR * S + 16) + (size_t)Rings * kLR + (size_t)kStg * kBlk * RowCells);
   static constexpr int MinB = 2 * (Smem + 1024) <= 227 * 1024 ? 2 : 1;  // CTAs per SM the shared memory allows
   static constexpr int Back = REF ? 2 * kLam + 1 : kLam + 1;  // deepest ring read behind m
   // ring row i is last read in iteration i + Back and overwritten by row
@@ -212,7 +212,14 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
   using C = Cfg<REF, LC>;
   constexpr int kG = C::G, kPh = C::Ph, kS = C::S, kRings = C::Rings, kRowCells = C::RowCells, kNL = C::NL;
   extern __shared__ __align__(16) double smem[];
-  double* const lm1 = smem + (size_t)kRings * kR * kS;  // lane -1 staging [ring][kLR]
+  // Ring g starts rstride cells after ring g-1: kR rows plus a pad chosen so
+  // that a warp straddling two packed groups (lanes 96..99 of one, 0..27 of
+  // the next at lr = 100) touches 32 consecutive banks instead of the same
+  // ones twice (ncu: 9% of the kernel's shared-memory wavefronts were
+  // conflicts).  The pad is exact for lr = 100 (T = 100, capacity 102) and
+  // compile-time (a run-time stride costs the register the kernel lacks)
+  constexpr int rstride = kR * kS + (LC == 102 ? 100 % 16 : 0);
+  double* const lm1 = smem + (size_t)kRings * (kR * kS + 16);  // lane -1 staging [ring][kLR]
   double* const stg = lm1 + kRings * kLR;                 // phantom staging [kStg][kBlk][RowCells]
   __shared__ int s_ticket;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
@@ -222,7 +229,7 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
   const double bnd = p.bnd;
   // every ring cell starts as the boundary (iterations before 0 are columns
   // left of the grid)
-  for (int i = threadIdx.x; i < kRings * (kR * kS + kLR); i += blockDim.x) smem[i] = bnd;
+  for (int i = threadIdx.x; i < kRings * (kR * kS + 16 + kLR); i += blockDim.x) smem[i] = bnd;
   if (threadIdx.x == 0) s_ticket = atomicAdd(p.ticket, 1);
   __syncthreads();
   const int n = s_ticket;  // position in the CTA chain
@@ -266,9 +273,9 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
     const int g = unit / lr, l = unit - g * lr;
     const int d = d0 + g, row = d - l;
     const int col0 = -kLam * g - 2 * l - kB;  // my column at iteration 0
-    double* const ring_me = smem + (size_t)(g + kPh) * kR * kS;
-    const double* const ring_up = ring_me - kR * kS;
-    const double* const ring_up2 = ring_me - 2 * kR * kS;
+    double* const ring_me = smem + (size_t)(g + kPh) * rstride;
+    const double* const ring_up = ring_me - rstride;
+    const double* const ring_up2 = ring_me - 2 * rstride;
     const bool emit = live && l == p.tp - 1;  // last sweep of the pass: final values
     double* const arow = p.a + (long long)row * p.s0;
     const bool to_ring = live && has_down && g >= kG - kPh;  // phantom source of the next CTA
@@ -418,7 +425,7 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
           const int r0 = lw_r0;  // this loader warp's rows
           const double* sb = stg + fin_slot * kStgBlock + r0 * kRowCells + ph * LC + 2 * lane;
           double* const gb = gin + (long long)(i0 + r0 + kLam * kG) * kRowCells + ph * LC + 2 * lane;
-          double* const rb = smem + ((size_t)ph * kR + ((i0 + r0) & (kR - 1))) * kS + 2 + 2 * lane;
+          double* const rb = smem + (size_t)ph * rstride + ((i0 + r0) & (kR - 1)) * kS + 2 + 2 * lane;
           double2 got[kSubR * kSeg];
           unsigned live_mask = 0;  // pieces that come from the L2 ring
           bool bad = false;
@@ -477,10 +484,10 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
       // lane -1 of every ring -> ring slot 1
       if (lm_on) {
         const int i = i0 + lm_o;
-        lane_cell = (lm_ri * kR + (i & (kR - 1))) * kS + 1;
+        lane_cell = lm_ri * rstride + (i & (kR - 1)) * kS + 1;
         smem[lane_cell] = lm1[lm_ri * kLR + (i & (kLR - 1))];
       } else {
-        lane_cell = ((kPh - 1) * kR + ((i0 + lw_r0 + kSubR - 1) & (kR - 1))) * kS + 2 + 2 * lane;  // last row, segment 0
+        lane_cell = (kPh - 1) * rstride + ((i0 + lw_r0 + kSubR - 1) & (kR - 1)) * kS + 2 + 2 * lane;  // last row, segment 0
       }
     };
     // Hand-over: the block's shared-memory stores must be performed before

@@ -422,7 +422,10 @@ static void launch2d_one(int mode, cudaStream_t s, const double* src, double* ds
   // columns per lane: registers grow as 2 * P * D accumulators; P = 3 at
   // D = 5..8 keeps 12 warps/SM at D = 8 (168 registers) where P = 4 held 9
   // (config 3: D = 8 P = 4 1596, P = 3 1723 GSt/s; D > 8 at P = 3 is slower)
-  constexpr int P = D <= 4 ? 4 : (D <= 8 ? 3 : 2);
+#ifndef J2D_P4MAX
+#define J2D_P4MAX 4
+#endif
+  constexpr int P = D <= J2D_P4MAX ? 4 : (D <= 8 ? 3 : 2);
   const int64_t U = 32 * P - 2 * D;
   const int64_t ns = (geo.e1 + U - 1) / U;
   if (seg_rows <= 0) {

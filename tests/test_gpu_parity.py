@@ -155,7 +155,7 @@ def test_jacobi3d_streaming(cuda_ready, kernel, ext):
 @pytest.mark.parametrize("kernel", ["heat3d", "jac3d27p"])
 @pytest.mark.parametrize("ext", [(1, 1, 1), (2, 30, 62), (70, 31, 63), (65, 61, 125), (131, 29, 200)])
 def test_jacobi3d_two_level_blocking(cuda_ready, kernel, ext):
-    """K4b (two time levels per pass) against the oracle and against K4
+    """K4c / K4b (two time levels per pass) against the oracle and against K4
     (depth 1) across frame edges (62 x 30 useful per block, 64-plane
     segments), odd step counts (2-level launches + one single step) and both
     FMA contracts."""
@@ -460,6 +460,19 @@ def test_cli_tiles_threads_life_lcs(cuda_ready, tmp_path):
     rng = np.random.default_rng(0)
     a, b = rng.integers(0, 4, 300, dtype=np.int32), rng.integers(0, 4, 200, dtype=np.int32)
     assert int(rows[3][11], 16) == int(rows[4][11], 16) == npo.lcs_length(a, b)
+
+
+def test_jacobi3d_cpasync_fallback(cuda_ready):
+    """K4b, the cp.async-staged two-level 3D kernel K4c (TMA) falls back to
+    when a block cannot be a tensor map, selected with TVS_J3D=cpasync (read
+    once per process): bit-exact against the oracle."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, TVS_J3D="cpasync")
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "j3d_cpasync_check.py")],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
 
 
 @pytest.mark.parametrize("cluster", [1, 2, 4, 8])

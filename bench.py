@@ -203,6 +203,11 @@ def dp_instr_per_update(cfg, fma=None):
     policy = fma or config.current().fma
     pow2 = all(c == 0.0 or math.frexp(abs(c))[0] == 0.5 for c in cs)
     fused = policy == "allow" or (policy == "exact" and pow2)
+    if fused and pow2 and len(cfg["extents"]) == 2 and os.environ.get("TVS_J2D_SCALED", "1") != "0":
+        # K3's scaled power-of-two taps: the first tap is free, k - 1 DFMAs,
+        # and one rescaling DMUL per stored value (1 / depth per update)
+        depth = config.current().depth or 8
+        return k - 1 + 1.0 / depth, fused
     return (k if fused else 2 * k - 1), fused
 
 

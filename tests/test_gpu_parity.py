@@ -568,7 +568,7 @@ def test_pipelined_drop_in_repeated_calls(cuda_ready):
 
 @pytest.mark.parametrize("order", ["lexicographic", "reference"])
 def test_gs2d_lane_ring_slot_reuse(cuda_ready, order):
-    """K6v2 hands rows between CTAs through an L2 ring of 320 slots: narrow
+    """K6v3 hands rows between CTAs through an L2 ring of 320 slots: narrow
     grids (short CTA lifetimes, > 320 CTAs) reuse slots while older CTAs are
     still running.  A consumer may read a reused slot only after its producer
     took it over from the previous consumer (regression: stale cells read as
@@ -588,6 +588,25 @@ def test_gs2d_lane_ring_slot_reuse(cuda_ready, order):
         plan.download(out.data, out.offset)
         plan.close()
         assert np.array_equal(out.interior, want), (rows, cols, steps, "plan")
+
+
+@pytest.mark.parametrize("order", ["lexicographic", "reference"])
+def test_gs2d_lane_capacities(cuda_ready, order):
+    """K6v3 packs lr = sweeps-per-pass (rounded up to even) lanes per group
+    into warps and picks a lane capacity of 32 / 64 / 102 / 128: sweep counts
+    on both sides of every capacity, odd counts (one idle lane), more than
+    128 sweeps (balanced passes), grids narrower than a loader block and with
+    fewer rows than a CTA's groups -- bit-exact against the oracle."""
+    for kernel in ("gs2d9p", "gs2d"):
+        spec = get(kernel).spec
+        for ext, steps in [((9, 3), 2), ((3, 70), 31), ((40, 33), 33), ((70, 50), 63), ((33, 120), 64),
+                           ((50, 40), 65), ((45, 260), 101), ((120, 45), 102), ((60, 60), 103), ((30, 90), 128),
+                           ((64, 64), 129), ((40, 70), 200), ((2, 2), 257)]:
+            g = Grid.random(ext, seed=ext[0] + steps, boundary=-0.5 if steps % 2 else 0.0)
+            sp = spec_for(kernel, g.boundary)
+            want = cref.scalar_reference(sp, g, steps, order=order).interior
+            got = execute(sp, g, steps, order=order).interior
+            assert np.array_equal(got, want), (kernel, ext, steps)
 
 
 def test_staged_pageable_uploads(cuda_ready):

@@ -58,7 +58,17 @@
 
 namespace tvs {
 namespace gsl {
-constexpr int kLam = 2;          // group lag (iterations)
+#ifndef GSL_SLACK
+#define GSL_SLACK 0
+#endif
+// Group lag and lane skew: 2 is the dependence graph's own slope (a value is
+// read the iteration after it is produced); 3 gives every cross-lane value a
+// spare iteration, so the compute warps load the next iteration's inputs
+// before the barrier and the shared-memory round trip leaves the
+// per-iteration critical path (one more column of pipeline per lane / group).
+constexpr int kLam = 2 + GSL_SLACK;  // group lag (iterations)
+constexpr int kSk = 2 + GSL_SLACK;   // lane skew (columns)
+constexpr bool kPrefetch = GSL_SLACK > 0;
 constexpr int kB = 2;            // every lane starts >= 2 columns left of column 0
 constexpr int kR = 16;           // smem ring rows (iterations, power of two; the unroll of the compute loop)
 #ifndef GSL_BLK
@@ -69,12 +79,12 @@ constexpr int kR = 16;           // smem ring rows (iterations, power of two; th
 #endif
 constexpr int kBlk = GSL_BLK;    // iterations per loader block
 constexpr int kDist = GSL_DIST;  // blocks requested ahead of their hand-over (L2 / HBM latency)
-constexpr int kStg = kDist + 1;  // phantom staging slots
+constexpr int kProRows = GSL_SLACK > 0 ? 12 : 8;  // phantom / lane -1 rows handed over before iteration 0
+constexpr int kStg = kDist + 1 > kProRows / kBlk ? kDist + 1 : kProRows / kBlk;  // phantom staging slots
 #ifndef GSL_NL
 #define GSL_NL 0
 #endif
 constexpr int kLR = 32;          // lane -1 staging ring (iterations), power of two
-constexpr int kProRows = 8;      // phantom / lane -1 rows handed over before iteration 0 (rows -8..-1)
 constexpr int kNumSlots = 320;   // global ring slots (CTA boundaries in flight) >= resident CTAs
 // sentinel of an unwritten global-ring cell: a signalling NaN (quiet bit
 // clear), which no arithmetic result can be
@@ -105,7 +115,7 @@ struct Cfg {
   static constexpr size_t Smem =
       sizeof(double) * ((size_t)Rings * (kR * S + 16) + (size_t)Rings * kLR + (size_t)kStg * kBlk * RowCells);
   static constexpr int MinB = 2 * (Smem + 1024) <= 227 * 1024 ? 2 : 1;  // CTAs per SM the shared memory allows
-  static constexpr int Back = REF ? 2 * kLam + 1 : kLam + 1;  // deepest ring read behind m
+  static constexpr int Back = REF ? kSk + 2 * kLam - 1 : kSk + kLam - 1;  // deepest ring read behind m
   // ring row i is last read in iteration i + Back and overwritten by row
   // i + kR: the loader may write block b once block b - Ahead is complete
   static constexpr int Ahead = (kR - Back) / kBlk < 3 ? (kR - Back) / kBlk : 3;  // <= 3: four barriers per direction
@@ -222,7 +232,9 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
   double* const lm1 = smem + (size_t)kRings * (kR * kS + 16);  // lane -1 staging [ring][kLR]
   double* const stg = lm1 + kRings * kLR;                 // phantom staging [kStg][kBlk][RowCells]
   __shared__ int s_ticket;
-  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  // the warp index through a shuffle: the compiler then knows it is warp-uniform
+  // (uniform branches and uniform registers for the role split)
+  const int lane = threadIdx.x & 31, wi = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lr = p.lr, nunits = kG * lr;
   const int ncomp = (nunits + 31) >> 5;  // compute warps; the loader is warp ncomp
   const int cthreads = ncomp * 32;
@@ -272,7 +284,7 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
     const int unit = live ? (int)threadIdx.x : nunits - 1;
     const int g = unit / lr, l = unit - g * lr;
     const int d = d0 + g, row = d - l;
-    const int col0 = -kLam * g - 2 * l - kB;  // my column at iteration 0
+    const int col0 = -kLam * g - kSk * l - kB;  // my column at iteration 0
     double* const ring_me = smem + (size_t)(g + kPh) * rstride;
     const double* const ring_up = ring_me - rstride;
     const double* const ring_up2 = ring_me - 2 * rstride;
@@ -288,6 +300,14 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
     double nw = bnd, nn = bnd, ne = bnd, ww = bnd, cc = bnd, ee = bnd, sw = bnd, ss = bnd, se = bnd;
     double out = bnd;
     bar_sync(kBarPro, cthreads + 32 * kNL);  // prologue rows handed over
+    double ne_p = bnd, e_p = bnd, se_p = bnd, rn_p = bnd;  // inputs of the next iteration (kPrefetch)
+    if constexpr (kPrefetch) {
+      ne_p = ring_up[((-(kLam - 1)) & (kR - 1)) * kS + 2 + l];
+      e_p = ring_up[((-(kSk + kLam - 1)) & (kR - 1)) * kS + 1 + l];
+      se_p = ring_me[((-(kSk - 1)) & (kR - 1)) * kS + 1 + l];
+      if constexpr (REF) rn_p = ring_up2[((-(kSk + 2 * kLam - 1)) & (kR - 1)) * kS + 1 + l];
+    }
+    (void)ne_p, (void)e_p, (void)se_p, (void)rn_p;
 #ifdef GSL_TRACE
     if (wi == 0 && lane == 0 && n < 8192) g_gsl_trace[n][1] = gsl_now();
 #endif
@@ -301,18 +321,30 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
           // every input is a shared-memory ring read at a compile-time offset
           // (slot 1 of a ring = its lane -1, a grid row, copied in by the
           // loader); no shuffles, no per-lane special cases
-          const int r1 = ((u - 1) & (kR - 1)) * kS, r3 = ((u - kLam - 1) & (kR - 1)) * kS;
-          const double ne_new = ring_up[r1 + 2 + l];  // group d-1, lane l, iteration m-1
-          const double e_new = ring_up[r3 + 1 + l];   // group d-1, lane l-1, iteration m-3 (lane 0: grid row d)
-          const double se_new = ring_me[r1 + 1 + l];  // my group, lane l-1, iteration m-1 (lane 0: grid row d+1)
-          nw = nn; nn = ne; ne = ne_new;
-          cc = ee; ee = e_new;
-          sw = ss; ss = se; se = se_new;
-          double ne_use = ne;
-          if constexpr (REF) {
-            // group d-2, lane l-1, iteration m-5 (lane 0: grid row d-1)
-            const int r5 = ((u - 2 * kLam - 1) & (kR - 1)) * kS;
-            ne_use = ring_up2[r5 + 1 + l];
+          // ring rows behind m: NE kLam - 1, SE kSk - 1, E kSk + kLam - 1 (REF NE: kSk + 2 kLam - 1)
+          constexpr int dNE = kLam - 1, dSE = kSk - 1, dE = kSk + kLam - 1;
+          [[maybe_unused]] constexpr int dRN = kSk + 2 * kLam - 1;
+          double ne_use;
+          if constexpr (kPrefetch) {
+            // this iteration's inputs were loaded before the previous barrier;
+            // the next iteration's (rows <= m - 1, visible since that barrier) go out now
+            nw = nn; nn = ne; ne = ne_p;
+            cc = ee; ee = e_p;
+            sw = ss; ss = se; se = se_p;
+            ne_use = REF ? rn_p : ne;
+            ne_p = ring_up[((u + 1 - dNE) & (kR - 1)) * kS + 2 + l];
+            e_p = ring_up[((u + 1 - dE) & (kR - 1)) * kS + 1 + l];
+            se_p = ring_me[((u + 1 - dSE) & (kR - 1)) * kS + 1 + l];
+            if constexpr (REF) rn_p = ring_up2[((u + 1 - dRN) & (kR - 1)) * kS + 1 + l];
+          } else {
+            const double ne_new = ring_up[((u - dNE) & (kR - 1)) * kS + 2 + l];  // group d-1, lane l
+            const double e_new = ring_up[((u - dE) & (kR - 1)) * kS + 1 + l];    // group d-1, lane l-1 (lane 0: grid row d)
+            const double se_new = ring_me[((u - dSE) & (kR - 1)) * kS + 1 + l];  // my group, lane l-1 (lane 0: grid row d+1)
+            nw = nn; nn = ne; ne = ne_new;
+            cc = ee; ee = e_new;
+            sw = ss; ss = se; se = se_new;
+            ne_use = ne;
+            if constexpr (REF) ne_use = ring_up2[((u - dRN) & (kR - 1)) * kS + 1 + l];  // group d-2, lane l-1 (lane 0: grid row d-1)
           }
           const double v = gsl_taps<MASK>(p.w, nw, nn, ne_use, ww, cc, ee, sw, ss, se);
           bool inside = true;
@@ -382,7 +414,7 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
     constexpr int kSubR = kBlk / kNL;
     const int lw_r0 = lw * kSubR;
     const bool lm_on = lw == 0 && lane < kRings * kBlk, lm_row = lm_r >= 0 && lm_r < e0;
-    const int lm_c0 = lm_o - kLam * lm_g + 2 - kB;  // grid column of row 4q + lm_o at q = 0
+    const int lm_c0 = lm_o - kLam * lm_g + kSk - kB;  // grid column of row 4q + lm_o at q = 0
     const double* const lm_src = p.a + (long long)lm_r * p.s0;
     auto rows_in_ring = [&](int i) { return has_up && i + kLam * kG < m_end; };
     // a ring cell only this lane stores in every finish() (read back before the hand-over):
@@ -634,7 +666,7 @@ static int gsl_launch(GslArgs a, int64_t steps, int64_t per, cudaStream_t s, con
   a.lr = (int)std::min<int64_t>((per + 1) / 2 * 2, LC);  // lanes in use per group (even: 16-byte hand-off pieces)
 #endif
   // the last group's lanes reach column e1 (the boundary the consumer reads)
-  const int m_need = a.e1 + kLam * (C::G - 1) + 2 * (a.lr - 1) + kB + 2;
+  const int m_need = a.e1 + kLam * (C::G - 1) + kSk * (a.lr - 1) + kB + 2;
   a.m_end = (m_need + kR - 1) / kR * kR;
   const size_t cells = (size_t)kNumSlots * a.m_end * C::RowCells;
   const size_t ctrl_bytes = sizeof(int) * 2 * kNumSlots + 64;

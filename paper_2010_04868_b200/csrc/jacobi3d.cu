@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include <cuda.h>
 
@@ -382,10 +383,20 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tb_kernel(const double*
 //     of 36 LDS.64), consumed row by row so the window is never held whole;
 //   * one CTA barrier per plane: level 2 runs one plane behind level 1.
 constexpr int kPW = kTBW + 2;                 // staged box width (frame + ring)
-constexpr int kPR = kTBH + 2;                 // staged box rows
-constexpr int kPSlot = (kPR * kPW * 8 + 127) / 128 * 128 / 8;  // slot pitch (elements), 128-byte multiple
-constexpr unsigned kPBytes = kPR * kPW * 8;   // bytes one plane copy delivers
-constexpr size_t kPSmem = (size_t)5 * kPSlot * sizeof(double) + 3 * sizeof(unsigned long long) + 128;
+// NW warps of kRY frame rows each: 8 (64 x 32 frame, two CTAs per SM, K4b's
+// frame; the default) or 16 (64 x 64, one CTA per SM: 62 x 62 useful of
+// 64 x 64 instead of 62 x 30 of 64 x 32; slower, see jacobi3d_blocked2)
+template <int NW>
+struct TmaCfg {
+  static constexpr int H = NW * kRY;        // frame rows
+  static constexpr int OY = H - 2;          // useful output rows per block
+  static constexpr int R = H + 2;           // staged box rows
+  static constexpr int Slot = (R * kPW * 8 + 127) / 128 * 128 / 8;  // slot pitch (elements), 128-byte multiple
+  static constexpr unsigned Bytes = R * kPW * 8;                   // bytes one plane copy delivers
+  static constexpr size_t Smem = (size_t)5 * Slot * sizeof(double) + 3 * sizeof(unsigned long long) + 128;
+  static constexpr int Threads = 32 * NW;
+  static constexpr int MinB = NW <= 8 ? 2 : 1;
+};
 
 template <unsigned MASK, int G>
 constexpr int first_tap() {
@@ -443,11 +454,13 @@ __device__ __forceinline__ void pair_level(const double* __restrict__ win, doubl
     for (int r = 0; r < kRY; ++r) A[h][r] = An[h][r];
 }
 
-template <unsigned MASK, bool FMA, bool MIR>
-__global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+template <unsigned MASK, bool FMA, bool MIR, int NW>
+__global__ void __launch_bounds__(TmaCfg<NW>::Threads, TmaCfg<NW>::MinB) jacobi3d_tma_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                     double* __restrict__ dst, Geo g, int64_t origin,
                                                                     Coeff27 cf, double bnd, int64_t plo,
                                                                     int64_t phi, int seg, Mirror mir) {
+  constexpr int kPSlot = TmaCfg<NW>::Slot, kFH = TmaCfg<NW>::H, kFOY = TmaCfg<NW>::OY;
+  constexpr unsigned kPBytes = TmaCfg<NW>::Bytes;
   extern __shared__ unsigned char tma_smem_raw[];
   // 128-byte aligned slots (TMA destination alignment)
   const unsigned raw = smaddr(tma_smem_raw);
@@ -456,7 +469,7 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tma_kernel(const __grid
   unsigned long long* const full = reinterpret_cast<unsigned long long*>(l1 + 2 * kPSlot);
   const int lane = threadIdx.x, w = threadIdx.y;
   const int tid = w * 32 + lane;
-  const int64_t x0 = (int64_t)blockIdx.x * kTBOX, y0 = (int64_t)blockIdx.y * kTBOY;
+  const int64_t x0 = (int64_t)blockIdx.x * kTBOX, y0 = (int64_t)blockIdx.y * kFOY;
   const int64_t p0 = plo + (int64_t)blockIdx.z * seg;
   const int64_t p1 = min(p0 + seg, phi);  // level-2 outputs [p0, p1)
   if (tid == 0) {
@@ -477,7 +490,7 @@ __global__ void __launch_bounds__(kThreads3, 2) jacobi3d_tma_kernel(const __grid
       const int64_t y = y0 - 1 + i, x = x0 - 1 + j;
       const bool dom = y >= 0 && y < g.e1 && x >= 0 && x < g.e2;
       in_dom |= (dom ? 1u : 0u) << (h * kRY + r);
-      store_ok |= (dom && i >= 1 && i < kTBH - 1 && j >= 1 && j < kTBW - 1 ? 1u : 0u) << (h * kRY + r);
+      store_ok |= (dom && i >= 1 && i < kFH - 1 && j >= 1 && j < kTBW - 1 ? 1u : 0u) << (h * kRY + r);
     }
   const bool all_dom = in_dom == 0xFFu;
 
@@ -656,28 +669,29 @@ static bool tma_usable(const tvs_geometry& g, const double* src) {
          s1 < ((int64_t)1 << 31) && s0 / s1 < ((int64_t)1 << 31) && g.alloc_elems / s0 < ((int64_t)1 << 31);
 }
 
-template <unsigned MASK, bool FMA>
+template <unsigned MASK, bool FMA, int NW>
 static int launch_tma(const Geo& geo, const tvs_geometry& g, const double* src, double* dst, const Coeff27& cf,
                       double bnd, cudaStream_t s, int64_t plo, int64_t phi, int seg, const Mirror& mir) {
+  using T = TmaCfg<NW>;
   // the whole allocation as a (pitch, rows, planes) tensor; one box = the
   // 66 x 34 cells a block needs of one plane
   CUtensorMap tm;
   const cuuint64_t dims[3] = {(cuuint64_t)g.strides[1], (cuuint64_t)(g.strides[0] / g.strides[1]),
                               (cuuint64_t)(g.alloc_elems / g.strides[0])};
   const cuuint64_t strides[2] = {(cuuint64_t)g.strides[1] * 8, (cuuint64_t)g.strides[0] * 8};
-  const cuuint32_t box[3] = {(cuuint32_t)kPW, (cuuint32_t)kPR, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)kPW, (cuuint32_t)T::R, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult rc = encode_tiled_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(src), dims, strides,
                                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (rc != CUDA_SUCCESS) return fail(TVS_ERR_CUDA, "jacobi3d: cuTensorMapEncodeTiled failed");
   const bool mirrored = mir.p[0] != nullptr || mir.p[1] != nullptr;
-  auto kern = mirrored ? jacobi3d_tma_kernel<MASK, FMA, true> : jacobi3d_tma_kernel<MASK, FMA, false>;
-  TVS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmem));
-  const dim3 block(kTX3, kTYT);
-  const dim3 grid((unsigned)((geo.e2 + kTBOX - 1) / kTBOX), (unsigned)((geo.e1 + kTBOY - 1) / kTBOY),
+  auto kern = mirrored ? jacobi3d_tma_kernel<MASK, FMA, true, NW> : jacobi3d_tma_kernel<MASK, FMA, false, NW>;
+  TVS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::Smem));
+  const dim3 block(kTX3, NW);
+  const dim3 grid((unsigned)((geo.e2 + kTBOX - 1) / kTBOX), (unsigned)((geo.e1 + T::OY - 1) / T::OY),
                   (unsigned)((phi - plo + seg - 1) / seg));
-  kern<<<grid, block, kPSmem, s>>>(tm, dst, geo, g.origin, cf, bnd, plo, phi, seg, mir);
+  kern<<<grid, block, T::Smem, s>>>(tm, dst, geo, g.origin, cf, bnd, plo, phi, seg, mir);
   TVS_LAUNCHED("jacobi3d_tma_kernel");
   return TVS_OK;
 }
@@ -696,12 +710,26 @@ int jacobi3d_blocked2(const tvs_stencil& st, const tvs_geometry& g, const double
   // the kernel keeps its staging offsets within a plane in 32 bits
   if (geo.s0 >= ((int64_t)1 << 31) - 4 * geo.s1) return fail(TVS_ERR_UNSUPPORTED, "jacobi3d_blocked2: plane of 2^31 elements");
   if (tma_usable(g, src)) {
-    if (mask == kBox27)
-      return fma ? launch_tma<kBox27, true>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m)
-                 : launch_tma<kBox27, false>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m);
-    if (mask == kStar7)
-      return fma ? launch_tma<kStar7, true>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m)
-                 : launch_tma<kStar7, false>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m);
+    // frame rows: 32 (two 8-warp CTAs per SM); TVS_J3D_FRAME=64 selects the
+    // 64 x 64 frame (one 16-warp CTA per SM, 11% instead of 14% overlap), which
+    // measured slower -- config 5: 238.6 / 366.9 against 258.8 / 389.3 GSt/s
+    // (bit-exact / fma allow): one CTA per SM leaves nothing to run while its
+    // 16 warps meet at the plane barrier
+    static const int frame_env = [] {
+      const char* e = std::getenv("TVS_J3D_FRAME");
+      return e ? std::atoi(e) : 0;
+    }();
+    const bool tall = frame_env == 64;
+    auto go = [&](auto mask_tag, auto fma_tag) -> int {
+      constexpr unsigned M = decltype(mask_tag)::value;
+      constexpr bool F = decltype(fma_tag)::value;
+      return tall ? launch_tma<M, F, 16>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m)
+                  : launch_tma<M, F, 8>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m);
+    };
+    using Box = std::integral_constant<unsigned, kBox27>;
+    using Star = std::integral_constant<unsigned, kStar7>;
+    if (mask == kBox27) return fma ? go(Box{}, std::true_type{}) : go(Box{}, std::false_type{});
+    if (mask == kStar7) return fma ? go(Star{}, std::true_type{}) : go(Star{}, std::false_type{});
   }
   if (mask == kBox27)
     return fma ? launch_tb<kBox27, true>(geo, g, src, dst, cf, st.boundary, s, plo, phi, seg, m)

@@ -1,8 +1,9 @@
-"""K4b (the cp.async-staged two-level 3D kernel) parity: run with
-TVS_J3D=cpasync, read once per process -- K4c (TMA-staged) is the default
-whenever the block can be described by a tensor map, so K4b only runs as its
-fallback.  Run by tests/test_gpu_parity.py::test_jacobi3d_cpasync_fallback;
-exits non-zero on any mismatch."""
+"""Parity of the two-level 3D kernels in a mode fixed per process by the
+environment: TVS_J3D=cpasync (K4b, the cp.async-staged kernel K4c falls back
+to when a block cannot be a tensor map) or TVS_J3D_FRAME=32 / 64 (K4c's frame
+height; 32 by default).  Run by
+tests/test_gpu_parity.py::test_jacobi3d_modes; exits non-zero on any
+mismatch."""
 import os
 import sys
 
@@ -17,10 +18,10 @@ from paper_2010_04868_b200.catalog import get  # noqa: E402
 from paper_2010_04868_b200.kernels._common import execute  # noqa: E402
 import dataclasses  # noqa: E402
 
-assert os.environ.get("TVS_J3D") == "cpasync"
+assert os.environ.get("TVS_J3D") == "cpasync" or os.environ.get("TVS_J3D_FRAME") in ("32", "64")
 bad = 0
 for kernel in ("heat3d", "jac3d27p"):
-    for ext in ((1, 1, 1), (2, 30, 62), (70, 31, 63), (65, 61, 125), (131, 29, 200)):
+    for ext in ((1, 1, 1), (2, 30, 62), (70, 31, 63), (65, 61, 125), (131, 29, 200), (9, 63, 62), (20, 130, 70)):
         g = Grid.random(ext, seed=sum(ext), boundary=0.375)
         spec = dataclasses.replace(get(kernel).spec, boundary=g.boundary)
         want = cref.scalar_reference(spec, g, 7)

@@ -462,15 +462,17 @@ def test_cli_tiles_threads_life_lcs(cuda_ready, tmp_path):
     assert int(rows[3][11], 16) == int(rows[4][11], 16) == npo.lcs_length(a, b)
 
 
-def test_jacobi3d_cpasync_fallback(cuda_ready):
-    """K4b, the cp.async-staged two-level 3D kernel K4c (TMA) falls back to
-    when a block cannot be a tensor map, selected with TVS_J3D=cpasync (read
-    once per process): bit-exact against the oracle."""
+@pytest.mark.parametrize("mode", [{"TVS_J3D": "cpasync"}, {"TVS_J3D_FRAME": "32"}, {"TVS_J3D_FRAME": "64"}])
+def test_jacobi3d_modes(cuda_ready, mode):
+    """The two-level 3D kernels in every mode (read once per process): K4b,
+    the cp.async-staged kernel K4c (TMA) falls back to when a block cannot be
+    a tensor map, and K4c with 64 x 32 (default) and 64 x 64 frames --
+    bit-exact against the oracle across frame edges."""
     import subprocess
     import sys
 
-    env = dict(os.environ, TVS_J3D="cpasync")
-    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "j3d_cpasync_check.py")],
+    env = dict(os.environ, **mode)
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "j3d_mode_check.py")],
                        env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
 

@@ -208,6 +208,9 @@ def dp_instr_per_update(cfg, fma=None):
         # and one rescaling DMUL per stored value (1 / depth per update)
         depth = config.current().depth or 8
         return k - 1 + 1.0 / depth, fused
+    if fused and pow2 and len(cfg["extents"]) == 1 and os.environ.get("TVS_J1D_SCALED", "1") != "0":
+        depth = config.current().depth or 64  # K2: the same scheme, plus one pin-scale DMUL per step and lane
+        return k - 1 + 1.0 / depth + 1.0 / 32, fused
     return (k if fused else 2 * k - 1), fused
 
 

@@ -17,6 +17,8 @@
 // kernel is FP64-issue bound: 5 DP ops / update unfused, 3 with the exact
 // power-of-two FMA form (heat1d: 0.25/0.5/0.25).
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -32,21 +34,28 @@ constexpr int kP1 = J1D_P;          // points per lane
 constexpr int kMaxDepth1 = 2 * J1D_DEPTH;  // deepest block a launch accepts
 constexpr int kWarps1 = 8;          // warps per block
 
-template <unsigned MASK, bool FMA>
+// SC (scaled power-of-two taps, as K3's): w holds w_k / w_first, all powers of
+// two, and the values of level s are carried divided by w_first^s: the first
+// tap is the input itself and every other tap one DFMA whose product is exact
+// -- bit for bit the reference's separately rounded w*v then +acc, because
+// scaling by a power of two commutes with rounding (barring under/overflow).
+// heat1d: 2 FP64 instructions per update instead of 3.
+template <unsigned MASK, bool FMA, bool SC>
 __device__ __forceinline__ double upd1(double l, double c, double r, const double w[3]) {
   double acc = 0.0;
   bool first = true;
-  if constexpr (MASK & 1u) { acc = tap_first(w[0], l); first = false; }
-  if constexpr (MASK & 2u) { acc = first ? tap_first(w[1], c) : tap_next<FMA>(w[1], c, acc); first = false; }
-  if constexpr (MASK & 4u) { acc = first ? tap_first(w[2], r) : tap_next<FMA>(w[2], r, acc); }
+  if constexpr (MASK & 1u) { acc = SC ? l : tap_first(w[0], l); first = false; }
+  if constexpr (MASK & 2u) { acc = first ? (SC ? c : tap_first(w[1], c)) : tap_next<FMA || SC>(w[1], c, acc); first = false; }
+  if constexpr (MASK & 4u) { acc = first ? (SC ? r : tap_first(w[2], r)) : tap_next<FMA || SC>(w[2], r, acc); }
   return acc;
 }
 
-template <unsigned MASK, bool FMA>
+template <unsigned MASK, bool FMA, bool SC>
 __global__ void __launch_bounds__(kWarps1 * 32) jacobi1d_kernel(const double* __restrict__ src,
                                                                 double* __restrict__ dst, int64_t n, int depth,
                                                                 double w0, double w1, double w2, double bnd,
-                                                                int64_t rlo, int64_t rhi) {
+                                                                int64_t rlo, int64_t rhi, double inv_first,
+                                                                double out_scale) {
   const double w[3] = {w0, w1, w2};
   const int lane = threadIdx.x & 31;
   const int64_t warp = (int64_t)blockIdx.x * kWarps1 + (threadIdx.x >> 5);
@@ -66,6 +75,7 @@ __global__ void __launch_bounds__(kWarps1 * 32) jacobi1d_kernel(const double* __
   }
   const bool any_out = __any_sync(0xffffffffu, out_mask != 0);
 
+  double pin = bnd;  // the boundary at the current level's scale
   for (int s = 0; s < depth; ++s) {
     const double left = __shfl_up_sync(0xffffffffu, v[kP1 - 1], 1);
     const double right = __shfl_down_sync(0xffffffffu, v[0], 1);
@@ -74,13 +84,14 @@ __global__ void __launch_bounds__(kWarps1 * 32) jacobi1d_kernel(const double* __
     for (int m = 0; m < kP1; ++m) {
       const double cur = v[m];
       const double nxt = m + 1 < kP1 ? v[m + 1] : right;
-      v[m] = upd1<MASK, FMA>(prev, cur, nxt, w);
+      v[m] = upd1<MASK, FMA, SC>(prev, cur, nxt, w);
       prev = cur;
     }
+    if constexpr (SC) pin = __dmul_rn(pin, inv_first);  // exact: a power of two
     if (any_out) {
 #pragma unroll
       for (int m = 0; m < kP1; ++m)
-        if (out_mask >> m & 1u) v[m] = bnd;
+        if (out_mask >> m & 1u) v[m] = pin;
     }
   }
 
@@ -88,7 +99,7 @@ __global__ void __launch_bounds__(kWarps1 * 32) jacobi1d_kernel(const double* __
 #pragma unroll
   for (int m = 0; m < kP1; ++m) {
     const int64_t x = xl + m;
-    if (x >= lo && x < hi && x >= rlo && x < rhi) dst[x] = v[m];
+    if (x >= lo && x < hi && x >= rlo && x < rhi) dst[x] = SC ? __dmul_rn(v[m], out_scale) : v[m];
   }
 }
 
@@ -108,13 +119,19 @@ static int slots1d(const tvs_stencil& st, double w[3]) {
   return (int)mask;
 }
 
+// mode 0: unfused taps, 1: fused (FMA), 2: scaled power-of-two taps (SC)
 template <unsigned MASK>
-static void launch1d(bool fma, unsigned blocks, cudaStream_t s, const double* src, double* dst, int64_t n, int depth,
-                     const double w[3], double bnd, int64_t rlo, int64_t rhi) {
-  if (fma)
-    jacobi1d_kernel<MASK, true><<<blocks, kWarps1 * 32, 0, s>>>(src, dst, n, depth, w[0], w[1], w[2], bnd, rlo, rhi);
+static void launch1d(int mode, unsigned blocks, cudaStream_t s, const double* src, double* dst, int64_t n, int depth,
+                     const double w[3], double bnd, int64_t rlo, int64_t rhi, double inv_first, double out_scale) {
+  if (mode == 2)
+    jacobi1d_kernel<MASK, true, true><<<blocks, kWarps1 * 32, 0, s>>>(src, dst, n, depth, w[0], w[1], w[2], bnd, rlo, rhi,
+                                                                       inv_first, out_scale);
+  else if (mode == 1)
+    jacobi1d_kernel<MASK, true, false><<<blocks, kWarps1 * 32, 0, s>>>(src, dst, n, depth, w[0], w[1], w[2], bnd, rlo,
+                                                                        rhi, 1.0, 1.0);
   else
-    jacobi1d_kernel<MASK, false><<<blocks, kWarps1 * 32, 0, s>>>(src, dst, n, depth, w[0], w[1], w[2], bnd, rlo, rhi);
+    jacobi1d_kernel<MASK, false, false><<<blocks, kWarps1 * 32, 0, s>>>(src, dst, n, depth, w[0], w[1], w[2], bnd, rlo,
+                                                                         rhi, 1.0, 1.0);
 }
 
 int jacobi1d_default_depth() { return J1D_DEPTH; }
@@ -139,14 +156,43 @@ int jacobi1d_blocked(const tvs_stencil& st, const tvs_geometry& g, const double*
   const unsigned blocks = (unsigned)((warps + kWarps1 - 1) / kWarps1);
   const double* s0 = src + g.origin;
   double* d0 = dst + g.origin;
+  // Scaled taps when every coefficient is a power of two (the fused form is
+  // already exact then).  The carried values grow by 1 / |w_first| per step
+  // (heat1d: 4^depth, 2^128 at depth 64), so |values| must stay below
+  // 2^(1023 - depth log2(1 / |w_first|)) -- the caveat of K3's scaled taps;
+  // TVS_J1D_SCALED=0 disables it.
+  static const bool sc_off = [] {
+    const char* e = getenv("TVS_J1D_SCALED");
+    return e && atoi(e) == 0;
+  }();
+  int mode = fma ? 1 : 0;
+  double inv_first = 1.0, out_scale = 1.0;
+  if (fma && !sc_off && coeffs_power_of_two(st)) {
+    const double wf = w[__builtin_ctz((unsigned)mask)];
+    int ex0;
+    std::frexp(wf, &ex0);
+    bool ok = std::abs(ex0 - 1) * depth <= 300;
+    for (int k = 0; k < 3 && ok; ++k) {
+      if (w[k] == 0.0) continue;
+      int ex;
+      std::frexp(w[k], &ex);
+      ok = std::abs(ex - ex0) <= 60;
+    }
+    if (ok) {
+      mode = 2;
+      inv_first = 1.0 / wf;
+      for (int k = 0; k < 3; ++k) w[k] /= wf;                   // exact: powers of two
+      for (int l = 0; l < depth; ++l) out_scale *= wf;          // exact
+    }
+  }
   switch (mask) {
-    case 1: launch1d<1>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
-    case 2: launch1d<2>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
-    case 3: launch1d<3>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
-    case 4: launch1d<4>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
-    case 5: launch1d<5>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
-    case 6: launch1d<6>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
-    default: launch1d<7>(fma, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi); break;
+    case 1: launch1d<1>(mode, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi, inv_first, out_scale); break;
+    case 2: launch1d<2>(mode, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi, inv_first, out_scale); break;
+    case 3: launch1d<3>(mode, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi, inv_first, out_scale); break;
+    case 4: launch1d<4>(mode, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi, inv_first, out_scale); break;
+    case 5: launch1d<5>(mode, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi, inv_first, out_scale); break;
+    case 6: launch1d<6>(mode, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi, inv_first, out_scale); break;
+    default: launch1d<7>(mode, blocks, s, s0, d0, n, depth, w, st.boundary, rlo, rhi, inv_first, out_scale); break;
   }
   TVS_LAUNCHED("jacobi1d_kernel");
   return TVS_OK;

@@ -1,0 +1,4 @@
+set -x
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_full_size.py tests/test_acceptance_gpu.py -m gpu -x -q -k "1d or heat1d or golden or acceptance or fma or pinned or jacobi1d or config1" 2>&1 | tail -2
+echo "== scaled"; timeout 300 python tools/profile_run.py --config 1 --reps 3 2>&1 | tail -2
+echo "== unscaled"; TVS_J1D_SCALED=0 timeout 300 python tools/profile_run.py --config 1 --reps 3 2>&1 | tail -2

@@ -22,9 +22,13 @@ _ORDER = {"lexicographic": _native.GS_LEXICOGRAPHIC, "reference": _native.GS_REF
 class ExecConfig:
     device: int = 0
     # "exact": fuse multiply-add only for power-of-two coefficient sets, where
-    # the product is exact and the result bit-identical (subnormal products
-    # excepted); "never": always separate mul/add;
-    # "allow": always fuse (tolerance mode, ~1e-15 relative).
+    # the product is exact and the result bit-identical.  The blocked 1D / 2D
+    # Jacobi kernels then carry values scaled by 1 / |first coefficient| per
+    # level of a temporal block (heat1d 4^64, heat2d 8^8): identical bits
+    # unless a value leaves the normal range on the way (|v| beyond ~2^890,
+    # or products / rescaled results that are subnormal), DESIGN.md section 1;
+    # "never": always separate mul/add, unconditionally the reference's
+    # arithmetic; "allow": always fuse (tolerance mode, ~1e-15 relative).
     fma: str = "exact"
     depth: int = 0  # temporal block depth (0 = kernel default)
     algo: str = "auto"

@@ -448,11 +448,15 @@ def untiled_legs(args):
     bandwidth = 16 B x update rate; ncu DRAM bytes per launch in profiles/."""
     hbm_peak, _ = peaks()
     out = {}
+    from paper_2010_04868_b200 import config
+
     for cid, algo, T in ((3, "naive", 20), (5, "auto", 10)):
         c = dict(CONFIGS[cid], T=T)
         try:
             clk = ClockSampler()
-            t, launches = device_time(c, max(2, min(args.steps, 3)), args.warmup, sampler=clk, algo=algo)
+            # depth 1 keeps config 5 on its single-step kernel (K4); the default is the two-level K4c
+            with config.using(depth=1):
+                t, launches = device_time(c, max(2, min(args.steps, 3)), args.warmup, sampler=clk, algo=algo)
             ms = statistics.mean(t)
             v = int(np.prod(c["extents"])) * T / (ms * 1e-3) / 1e9
             out[c["name"]] = {

@@ -99,7 +99,10 @@ struct Cfg {
 #endif
   // groups per CTA (two CTAs per SM).  Config 4 lexicographic, packed lanes,
   // K6v2 loader: G 4 / 5 21.2 / 19.1 ms; without hand-off 12.0 / 11.5 ms
-  static constexpr int G = REF ? 4 : (GSL_G > 0 ? GSL_G : (LC <= 102 ? 5 : 4));
+#ifndef GSL_GREF
+#define GSL_GREF 0
+#endif
+  static constexpr int G = REF ? (GSL_GREF > 0 ? GSL_GREF : 4) : (GSL_G > 0 ? GSL_G : (LC <= 102 ? 5 : 4));
   static constexpr int Ph = REF ? 2 : 1;        // phantom groups (reads reach group d-2 in REF)
   static constexpr int S = LC + 2;              // ring row: [pad][lane -1][lanes 0..LC-1] (16-B aligned lanes)
   static constexpr int Rings = G + Ph;          // ring index = local group + Ph

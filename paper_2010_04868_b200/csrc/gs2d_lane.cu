@@ -102,7 +102,8 @@ struct Cfg {
 #ifndef GSL_GREF
 #define GSL_GREF 0
 #endif
-  static constexpr int G = REF ? (GSL_GREF > 0 ? GSL_GREF : 4) : (GSL_G > 0 ? GSL_G : (LC <= 102 ? 5 : 4));
+  // reference order, config 4: G 4 / 5 18.85 / 17.95 ms
+  static constexpr int G = REF ? (GSL_GREF > 0 ? GSL_GREF : (LC <= 102 ? 5 : 4)) : (GSL_G > 0 ? GSL_G : (LC <= 102 ? 5 : 4));
   static constexpr int Ph = REF ? 2 : 1;        // phantom groups (reads reach group d-2 in REF)
   static constexpr int S = LC + 2;              // ring row: [pad][lane -1][lanes 0..LC-1] (16-B aligned lanes)
   static constexpr int Rings = G + Ph;          // ring index = local group + Ph
@@ -724,7 +725,7 @@ static int gsl_groups(int64_t steps, int order) {
   int64_t per;
   int lc;
   gsl_plan(std::max<int64_t>(steps, 1), &per, &lc);
-  if (order == TVS_GS_REFERENCE) return gsl::Cfg<true, 128>::G;
+  if (order == TVS_GS_REFERENCE) return lc <= 102 ? gsl::Cfg<true, 102>::G : gsl::Cfg<true, 128>::G;
   return lc <= 102 ? gsl::Cfg<false, 102>::G : gsl::Cfg<false, 128>::G;
 }
 // Drop-in pipeline hooks (api.cu gs2d_pipelined): one pass of <= 128 sweeps;

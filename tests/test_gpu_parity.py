@@ -611,6 +611,24 @@ def test_gs2d_lane_capacities(cuda_ready, order):
             assert np.array_equal(got, want), (kernel, ext, steps)
 
 
+def test_pipelined_kernels_repeat_stable(cuda_ready):
+    """Races in the kernels with device-side hand-offs (K6v3's loader /
+    compute barriers and L2 ring, K4c's TMA ring) would show as run-to-run
+    differences: mid-size grids (several CTA waves), ten runs each, every
+    result bit-identical to the first and the first to the oracle."""
+    for kernel, ext, steps, kw in (("gs2d9p", (1500, 2100), 100, {"order": "lexicographic"}),
+                                   ("gs2d9p", (1200, 1700), 100, {"order": "reference"}),
+                                   ("gs2d", (900, 1300), 64, {"order": "reference"}),
+                                   ("jac3d27p", (150, 130, 200), 8, {})):
+        g = Grid.random(ext, seed=7)
+        spec = get(kernel).spec
+        want = cref.scalar_reference(spec, g, steps, **kw).interior
+        first = execute(spec, g, steps, **kw).interior
+        assert np.array_equal(first, want), (kernel, ext)
+        for rep in range(9):
+            assert np.array_equal(execute(spec, g, steps, **kw).interior, first), (kernel, ext, rep)
+
+
 def test_staged_pageable_uploads(cuda_ready):
     """Pageable inputs are staged by the library (csrc/hostcopy.cu: host
     thread pool -> page-locked 32 MiB slots -> DMA per slot): 1D, 2D and 3D

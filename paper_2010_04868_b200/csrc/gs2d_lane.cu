@@ -530,8 +530,11 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
     // the arrival.  A block-scope fence would also wait for this warp's
     // global traffic in flight (the sentinel resets and the cp.async of the
     // next blocks: an L2 round trip per block, which made the loader the
-    // kernel's bottleneck); shared-memory accesses of a warp complete in
-    // order, so reading back the last cell this lane stored is enough.
+    // kernel's bottleneck).  bar.arrive already orders the arriving
+    // thread's earlier accesses for the threads the barrier releases; the
+    // read-back of the last cell this lane stored additionally keeps the
+    // arrival behind the stores in the warp's own instruction stream
+    // (shared-memory accesses of a warp complete in order).
     auto publish = [&](int bar, const double* last_store) {
       unsigned long long echo;
       asm volatile("ld.volatile.shared.b64 %0, [%1];" : "=l"(echo) : "r"(smaddr(last_store)) : "memory");

@@ -466,6 +466,9 @@ def untiled_legs(args):
                 "roofline": {"bound": "hbm", "achieved": v * BYTES_PER_UPDATE, "peak": hbm_peak, "unit": "GB/s",
                              "frac": v * BYTES_PER_UPDATE / hbm_peak},
             }
+            if cid == 5:
+                out[c["name"]]["note"] = ("single-step 27-point box, bit-exact: 53 FP64 instructions per update, so "
+                                          "FP64 issue (ceiling ~351 GSt/s at 1.965 GHz), not HBM, bounds it")
         except Exception as exc:  # report, never hide
             out[c["name"]] = {"error": repr(exc)}
     return out

@@ -79,13 +79,15 @@ constexpr int kR = 16;           // smem ring rows (iterations, power of two; th
 #endif
 constexpr int kBlk = GSL_BLK;    // iterations per loader block
 constexpr int kDist = GSL_DIST;  // blocks requested ahead of their hand-over (L2 / HBM latency)
-constexpr int kProRows = GSL_SLACK > 0 ? 12 : 8;  // phantom / lane -1 rows handed over before iteration 0
-constexpr int kStg = kDist + 1 > kProRows / kBlk ? kDist + 1 : kProRows / kBlk;  // phantom staging slots
+constexpr int kProMax = 12;      // most rows handed over before iteration 0 (Cfg::ProRows)
 #ifndef GSL_NL
 #define GSL_NL 0
 #endif
 constexpr int kLR = 32;          // lane -1 staging ring (iterations), power of two
-constexpr int kNumSlots = 320;   // global ring slots (CTA boundaries in flight) >= resident CTAs
+#ifndef GSL_SLOTS
+#define GSL_SLOTS 320
+#endif
+constexpr int kNumSlots = GSL_SLOTS;  // global ring slots (CTA boundaries in flight) >= resident CTAs
 // sentinel of an unwritten global-ring cell: a signalling NaN (quiet bit
 // clear), which no arithmetic result can be
 constexpr unsigned long long kSent = 0x7FF4DEADBEEF0001ull;
@@ -116,17 +118,23 @@ struct Cfg {
   static_assert(kBlk % NL == 0, "loader warps split a block's rows");
   static constexpr int Threads = (Compute + NL) * 32;
   static constexpr int RowCells = Ph * LC;      // cells of one phantom row (L2 ring and staging pitch)
-  static constexpr size_t Smem =
-      sizeof(double) * ((size_t)Rings * (kR * S + 16) + (size_t)Rings * kLR + (size_t)kStg * kBlk * RowCells);
-  static constexpr int MinB = 2 * (Smem + 1024) <= 227 * 1024 ? 2 : 1;  // CTAs per SM the shared memory allows
   static constexpr int Back = REF ? kSk + 2 * kLam - 1 : kSk + kLam - 1;  // deepest ring read behind m
   // ring row i is last read in iteration i + Back and overwritten by row
   // i + kR: the loader may write block b once block b - Ahead is complete
   static constexpr int Ahead = (kR - Back) / kBlk < 3 ? (kR - Back) / kBlk : 3;  // <= 3: four barriers per direction
   static_assert(Ahead >= 2, "the loader must be able to run a block ahead");
-  static_assert(kProRows >= Back + 1 && kProRows % kBlk == 0, "prologue rows");
+  // phantom / lane -1 rows handed over before iteration 0: the rows the first
+  // iterations read behind them, in whole blocks (4 lexicographic, 8 reference order)
+  static constexpr int ProRows = (Back + 1 + kBlk - 1) / kBlk * kBlk;
+  static_assert(ProRows <= kProMax && kLam * G >= ProRows, "prologue rows must be rows the producer hands over");
+  static constexpr int Stg = kDist + 1 > ProRows / kBlk ? kDist + 1 : ProRows / kBlk;  // phantom staging slots
+  static constexpr size_t Smem =
+      sizeof(double) * ((size_t)Rings * (kR * S + 16) + (size_t)Rings * kLR + (size_t)Stg * kBlk * RowCells);
+  // CTAs per SM the shared memory (and 2048 threads) allow, at most 3
+  static constexpr int MinB = (3 * (Smem + 1024) <= 227 * 1024 && 3 * Threads <= 2048) ? 3
+                              : (2 * (Smem + 1024) <= 227 * 1024 ? 2 : 1);
   static_assert(Rings * kBlk <= 32, "one lane -1 cell per loader lane and block");
-  static_assert(kLR >= (kDist + 1) * kBlk + kProRows, "lane -1 staging ring too shallow");
+  static_assert(kLR >= (kDist + 1) * kBlk + kProMax, "lane -1 staging ring too shallow");
   static_assert(LC % 2 == 0 && (S * 8) % 16 == 0, "16-byte ring rows");
 };
 }  // namespace gsl
@@ -234,7 +242,7 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
   // compile-time (a run-time stride costs the register the kernel lacks)
   constexpr int rstride = kR * kS + (LC == 102 ? 100 % 16 : 0);
   double* const lm1 = smem + (size_t)kRings * (kR * kS + 16);  // lane -1 staging [ring][kLR]
-  double* const stg = lm1 + kRings * kLR;                 // phantom staging [kStg][kBlk][RowCells]
+  double* const stg = lm1 + kRings * kLR;                 // phantom staging [Stg][kBlk][RowCells]
   __shared__ int s_ticket;
   // the warp index through a shuffle: the compiler then knows it is warp-uniform
   // (uniform branches and uniform registers for the role split)
@@ -278,8 +286,8 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.epoch + slot_out), "r"(n + 1) : "memory");
   }
   __syncthreads();
-  // producer rows a consumer reads: its rows >= -kProRows, i.e. >= LAM*G - kProRows here
-  const int ring_lo = kLam * kG - kProRows;
+  // producer rows a consumer reads: its rows >= -ProRows, i.e. >= LAM*G - ProRows here
+  const int ring_lo = kLam * kG - C::ProRows;
 
   if (wi < ncomp) {
     // ---------------- compute warp: packed unit = group g, lane l ----------
@@ -450,7 +458,7 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
         }
       }
       asm volatile("cp.async.commit_group;\n" ::: "memory");
-      rq_slot = rq_slot == kStg - 1 ? 0 : rq_slot + 1;
+      rq_slot = rq_slot == C::Stg - 1 ? 0 : rq_slot + 1;
     };
     auto finish = [&](int q) {
       const int i0 = q * kBlk;
@@ -516,7 +524,7 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
             }
         }
       }
-      fin_slot = fin_slot == kStg - 1 ? 0 : fin_slot + 1;
+      fin_slot = fin_slot == C::Stg - 1 ? 0 : fin_slot + 1;
       // lane -1 of every ring -> ring slot 1
       if (lm_on) {
         const int i = i0 + lm_o;
@@ -565,13 +573,20 @@ __global__ void __launch_bounds__(gsl::Cfg<REF, LC>::Threads, gsl::Cfg<REF, LC>:
       }
     }
     const int nb = m_end / kBlk;
-    constexpr int kProBlocks = kProRows / kBlk;
-    // prologue rows -kProRows..-1, then blocks 0 .. kDist-1 in flight
-    static_assert(kProBlocks <= kStg, "prologue blocks share the staging slots");
-    for (int q = -kProBlocks; q < 0; ++q) request(q);  // one L2 round trip for all of them
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    for (int q = -kProBlocks; q < 0; ++q) finish(q);
-    for (int q = 0; q < kDist; ++q) request(q);
+    constexpr int kProBlocks = C::ProRows / kBlk;
+    // prologue rows -ProRows..-1, then blocks 0 .. kDist-1 in flight
+    static_assert(kProBlocks <= C::Stg, "prologue blocks share the staging slots");
+    if constexpr (kProBlocks + kDist <= C::Stg) {
+      // the prologue blocks and the first kDist blocks in one L2 round trip
+      for (int q = -kProBlocks; q < kDist; ++q) request(q);
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kDist) : "memory");  // the prologue blocks landed
+      for (int q = -kProBlocks; q < 0; ++q) finish(q);
+    } else {
+      for (int q = -kProBlocks; q < 0; ++q) request(q);  // one L2 round trip for all of them
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      for (int q = -kProBlocks; q < 0; ++q) finish(q);
+      for (int q = 0; q < kDist; ++q) request(q);
+    }
     publish(kBarPro, smem + (size_t)lane_cell);
     for (int b = 0; b < nb; ++b) {
       if (b + kDist < nb)

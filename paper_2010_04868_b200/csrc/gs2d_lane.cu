@@ -743,8 +743,14 @@ static int gsl_groups(int64_t steps, int order) {
   int64_t per;
   int lc;
   gsl_plan(std::max<int64_t>(steps, 1), &per, &lc);
-  if (order == TVS_GS_REFERENCE) return lc <= 102 ? gsl::Cfg<true, 102>::G : gsl::Cfg<true, 128>::G;
-  return lc <= 102 ? gsl::Cfg<false, 102>::G : gsl::Cfg<false, 128>::G;
+  // the groups per CTA of exactly the instantiation gs2d_lane() launches
+  const bool ref = order == TVS_GS_REFERENCE;
+  switch (lc) {
+    case 32: return ref ? gsl::Cfg<true, 32>::G : gsl::Cfg<false, 32>::G;
+    case 64: return ref ? gsl::Cfg<true, 64>::G : gsl::Cfg<false, 64>::G;
+    case 102: return ref ? gsl::Cfg<true, 102>::G : gsl::Cfg<false, 102>::G;
+    default: return ref ? gsl::Cfg<true, 128>::G : gsl::Cfg<false, 128>::G;
+  }
 }
 // Drop-in pipeline hooks (api.cu gs2d_pipelined): one pass of <= 128 sweeps;
 // CTAs of that pass, and how many must have exited before row `row` holds

@@ -1,5 +1,5 @@
 // K6v3: 2D radius-1 Gauss-Seidel (9-point box / 5-point star) as time-lane
-// groups advancing in per-iteration lockstep, fed by a decoupled loader warp.
+// groups advancing in per-iteration lockstep, fed by decoupled loader warps.
 //
 // Replaces gs2d_temporal (reference kernels_nd.py:48-50, star-only there) for
 // the row-major in-place sweep of BASELINE config 4, bit-exact with the
@@ -25,26 +25,30 @@
 // Taps are summed in sorted order (NW N NE W C E SW S SE), unfused: bit-exact.
 //
 // CTA = G groups packed back to back into compute warps (T = 100: 5 x 100
-// units on 16 warps -- a unit costs the same shared-memory traffic, the
-// kernel's throughput bound, whether its sweep is real or not) + one loader
-// warp.  The compute warps meet at one named barrier per iteration (every
-// warp does identical work; all ring reads are at compile-time offsets).
-// The loader is NOT in that barrier: it runs up to two 4-iteration blocks
-// ahead and hands rows over through two shared counters (rows filled /
-// iterations done), so neither the L2 latency of the CTA-to-CTA hand-off nor
-// the loader's instruction stream sits on the per-iteration critical path
-// (K6v2 had the loader in the barrier: 19.1 ms at config 4, 14.5 ms with the
-// hand-off compiled out).  Per block the loader
-//   * copies lane -1 of every group (grid rows, prefetched by cp.async two
-//     blocks ahead) into ring slot 1;
-//   * copies the previous CTA's last group(s) ("phantom" groups) from an L2
+// units on 16 warps; lanes beyond the pass's sweeps would cost the same as
+// real ones) + 2 loader warps (4 in reference order), two CTAs per SM.  The
+// compute warps meet at one named barrier per iteration (every warp does
+// identical work; all ring reads are at compile-time offsets).  The loader
+// warps are NOT in that barrier: they hand 4-iteration blocks over through
+// named producer / consumer barriers (bar.arrive / bar.sync, four per
+// direction) and run up to two blocks ahead, so neither the L2 latency of the
+// CTA-to-CTA hand-off nor the loaders' instruction stream sits on the
+// per-iteration critical path (K6v2 had one loader warp inside the
+// barrier: 19.1 ms at config 4, 14.5 ms with the hand-off compiled out; this
+// kernel: 13.8 ms, 11.2 ms).  Per block the loaders
+//   * copy lane -1 of every group (grid rows, prefetched by cp.async one
+//     block ahead) into ring slot 1;
+//   * copy the previous CTA's last group(s) ("phantom" groups) from an L2
 //     ring into the phantom rings.  The hand-off is fence-free: the producer
 //     stores every output to an L2 ring whose cells hold a signalling-NaN
 //     sentinel until written (arithmetic never yields a signalling NaN; the
 //     boundary value is checked on the host); the consumer prefetches blocks
-//     by cp.async two blocks ahead, re-polls cells that still hold the
+//     by cp.async one block ahead, re-polls cells that still hold the
 //     sentinel and puts the sentinel back, so the ring is clean for its next
 //     use.
+// The run is a chain: a CTA starts one hop (~7 us: 10 iterations of lag, the
+// L2 round trips of its first rows) after its producer, 1659 CTAs at config
+// 4, 296 of them resident.
 // CTAs take tickets and only wait on lower tickets; a ring slot is reused
 // only after its consumer has exited.  Units outside the grid output the
 // boundary; lane Tp-1 (the pass's last sweep) writes its row's final values

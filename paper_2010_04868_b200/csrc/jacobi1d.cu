@@ -10,12 +10,16 @@
 // neighbours (__shfl_up/__shfl_down of its edge points); each warp owns a
 // 32*P-point tile whose outer `depth` points on each side are the ghost
 // trapezoid (their values decay into garbage one point per step and are
-// never stored).  No shared memory, no block barriers.
+// never stored).  No block barriers; shared memory only as a per-warp
+// staging tile that turns fully coalesced 16-byte loads / stores of the
+// warp's 1024-point tile into the lanes' contiguous runs (a lane's run lies
+// 256 bytes from the next lane's: per-lane 8-byte accesses cost 4 requests
+// per sector and 30% of the run time).
 //
 // Per launch: reads 32*P doubles and writes 32*P - 2*depth per warp; the
 // data (2^20 points = 8 MiB) stays L2-resident between launches, so the
 // kernel is FP64-issue bound: 5 DP ops / update unfused, 3 with the exact
-// power-of-two FMA form (heat1d: 0.25/0.5/0.25).
+// power-of-two FMA form (heat1d: 0.25/0.5/0.25), 2 with the scaled taps.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
